@@ -1,0 +1,469 @@
+// ref_driver.cpp -- runs the UNMODIFIED reference (/root/reference/proj/include/lmoe,
+// header-only C++20) to (1) emit golden vectors that pin oracle/lmoe_oracle.c and the
+// CUDA path, and (2) time the reference CPU path for bench.py's cpu_baseline /
+// --impl reference arm.
+//
+// TEST INFRASTRUCTURE ONLY.  Built by oracle/Makefile into oracle/_ref/ (git-ignored,
+// travels to the GPU box with gpurun).  This file contains no reference source; it
+// only #includes the reference headers from their read-only location.
+//
+//   ref_driver golden <out.bin>
+//   ref_driver bench-lsm <instance> <B> <N> <H> <d> <chunk> <threads> <budget_s> [gate_mean]
+//   ref_driver bench-moe <T> <hidden> <ffn> <E> <k> <threads> <budget_s>
+//
+// Golden stream format: records of
+//   u32 name_len, name bytes, u32 ndim, u32 shape[ndim], f64 data[prod(shape)]
+
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "lmoe/attention.hpp"
+#include "lmoe/lsm.hpp"
+#include "lmoe/moe.hpp"
+#include "lmoe/parallel.hpp"
+
+using namespace lmoe;
+
+namespace {
+
+FILE* g_out = nullptr;
+
+void emit(const std::string& name, const std::vector<int>& shape, const std::vector<double>& d) {
+    uint32_t nl = (uint32_t)name.size();
+    fwrite(&nl, 4, 1, g_out);
+    fwrite(name.data(), 1, nl, g_out);
+    uint32_t nd = (uint32_t)shape.size();
+    fwrite(&nd, 4, 1, g_out);
+    for (int s : shape) {
+        uint32_t u = (uint32_t)s;
+        fwrite(&u, 4, 1, g_out);
+    }
+    fwrite(d.data(), 8, d.size(), g_out);
+}
+void emit(const std::string& name, const Tensor& t) {
+    if (!t.defined()) return;
+    emit(name, t.shape(), t.data());
+}
+void emit_scalar(const std::string& name, double v) { emit(name, {1}, {v}); }
+
+// bf16 round-to-nearest-even, as the device sees bf16 inputs
+double to_bf16(double x) {
+    float f = (float)x;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    uint32_t lsb = (u >> 16) & 1u;
+    u = (u + 0x7FFFu + lsb) & 0xFFFF0000u;
+    std::memcpy(&f, &u, 4);
+    return (double)f;
+}
+Tensor round_bf16(const Tensor& t) {
+    std::vector<double> d = t.data();
+    for (auto& x : d) x = to_bf16(x);
+    return Tensor::from_data(t.shape(), d);
+}
+
+struct Variant {
+    const char* tag;
+    LsmInstance inst;
+    int fm;    // -1: reference default
+    int norm;  // -1: reference default
+};
+
+LsmSpec make_spec(const Variant& v, int d, Rng& rng) {
+    LsmSpec s = LsmSpec::make(v.inst, d, d, &rng);
+    if (v.fm >= 0) s.feature_map = (FeatureMap)v.fm;
+    if (v.norm >= 0) s.use_normalizer = v.norm != 0;
+    return s;
+}
+
+void emit_spec(const std::string& p, const LsmSpec& s) {
+    emit_scalar(p + "/instance", (double)(int)s.instance);
+    emit_scalar(p + "/feature_map", (double)(int)s.feature_map);
+    emit_scalar(p + "/use_normalizer", s.use_normalizer ? 1.0 : 0.0);
+    emit_scalar(p + "/scalar_decay", s.scalar_decay);
+    emit_scalar(p + "/mamba2_a_raw", s.mamba2_a_raw.defined() ? s.mamba2_a_raw.item() : 0.0);
+}
+
+const Variant kVariants[] = {
+    {"bla", LsmInstance::BLA, -1, -1},
+    {"bla_plain", LsmInstance::BLA, 0, 0},
+    {"rebased", LsmInstance::Rebased, -1, -1},
+    {"rebased_plain", LsmInstance::Rebased, -1, 0},
+    {"lightning", LsmInstance::Lightning, -1, -1},
+    {"retnet", LsmInstance::RetNet, -1, -1},
+    {"retnet_norm", LsmInstance::RetNet, 1, 1},
+    {"gla", LsmInstance::GLA, -1, -1},
+    {"gla_norm", LsmInstance::GLA, 1, 1},
+    {"hgrn2", LsmInstance::HGRN2, -1, -1},
+    {"rwkv6", LsmInstance::RWKV6, -1, -1},
+    {"mamba2", LsmInstance::Mamba2, -1, -1},
+};
+
+// ---- LSM: chunked vs sequential, tiny head dims (acceptance.cpp:44-69 style) ----
+void golden_lsm_small() {
+    int vi = 0;
+    for (const Variant& var : kVariants) {
+        for (int n : {7, 33}) {
+            const int d = 4;
+            Rng rng(1000 + 17 * vi + n);
+            LsmSpec spec = make_spec(var, d, rng);
+            const Tensor q = Tensor::randn({n, d}, rng, 0.5);
+            const Tensor k = Tensor::randn({n, d}, rng, 0.5);
+            const Tensor v = Tensor::randn({n, d}, rng, 0.5);
+            const LsmGates g = LsmGates::random_for(spec, n, rng);
+            const std::string p = std::string("lsm_small/") + var.tag + "_n" + std::to_string(n);
+            emit_spec(p, spec);
+            emit(p + "/q", q);
+            emit(p + "/k", k);
+            emit(p + "/v", v);
+            emit(p + "/a_pre", g.a_pre);
+            emit(p + "/b_pre", g.b_pre);
+            MemoryState fs;
+            emit(p + "/o_seq", lsm_forward_sequential(q, k, v, g, spec, &fs));
+            emit(p + "/M_seq", fs.M);
+            emit(p + "/z_seq", fs.z);
+            for (int c : {1, 3, 8, n}) {
+                MemoryState fc;
+                emit(p + "/o_c" + std::to_string(c), lsm_forward_chunked(q, k, v, g, spec, c, &fc));
+                emit(p + "/M_c" + std::to_string(c), fc.M);
+                emit(p + "/z_c" + std::to_string(c), fc.z);
+            }
+        }
+        ++vi;
+    }
+}
+
+// ---- LSM at device head dims, bf16-exact inputs (GPU golden) ----
+void golden_lsm_device() {
+    struct Case { const char* var; int n; int d; int chunk; double gate_mean; double gate_std; };
+    const Case cases[] = {
+        {"bla_plain", 300, 64, 64, 0, 1},  {"bla", 300, 64, 64, 0, 1},
+        {"lightning", 300, 64, 64, 0, 1},  {"retnet", 257, 128, 64, 0, 1},
+        {"mamba2", 300, 64, 64, 0, 1},     {"mamba2", 260, 128, 64, -3, 0.5},
+        {"gla", 300, 64, 64, 0, 1},        {"gla", 260, 128, 64, 4, 0.5},
+        {"hgrn2", 300, 64, 64, 0, 1},      {"rwkv6", 200, 64, 64, 0, 1},
+        {"rebased", 200, 64, 64, 0, 1},    {"gla_norm", 200, 64, 64, 0, 1},
+    };
+    int ci = 0;
+    for (const Case& c : cases) {
+        const Variant* var = nullptr;
+        for (const Variant& v : kVariants) if (std::string(v.tag) == c.var) var = &v;
+        Rng rng(5000 + ci);
+        LsmSpec spec = make_spec(*var, c.d, rng);
+        if (spec.mamba2_a_raw.defined())
+            spec.mamba2_a_raw = Tensor::from_data({1}, {to_bf16(spec.mamba2_a_raw.item())});
+        const Tensor q = round_bf16(Tensor::randn({c.n, c.d}, rng, 0.5));
+        const Tensor k = round_bf16(Tensor::randn({c.n, c.d}, rng, 0.5));
+        const Tensor v = round_bf16(Tensor::randn({c.n, c.d}, rng, 0.5));
+        LsmGates g = LsmGates::random_for(spec, c.n, rng, c.gate_std);
+        if (g.a_pre.defined()) {
+            std::vector<double> a = g.a_pre.data();
+            for (auto& x : a) x = to_bf16(x + c.gate_mean);
+            g.a_pre = Tensor::from_data(g.a_pre.shape(), a);
+        }
+        if (g.b_pre.defined()) {
+            std::vector<double> b = g.b_pre.data();
+            for (auto& x : b) x = (double)(float)(x + c.gate_mean);
+            g.b_pre = Tensor::from_data(g.b_pre.shape(), b);
+        }
+        const std::string p = std::string("lsm_dev/") + c.var + "_n" + std::to_string(c.n) +
+                              "_d" + std::to_string(c.d) + (c.gate_mean != 0 ? "_long" : "");
+        emit_spec(p, spec);
+        emit_scalar(p + "/chunk", c.chunk);
+        emit(p + "/q", q);
+        emit(p + "/k", k);
+        emit(p + "/v", v);
+        emit(p + "/a_pre", g.a_pre);
+        emit(p + "/b_pre", g.b_pre);
+        MemoryState fs;
+        emit(p + "/o", lsm_forward_chunked(q, k, v, g, spec, c.chunk, &fs));
+        emit(p + "/M", fs.M);
+        emit(p + "/z", fs.z);
+        ++ci;
+    }
+}
+
+// ---- LSM gradients from the reference tape (tensor.hpp:1178) ----
+void golden_lsm_grad() {
+    const char* tags[] = {"bla_plain", "lightning", "retnet", "gla", "hgrn2", "rwkv6", "mamba2",
+                          "rebased_plain"};
+    int ci = 0;
+    for (const char* tag : tags) {
+        const Variant* var = nullptr;
+        for (const Variant& v : kVariants) if (std::string(v.tag) == tag) var = &v;
+        const int n = 20, d = 4;
+        Rng rng(7000 + ci);
+        LsmSpec spec = make_spec(*var, d, rng);
+        if (spec.mamba2_a_raw.defined()) spec.mamba2_a_raw.set_requires_grad(true);
+        Tensor q = Tensor::randn({n, d}, rng, 0.5, DType::f64, true);
+        Tensor k = Tensor::randn({n, d}, rng, 0.5, DType::f64, true);
+        Tensor v = Tensor::randn({n, d}, rng, 0.5, DType::f64, true);
+        LsmGates g = LsmGates::random_for(spec, n, rng);
+        if (g.a_pre.defined()) g.a_pre.set_requires_grad(true);
+        if (g.b_pre.defined()) g.b_pre.set_requires_grad(true);
+        const Tensor w = Tensor::randn({n, d}, rng, 1.0);
+        const Tensor o = lsm_forward_chunked(q, k, v, g, spec, 8);
+        backward(sum(mul(o, w)));
+        const std::string p = std::string("lsm_grad/") + tag;
+        emit_spec(p, spec);
+        emit(p + "/q", q);
+        emit(p + "/k", k);
+        emit(p + "/v", v);
+        emit(p + "/a_pre", g.a_pre);
+        emit(p + "/b_pre", g.b_pre);
+        emit(p + "/dO", w);
+        emit(p + "/o", o);
+        emit(p + "/dq", {n, d}, q.grad());
+        emit(p + "/dk", {n, d}, k.has_grad() ? k.grad() : std::vector<double>(n * d, 0.0));
+        emit(p + "/dv", {n, d}, v.grad());
+        if (g.a_pre.defined()) emit(p + "/da_pre", g.a_pre.shape(), g.a_pre.grad());
+        if (g.b_pre.defined()) emit(p + "/db_pre", g.b_pre.shape(), g.b_pre.grad());
+        if (spec.mamba2_a_raw.defined()) emit(p + "/da_raw", {1}, spec.mamba2_a_raw.grad());
+        ++ci;
+    }
+}
+
+// ---- routing (moe.hpp:58-103), KATs of test_moe.cpp:9-62 plus random ----
+void golden_route() {
+    NoGradGuard ng;
+    struct RC { const char* tag; int t; int e; int k; int kind; };
+    const RC cases[] = {{"tie", 2, 4, 2, 0}, {"rand_k1", 64, 8, 1, 1}, {"rand_k2", 64, 8, 2, 1},
+                        {"rand_k3", 64, 8, 3, 1}, {"rand_k8", 64, 8, 8, 1},
+                        {"e64_k8", 256, 64, 8, 1}, {"e64_k8_ties", 128, 64, 8, 2}};
+    int ci = 0;
+    for (const RC& c : cases) {
+        Rng rng(9000 + ci);
+        Tensor logits;
+        if (c.kind == 0) {
+            logits = Tensor::from_data({2, 4}, {0.1, 0.9, 0.9, 0.2, -1.0, -1.0, -1.0, -1.0});
+        } else if (c.kind == 1) {
+            logits = round_bf16(Tensor::randn({c.t, c.e}, rng, 1.0));
+            std::vector<double> d = logits.data();
+            for (auto& x : d) x = (double)(float)x;
+            logits = Tensor::from_data({c.t, c.e}, d);
+        } else {  // heavy ties: small integer grid
+            std::vector<double> d((size_t)c.t * c.e);
+            for (auto& x : d) x = (double)(int)rng.randint(5) * 0.25;
+            logits = Tensor::from_data({c.t, c.e}, d);
+        }
+        const RoutingDecision dec = route(logits, c.k);
+        const std::string p = std::string("route/") + c.tag;
+        emit(p + "/logits", logits);
+        emit_scalar(p + "/top_k", c.k);
+        std::vector<double> ids;
+        for (const auto& row : dec.expert_ids) for (int id : row) ids.push_back(id);
+        emit(p + "/ids", {c.t, c.k}, ids);
+        emit(p + "/gates", dec.gates);
+        emit(p + "/probs", dec.full_probs);
+        emit_scalar(p + "/aux", load_balance_loss(dec).item());
+        ++ci;
+    }
+}
+
+// ---- MoE layer forward (moe.hpp:133-149) ----
+void golden_moe() {
+    NoGradGuard ng;
+    struct MC { const char* tag; int t; int hidden; int ffn; int e; int k; };
+    const MC cases[] = {{"small", 10, 6, 8, 4, 2}, {"mid", 40, 16, 12, 8, 2}, {"dense", 16, 8, 8, 4, 4}};
+    int ci = 0;
+    for (const MC& c : cases) {
+        Rng rng(11000 + ci);
+        const MoeConfig cfg{c.e, c.k, c.hidden, c.ffn, 0.01};
+        const MoeLayer layer = MoeLayer::init(cfg, rng, DType::f64);
+        const Tensor x = Tensor::randn({c.t, c.hidden}, rng, 0.5);
+        auto [y, aux] = layer.forward(x);
+        const std::string p = std::string("moe/") + c.tag;
+        emit_scalar(p + "/top_k", c.k);
+        emit(p + "/x", x);
+        emit(p + "/router", layer.router);
+        std::vector<double> wg, wu, wd;
+        for (const auto& ex : layer.experts) {
+            wg.insert(wg.end(), ex.w_gate.data().begin(), ex.w_gate.data().end());
+            wu.insert(wu.end(), ex.w_up.data().begin(), ex.w_up.data().end());
+            wd.insert(wd.end(), ex.w_down.data().begin(), ex.w_down.data().end());
+        }
+        emit(p + "/w_gate", {c.e, c.hidden, c.ffn}, wg);
+        emit(p + "/w_up", {c.e, c.hidden, c.ffn}, wu);
+        emit(p + "/w_down", {c.e, c.ffn, c.hidden}, wd);
+        emit(p + "/y", y);
+        emit_scalar(p + "/aux", aux.item());
+        ++ci;
+    }
+}
+
+// ---- sequence parallelism (parallel.hpp:282-418) ----
+void golden_sp() {
+    NoGradGuard ng;
+    const int n = 32, d = 4;
+    int ci = 0;
+    for (const char* tag : {"bla", "bla_plain", "lightning", "gla", "mamba2", "hgrn2", "gla_norm"}) {
+        const Variant* var = nullptr;
+        for (const Variant& v : kVariants) if (std::string(v.tag) == tag) var = &v;
+        Rng rng(13000 + ci);
+        LsmSpec spec = make_spec(*var, d, rng);
+        const Tensor q = Tensor::randn({n, d}, rng, 0.5);
+        const Tensor k = Tensor::randn({n, d}, rng, 0.5);
+        const Tensor v = Tensor::randn({n, d}, rng, 0.5);
+        const LsmGates g = LsmGates::random_for(spec, n, rng);
+        const std::string p = std::string("sp/") + tag;
+        emit_spec(p, spec);
+        emit(p + "/q", q);
+        emit(p + "/k", k);
+        emit(p + "/v", v);
+        emit(p + "/a_pre", g.a_pre);
+        emit(p + "/b_pre", g.b_pre);
+        emit(p + "/o_seq", lsm_forward_sequential(q, k, v, g, spec));
+        for (int t : {1, 2, 4, 8}) {
+            RankGroup grp(t);
+            emit(p + "/o_t" + std::to_string(t), sp_forward_masked(grp, q, k, v, g, spec));
+            emit_scalar(p + "/comm_elems_t" + std::to_string(t),
+                        (double)(grp.comm_log().empty() ? 0 : grp.comm_log()[0].elements));
+        }
+        ++ci;
+    }
+    // attention with row offset + KV all-gather SP (attention.hpp:18-38, parallel.hpp:380-387)
+    Rng rng(14000);
+    const int na = 24;
+    const Tensor q = Tensor::randn({na, 8}, rng, 0.5);
+    const Tensor k = Tensor::randn({na, 8}, rng, 0.5);
+    const Tensor v = Tensor::randn({na, 8}, rng, 0.5);
+    emit("attn/q", q);
+    emit("attn/k", k);
+    emit("attn/v", v);
+    emit("attn/o_full", softmax_attention_parallel(q, k, v, true));
+    emit("attn/o_off", softmax_attention_parallel(slice_rows(q, 16, 24), k, v, true, 16));
+    for (int t : {2, 4}) {
+        RankGroup grp(t);
+        emit("attn/o_sp_t" + std::to_string(t), sp_attention_allgather(grp, q, k, v));
+        long el = 0;
+        for (const auto& r : grp.comm_log()) el += r.elements;
+        emit_scalar("attn/comm_elems_t" + std::to_string(t), (double)el);
+    }
+}
+
+int cmd_golden(const char* path) {
+    g_out = fopen(path, "wb");
+    if (!g_out) return 2;
+    golden_lsm_small();
+    golden_lsm_device();
+    golden_lsm_grad();
+    golden_route();
+    golden_moe();
+    golden_sp();
+    fclose(g_out);
+    return 0;
+}
+
+// ---- CPU baseline timers (SURVEY 8d "CPU baseline timing") ----
+int cmd_bench_lsm(int argc, char** argv) {
+    if (argc < 10) return 2;
+    auto inst = instance_from_name(argv[2]);
+    if (!inst) return 3;
+    const int B = atoi(argv[3]), N = atoi(argv[4]), H = atoi(argv[5]), d = atoi(argv[6]);
+    const int chunk = atoi(argv[7]);
+    int threads = atoi(argv[8]);
+    const double budget = atof(argv[9]);
+    const double gate_mean = argc > 10 ? atof(argv[10]) : 0.0;
+    if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
+    NoGradGuard ng;
+    // f32 mode everywhere, gates included (BASELINE.md CPU-baseline plan step 4)
+    const int heads = B * H;
+    std::vector<std::thread> pool;
+    std::vector<int> done(threads, 0);
+    auto t0 = std::chrono::steady_clock::now();
+    std::atomic<int> next{0};
+    for (int w = 0; w < threads; ++w)
+        pool.emplace_back([&, w]() {
+            Rng rng(100 + w);
+            LsmSpec spec = LsmSpec::make(*inst, d, d, &rng, DType::f32);
+            const Tensor q = Tensor::randn({N, d}, rng, 0.5, DType::f32);
+            const Tensor k = Tensor::randn({N, d}, rng, 0.5, DType::f32);
+            const Tensor v = Tensor::randn({N, d}, rng, 0.5, DType::f32);
+            LsmGates g = LsmGates::random_for(spec, N, rng);
+            for (Tensor* t : {&g.a_pre, &g.b_pre}) {
+                if (!t->defined()) continue;
+                std::vector<double> x = t->data();
+                for (auto& e : x) e += gate_mean;
+                *t = Tensor::from_data(t->shape(), x, DType::f32);
+            }
+            while (true) {
+                const int h = next.fetch_add(1);
+                if (h >= heads) break;
+                double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                if (el > budget) break;
+                (void)lsm_forward_chunked(q, k, v, g, spec, chunk);
+                done[w]++;
+            }
+        });
+    for (auto& th : pool) th.join();
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    int total = 0;
+    for (int x : done) total += x;
+    // heads_done sequences of N tokens each; tokens/s counts (token, all H heads) units
+    const double tok_s = (double)total * N / (double)H / secs;
+    printf("{\"heads_done\": %d, \"heads_total\": %d, \"seconds\": %.6f, \"threads\": %d, "
+           "\"tokens_per_sec\": %.3f}\n", total, heads, secs, threads, tok_s);
+    return 0;
+}
+
+int cmd_bench_moe(int argc, char** argv) {
+    if (argc < 9) return 2;
+    const int T = atoi(argv[2]), hidden = atoi(argv[3]), ffn = atoi(argv[4]), E = atoi(argv[5]);
+    const int K = atoi(argv[6]);
+    int threads = atoi(argv[7]);
+    const double budget = atof(argv[8]);
+    if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
+    NoGradGuard ng;
+    Rng rng(3);
+    const MoeConfig cfg{E, K, hidden, ffn, 0.01};
+    const MoeLayer layer = MoeLayer::init(cfg, rng, DType::f32);
+    const int shard = 64;
+    std::atomic<int> next{0};
+    std::vector<int> done(threads, 0);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w)
+        pool.emplace_back([&, w]() {
+            Rng r2(50 + w);
+            const Tensor x = Tensor::randn({shard, hidden}, r2, 1.0, DType::f32);
+            while (true) {
+                const int s = next.fetch_add(1);
+                if (s * shard >= T) break;
+                double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                if (el > budget) break;
+                (void)layer.forward(x);
+                done[w] += shard;
+            }
+        });
+    for (auto& th : pool) th.join();
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    int total = 0;
+    for (int x : done) total += x;
+    printf("{\"tokens_done\": %d, \"tokens_total\": %d, \"seconds\": %.6f, \"threads\": %d, "
+           "\"tokens_per_sec\": %.3f}\n", total, T, secs, threads, total / secs);
+    return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        fprintf(stderr, "usage: ref_driver golden <out> | bench-lsm ... | bench-moe ...\n");
+        return 2;
+    }
+    try {
+        if (!strcmp(argv[1], "golden") && argc >= 3) return cmd_golden(argv[2]);
+        if (!strcmp(argv[1], "bench-lsm")) return cmd_bench_lsm(argc, argv);
+        if (!strcmp(argv[1], "bench-moe")) return cmd_bench_moe(argc, argv);
+    } catch (const std::exception& e) {
+        fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
+    return 2;
+}
