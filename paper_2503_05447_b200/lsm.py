@@ -1,0 +1,167 @@
+"""Host mirror of the reference LSM interface (lsm.hpp) over the C-ABI.
+
+Names, argument meaning and error texts follow /root/reference/proj/include/lmoe/lsm.hpp:
+  LsmInstance / FeatureMap / LsmSpec.make / LsmGates / MemoryState  (lsm.hpp:30-273)
+  lsm_forward_chunked(q, k, v, gates, spec, chunk_size, final_state) (lsm.hpp:668-708)
+Tensors are torch CUDA tensors (torch is plumbing for device memory and streams only).
+A single head is (N, d) exactly like the reference; the batched device layout is
+[B, N, H, d] (per batch row, the reference's (N x H*d) projection, model.hpp:234-243).
+"""
+import ctypes
+import dataclasses
+import math
+from typing import Optional
+
+import torch
+
+from . import _lib
+
+INSTANCES = ["bla", "lightning", "retnet", "gla", "deltanet", "gated_deltanet", "rebased",
+             "gfw", "gateloop", "ttt", "titans", "s4", "mamba", "mamba2", "hgrn2", "rwkv6",
+             "rwkv7"]
+
+
+class LsmInstance:
+    BLA, LIGHTNING, RETNET, GLA, REBASED, MAMBA2, HGRN2, RWKV6 = 0, 1, 2, 3, 6, 13, 14, 15
+
+
+class FeatureMap:
+    IDENTITY, ELU_PLUS_ONE, SQUARED = 0, 1, 2
+
+
+@dataclasses.dataclass
+class LsmSpec:
+    """lmoe::LsmSpec (lsm.hpp:126-204).  mamba2_a_raw is per head ([H] tensor or float)."""
+    instance: int = LsmInstance.BLA
+    feature_map: int = FeatureMap.IDENTITY
+    use_normalizer: bool = False
+    d_k: int = 0
+    d_v: int = 0
+    scalar_decay: float = 1.0
+    mamba2_a_raw: Optional[torch.Tensor] = None
+
+    @staticmethod
+    def make(instance, d_k, d_v=None):
+        """Defaults of LsmSpec::make (lsm.hpp:146-165)."""
+        if isinstance(instance, str):
+            instance = INSTANCES.index(instance)
+        s = LsmSpec(instance=instance, d_k=d_k, d_v=d_v or d_k)
+        if instance == LsmInstance.BLA:
+            s.feature_map, s.use_normalizer = FeatureMap.ELU_PLUS_ONE, True
+        elif instance == LsmInstance.REBASED:
+            s.feature_map, s.use_normalizer = FeatureMap.SQUARED, True
+        elif instance == LsmInstance.LIGHTNING:
+            s.scalar_decay = 0.95
+        elif instance == LsmInstance.RETNET:
+            s.scalar_decay = 1.0 - 1.0 / 32.0
+        return s
+
+    def name(self):
+        return INSTANCES[self.instance]
+
+
+@dataclasses.dataclass
+class LsmGates:
+    """lmoe::LsmGates (lsm.hpp:216-261): a_pre [.., N, d_k] (TokenVector), b_pre [.., N]."""
+    a_pre: Optional[torch.Tensor] = None
+    b_pre: Optional[torch.Tensor] = None
+
+
+@dataclasses.dataclass
+class MemoryState:
+    """lmoe::MemoryState (lsm.hpp:264-281): M (d_k x d_v) fp32, z (d_k) fp32 or None."""
+    M: Optional[torch.Tensor] = None
+    z: Optional[torch.Tensor] = None
+    step: int = 0
+
+
+_DTYPES = {torch.bfloat16: 1, torch.float32: 0}
+_ws_cache = {}
+
+
+def _workspace(nbytes, device):
+    key = (device, nbytes)
+    ws = _ws_cache.get(key)
+    if ws is None:
+        _ws_cache.clear()
+        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def make_desc(spec, chunk_size, check=True):
+    d = _lib.LsmDesc()
+    d.instance = int(spec.instance)
+    d.feature_map = int(spec.feature_map)
+    d.use_normalizer = int(bool(spec.use_normalizer))
+    d.scalar_decay = float(spec.scalar_decay)
+    d.chunk_size = int(chunk_size)
+    d.flags = 1 if check else 0
+    return d
+
+
+def lsm_forward_batched(q, k, v, gates, spec, chunk_size=64, initial_state=None,
+                        final_state=None, out=None, check=True, stream=None):
+    """[B,N,H,D] forward for all heads.  final_state (MemoryState) receives [B,H,D,D] / [B,H,D]."""
+    B, N, H, D = q.shape
+    for t in (k, v):
+        if t.shape != q.shape or t.dtype != q.dtype:
+            raise RuntimeError("shape mismatch in lsm_forward_chunked: %s vs %s"
+                               % (tuple(q.shape), tuple(t.shape)))
+    if q.dtype not in _DTYPES:
+        raise RuntimeError("lsm_forward_chunked: dtype must be bf16 or fp32")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    o = out if out is not None else torch.empty_like(q)
+    a_raw = None
+    if spec.instance == LsmInstance.MAMBA2:
+        ar = spec.mamba2_a_raw
+        if ar is None:
+            raise RuntimeError("LsmSpec: mamba2_a_raw required for mamba2")
+        a_raw = torch.as_tensor(ar, dtype=torch.float32, device=q.device).reshape(-1).expand(H).contiguous()
+    b_pre = None
+    if gates is not None and gates.b_pre is not None:
+        b_pre = gates.b_pre.to(torch.float32).contiguous()
+    a_pre = None
+    if gates is not None and gates.a_pre is not None:
+        a_pre = gates.a_pre.to(q.dtype).contiguous()
+    M0 = z0 = None
+    if initial_state is not None:
+        M0 = initial_state.M.to(torch.float32).contiguous()
+        if initial_state.z is not None:
+            z0 = initial_state.z.to(torch.float32).contiguous()
+    M_out = z_out = None
+    if final_state is not None:
+        M_out = torch.empty(B, H, D, D, dtype=torch.float32, device=q.device)
+        z_out = torch.empty(B, H, D, dtype=torch.float32, device=q.device) if spec.use_normalizer else None
+    desc = make_desc(spec, chunk_size, check)
+    L = _lib.lib()
+    dt = _DTYPES[q.dtype]
+    nbytes = L.lmoe_lsm_fwd_workspace_size(ctypes.byref(desc), B, N, H, D, dt)
+    ws = _workspace(nbytes, q.device)
+    st = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+    rc = L.lmoe_lsm_fwd(ctypes.byref(desc), B, N, H, D, dt, _lib.ptr(q), _lib.ptr(k), _lib.ptr(v),
+                        _lib.ptr(a_pre), _lib.ptr(b_pre), _lib.ptr(a_raw), _lib.ptr(M0),
+                        _lib.ptr(z0), _lib.ptr(o), _lib.ptr(M_out), _lib.ptr(z_out),
+                        _lib.ptr(ws), ws.numel(), ctypes.c_void_p(st))
+    _lib.check(rc)
+    if final_state is not None:
+        final_state.M, final_state.z, final_state.step = M_out, z_out, N
+    return o
+
+
+def lsm_forward_chunked(q, k, v, gates, spec, chunk_size, final_state=None):
+    """lsm_forward_chunked (lsm.hpp:668-708) for one head: q, k (N, d_k), v (N, d_v)."""
+    if q.dim() != 2:
+        raise RuntimeError("lsm_forward_chunked: expects (N, d) per-head matrices")
+    g = None
+    if gates is not None:
+        g = LsmGates(a_pre=None if gates.a_pre is None else gates.a_pre[None, :, None, :],
+                     b_pre=None if gates.b_pre is None else gates.b_pre[None, :, None])
+    fs = MemoryState() if final_state is not None else None
+    o = lsm_forward_batched(q[None, :, None, :], k[None, :, None, :], v[None, :, None, :], g,
+                            spec, chunk_size, final_state=fs)
+    if final_state is not None:
+        final_state.M = fs.M[0, 0]
+        final_state.z = None if fs.z is None else fs.z[0, 0]
+        final_state.step = q.shape[0]
+    return o[0, :, 0, :]
