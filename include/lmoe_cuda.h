@@ -51,7 +51,7 @@ enum lmoe_instance {
     LMOE_MAMBA2 = 13, LMOE_HGRN2 = 14, LMOE_RWKV6 = 15
 };
 enum lmoe_feature_map { LMOE_FM_IDENTITY = 0, LMOE_FM_ELU1 = 1, LMOE_FM_SQUARED = 2 };
-enum lmoe_flags { LMOE_FLAG_CHECK = 1 };
+enum lmoe_flags { LMOE_FLAG_CHECK = 1, LMOE_FLAG_TIMING = 2 };
 
 /* Mirrors the fields of lmoe::LsmSpec (lsm.hpp:126-140) that the separable kinds use.
  * Static per-head parameters (Mamba2 a_raw) are passed as arrays. */
@@ -89,6 +89,12 @@ int lmoe_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dty
 
 /* Number of kernels one lmoe_lsm_fwd call launches (for launch accounting). */
 int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc);
+
+/* Per-phase device time of calls made with LMOE_FLAG_TIMING since the last read (CUDA
+ * events on the caller's stream).  Returns the number of calls, or -status on error. */
+int lmoe_timing_read(float* ms_out, int nphase);
+/* Kernels of this library enqueued since process start. */
+long long lmoe_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -20,8 +20,8 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["common.cu", "lsm_host.cu"]  # lsm_host.cu includes lsm_fwd.cu (kernels + launches in one TU)
-LIBS = []
+SOURCES = ["common.cu", "lsm_host.cu", "lsm_combine.cu", "lsm_inst_bf16.cu", "lsm_inst_f32.cu"]
+LIBS = ["-lnccl"]
 
 
 def _sources():

@@ -50,6 +50,8 @@ def lib():
     L.lmoe_lsm_fwd.restype = i
     L.lmoe_lsm_fwd.argtypes = [ctypes.POINTER(LsmDesc), i, i, i, i, i, vp, vp, vp, vp, vp, vp,
                                vp, vp, vp, vp, vp, vp, sz, vp]
+    L.lmoe_timing_read.restype = i
+    L.lmoe_timing_read.argtypes = [ctypes.POINTER(ctypes.c_float), i]
     _lib = L
     return L
 
@@ -66,3 +68,11 @@ def ptr(t):
 
 def launch_count():
     return int(lib().lmoe_launch_count())
+
+
+def timing_read(nphase=3):
+    arr = (ctypes.c_float * nphase)()
+    calls = lib().lmoe_timing_read(arr, nphase)
+    if calls < 0:
+        raise LmoeError(-calls, lib().lmoe_last_error().decode())
+    return calls, [float(x) for x in arr]

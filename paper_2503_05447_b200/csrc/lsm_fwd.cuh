@@ -12,16 +12,21 @@
 //                             weights are known without a pre-pass; S accumulates in TMEM.
 //   phase 2  lsm_seg_combine  per (b,h): decayed exclusive prefix over segments
 //                             M_in(s+1) = D_s M_in(s) + S_s (+ initial state M0).
-//   phase 3  lsm_output_pass  per (b,h,segment), chunk by chunk (C = 128 tokens):
-//                S  = phiQ Keff^T                           (tcgen05, TMEM)
-//                P  = S . exp(G_i - G_j) . [j <= i]         (registers -> TMEM, bf16/tf32)
-//                O  = P V + (phiQ . e^{G}) M                (tcgen05, P read from TMEM)
-//                dM = (Keff . e^{G_end - G})^T V            (tcgen05)
-//                M  = e^{G_end} M + dM                      (fp32 master state in registers)
+//   phase 3  lsm_output_pass  per (b,h,segment), chunk by chunk (C = 128 tokens), with
+//            G_t = inclusive chunk-local log decay, kf_t = Mamba2 softplus(b_t) (else 1):
+//                S  = phiQ phiK^T                               (tcgen05 -> TMEM, 2 buffers)
+//                P  = S . e^{G_i} . (e^{-G_j} kf_j) . [j <= i]  (registers -> TMEM)
+//                O  = P V + (phiQ . e^{G}) M                    (tcgen05; P read from TMEM)
+//                M' = e^{G_end} M + (phiK . kf . e^{G_end-G})^T V (tcgen05, accumulated
+//                                                              onto the TMEM-resident state)
+//            The pairwise factor is split as e^{G_i} e^{-G_j} when the chunk's total decay
+//            is > e^-80 (no overflow); otherwise P uses exact e^{G_i - G_j} per element.
 //
-// Tile layout in shared memory: every Q/K/V tile is 128 token rows x 256 bytes, stored as
-// two SWIZZLE_128B column blocks of [128 rows x 128 B] exactly as TMA writes them; this
-// covers bf16 d=128 and fp32 (tf32 MMA) d=64 with the same byte arithmetic.
+// Tile layout in shared memory: every Q/K/V tile is 128 token rows x 256 bytes, two
+// SWIZZLE_128B column blocks of [128 rows x 128 B] exactly as TMA writes them; this covers
+// bf16 d=128 and fp32 (tf32 MMA) d=64 with the same byte arithmetic.  tf32 operands must be
+// K-major (measured: MN-major tf32 descriptors yield zeros), so the fp32 path transposes
+// K~ and V into K-major [d rows x 128 tokens] tiles and keeps the state operand as M^T.
 #pragma once
 #include "ptx.cuh"
 
@@ -31,18 +36,16 @@ constexpr int kC = 128;                         // chunk rows (tokens) per devic
 constexpr int kRowBytes = 256;                  // head_dim * sizeof(T)
 constexpr int kTileBytes = kC * kRowBytes;      // 32 KB
 constexpr int kBlockBytes = kC * 128;           // one SW128 column block of a tile: 16 KB
-constexpr int kMathThreads = 256;               // 8 epilogue/transform warps
+constexpr int kMathThreads = 256;               // 8 epilogue warps (output pass)
+constexpr float kSafeLogDecay = -80.f;          // e^{-G} stays finite in fp32 above this
 
 enum DecayMode { kDecayNone = 0, kDecayConst = 1, kDecayTokenScalar = 2 };
 
 struct LsmFwdParams {
     int B, N, H;
+    int Nstride;       // sequence length of the underlying [B, Nstride, H] gate buffer
     int seg_len;       // tokens per segment, multiple of kC
     int nseg;          // segments per (b,h)
-    int decay;         // DecayMode
-    int fm;            // 0 identity, 1 elu+1, 2 squared
-    int norm;          // normaliser on
-    int mamba2_keff;   // keff = phi(k) * softplus(b)
     float log_a;       // ConstScalar: log(a)
     const float* b_pre;  // [B,N,H]   TokenScalar gate pre-activation
     const float* a_raw;  // [H]       Mamba2 static parameter
@@ -51,8 +54,19 @@ struct LsmFwdParams {
     float* logDseg;      // [B*H][nseg]
     const float* Min;    // [B*H][nseg][dk][dv]  (phase 3 input)
     const float* zin;    // [B*H][nseg][dk]
+    void* o;             // [B, Nstride, H, D] output (phase 3), written from registers
     int* err;            // [0] degenerate normaliser, [1] non-finite state
+    int order;           // phase-3 schedule: 0 = P epilogue first, 1 = transforms first
+    unsigned long long* trace;  // optional clock64 trace of CTA (0,0,0) [64 chunks][16]
 };
+
+__device__ __forceinline__ void trace_mark(const LsmFwdParams& p, int c, int slot) {
+    if (p.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && c < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+        p.trace[c * 16 + slot] = t;
+    }
+}
 
 template <typename T>
 struct TileTraits;
@@ -63,7 +77,10 @@ struct TileTraits<__nv_bfloat16> {
     static constexpr int EPB = 64;         // elements per 128-byte block row
     static constexpr int KSTEP = 16;       // UMMA K per instruction
     static constexpr uint32_t FMT = 1;     // BF16
-    static constexpr int MBUF_BYTES = 128 * 128 * 2;
+    static constexpr int MOP_BYTES = 128 * 128 * 2;   // state operand
+    static constexpr int OUT_STAGES = 2;
+    static constexpr int SP_STAGES = 3;
+    static constexpr bool kTransposed = false;
 };
 template <>
 struct TileTraits<float> {
@@ -72,80 +89,52 @@ struct TileTraits<float> {
     static constexpr int EPB = 32;
     static constexpr int KSTEP = 8;        // tf32
     static constexpr uint32_t FMT = 2;     // TF32
-    static constexpr int MBUF_BYTES = 64 * 64 * 4;
+    static constexpr int MOP_BYTES = 64 * 64 * 4;
+    static constexpr int OUT_STAGES = 1;
+    static constexpr int SP_STAGES = 2;
+    static constexpr bool kTransposed = true;  // K-major-only operands
 };
 
 __device__ __forceinline__ float softplus_f(float x) {
     return x > 30.f ? x : log1pf(__expf(x));
 }
-__device__ __forceinline__ float fmap_f(int fm, float x) {
-    if (fm == 1) return x > 0.f ? x + 1.f : __expf(x);
-    if (fm == 2) return x * x;
-    return x;
+template <int FM>
+__device__ __forceinline__ float fmap_t(float x) {
+    if constexpr (FM == 1) return x > 0.f ? x + 1.f : __expf(x);
+    else if constexpr (FM == 2) return x * x;
+    else return x;
 }
 
-// Elementwise transform of one 16-byte chunk (8 bf16 or 4 fp32) in place.
+// Shared-memory sizes (bytes).
 template <typename T>
-__device__ __forceinline__ void xform_chunk(uint8_t* p, int fm, float scale, bool apply_fm) {
-    uint4 v = *reinterpret_cast<uint4*>(p);
-    if constexpr (sizeof(T) == 2) {
-        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            float2 f = unpack_bf16(w[i]);
-            if (apply_fm) { f.x = fmap_f(fm, f.x); f.y = fmap_f(fm, f.y); }
-            w[i] = pack_bf16(f.x * scale, f.y * scale);
-        }
-    } else {
-        float* f = reinterpret_cast<float*>(&v);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            float x = apply_fm ? fmap_f(fm, f[i]) : f[i];
-            f[i] = x * scale;
-        }
-    }
-    *reinterpret_cast<uint4*>(p) = v;
+constexpr int output_pass_smem() {
+    using TT = TileTraits<T>;
+    return TT::OUT_STAGES * 3 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) +
+           TT::MOP_BYTES + 2800;
 }
-
-// Inclusive scan of one float per thread over `n` consecutive threads starting at thread 0
-// of a group of warps; `tmp` holds >= n/32 floats.  Must be called by all threads of the
-// group (count `nthreads`, named barrier `bar_id`).
-__device__ __forceinline__ float group_inclusive_scan(float x, float* tmp, int tid,
-                                                      uint32_t bar_id, uint32_t nthreads) {
-    const int lane = tid & 31, w = tid >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        float y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) tmp[w] = x;
-    named_bar_sync(bar_id, nthreads);
-    float off = 0.f;
-    for (int i = 0; i < w; ++i) off += tmp[i];
-    named_bar_sync(bar_id, nthreads);
-    return x + off;
-}
-
-}  // namespace lmoe_dev
-
-namespace lmoe_dev {
 template <typename T>
+constexpr int state_pass_smem() {
+    using TT = TileTraits<T>;
+    return TT::SP_STAGES * 2 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + 4096;
+}
+constexpr int kStatePassThreads = 256;
+constexpr int kOutputPassThreads = 384;
+
+template <typename T, int DECAY, int FM, bool NORM>
 __global__ void lsm_state_pass(const __grid_constant__ CUtensorMap tmK,
                                const __grid_constant__ CUtensorMap tmV, LsmFwdParams p);
-template <typename T>
+template <typename T, int DECAY, int FM, bool NORM>
 __global__ void lsm_output_pass(const __grid_constant__ CUtensorMap tmQ,
                                 const __grid_constant__ CUtensorMap tmK,
-                                const __grid_constant__ CUtensorMap tmV,
-                                const __grid_constant__ CUtensorMap tmO, LsmFwdParams p);
+                                const __grid_constant__ CUtensorMap tmV, LsmFwdParams p);
 __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __restrict__ zS,
                                 const float* __restrict__ logD, const float* __restrict__ M0,
                                 const float* __restrict__ z0, float* __restrict__ Min,
                                 float* __restrict__ zin, float* __restrict__ Mfin,
-                                float* __restrict__ zfin, int nseg, int dk, int dv, int norm,
-                                int* err);
-constexpr int kStatePassSmem = 3 * 2 * kTileBytes + 2048;
-constexpr int kStatePassThreads = 192;
-constexpr int kOutputPassThreads = 320;
-template <typename T>
-constexpr int output_pass_smem() { return 2 * 3 * kTileBytes + TileTraits<T>::MBUF_BYTES + 1280; }
+                                float* __restrict__ zfin, float* __restrict__ logDtot,
+                                int fin_stride, int nseg, int dk, int dv, int norm, int* err);
+__global__ void sp_rank_combine(const float* __restrict__ gathered, int P, int BH, int rank,
+                                int dk, int dv, int norm, float* __restrict__ M0,
+                                float* __restrict__ z0);
+
 }  // namespace lmoe_dev

@@ -1,12 +1,35 @@
-// lsm_host.cu -- host orchestration of the LSM forward: argument validation with the
-// reference's error texts, segment planning, workspace carving, TMA descriptors, launches.
+// lsm_host.cu -- host orchestration of the LSM forward and of LSM sequence parallelism:
+// argument validation with the reference's error texts, segment planning, workspace
+// carving, TMA descriptors, launches, NCCL all-gather of the per-rank state payload.
+#include <nccl.h>
+
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "common.h"
-#include "lsm_fwd.cu"
+#include "lsm_launch.h"
 
 namespace lmoe_host {
+
+// Optional per-phase timing (LMOE_FLAG_TIMING): CUDA events recorded on the caller's stream
+// around each kernel; lmoe_timing_read() sums elapsed milliseconds per phase.
+struct PhaseTimer {
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::vector<cudaEvent_t>> pending;
+    size_t next = 0;
+    cudaEvent_t get() {
+        if (next == pool.size()) {
+            cudaEvent_t e;
+            LMOE_CUDA_CHECK(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[next++];
+    }
+};
+static PhaseTimer g_timer;
+static long long g_last_gather_elements = 0;
+static unsigned long long* g_trace = nullptr;
 
 static const char* kInstanceNames[] = {"bla",    "lightning", "retnet", "gla",   "deltanet",
                                        "gated_deltanet", "rebased", "gfw", "gateloop", "ttt",
@@ -49,8 +72,7 @@ static LsmPlan plan_lsm(int B, int N, int H, int D) {
         long long ctas = heads * nseg;
         long long w = (ctas + sms - 1) / sms;
         double eff = (double)(heads * chunks) / (double)(w * sms * seg_chunks);
-        // prefer fuller waves, then fewer segments (less combine traffic)
-        double score = eff - 0.002 * waves;
+        double score = eff - 0.002 * waves;  // fuller waves first, then fewer segments
         if (score > best) {
             best = score;
             pl.seg_len = seg_chunks * C;
@@ -98,65 +120,111 @@ static void validate(const lmoe_lsm_desc* d, int B, int N, int H, int D, lmoe_dt
     if (!q || !k || !v || !o) throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd: null tensor");
 }
 
-template <typename T>
-static void launch_lsm(const lmoe_lsm_desc* d, int B, int N, int H, lmoe_dtype dt, const void* q,
-                       const void* k, const void* v, const float* b_pre, const float* a_raw,
-                       const float* M0, const float* z0, void* o, float* M_out, float* z_out,
-                       uint8_t* ws, const LsmPlan& pl, cudaStream_t st) {
-    using TT = lmoe_dev::TileTraits<T>;
-    constexpr int D = TT::D;
-    const CUtensorMapDataType tdt =
-        sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    const CUtensorMap tq = make_tmap_4d(q, tdt, sizeof(T), D, H, N, B, TT::EPB, lmoe_dev::kC);
-    const CUtensorMap tk = make_tmap_4d(k, tdt, sizeof(T), D, H, N, B, TT::EPB, lmoe_dev::kC);
-    const CUtensorMap tv = make_tmap_4d(v, tdt, sizeof(T), D, H, N, B, TT::EPB, lmoe_dev::kC);
-    const CUtensorMap to = make_tmap_4d(o, tdt, sizeof(T), D, H, N, B, TT::EPB, lmoe_dev::kC);
-
+// One LSM evaluation over a [B, N, H, D] view whose sequence stride is Nstride (>= N):
+// the full tensor for lmoe_lsm_fwd, a rank slice for sequence parallelism.
+struct LsmCall {
+    const lmoe_lsm_desc* d;
+    int B, N, Nstride, H, D;
+    lmoe_dtype dt;
+    const void *q, *k, *v;
+    const float *b_pre, *a_raw;
+    void* o;
+    uint8_t* ws;
+    LsmPlan pl;
+    cudaStream_t st;
+    std::vector<cudaEvent_t> ev;
     lmoe_dev::LsmFwdParams p{};
-    p.B = B; p.N = N; p.H = H;
-    p.seg_len = pl.seg_len;
-    p.nseg = pl.nseg;
-    p.decay = device_decay_mode(d->instance);
-    p.fm = d->feature_map;
-    p.norm = d->use_normalizer;
-    p.mamba2_keff = d->instance == LMOE_MAMBA2;
-    p.log_a = p.decay == lmoe_dev::kDecayConst ? logf(d->scalar_decay) : 0.f;
-    p.b_pre = b_pre;
-    p.a_raw = a_raw;
-    p.Sseg = reinterpret_cast<float*>(ws + pl.off_S);
-    p.zseg = reinterpret_cast<float*>(ws + pl.off_z);
-    p.logDseg = reinterpret_cast<float*>(ws + pl.off_logD);
-    p.Min = reinterpret_cast<const float*>(ws + pl.off_Min);
-    p.zin = reinterpret_cast<const float*>(ws + pl.off_zin);
-    p.err = reinterpret_cast<int*>(ws + pl.off_err);
-    if (p.decay == lmoe_dev::kDecayTokenScalar && (!b_pre || !a_raw))
-        throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd: Mamba2 needs b_pre and a_raw");
+    lmoe_dev::LsmVariant var{};
+    bool norm = false;
 
-    static bool attr_done[2] = {false, false};
-    const int ai = sizeof(T) == 2 ? 0 : 1;
-    if (!attr_done[ai]) {
-        LMOE_CUDA_CHECK(cudaFuncSetAttribute(lmoe_dev::lsm_state_pass<T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             lmoe_dev::kStatePassSmem));
-        LMOE_CUDA_CHECK(cudaFuncSetAttribute(lmoe_dev::lsm_output_pass<T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             lmoe_dev::output_pass_smem<T>()));
-        attr_done[ai] = true;
+    void mark() {
+        if (!(d->flags & LMOE_FLAG_TIMING)) return;
+        ev.push_back(g_timer.get());
+        LMOE_CUDA_CHECK(cudaEventRecord(ev.back(), st));
     }
-    LMOE_CUDA_CHECK(cudaMemsetAsync(p.err, 0, 64, st));
-    const dim3 grid(pl.nseg, H, B);
-    lmoe_dev::lsm_state_pass<T><<<grid, lmoe_dev::kStatePassThreads, lmoe_dev::kStatePassSmem, st>>>(tk, tv, p);
-    LMOE_CUDA_CHECK(cudaGetLastError());
-    const int nel = D * D + (p.norm ? D : 0);
-    lmoe_dev::lsm_seg_combine<<<dim3((nel + 255) / 256, B * H), 256, 0, st>>>(
-        p.Sseg, p.zseg, p.logDseg, M0, z0, const_cast<float*>(p.Min), const_cast<float*>(p.zin),
-        M_out, z_out, pl.nseg, D, D, p.norm, p.err);
-    LMOE_CUDA_CHECK(cudaGetLastError());
-    lmoe_dev::lsm_output_pass<T><<<grid, lmoe_dev::kOutputPassThreads, lmoe_dev::output_pass_smem<T>(), st>>>(
-        tq, tk, tv, to, p);
-    LMOE_CUDA_CHECK(cudaGetLastError());
-    g_launch_count += 3;
-    if (d->flags & LMOE_FLAG_CHECK) {
+    void finish_timing() {
+        if (!ev.empty()) g_timer.pending.push_back(ev);
+        ev.clear();
+    }
+
+    void setup() {
+        p.B = B; p.N = N; p.H = H; p.Nstride = Nstride;
+        p.seg_len = pl.seg_len;
+        p.nseg = pl.nseg;
+        var.decay = device_decay_mode(d->instance);
+        var.fm = d->feature_map;
+        var.norm = d->use_normalizer ? 1 : 0;
+        norm = var.norm != 0;
+        p.log_a = var.decay == lmoe_dev::kDecayConst ? logf(d->scalar_decay) : 0.f;
+        p.b_pre = b_pre;
+        p.a_raw = a_raw;
+        p.Sseg = reinterpret_cast<float*>(ws + pl.off_S);
+        p.zseg = reinterpret_cast<float*>(ws + pl.off_z);
+        p.logDseg = reinterpret_cast<float*>(ws + pl.off_logD);
+        p.Min = reinterpret_cast<const float*>(ws + pl.off_Min);
+        p.zin = reinterpret_cast<const float*>(ws + pl.off_zin);
+        p.o = o;
+        p.err = reinterpret_cast<int*>(ws + pl.off_err);
+        // developer knobs: phase-3 schedule and a clock64 trace of CTA (0,0,0)
+        static const int order = getenv("LMOE_OP_ORDER") ? atoi(getenv("LMOE_OP_ORDER")) : 0;
+        p.order = order;
+        p.trace = nullptr;
+        if (getenv("LMOE_TRACE")) {
+            if (!g_trace) {
+                LMOE_CUDA_CHECK(cudaMalloc(&g_trace, 64 * 16 * 8));
+                LMOE_CUDA_CHECK(cudaMemset(g_trace, 0, 64 * 16 * 8));
+            }
+            p.trace = g_trace;
+        }
+        if (var.decay == lmoe_dev::kDecayTokenScalar && (!b_pre || !a_raw))
+            throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd: Mamba2 needs b_pre and a_raw");
+    }
+
+    template <typename T>
+    CUtensorMap tmap(const void* base) const {
+        using TT = lmoe_dev::TileTraits<T>;
+        const CUtensorMapDataType tdt =
+            sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        return make_tmap_4d(base, tdt, sizeof(T), TT::D, H, N, B, TT::EPB, lmoe_dev::kC, Nstride);
+    }
+
+    template <typename T>
+    void state_pass() {
+        const CUtensorMap tk = tmap<T>(k), tv = tmap<T>(v);
+        mark();
+        if constexpr (sizeof(T) == 2)
+            LMOE_CUDA_CHECK(lmoe_dev::launch_state_pass_bf16(var, dim3(pl.nseg, H, B), st, tk, tv, p));
+        else
+            LMOE_CUDA_CHECK(lmoe_dev::launch_state_pass_f32(var, dim3(pl.nseg, H, B), st, tk, tv, p));
+        ++g_launch_count;
+    }
+    // Segment prefix with carried-in state (M0, z0); writes per-segment M_in and the
+    // inclusive total (Mfin/zfin with row stride fin_stride, and its total log decay).
+    void combine(const float* M0, const float* z0, bool write_min, float* Mfin, float* zfin,
+                 float* logDtot, int fin_stride) {
+        mark();
+        const int nel = D * D + (norm ? D : 0);
+        LMOE_CUDA_CHECK(lmoe_dev::launch_seg_combine(
+            dim3((nel + 255) / 256, B * H), st, p.Sseg, p.zseg, p.logDseg, M0, z0,
+            write_min ? const_cast<float*>(p.Min) : nullptr,
+            write_min ? const_cast<float*>(p.zin) : nullptr, Mfin, zfin, logDtot, fin_stride,
+            pl.nseg, D, D, norm ? 1 : 0, p.err));
+        ++g_launch_count;
+    }
+    template <typename T>
+    void output_pass() {
+        const CUtensorMap tq = tmap<T>(q), tk = tmap<T>(k), tv = tmap<T>(v), to = tmap<T>(o);
+        mark();
+        if constexpr (sizeof(T) == 2)
+            LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_bf16(var, dim3(pl.nseg, H, B), st, tq, tk, tv, to, p));
+        else
+            LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_f32(var, dim3(pl.nseg, H, B), st, tq, tk, tv, to, p));
+        ++g_launch_count;
+        mark();
+    }
+    void clear_err() { LMOE_CUDA_CHECK(cudaMemsetAsync(p.err, 0, 64, st)); }
+    void check_err() {
+        if (!(d->flags & LMOE_FLAG_CHECK)) return;
         int err[2] = {0, 0};
         LMOE_CUDA_CHECK(cudaMemcpyAsync(err, p.err, sizeof(err), cudaMemcpyDeviceToHost, st));
         LMOE_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -167,8 +235,73 @@ static void launch_lsm(const lmoe_lsm_desc* d, int B, int N, int H, lmoe_dtype d
             throw Error(LMOE_ERR_NONFINITE,
                         std::string("non-finite memory state in instance ") + instance_name(d->instance));
     }
-    (void)dt;
+};
+
+template <typename T>
+static void run_local(LsmCall& c, const float* M0, const float* z0, float* M_out, float* z_out) {
+    c.setup();
+    c.clear_err();
+    c.state_pass<T>();
+    c.combine(M0, z0, true, M_out, z_out, nullptr, 0);
+    c.output_pass<T>();
+    c.finish_timing();
+    c.check_err();
 }
+
+static size_t payload_floats(const lmoe_lsm_desc* d, int D) {
+    return (size_t)D * D + (d->use_normalizer ? D : 0) + 1;
+}
+
+struct SpWorkspace {
+    LsmPlan pl;
+    size_t off_payload = 0, off_gathered = 0, off_M0 = 0, off_z0 = 0, total = 0;
+};
+
+static SpWorkspace plan_sp(const lmoe_lsm_desc* d, int B, int N_local, int H, int D, int world) {
+    SpWorkspace w;
+    w.pl = plan_lsm(B, N_local, H, D);
+    const size_t BH = (size_t)B * H, P = payload_floats(d, D);
+    size_t off = align_up(w.pl.total, 256);
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    w.off_payload = take(BH * P * 4);
+    w.off_gathered = take((size_t)world * BH * P * 4);
+    w.off_M0 = take(BH * D * D * 4);
+    w.off_z0 = take(BH * D * 4);
+    w.total = off;
+    return w;
+}
+
+// Phase A of sp_lsm_masked_rank (parallel.hpp:313-327): local state from zero and the
+// payload [M | z? | log D] per (b,h), written to `payload`.
+template <typename T>
+static void sp_phase_a(LsmCall& c, float* payload) {
+    const int P = (int)payload_floats(c.d, c.D);
+    c.state_pass<T>();
+    c.combine(nullptr, nullptr, false, payload, c.norm ? payload + c.D * c.D : nullptr,
+              payload + P - 1, P);
+}
+// Phase B (parallel.hpp:340-373): decayed exclusive prefix over ranks < rank, then the
+// output pass with the carried-in state.
+template <typename T>
+static void sp_phase_b(LsmCall& c, const float* gathered, int rank, float* M0, float* z0,
+                       float* M_out, float* z_out) {
+    const int P = (int)payload_floats(c.d, c.D);
+    const int nel = c.D * c.D + (c.norm ? c.D : 0);
+    c.mark();
+    LMOE_CUDA_CHECK(lmoe_dev::launch_rank_combine(dim3((nel + 255) / 256, c.B * c.H), c.st,
+                                                  gathered, P, c.B * c.H, rank, c.D, c.D,
+                                                  c.norm ? 1 : 0, M0, z0));
+    ++g_launch_count;
+    c.combine(M0, c.norm ? z0 : nullptr, true, M_out, z_out, nullptr, 0);
+    c.output_pass<T>();
+}
+
+#define NCCL_CHECK(x)                                                                      \
+    do {                                                                                   \
+        ncclResult_t r_ = (x);                                                             \
+        if (r_ != ncclSuccess)                                                             \
+            throw Error(LMOE_ERR_NCCL, std::string("NCCL error: ") + ncclGetErrorString(r_)); \
+    } while (0)
 
 }  // namespace lmoe_host
 
@@ -186,6 +319,26 @@ extern "C" int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc) {
     return 3;
 }
 
+// Sums per-phase device milliseconds over all LMOE_FLAG_TIMING calls since the last read.
+extern "C" int lmoe_timing_read(float* ms_out, int nphase) {
+    int calls = 0;
+    int rc = guarded([&]() {
+        for (int i = 0; i < nphase; ++i) ms_out[i] = 0.f;
+        for (auto& ev : g_timer.pending) {
+            LMOE_CUDA_CHECK(cudaEventSynchronize(ev.back()));
+            for (size_t i = 0; i + 1 < ev.size() && (int)i < nphase; ++i) {
+                float ms = 0.f;
+                LMOE_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+                ms_out[i] += ms;
+            }
+            ++calls;
+        }
+        g_timer.pending.clear();
+        g_timer.next = 0;
+    });
+    return rc == LMOE_OK ? calls : -rc;
+}
+
 extern "C" int lmoe_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
                             lmoe_dtype dtype, const void* q, const void* k, const void* v,
                             const void* a_pre, const float* b_pre, const float* a_raw,
@@ -195,16 +348,166 @@ extern "C" int lmoe_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
     return guarded([&]() {
         validate(desc, B, N, H, D, dtype, q, k, v, o);
         (void)a_pre;
-        const LsmPlan pl = plan_lsm(B, N, H, D);
-        if (!workspace || workspace_bytes < pl.total)
+        LsmCall c{desc, B, N, N, H, D, dtype, q, k, v, b_pre, a_raw, o,
+                  static_cast<uint8_t*>(workspace), plan_lsm(B, N, H, D),
+                  reinterpret_cast<cudaStream_t>(stream)};
+        if (!workspace || workspace_bytes < c.pl.total)
             throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd: workspace too small (need " +
-                                          std::to_string(pl.total) + " bytes)");
+                                          std::to_string(c.pl.total) + " bytes)");
+        if (dtype == LMOE_BF16) run_local<__nv_bfloat16>(c, M0, z0, M_out, z_out);
+        else run_local<float>(c, M0, z0, M_out, z_out);
+    });
+}
+
+// ------------------------------------------------------------------ sequence parallelism
+extern "C" size_t lmoe_sp_payload_floats(const lmoe_lsm_desc* desc, int B, int H, int D) {
+    return (size_t)B * H * payload_floats(desc, D);
+}
+
+extern "C" size_t lmoe_sp_lsm_fwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local,
+                                                 int H, int D, lmoe_dtype dtype, int world) {
+    (void)dtype;
+    if (!desc || B < 1 || N_local < 1 || H < 1 || D < 1 || world < 1) return 0;
+    return plan_sp(desc, B, N_local, H, D, world).total;
+}
+
+extern "C" long long lmoe_sp_last_gather_elements(void) { return g_last_gather_elements; }
+
+extern "C" int lmoe_nccl_unique_id(void* id128) {
+    return guarded([&]() {
+        ncclUniqueId id;
+        NCCL_CHECK(ncclGetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "ncclUniqueId size");
+        memcpy(id128, &id, sizeof(id));
+    });
+}
+
+extern "C" int lmoe_nccl_comm_init(void** comm, int world, int rank, const void* id128) {
+    return guarded([&]() {
+        ncclUniqueId id;
+        memcpy(&id, id128, sizeof(id));
+        ncclComm_t c;
+        NCCL_CHECK(ncclCommInitRank(&c, world, id, rank));
+        *comm = c;
+    });
+}
+
+extern "C" int lmoe_nccl_comm_destroy(void* comm) {
+    return guarded([&]() { NCCL_CHECK(ncclCommDestroy(static_cast<ncclComm_t>(comm))); });
+}
+
+// sp_lsm_masked_rank (parallel.hpp:303-376) for this rank's contiguous slice
+// (chunk_range, parallel.hpp:192-197): local pass, ONE ncclAllGather of the all-heads
+// payload, decayed prefix over earlier ranks, output pass.
+extern "C" int lmoe_sp_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
+                               lmoe_dtype dtype, const void* q, const void* k, const void* v,
+                               const void* a_pre, const float* b_pre, const float* a_raw,
+                               void* o, float* M_out, float* z_out, void* nccl_comm, int rank,
+                               int world, void* workspace, size_t workspace_bytes,
+                               lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, B, N_local, H, D, dtype, q, k, v, o);
+        (void)a_pre;
+        if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: bad rank");
+        if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: null communicator");
+        const SpWorkspace w = plan_sp(desc, B, N_local, H, D, world);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: workspace too small (need " +
+                                          std::to_string(w.total) + " bytes)");
+        uint8_t* ws = static_cast<uint8_t*>(workspace);
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-        if (dtype == LMOE_BF16)
-            launch_lsm<__nv_bfloat16>(desc, B, N, H, dtype, q, k, v, b_pre, a_raw, M0, z0, o,
-                                      M_out, z_out, static_cast<uint8_t*>(workspace), pl, st);
-        else
-            launch_lsm<float>(desc, B, N, H, dtype, q, k, v, b_pre, a_raw, M0, z0, o, M_out,
-                              z_out, static_cast<uint8_t*>(workspace), pl, st);
+        LsmCall c{desc, B, N_local, N_local, H, D, dtype, q, k, v, b_pre, a_raw, o, ws, w.pl, st};
+        c.setup();
+        c.clear_err();
+        float* payload = reinterpret_cast<float*>(ws + w.off_payload);
+        float* gathered = reinterpret_cast<float*>(ws + w.off_gathered);
+        float* M0 = reinterpret_cast<float*>(ws + w.off_M0);
+        float* z0 = reinterpret_cast<float*>(ws + w.off_z0);
+        const size_t P = (size_t)B * H * payload_floats(desc, D);
+        if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, payload);
+        else sp_phase_a<float>(c, payload);
+        c.mark();
+        if (world > 1) {
+            NCCL_CHECK(ncclAllGather(payload, gathered, P, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
+        } else {
+            LMOE_CUDA_CHECK(cudaMemcpyAsync(gathered, payload, P * 4, cudaMemcpyDeviceToDevice, st));
+        }
+        g_last_gather_elements = (long long)world * (long long)P;
+        if (dtype == LMOE_BF16) sp_phase_b<__nv_bfloat16>(c, gathered, rank, M0, z0, M_out, z_out);
+        else sp_phase_b<float>(c, gathered, rank, M0, z0, M_out, z_out);
+        c.finish_timing();
+        c.check_err();
+    });
+}
+
+// The same algorithm with `world` virtual ranks on this device over the full [B,N,H,D]
+// sequence: the all-gather is a device copy of each rank's payload into its slot.
+extern "C" size_t lmoe_sp_lsm_fwd_loopback_workspace_size(const lmoe_lsm_desc* desc, int B, int N,
+                                                          int H, int D, lmoe_dtype dtype, int world) {
+    (void)dtype;
+    if (!desc || world < 1 || N < world) return 0;
+    return plan_sp(desc, B, (N + world - 1) / world, H, D, world).total;
+}
+
+extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                                        lmoe_dtype dtype, const void* q, const void* k,
+                                        const void* v, const void* a_pre, const float* b_pre,
+                                        const float* a_raw, void* o, float* M_out, float* z_out,
+                                        int world, void* workspace, size_t workspace_bytes,
+                                        lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, B, N, H, D, dtype, q, k, v, o);
+        (void)a_pre;
+        if (world < 1 || N < world) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");
+        const SpWorkspace w = plan_sp(desc, B, (N + world - 1) / world, H, D, world);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd_loopback: workspace too small");
+        uint8_t* ws = static_cast<uint8_t*>(workspace);
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const size_t esz = dtype == LMOE_BF16 ? 2 : 4;
+        const size_t P = (size_t)B * H * payload_floats(desc, D);
+        float* gathered = reinterpret_cast<float*>(ws + w.off_gathered);
+        float* M0 = reinterpret_cast<float*>(ws + w.off_M0);
+        float* z0 = reinterpret_cast<float*>(ws + w.off_z0);
+        auto slice_call = [&](int r) {
+            const int base = N / world, rem = N % world;  // chunk_range (parallel.hpp:192-197)
+            const int r0 = r * base + std::min(r, rem);
+            const int len = base + (r < rem ? 1 : 0);
+            const size_t off = (size_t)r0 * H * D * esz;
+            LsmCall c{desc, B, len, N, H, D, dtype,
+                      static_cast<const uint8_t*>(q) + off, static_cast<const uint8_t*>(k) + off,
+                      static_cast<const uint8_t*>(v) + off, b_pre ? b_pre + (size_t)r0 * H : nullptr,
+                      a_raw, static_cast<uint8_t*>(o) + off, ws, plan_lsm(B, len, H, D), st};
+            c.setup();
+            return c;
+        };
+        slice_call(0).clear_err();
+        for (int r = 0; r < world; ++r) {
+            LsmCall c = slice_call(r);
+            if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, gathered + r * P);
+            else sp_phase_a<float>(c, gathered + r * P);
+        }
+        g_last_gather_elements = (long long)world * (long long)P;
+        for (int r = 0; r < world; ++r) {
+            LsmCall c = slice_call(r);
+            const bool last = r == world - 1;
+            if (dtype == LMOE_BF16) {
+                c.state_pass<__nv_bfloat16>();
+                sp_phase_b<__nv_bfloat16>(c, gathered, r, M0, z0, last ? M_out : nullptr, last ? z_out : nullptr);
+            } else {
+                c.state_pass<float>();
+                sp_phase_b<float>(c, gathered, r, M0, z0, last ? M_out : nullptr, last ? z_out : nullptr);
+            }
+            if (last) c.check_err();
+        }
+    });
+}
+
+// Developer aid: copies the clock64 phase trace of the last LMOE_TRACE run (64 x 16 u64).
+extern "C" int lmoe_debug_trace_read(unsigned long long* out) {
+    return guarded([&]() {
+        if (!g_trace) throw Error(LMOE_ERR_ARG, "no trace (set LMOE_TRACE)");
+        LMOE_CUDA_CHECK(cudaDeviceSynchronize());
+        LMOE_CUDA_CHECK(cudaMemcpy(out, g_trace, 64 * 16 * 8, cudaMemcpyDeviceToHost));
     });
 }

@@ -1,0 +1,37 @@
+// lsm_launch.h -- host-callable launchers of the LSM forward kernels (one per dtype and
+// phase), dispatching the compile-time (decay, feature map, normaliser) variant.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "lsm_fwd.cuh"
+
+namespace lmoe_dev {
+
+struct LsmVariant {
+    int decay;  // DecayMode
+    int fm;     // 0 identity, 1 elu+1, 2 squared
+    int norm;   // normaliser
+};
+
+cudaError_t launch_state_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
+                                   const CUtensorMap& val, const LsmFwdParams& p);
+cudaError_t launch_output_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
+                                    const CUtensorMap& k, const CUtensorMap& val,
+                                    const CUtensorMap& o, const LsmFwdParams& p);
+cudaError_t launch_state_pass_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
+                                  const CUtensorMap& val, const LsmFwdParams& p);
+cudaError_t launch_output_pass_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
+                                   const CUtensorMap& k, const CUtensorMap& val,
+                                   const CUtensorMap& o, const LsmFwdParams& p);
+
+}  // namespace lmoe_dev
+
+namespace lmoe_dev {
+cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const float* zS,
+                               const float* logD, const float* M0, const float* z0, float* Min,
+                               float* zin, float* Mfin, float* zfin, float* logDtot, int fin_stride,
+                               int nseg, int dk, int dv, int norm, int* err);
+cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,
+                                int rank, int dk, int dv, int norm, float* M0, float* z0);
+}  // namespace lmoe_dev

@@ -89,19 +89,19 @@ def _workspace(nbytes, device):
     return ws
 
 
-def make_desc(spec, chunk_size, check=True):
+def make_desc(spec, chunk_size, check=True, timing=False):
     d = _lib.LsmDesc()
     d.instance = int(spec.instance)
     d.feature_map = int(spec.feature_map)
     d.use_normalizer = int(bool(spec.use_normalizer))
     d.scalar_decay = float(spec.scalar_decay)
     d.chunk_size = int(chunk_size)
-    d.flags = 1 if check else 0
+    d.flags = (1 if check else 0) | (2 if timing else 0)
     return d
 
 
 def lsm_forward_batched(q, k, v, gates, spec, chunk_size=64, initial_state=None,
-                        final_state=None, out=None, check=True, stream=None):
+                        final_state=None, out=None, check=True, stream=None, timing=False):
     """[B,N,H,D] forward for all heads.  final_state (MemoryState) receives [B,H,D,D] / [B,H,D]."""
     B, N, H, D = q.shape
     for t in (k, v):
@@ -133,7 +133,7 @@ def lsm_forward_batched(q, k, v, gates, spec, chunk_size=64, initial_state=None,
     if final_state is not None:
         M_out = torch.empty(B, H, D, D, dtype=torch.float32, device=q.device)
         z_out = torch.empty(B, H, D, dtype=torch.float32, device=q.device) if spec.use_normalizer else None
-    desc = make_desc(spec, chunk_size, check)
+    desc = make_desc(spec, chunk_size, check, timing)
     L = _lib.lib()
     dt = _DTYPES[q.dtype]
     nbytes = L.lmoe_lsm_fwd_workspace_size(ctypes.byref(desc), B, N, H, D, dt)

@@ -146,6 +146,7 @@ def test_errors_mirror_reference_text():
     import paper_2503_05447_b200 as pk
     q = torch.zeros(1, 8, 1, 128, dtype=torch.bfloat16, device="cuda")
     spec = pk.LsmSpec.make("mamba2", 128)
+    spec.mamba2_a_raw = 0.5
     spec.use_normalizer = True
     with pytest.raises(pk.LmoeError, match="LsmSpec: normalizer unsupported for instance mamba2"):
         pk.lsm_forward_batched(q, q, q, None, spec, 64)

@@ -35,7 +35,7 @@ def run(inst, fm, norm, dtype, N, H=1, seed=0):
     return res
 
 cases = [("bla",0,0,"bf16",128),("bla",0,0,"bf16",300),("bla",0,0,"f32",256),("lightning",0,0,"bf16",1000),
-         ("mamba2",0,0,"bf16",1000),("bla",1,1,"f32",2048),("retnet",0,0,"f32",515),("rebased",2,1,"bf16",700)]
+         ("mamba2",0,0,"bf16",1000),("bla",1,1,"f32",2048),("retnet",0,0,"f32",515),("rebased",2,1,"bf16",700),("bla",1,1,"bf16",1000),("bla",1,1,"f32",256),("bla",1,1,"f32",200)]
 for c in cases:
     try:
         t=time.time(); r = run(*c)

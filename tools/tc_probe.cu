@@ -127,7 +127,99 @@ static void run(int K, int N, int a_major, int b_major) {
     cudaFree(da); cudaFree(db); cudaFree(dout);
 }
 
+
+template <bool kTF32>
+__global__ void probe_ts(const float* A, const uint8_t* b_img, int b_bytes, int K, int N, float* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tm;
+    for (int i = threadIdx.x * 16; i < b_bytes; i += blockDim.x * 16) *(uint4*)(smem + i) = *(const uint4*)(b_img + i);
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (warp_id() == 0) tmem_alloc<512>(&tm);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    // A -> TMEM columns [256, ...): row = lane of quarter
+    const int row = warp_id() * 32 + lane_id();
+    const uint32_t ta = tm + 256 + ((uint32_t)(warp_id() * 32) << 16);
+    if (kTF32) {
+        for (int c0 = 0; c0 < K; c0 += 32) {
+            uint32_t r[32];
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(A[row * K + c0 + j]);
+            tmem_st32(ta + c0, r);
+        }
+    } else {
+        for (int c0 = 0; c0 < K; c0 += 64) {
+            uint32_t r[32];
+            for (int j = 0; j < 32; ++j) r[j] = pack_bf16(A[row * K + c0 + 2 * j], A[row * K + c0 + 2 * j + 1]);
+            tmem_st32(ta + c0 / 2, r);
+        }
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (threadIdx.x == 0) {
+        uint32_t idesc = umma_idesc(kTF32 ? 2 : 1, 0, 0, 128, N);
+        const int kstep = kTF32 ? 8 : 16;
+        for (int kk = 0; kk < K / kstep; ++kk) {
+            uint32_t boff = (kk * 32 / 128) * (N * 128) + (kk * 32 % 128);
+            uint64_t bd = umma_desc_sw128(smem_u32(smem) + boff, 16, 1024);
+            if (kTF32) mma_ts_tf32(tm, tm + 256 + kk * 8, bd, idesc, kk > 0);
+            else mma_ts_f16(tm, tm + 256 + kk * 8, bd, idesc, kk > 0);
+        }
+        mma_commit(&bar);
+    }
+    mbar_wait(&bar, 0);
+    tc_fence_after();
+    for (int c = 0; c < N; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tm + ((uint32_t)(warp_id() * 32) << 16) + c, r);
+        tmem_wait_ld();
+        for (int j = 0; j < 32; ++j) out[row * N + c + j] = __uint_as_float(r[j]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp_id() == 0) tmem_dealloc<512>(tm);
+}
+
+template <bool kTF32>
+static void run_ts(int K, int N) {
+    const int M = 128, esz = kTF32 ? 4 : 2;
+    std::vector<float> A(M * K), B(K * N);
+    srand(2);
+    for (auto& x : A) x = (rand() % 17 - 8) / 8.0f;
+    for (auto& x : B) x = (rand() % 17 - 8) / 8.0f;
+    std::vector<uint8_t> bi(N * K * esz, 0);
+    for (int n = 0; n < N; ++n) for (int k = 0; k < K; ++k) put(bi, N, esz, n, k, B[k * N + n]);
+    float *dA, *dout; uint8_t* db;
+    cudaMalloc(&dA, M * K * 4); cudaMalloc(&db, bi.size()); cudaMalloc(&dout, M * N * 4);
+    cudaMemcpy(dA, A.data(), M * K * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(db, bi.data(), bi.size(), cudaMemcpyHostToDevice);
+    int smem = (int)bi.size() + 1024;
+    cudaFuncSetAttribute(probe_ts<kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    probe_ts<kTF32><<<1, 128, smem>>>(dA, db, (int)bi.size(), K, N, dout);
+    cudaError_t e = cudaDeviceSynchronize();
+    std::vector<float> out(M * N);
+    cudaMemcpy(out.data(), dout, M * N * 4, cudaMemcpyDeviceToHost);
+    double maxerr = 0, maxref = 0;
+    for (int m = 0; m < M; ++m) for (int n = 0; n < N; ++n) {
+        double ref = 0;
+        for (int k = 0; k < K; ++k) ref += (double)A[m * K + k] * B[k * N + n];
+        maxerr = std::max(maxerr, std::fabs(ref - out[m * N + n]));
+        maxref = std::max(maxref, std::fabs(ref));
+    }
+    printf("TS %s K=%3d N=%3d : err=%s maxerr=%.3e maxref=%.3e\n", kTF32 ? "tf32" : "bf16", K, N,
+           cudaGetErrorString(e), maxerr, maxref);
+}
+
 int main() {
+    run_ts<false>(128, 128);
+    run_ts<true>(128, 64);
+    run_ts<true>(64, 64);
+    return 0;
+
     for (int am = 0; am < 2; ++am) for (int bm = 0; bm < 2; ++bm) {
         run<false>(128, 128, am, bm);
         run<true>(64, 64, am, bm);
