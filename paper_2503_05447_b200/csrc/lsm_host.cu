@@ -166,7 +166,7 @@ struct LsmCall {
         p.o = o;
         p.err = reinterpret_cast<int*>(ws + pl.off_err);
         // developer knobs: phase-3 schedule and a clock64 trace of CTA (0,0,0)
-        static const int order = getenv("LMOE_OP_ORDER") ? atoi(getenv("LMOE_OP_ORDER")) : 0;
+        static const int order = getenv("LMOE_OP_ORDER") ? atoi(getenv("LMOE_OP_ORDER")) : 1;
         p.order = order;
         p.trace = nullptr;
         if (getenv("LMOE_TRACE")) {

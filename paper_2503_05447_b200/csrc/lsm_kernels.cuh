@@ -514,14 +514,22 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             if (c >= 2) mbar_wait(&gfree[slot], ((c >> 1) - 1) & 1);
             float G[4], kf[4];
             const float gend = chunk_scan<DECAY>(p, bvA, nval(c), spa, lane, G, kf);
-            const bool safe = gend > kSafeLogDecay;
+            // split e^{G_i - G_j} = e^{G_i - r} e^{r - G_j} around the chunk midpoint r = G_63:
+            // both factors stay finite while each half-chunk's decay span is < 80
+            const float r = __shfl_sync(0xFFFFFFFFu, G[3], 15);
+            const float g0 = __shfl_sync(0xFFFFFFFFu, G[0], 0);
+            const bool safe = (g0 - r) < -kSafeLogDecay && (r - gend) < -kSafeLogDecay;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 ringG[slot * 128 + lane * 4 + u] = G[u];
                 ringF[slot * 128 + lane * 4 + u] =
-                    (DECAY != kDecayNone && safe) ? __expf(-G[u]) * kf[u] : kf[u];
+                    (DECAY != kDecayNone && safe) ? __expf(r - G[u]) * kf[u] : kf[u];
             }
-            if (lane == 0) { ringS[slot * 4] = gend; ringS[slot * 4 + 1] = safe ? 1.f : 0.f; }
+            if (lane == 0) {
+                ringS[slot * 4] = gend;
+                ringS[slot * 4 + 1] = safe ? 1.f : 0.f;
+                ringS[slot * 4 + 2] = r;
+            }
             __syncwarp();
             mbar_arrive(&gfull[slot]);
 #pragma unroll
@@ -616,6 +624,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             mbar_wait(&gfull[slot], (c >> 1) & 1);
             const float gend = ringS[slot * 4];
             const bool safe = ringS[slot * 4 + 1] != 0.f;
+            const float gref = ringS[slot * 4 + 2];  // factorisation reference r
             const float gi = ringG[slot * 128 + row];
             const float* Fs = ringF + slot * 128;
             const float* Gs = ringG + slot * 128;
@@ -637,7 +646,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 const float fq = (DECAY != kDecayNone) ? __expf(gi) : 1.f;
                 float fk = 1.f;
                 if constexpr (DECAY != kDecayNone)
-                    fk = safe ? __expf(gend) * Fs[row] : __expf(gend - gi) * Fs[row];
+                    fk = safe ? __expf(gend - gref) * Fs[row] : __expf(gend - gi) * Fs[row];
                 uint8_t* qb = qt + hh * kBlockBytes;
                 if constexpr (DECAY != kDecayNone || NORM) {
 #pragma unroll
@@ -708,7 +717,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 tmem_ld32(tS, r0);
                 tmem_ld32(tS + 32, r1);
                 tmem_wait_ld();
-                const float eq = (DECAY != kDecayNone && safe) ? __expf(gi) : 1.f;
+                const float eq = (DECAY != kDecayNone && safe) ? __expf(gi - gref) : 1.f;
                 float rs = 0.f;
 #pragma unroll
                 for (int j = 0; j < 64; ++j) {
