@@ -48,6 +48,22 @@ CUtensorMap make_tmap_4d(const void* base, CUtensorMapDataType dt, int esize, ui
     return m;
 }
 
+CUtensorMap make_tmap_3d(const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
+                         uint64_t d1, uint64_t d2, uint32_t box0, uint32_t box1) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {d0 * esize, d0 * d1 * esize};
+    cuuint32_t box[3] = {box0, box1, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, dt, 3, const_cast<void*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw Error(LMOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
 CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dt, int esize, uint64_t cols,
                          uint64_t rows, uint64_t row_stride_elems, uint32_t box_cols,
                          uint32_t box_rows) {

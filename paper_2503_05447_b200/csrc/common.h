@@ -34,6 +34,9 @@ void set_last_error(const std::string& msg);
 CUtensorMap make_tmap_4d(const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
                          uint64_t d1, uint64_t d2, uint64_t d3, uint32_t box0, uint32_t box2,
                          uint64_t d2_stride = 0 /* elements of dim 2 per dim-3 step; 0 = d2 */);
+// 3-D row-major tensor [d2][d1][d0], SWIZZLE_128B, box {box0, box1, 1}.
+CUtensorMap make_tmap_3d(const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
+                         uint64_t d1, uint64_t d2, uint32_t box0, uint32_t box1);
 // 2-D row-major tensor [rows][cols], SWIZZLE_128B, box {box_cols, box_rows}.
 CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dt, int esize, uint64_t cols,
                          uint64_t rows, uint64_t row_stride_elems, uint32_t box_cols,

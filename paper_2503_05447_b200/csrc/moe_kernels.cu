@@ -1,0 +1,397 @@
+// moe_kernels.cu -- Linear-MoE expert layer on sm_100a.
+//
+// Restates MoeLayer::forward (/root/reference/proj/include/lmoe/moe.hpp:133-149):
+//   route (moe.hpp:58-85)           warp-per-token top-k on fp32 logits, ties to the lower id,
+//                                   ids ascending, renormalised gates, full softmax, counts
+//   dispatch (moe.hpp:137-143)      stable counting sort by expert (token-ascending per
+//                                   expert) -> permuted rows x_perm
+//   Expert::forward (moe.hpp:45-47) grouped tcgen05 GEMMs: H = silu(X Wg) * (X Wu) fused in
+//                                   one kernel (two TMEM accumulators), then Y = H Wd
+//   combine (moe.hpp:144-146)       y[t] = sum over the token's experts, in ascending expert
+//                                   order, of gate * Y[perm row]
+//   load_balance_loss (:90-103)     E * sum_e f_e P_e
+#include "moe_kernels.cuh"
+
+namespace lmoe_dev {
+
+// ====================================================================================
+// Grouped GEMM  C[rows of group g] = A[rows] (K-major, bf16) x B_g (MN-major [K][N], bf16)
+// warps: 0 TMA producer, 1 MMA issuer, 2..5 epilogue (one thread per output row)
+// ====================================================================================
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    moe_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+             const __grid_constant__ CUtensorMap tmB1, GemmParams p) {
+    constexpr int NB = (EPI == kEpiSwiGLU) ? 2 : 1;         // B operands per stage
+    constexpr int A_BYTES = 128 * 128;                       // 128 rows x 64 K (bf16)
+    constexpr int B_BYTES = 64 * 2 * BN;                     // 64 K rows x BN cols (bf16)
+    constexpr int STAGE = A_BYTES + NB * B_BYTES;
+    constexpr int NST = gemm_stages<BN, EPI>();
+    constexpr uint32_t TCOLS = (NB * BN <= 128) ? 128 : (NB * BN <= 256 ? 256 : 512);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if (smem_u32(smem) & 1023) __trap();
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+    uint64_t* full = bars;             // [NST]
+    uint64_t* empty = bars + NST;      // [NST]
+    uint64_t* acc_full = bars + 2 * NST;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const int tile = blockIdx.x;
+    if (tile >= *p.num_tiles) return;
+    const int g = p.tile_group[tile];
+    const int row0 = p.tile_row0[tile];
+    const int rows_left = p.group_end[g] - row0;  // valid rows of this tile (<= 128)
+    const int n0 = blockIdx.y * BN;
+    const int kblocks = p.K / 64;
+    const int warp = warp_id(), lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        mbar_init(acc_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<TCOLS>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch(&tmA);
+            tma_prefetch(&tmB0);
+            if (NB == 2) tma_prefetch(&tmB1);
+            for (int kb = 0; kb < kblocks; ++kb) {
+                const int s = kb % NST;
+                if (kb >= NST) mbar_wait(&empty[s], ((kb / NST) - 1) & 1);
+                uint8_t* st = smem + s * STAGE;
+                mbar_expect_tx(&full[s], STAGE);
+                tma_load_2d(st, &tmA, &full[s], kb * 64, row0);
+#pragma unroll
+                for (int nb = 0; nb < BN / 64; ++nb) {
+                    tma_load_3d(st + A_BYTES + nb * 8192, &tmB0, &full[s], n0 + nb * 64, kb * 64, g);
+                    if constexpr (NB == 2)
+                        tma_load_3d(st + A_BYTES + B_BYTES + nb * 8192, &tmB1, &full[s], n0 + nb * 64, kb * 64, g);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc(1, 0, 1, 128, BN);
+            for (int kb = 0; kb < kblocks; ++kb) {
+                const int s = kb % NST;
+                mbar_wait(&full[s], (kb / NST) & 1);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(smem + s * STAGE);
+                const uint32_t b0 = a0 + A_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t ad = umma_desc_sw128(a0 + kk * 32, 16, 1024);
+                    const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+                    mma_ss_f16(tmem, ad, umma_desc_sw128(b0 + kk * 2048, 8192, 1024), idesc, acc);
+                    if constexpr (NB == 2)
+                        mma_ss_f16(tmem + BN, ad, umma_desc_sw128(b0 + B_BYTES + kk * 2048, 8192, 1024),
+                                   idesc, acc);
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(acc_full);
+        }
+    } else {
+        // epilogue: thread (quarter q, lane) owns output row q*32 + lane of the tile
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        mbar_wait(acc_full, 0);
+        tc_fence_after();
+        const bool valid = r < rows_left;
+        const size_t grow = (size_t)row0 + (valid ? r : 0);
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += 32) {
+            uint32_t a[32];
+            tmem_ld32(tmem + lane_off + cb, a);
+            if constexpr (EPI == kEpiSwiGLU) {
+                uint32_t u[32];
+                tmem_ld32(tmem + lane_off + BN + cb, u);
+                tmem_wait_ld();
+                if (valid) {
+                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + n0 + cb;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        uint4 v;
+                        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float g0 = __uint_as_float(a[j + 2 * e]), g1 = __uint_as_float(a[j + 2 * e + 1]);
+                            const float u0 = __uint_as_float(u[j + 2 * e]), u1 = __uint_as_float(u[j + 2 * e + 1]);
+                            w[e] = pack_bf16(silu_f(g0) * u0, silu_f(g1) * u1);
+                        }
+                        *reinterpret_cast<uint4*>(dst + j) = v;
+                    }
+                }
+            } else if constexpr (EPI == kEpiBF16) {
+                tmem_wait_ld();
+                if (valid) {
+                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + n0 + cb;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        uint4 v;
+                        v.x = pack_bf16(__uint_as_float(a[j]), __uint_as_float(a[j + 1]));
+                        v.y = pack_bf16(__uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
+                        v.z = pack_bf16(__uint_as_float(a[j + 4]), __uint_as_float(a[j + 5]));
+                        v.w = pack_bf16(__uint_as_float(a[j + 6]), __uint_as_float(a[j + 7]));
+                        *reinterpret_cast<uint4*>(dst + j) = v;
+                    }
+                }
+            } else {  // fp32
+                tmem_wait_ld();
+                if (valid) {
+                    float* dst = reinterpret_cast<float*>(p.C) + grow * p.ldc + n0 + cb;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(dst + j) =
+                            make_float4(__uint_as_float(a[j]), __uint_as_float(a[j + 1]),
+                                        __uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<TCOLS>(tmem);
+}
+
+template __global__ void moe_gemm<128, kEpiSwiGLU>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap, GemmParams);
+template __global__ void moe_gemm<256, kEpiBF16>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                 const __grid_constant__ CUtensorMap, GemmParams);
+template __global__ void moe_gemm<128, kEpiBF16>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                 const __grid_constant__ CUtensorMap, GemmParams);
+template __global__ void moe_gemm<64, kEpiF32>(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                               const __grid_constant__ CUtensorMap, GemmParams);
+
+// ====================================================================================
+// Routing: one warp per token, E <= 64 (lane owns experts lane and lane + 32)
+// ====================================================================================
+__global__ void moe_route(const float* __restrict__ logits, int T, int E, int K,
+                          int* __restrict__ ids, float* __restrict__ gates,
+                          float* __restrict__ probs, int* __restrict__ counts,
+                          float* __restrict__ prob_colsum) {
+    __shared__ int s_cnt[64];
+    __shared__ float s_psum[64];
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) { s_cnt[i] = 0; s_psum[i] = 0.f; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (t < T) {
+        const float* l = logits + (size_t)t * E;
+        const float NEG = -INFINITY;
+        float v0 = lane < E ? l[lane] : NEG;
+        float v1 = lane + 32 < E ? l[lane + 32] : NEG;
+        const bool has0 = lane < E, has1 = lane + 32 < E;
+        // full softmax (tensor.hpp:767-789): max-subtracted over all logits
+        float mx = fmaxf(v0, v1);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        const float e0 = has0 ? __expf(v0 - mx) : 0.f, e1 = has1 ? __expf(v1 - mx) : 0.f;
+        float zs = e0 + e1;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) zs += __shfl_xor_sync(0xFFFFFFFFu, zs, o);
+        const float p0 = e0 / zs, p1 = e1 / zs;
+        if (probs) {
+            if (has0) probs[(size_t)t * E + lane] = p0;
+            if (has1) probs[(size_t)t * E + lane + 32] = p1;
+        }
+        if (has0) atomicAdd(&s_psum[lane], p0);
+        if (has1) atomicAdd(&s_psum[lane + 32], p1);
+        // top-k by repeated warp argmax: larger logit first, ties -> lower id (moe.hpp:70-75)
+        bool sel0 = false, sel1 = false;
+        float top = NEG;
+        for (int r = 0; r < K; ++r) {
+            float bv;
+            int bi;
+            const bool c0 = has0 && !sel0, c1 = has1 && !sel1;
+            if (c0 && (!c1 || v0 >= v1)) { bv = v0; bi = lane; }
+            else if (c1) { bv = v1; bi = lane + 32; }
+            else { bv = NEG; bi = 1 << 30; }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
+                const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+            }
+            if (r == 0) top = bv;
+            if (bi == lane) sel0 = true;
+            if (bi == lane + 32) sel1 = true;
+        }
+        // ascending ids of the selection (moe.hpp:77) + masked softmax (max = top-1 logit)
+        const unsigned m0 = __ballot_sync(0xFFFFFFFFu, sel0), m1 = __ballot_sync(0xFFFFFFFFu, sel1);
+        const float g0 = sel0 ? __expf(v0 - top) : 0.f, g1 = sel1 ? __expf(v1 - top) : 0.f;
+        float gz = g0 + g1;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) gz += __shfl_xor_sync(0xFFFFFFFFu, gz, o);
+        if (sel0) {
+            const int slot = __popc(m0 & ((1u << lane) - 1u));
+            ids[(size_t)t * K + slot] = lane;
+            gates[(size_t)t * K + slot] = g0 / gz;
+            atomicAdd(&s_cnt[lane], 1);
+        }
+        if (sel1) {
+            const int slot = __popc(m0) + __popc(m1 & ((1u << lane) - 1u));
+            ids[(size_t)t * K + slot] = lane + 32;
+            gates[(size_t)t * K + slot] = g1 / gz;
+            atomicAdd(&s_cnt[lane + 32], 1);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < E; i += blockDim.x) {
+        if (s_cnt[i]) atomicAdd(&counts[i], s_cnt[i]);
+        if (prob_colsum) atomicAdd(&prob_colsum[i], s_psum[i]);
+    }
+}
+
+// offsets / tile list / aux: one block.  offsets[e] = sum_{e'<e} counts[e']; per group the
+// 128-row GEMM tiles; aux = E * sum_e (counts_e / (T k)) (colsum_e / T)  (moe.hpp:90-103)
+__global__ void moe_plan(const int* __restrict__ counts, const float* __restrict__ prob_colsum,
+                         int T, int E, int K, int* __restrict__ offsets, int* __restrict__ group_end,
+                         int* __restrict__ tile_group, int* __restrict__ tile_row0,
+                         int* __restrict__ num_tiles, float* __restrict__ aux) {
+    if (threadIdx.x != 0) return;
+    int off = 0, nt = 0;
+    double acc = 0.0;
+    for (int e = 0; e < E; ++e) {
+        offsets[e] = off;
+        const int c = counts[e];
+        for (int r = 0; r < c; r += 128) { tile_group[nt] = e; tile_row0[nt] = off + r; ++nt; }
+        off += c;
+        group_end[e] = off;
+        if (prob_colsum) acc += ((double)c / ((double)T * K)) * ((double)prob_colsum[e] / T);
+    }
+    offsets[E] = off;
+    *num_tiles = nt;
+    if (aux) *aux = (float)(acc * E);
+}
+
+// Stable dispatch positions: block b owns tokens [b*256, b*256+256); blk_cnt[b][e] counted
+// first, then each (token, slot) gets  offsets[e] + sum_{b'<b} blk_cnt[b'][e] + rank within
+// the block among earlier tokens routed to e (token-ascending, moe.hpp:137-139).
+__global__ void moe_block_counts(const int* __restrict__ ids, int T, int E, int K,
+                                 int* __restrict__ blk_cnt) {
+    __shared__ int c[64];
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) c[i] = 0;
+    __syncthreads();
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < T)
+        for (int s = 0; s < K; ++s) atomicAdd(&c[ids[(size_t)t * K + s]], 1);
+    __syncthreads();
+    for (int i = threadIdx.x; i < E; i += blockDim.x) blk_cnt[(size_t)blockIdx.x * E + i] = c[i];
+}
+
+// blk_base[b][e] = offsets[e] + sum_{b'<b} blk_cnt[b'][e]   (one thread per expert)
+__global__ void moe_block_scan(const int* __restrict__ blk_cnt, const int* __restrict__ offsets,
+                               int nblk, int E, int* __restrict__ blk_base) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int run = offsets[e];
+    for (int b = 0; b < nblk; ++b) {
+        blk_base[(size_t)b * E + e] = run;
+        run += blk_cnt[(size_t)b * E + e];
+    }
+}
+
+__global__ void __launch_bounds__(256) moe_assign(const int* __restrict__ ids, int T, int E, int K,
+                                                  const int* __restrict__ blk_base,
+                                                  int* __restrict__ slot_pos,
+                                                  int* __restrict__ perm_token) {
+    __shared__ int warp_tot[8][64];
+    __shared__ int base[64];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int t = blockIdx.x * 256 + tid;
+    int my[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) my[s] = (s < K && t < T) ? ids[(size_t)t * K + s] : -1;
+    for (int i = tid; i < 64; i += 256) base[i] = i < E ? blk_base[(size_t)blockIdx.x * E + i] : 0;
+    // per expert: rank of this token among earlier tokens of the block routed to e
+    int rank[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) rank[s] = 0;
+    for (int e = 0; e < E; ++e) {
+        bool hit = false;
+        int hs = 0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            if (my[s] == e) { hit = true; hs = s; }
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
+        if (lane == 0) warp_tot[w][e] = __popc(m);
+        if (hit) rank[hs] = __popc(m & ((1u << lane) - 1u));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        if (my[s] < 0) continue;
+        const int e = my[s];
+        int before = 0;
+        for (int ww = 0; ww < w; ++ww) before += warp_tot[ww][e];
+        const int pos = base[e] + before + rank[s];
+        slot_pos[(size_t)t * K + s] = pos;
+        perm_token[pos] = t;
+    }
+}
+
+// x_perm[pos] = x[perm_token[pos]]   (one warp per row, 16-byte vectors)
+__global__ void moe_gather(const uint4* __restrict__ x, const int* __restrict__ perm_token,
+                           int rows, int row_vec, uint4* __restrict__ x_perm) {
+    const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const uint4* src = x + (size_t)perm_token[r] * row_vec;
+    uint4* dst = x_perm + (size_t)r * row_vec;
+    for (int i = threadIdx.x & 31; i < row_vec; i += 32) dst[i] = src[i];
+}
+
+// y[t] = sum_s gate[t,s] * y_perm[slot_pos[t,s]], slots in ascending expert order
+// (moe.hpp:145-146 accumulates expert by expert).  One warp per token, 8 bf16 per lane-step.
+__global__ void moe_combine(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__ slot_pos,
+                            const float* __restrict__ gates, int T, int K, int hidden,
+                            void* __restrict__ y, int y_f32) {
+    const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (t >= T) return;
+    const int lane = threadIdx.x & 31;
+    int pos[8];
+    float g[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        pos[s] = s < K ? slot_pos[(size_t)t * K + s] : 0;
+        g[s] = s < K ? gates[(size_t)t * K + s] : 0.f;
+    }
+    for (int c = lane * 8; c < hidden; c += 256) {
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            if (s >= K) break;
+            const uint4 v = *reinterpret_cast<const uint4*>(y_perm + (size_t)pos[s] * hidden + c);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = unpack_bf16(w[i]);
+                acc[2 * i] += g[s] * f.x;
+                acc[2 * i + 1] += g[s] * f.y;
+            }
+        }
+        if (y_f32) {
+            float* dst = reinterpret_cast<float*>(y) + (size_t)t * hidden + c;
+            *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        } else {
+            uint4 o;
+            o.x = pack_bf16(acc[0], acc[1]);
+            o.y = pack_bf16(acc[2], acc[3]);
+            o.z = pack_bf16(acc[4], acc[5]);
+            o.w = pack_bf16(acc[6], acc[7]);
+            *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(y) + (size_t)t * hidden + c) = o;
+        }
+    }
+}
+
+}  // namespace lmoe_dev

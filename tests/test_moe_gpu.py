@@ -1,0 +1,122 @@
+"""GPU parity of the MoE layer (moe.hpp) on sm_100a.
+
+Routing is checked BIT-EXACT (ids and the stable per-expert token order) on identical fp32
+logits; outputs within the bf16 tolerance (norm-relative 2e-2) against the
+float64 oracle fed the same bf16-rounded inputs and the device's routing decision."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import load_golden, norm_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def test_route_golden_bit_exact():
+    torch = _torch()
+    from paper_2503_05447_b200 import moe
+    d = load_golden("route")
+    for p in sorted({k.split("/")[0] for k in d}):
+        k = int(d[p + "/top_k"][0])
+        logits = torch.tensor(d[p + "/logits"], dtype=torch.float32, device="cuda")
+        dec = moe.route(logits, k)
+        torch.cuda.synchronize()
+        assert np.array_equal(dec.expert_ids.cpu().numpy(), d[p + "/ids"].astype(np.int32)), p
+        assert np.abs(dec.gates.cpu().numpy() - d[p + "/gates"]).max() < 1e-6, p
+        assert np.abs(dec.full_probs.cpu().numpy() - d[p + "/probs"]).max() < 1e-6, p
+        assert abs(dec.aux.item() - d[p + "/aux"][0]) < 1e-5, p
+
+
+@pytest.mark.parametrize("T,E,k,kind", [(65536, 64, 8, "normal"), (4096, 64, 8, "ties"),
+                                         (3000, 48, 5, "normal"), (1000, 8, 2, "ties")])
+def test_route_random_bit_exact(T, E, k, kind):
+    torch = _torch()
+    from paper_2503_05447_b200 import moe
+    rng = np.random.default_rng(T + E + k)
+    if kind == "ties":
+        logits = (rng.integers(0, 6, (T, E)) * 0.25).astype(np.float32)
+    else:
+        logits = rng.normal(0, 1, (T, E)).astype(np.float32)
+    dec = moe.route(torch.tensor(logits, device="cuda"), k)
+    ids = dec.expert_ids.cpu().numpy()
+    want_ids, want_gates, want_probs = oracle.route(logits.astype(np.float64), k)
+    assert np.array_equal(ids, want_ids)
+    g = dec.gates_topk.cpu().numpy()
+    assert np.abs(g - np.take_along_axis(want_gates, want_ids.astype(np.int64), 1)).max() < 1e-5
+    counts = np.bincount(want_ids.ravel(), minlength=E)
+    assert np.array_equal(dec.counts.cpu().numpy(), counts)
+    aux = oracle.load_balance_loss(want_ids, want_probs)
+    assert abs(dec.aux.item() - aux) < 1e-4 * max(1.0, aux)
+
+
+def _bf(torch, t):
+    return t.to(torch.bfloat16).float().cpu().numpy().astype(np.float64)
+
+
+def _expected_rows(x, wg, wu, wd, ids, gates, rows):
+    """float64 SwiGLU experts + gate-weighted combine for selected tokens (moe.hpp:45-47, 141-146)."""
+    out = []
+    for t in rows:
+        acc = np.zeros(x.shape[1])
+        for s in range(ids.shape[1]):
+            e = ids[t, s]
+            g = x[t] @ wg[e]
+            u = x[t] @ wu[e]
+            h = (g / (1 + np.exp(-g))) * u
+            acc += gates[t, s] * (h @ wd[e])
+        out.append(acc)
+    return np.stack(out)
+
+
+@pytest.mark.parametrize("T,hidden,ffn,E,k", [(300, 256, 128, 8, 2), (1000, 256, 256, 64, 8),
+                                              (4096, 1024, 896, 64, 8)])
+def test_moe_forward_vs_oracle(T, hidden, ffn, E, k):
+    torch = _torch()
+    from paper_2503_05447_b200 import moe
+    g = torch.Generator(device="cuda").manual_seed(T + E)
+    cfg = moe.MoeConfig(E, k, hidden, ffn)
+    layer = moe.MoeLayer.init(cfg, generator=g)
+    x = torch.randn(T, hidden, device="cuda", generator=g).to(torch.bfloat16)
+    y, aux, dec, logits = layer.forward(x, y_f32=True, return_routing=True)
+    torch.cuda.synchronize()
+    X, WR = _bf(torch, x), _bf(torch, layer.router)
+    WG, WU, WD = _bf(torch, layer.w_gate), _bf(torch, layer.w_up), _bf(torch, layer.w_down)
+    # router GEMM: fp32 accumulation of identical bf16 operands
+    want_logits = X @ WR
+    assert norm_rel_err(logits.cpu().numpy(), want_logits) < 1e-5
+    # routing on the device's own logits is bit-exact with the reference algorithm
+    ids = dec.expert_ids.cpu().numpy()
+    oid, ogates, oprobs = oracle.route(logits.cpu().numpy().astype(np.float64), k)
+    assert np.array_equal(ids, oid)
+    gates = dec.gates_topk.cpu().numpy().astype(np.float64)
+    # stable dispatch: per expert, tokens ascending (moe.hpp:137-139)
+    sp, pt, off = layer.dispatch(T)
+    pt, off = pt.cpu().numpy(), off.cpu().numpy()
+    for e in range(E):
+        seg = pt[off[e]:off[e + 1]]
+        assert np.all(np.diff(seg) > 0)
+        assert np.array_equal(np.sort(seg), np.nonzero((ids == e).any(1))[0])
+    rows = np.arange(T) if T <= 300 else np.random.default_rng(0).choice(T, 64, replace=False)
+    want = _expected_rows(X, WG, WU, WD, ids, gates, rows)
+    got = y.cpu().numpy()[rows]
+    assert norm_rel_err(got, want) < 2e-2
+    aux_want = oracle.load_balance_loss(oid, oprobs)
+    assert abs(aux.item() - aux_want) < 1e-3 * max(1.0, aux_want)
+
+
+def test_moe_golden_small_via_oracle_path():
+    """The reference's own MoE outputs (tests/golden/moe.npz) -- f64 reference vs the
+    oracle; the device path needs hidden % 256 == 0, so the golden shapes pin the oracle
+    that the larger device tests compare against."""
+    d = load_golden("moe")
+    for p in sorted({k.split("/")[0] for k in d}):
+        y, aux, _ = oracle.moe_forward(d[p + "/x"], d[p + "/router"], d[p + "/w_gate"],
+                                       d[p + "/w_up"], d[p + "/w_down"], int(d[p + "/top_k"][0]))
+        assert np.abs(y - d[p + "/y"]).max() < 1e-13
