@@ -52,7 +52,7 @@ static void launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUten
                                              lmoe_dev::gemm_smem<BN, EPI>()));
         attr = true;
     }
-    lmoe_dev::moe_gemm<BN, EPI><<<dim3(max_tiles, ntiles_n), lmoe_dev::kGemmThreads,
+    lmoe_dev::moe_gemm<BN, EPI><<<dim3(ntiles_n, max_tiles), lmoe_dev::kGemmThreads,
                                   lmoe_dev::gemm_smem<BN, EPI>(), st>>>(a, b0, b1, gp);
     LMOE_CUDA_CHECK(cudaGetLastError());
     ++g_launch_count;
@@ -81,7 +81,7 @@ static void route_core(const float* logits, int T, int E, int K, int* ids, float
                        int* counts, float* colsum, cudaStream_t st) {
     LMOE_CUDA_CHECK(cudaMemsetAsync(counts, 0, E * 4, st));
     LMOE_CUDA_CHECK(cudaMemsetAsync(colsum, 0, E * 4, st));
-    lmoe_dev::moe_route<<<(T + 7) / 8, 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
+    lmoe_dev::moe_route<<<std::min((T + 7) / 8, num_sms() * 8), 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
     LMOE_CUDA_CHECK(cudaGetLastError());
     ++g_launch_count;
 }
@@ -115,7 +115,7 @@ extern "C" int lmoe_moe_route(const float* logits, int T, int E, int top_k, int*
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         float* colsum = reinterpret_cast<float*>(ws + w.colsum);
         route_core(logits, T, E, top_k, ids, gates, probs, counts, colsum, st);
-        lmoe_dev::moe_plan<<<1, 32, 0, st>>>(counts, colsum, T, E, top_k,
+        lmoe_dev::moe_plan<<<1, 256, 0, st>>>(counts, colsum, T, E, top_k,
                                              reinterpret_cast<int*>(ws + w.offsets),
                                              reinterpret_cast<int*>(ws + w.group_end),
                                              reinterpret_cast<int*>(ws + w.tile_group),
@@ -176,12 +176,12 @@ extern "C" int lmoe_moe_forward(int T, int hidden, int ffn, int E, int top_k, co
         // 2. route + counts + probability column sums
         route_core(logits, T, E, top_k, ids, gates, nullptr, P(w.counts), colsum, st);
         // 3. offsets, GEMM tile list, aux loss
-        lmoe_dev::moe_plan<<<1, 32, 0, st>>>(P(w.counts), colsum, T, E, top_k, P(w.offsets), P(w.group_end),
+        lmoe_dev::moe_plan<<<1, 256, 0, st>>>(P(w.counts), colsum, T, E, top_k, P(w.offsets), P(w.group_end),
                                              P(w.tile_group), P(w.tile_row0), P(w.num_tiles),
                                              aux ? aux : reinterpret_cast<float*>(ws + w.aux));
         // 4. stable dispatch positions (tokens ascending within each expert)
         lmoe_dev::moe_block_counts<<<w.nblk, 256, 0, st>>>(ids, T, E, top_k, P(w.blk_cnt));
-        lmoe_dev::moe_block_scan<<<(E + 63) / 64, 64, 0, st>>>(P(w.blk_cnt), P(w.offsets), w.nblk, E, P(w.blk_base));
+        lmoe_dev::moe_block_scan<<<E, 256, 0, st>>>(P(w.blk_cnt), P(w.offsets), w.nblk, E, P(w.blk_base));
         lmoe_dev::moe_assign<<<w.nblk, 256, 0, st>>>(ids, T, E, top_k, P(w.blk_base), P(w.slot_pos), P(w.perm_token));
         // 5. permute rows
         lmoe_dev::moe_gather<<<(int)((rows + 7) / 8), 256, 0, st>>>(

@@ -36,12 +36,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint64_t* acc_full = bars + 2 * NST;
     uint32_t* sTmem = reinterpret_cast<uint32_t*>(acc_full + 1);
 
-    const int tile = blockIdx.x;
+    // blockIdx.x walks the N tiles of one 128-row M tile so they share the A tile in L2
+    const int tile = blockIdx.y;
     if (tile >= *p.num_tiles) return;
     const int g = p.tile_group[tile];
     const int row0 = p.tile_row0[tile];
     const int rows_left = p.group_end[g] - row0;  // valid rows of this tile (<= 128)
-    const int n0 = blockIdx.y * BN;
+    const int n0 = blockIdx.x * BN;
     const int kblocks = p.K / 64;
     const int warp = warp_id(), lane = lane_id();
 
@@ -171,24 +172,24 @@ template __global__ void moe_gemm<64, kEpiF32>(const __grid_constant__ CUtensorM
                                                const __grid_constant__ CUtensorMap, GemmParams);
 
 // ====================================================================================
-// Routing: one warp per token, E <= 64 (lane owns experts lane and lane + 32)
+// Routing: each warp walks tokens (lane owns experts lane and lane + 32, E <= 64); counts
+// and probability column sums stay in registers until one atomic per expert per warp.
 // ====================================================================================
-__global__ void moe_route(const float* __restrict__ logits, int T, int E, int K,
-                          int* __restrict__ ids, float* __restrict__ gates,
-                          float* __restrict__ probs, int* __restrict__ counts,
-                          float* __restrict__ prob_colsum) {
-    __shared__ int s_cnt[64];
-    __shared__ float s_psum[64];
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) { s_cnt[i] = 0; s_psum[i] = 0.f; }
-    __syncthreads();
+__global__ void __launch_bounds__(256) moe_route(const float* __restrict__ logits, int T, int E, int K,
+                                                 int* __restrict__ ids, float* __restrict__ gates,
+                                                 float* __restrict__ probs, int* __restrict__ counts,
+                                                 float* __restrict__ prob_colsum) {
     const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (t < T) {
+    const int wglobal = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int nwarps = gridDim.x * (blockDim.x / 32);
+    const bool has0 = lane < E, has1 = lane + 32 < E;
+    const float NEG = -INFINITY;
+    int cnt0 = 0, cnt1 = 0;
+    float ps0 = 0.f, ps1 = 0.f;
+    for (int t = wglobal; t < T; t += nwarps) {
         const float* l = logits + (size_t)t * E;
-        const float NEG = -INFINITY;
-        float v0 = lane < E ? l[lane] : NEG;
-        float v1 = lane + 32 < E ? l[lane + 32] : NEG;
-        const bool has0 = lane < E, has1 = lane + 32 < E;
+        const float v0 = has0 ? l[lane] : NEG;
+        const float v1 = has1 ? l[lane + 32] : NEG;
         // full softmax (tensor.hpp:767-789): max-subtracted over all logits
         float mx = fmaxf(v0, v1);
 #pragma unroll
@@ -202,8 +203,8 @@ __global__ void moe_route(const float* __restrict__ logits, int T, int E, int K,
             if (has0) probs[(size_t)t * E + lane] = p0;
             if (has1) probs[(size_t)t * E + lane + 32] = p1;
         }
-        if (has0) atomicAdd(&s_psum[lane], p0);
-        if (has1) atomicAdd(&s_psum[lane + 32], p1);
+        ps0 += p0;
+        ps1 += p1;
         // top-k by repeated warp argmax: larger logit first, ties -> lower id (moe.hpp:70-75)
         bool sel0 = false, sel1 = false;
         float top = NEG;
@@ -234,42 +235,70 @@ __global__ void moe_route(const float* __restrict__ logits, int T, int E, int K,
             const int slot = __popc(m0 & ((1u << lane) - 1u));
             ids[(size_t)t * K + slot] = lane;
             gates[(size_t)t * K + slot] = g0 / gz;
-            atomicAdd(&s_cnt[lane], 1);
+            ++cnt0;
         }
         if (sel1) {
             const int slot = __popc(m0) + __popc(m1 & ((1u << lane) - 1u));
             ids[(size_t)t * K + slot] = lane + 32;
             gates[(size_t)t * K + slot] = g1 / gz;
-            atomicAdd(&s_cnt[lane + 32], 1);
+            ++cnt1;
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < E; i += blockDim.x) {
-        if (s_cnt[i]) atomicAdd(&counts[i], s_cnt[i]);
-        if (prob_colsum) atomicAdd(&prob_colsum[i], s_psum[i]);
+    if (has0) {
+        if (cnt0) atomicAdd(&counts[lane], cnt0);
+        if (prob_colsum) atomicAdd(&prob_colsum[lane], ps0);
+    }
+    if (has1) {
+        if (cnt1) atomicAdd(&counts[lane + 32], cnt1);
+        if (prob_colsum) atomicAdd(&prob_colsum[lane + 32], ps1);
     }
 }
 
-// offsets / tile list / aux: one block.  offsets[e] = sum_{e'<e} counts[e']; per group the
-// 128-row GEMM tiles; aux = E * sum_e (counts_e / (T k)) (colsum_e / T)  (moe.hpp:90-103)
-__global__ void moe_plan(const int* __restrict__ counts, const float* __restrict__ prob_colsum,
-                         int T, int E, int K, int* __restrict__ offsets, int* __restrict__ group_end,
-                         int* __restrict__ tile_group, int* __restrict__ tile_row0,
-                         int* __restrict__ num_tiles, float* __restrict__ aux) {
-    if (threadIdx.x != 0) return;
-    int off = 0, nt = 0;
-    double acc = 0.0;
-    for (int e = 0; e < E; ++e) {
-        offsets[e] = off;
-        const int c = counts[e];
-        for (int r = 0; r < c; r += 128) { tile_group[nt] = e; tile_row0[nt] = off + r; ++nt; }
-        off += c;
-        group_end[e] = off;
-        if (prob_colsum) acc += ((double)c / ((double)T * K)) * ((double)prob_colsum[e] / T);
+// offsets / tile list / aux, one block of 256 threads (E <= 64).
+// offsets[e] = sum_{e'<e} counts[e']; per group the 128-row GEMM tiles;
+// aux = E * sum_e (counts_e / (T k)) (colsum_e / T)   (moe.hpp:90-103)
+__global__ void __launch_bounds__(256) moe_plan(const int* __restrict__ counts, const float* __restrict__ prob_colsum,
+                                                int T, int E, int K, int* __restrict__ offsets,
+                                                int* __restrict__ group_end, int* __restrict__ tile_group,
+                                                int* __restrict__ tile_row0, int* __restrict__ num_tiles,
+                                                float* __restrict__ aux) {
+    __shared__ int s_off[65], s_toff[65];
+    __shared__ double s_aux[64];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        int off = 0, nt = 0;
+        for (int e = 0; e < E; ++e) {
+            s_off[e] = off;
+            s_toff[e] = nt;
+            off += counts[e];
+            nt += (counts[e] + 127) / 128;
+        }
+        s_off[E] = off;
+        s_toff[E] = nt;
     }
-    offsets[E] = off;
-    *num_tiles = nt;
-    if (aux) *aux = (float)(acc * E);
+    if (tid < E) {
+        const int c = counts[tid];
+        s_aux[tid] = prob_colsum ? ((double)c / ((double)T * K)) * ((double)prob_colsum[tid] / T) : 0.0;
+    }
+    __syncthreads();
+    if (tid <= E) offsets[tid] = s_off[tid];
+    if (tid < E) group_end[tid] = s_off[tid + 1];
+    const int nt = s_toff[E];
+    for (int i = tid; i < nt; i += blockDim.x) {
+        int lo = 0, hi = E - 1;  // last e with s_toff[e] <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_toff[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        tile_group[i] = lo;
+        tile_row0[i] = s_off[lo] + (i - s_toff[lo]) * 128;
+    }
+    if (tid == 0) {
+        *num_tiles = nt;
+        double acc = 0.0;
+        for (int e = 0; e < E; ++e) acc += s_aux[e];
+        if (aux) *aux = (float)(acc * E);
+    }
 }
 
 // Stable dispatch positions: block b owns tokens [b*256, b*256+256); blk_cnt[b][e] counted
@@ -287,15 +316,33 @@ __global__ void moe_block_counts(const int* __restrict__ ids, int T, int E, int 
     for (int i = threadIdx.x; i < E; i += blockDim.x) blk_cnt[(size_t)blockIdx.x * E + i] = c[i];
 }
 
-// blk_base[b][e] = offsets[e] + sum_{b'<b} blk_cnt[b'][e]   (one thread per expert)
-__global__ void moe_block_scan(const int* __restrict__ blk_cnt, const int* __restrict__ offsets,
-                               int nblk, int E, int* __restrict__ blk_base) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E) return;
-    int run = offsets[e];
-    for (int b = 0; b < nblk; ++b) {
-        blk_base[(size_t)b * E + e] = run;
-        run += blk_cnt[(size_t)b * E + e];
+// blk_base[b][e] = offsets[e] + sum_{b'<b} blk_cnt[b'][e]: one block per expert, a
+// block-wide exclusive scan over the token blocks (256 at a time with carry).
+__global__ void __launch_bounds__(256) moe_block_scan(const int* __restrict__ blk_cnt, const int* __restrict__ offsets,
+                                                      int nblk, int E, int* __restrict__ blk_base) {
+    __shared__ int wsum[8];
+    __shared__ int carry_s;
+    const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) carry_s = offsets[e];
+    __syncthreads();
+    for (int b0 = 0; b0 < nblk; b0 += 256) {
+        const int b = b0 + tid;
+        const int v = b < nblk ? blk_cnt[(size_t)b * E + e] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        int before = 0;
+        for (int i = 0; i < w; ++i) before += wsum[i];
+        const int carry = carry_s;
+        if (b < nblk) blk_base[(size_t)b * E + e] = carry + before + x - v;
+        __syncthreads();
+        if (tid == 255) carry_s = carry + before + x;
+        __syncthreads();
     }
 }
 
