@@ -95,6 +95,66 @@ int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc);
 int lmoe_timing_read(float* ms_out, int nphase);
 /* Kernels of this library enqueued since process start. */
 long long lmoe_launch_count(void);
+/* Developer aid: clock64 phase trace of output-pass CTA (0,0,0) when LMOE_TRACE is set. */
+int lmoe_debug_trace_read(unsigned long long* out /* 64 x 16 */);
+
+/* ---------------------------------------------------------------------------------------
+ * LSM sequence parallelism.  Replaces sp_lsm_masked_rank(RankGroup&, rank, q_loc, k_loc,
+ * v_loc, gates_loc, spec, layer, &final_state) (parallel.hpp:303-376): the rank's
+ * contiguous slice (chunk_range, parallel.hpp:192-197) is evaluated from the zero state,
+ * ONE ncclAllGather moves the all-heads payload [M | z? | log D] (B*H*(D*D [+D] + 1) fp32 per
+ * rank; the reference gathers per head, parallel.hpp:447-452), the decayed exclusive
+ * prefix over earlier ranks (parallel.hpp:340-361) gives the carried-in state, and the
+ * output pass re-evaluates the slice with it.  nccl_comm is an ncclComm_t (world > 1).
+ * ------------------------------------------------------------------------------------- */
+size_t lmoe_sp_payload_floats(const lmoe_lsm_desc* desc, int B, int H, int D);
+size_t lmoe_sp_lsm_fwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
+                                      lmoe_dtype dtype, int world);
+int lmoe_sp_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D, lmoe_dtype dtype,
+                    const void* q, const void* k, const void* v, const void* a_pre,
+                    const float* b_pre, const float* a_raw, void* o, float* M_out, float* z_out,
+                    void* nccl_comm, int rank, int world, void* workspace, size_t workspace_bytes,
+                    lmoe_stream_t stream);
+/* Same algorithm, `world` virtual ranks on one device over the full sequence (device copies
+ * instead of the all-gather): sp_forward_masked (parallel.hpp:405-418) for testing. */
+size_t lmoe_sp_lsm_fwd_loopback_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H,
+                                               int D, lmoe_dtype dtype, int world);
+int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                             lmoe_dtype dtype, const void* q, const void* k, const void* v,
+                             const void* a_pre, const float* b_pre, const float* a_raw, void* o,
+                             float* M_out, float* z_out, int world, void* workspace,
+                             size_t workspace_bytes, lmoe_stream_t stream);
+/* Elements moved by the last SP gather (RankGroup::comm_log accounting, parallel.hpp:87-93). */
+long long lmoe_sp_last_gather_elements(void);
+/* NCCL bootstrap: rank 0 creates the 128-byte id, the caller distributes it. */
+int lmoe_nccl_unique_id(void* id128);
+int lmoe_nccl_comm_init(void** comm, int world, int rank, const void* id128);
+int lmoe_nccl_comm_destroy(void* comm);
+
+/* ---------------------------------------------------------------------------------------
+ * MoE expert layer (moe.hpp).  bf16 activations / weights in the reference layouts
+ * (router (hidden, E); w_gate, w_up (E, hidden, ffn); w_down (E, ffn, hidden)).
+ * ------------------------------------------------------------------------------------- */
+size_t lmoe_moe_workspace_size(int T, int hidden, int ffn, int E, int top_k);
+/* route (moe.hpp:58-85) + load_balance_loss (moe.hpp:90-103) on fp32 logits [T, E]:
+ * ids [T, k] (ascending per token, ties -> lower id), gates [T, k] renormalised over the
+ * selection, probs [T, E] (nullable), counts [E], aux (nullable).  E <= 64, k <= 8. */
+int lmoe_moe_route(const float* logits, int T, int E, int top_k, int* ids, float* gates,
+                   float* probs, int* counts, float* aux, void* workspace, size_t workspace_bytes,
+                   lmoe_stream_t stream);
+/* MoeLayer::forward (moe.hpp:133-149): router GEMM, route, stable dispatch (tokens ascending
+ * per expert, moe.hpp:137-139), grouped SwiGLU experts (moe.hpp:45-47), combine in ascending
+ * expert order, aux loss.  hidden % 256 == 0, ffn % 128 == 0.  logits/ids/gates outputs are
+ * optional copies of the routing. */
+int lmoe_moe_forward(int T, int hidden, int ffn, int E, int top_k, const void* x,
+                     const void* w_router, const void* w_gate, const void* w_up,
+                     const void* w_down, void* y, int y_f32, float* aux, float* logits_out,
+                     int* ids_out, float* gates_out, void* workspace, size_t workspace_bytes,
+                     lmoe_stream_t stream);
+/* Dispatch of the last forward using `workspace`: slot positions [T,k], the token of each
+ * permuted row [T*k], expert offsets [E+1] (device buffers, nullable). */
+int lmoe_moe_dispatch_read(int T, int hidden, int ffn, int E, int top_k, const void* workspace,
+                           int* slot_pos, int* perm_token, int* offsets, lmoe_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -378,6 +378,7 @@ int cmd_bench_lsm(int argc, char** argv) {
     std::vector<int> done(threads, 0);
     auto t0 = std::chrono::steady_clock::now();
     std::atomic<int> next{0};
+    std::atomic<int> failed{0};
     for (int w = 0; w < threads; ++w)
         pool.emplace_back([&, w]() {
             Rng rng(100 + w);
@@ -397,7 +398,13 @@ int cmd_bench_lsm(int argc, char** argv) {
                 if (h >= heads) break;
                 double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
                 if (el > budget) break;
-                (void)lsm_forward_chunked(q, k, v, g, spec, chunk);
+                try {
+                    (void)lsm_forward_chunked(q, k, v, g, spec, chunk);
+                } catch (const std::exception& e) {
+                    fprintf(stderr, "reference error: %s\n", e.what());
+                    failed = 1;
+                    break;
+                }
                 done[w]++;
             }
         });
@@ -408,8 +415,9 @@ int cmd_bench_lsm(int argc, char** argv) {
     // heads_done sequences of N tokens each; tokens/s counts (token, all H heads) units
     const double tok_s = (double)total * N / (double)H / secs;
     printf("{\"heads_done\": %d, \"heads_total\": %d, \"seconds\": %.6f, \"threads\": %d, "
-           "\"tokens_per_sec\": %.3f}\n", total, heads, secs, threads, tok_s);
-    return 0;
+           "\"tokens_per_sec\": %.3f, \"failed\": %d}\n", total, heads, secs, threads, tok_s,
+           failed.load());
+    return failed.load() ? 1 : 0;
 }
 
 int cmd_bench_moe(int argc, char** argv) {

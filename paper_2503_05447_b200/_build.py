@@ -15,6 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "liblmoe_cuda.so")
+CPP_API_BIN = os.path.join(LIBDIR, "lsm_cpp_api")
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -69,6 +70,14 @@ def build(force=False, verbose=False):
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stderr[-4000:])
     os.replace(tmp, LIB)
+    # C++ consumer of include/lmoe/cuda.hpp (drop-in API), run by tests/test_cpp_api.py
+    src = os.path.join(ROOT, "tests", "cpp", "lsm_cpp_api.cpp")
+    if os.path.exists(src):
+        cmd = [NVCC, "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", CPP_API_BIN,
+               "-L" + LIBDIR, "-llmoe_cuda", "-Xlinker", "-rpath=" + LIBDIR, "-Xlinker", "-rpath=$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("C++ API test build failed:\n" + r.stderr[-3000:])
     if verbose:
         for s in SOURCES:
             with open(os.path.join(BUILD, s + ".log")) as f:
