@@ -1,2 +1,2 @@
-ls -la oracle/_ref/; nproc; lscpu | grep -i "model name\|^CPU(s)"
-timeout 120 ./oracle/_ref/ref_driver bench-lsm mamba2 1 262144 16 128 64 0 10 ; echo rc=$?
+python -c "from paper_2503_05447_b200 import _build; _build.build()" || exit 1
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -v "^  " | tail -30

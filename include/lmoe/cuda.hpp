@@ -118,11 +118,12 @@ inline void lsm_forward_chunked(const LsmView& x, const LsmGates& gates, const L
     Workspace& w = ws ? *ws : local;
     const lmoe_lsm_desc d = to_desc(spec, chunk_size, check_device);
     const size_t need = lmoe_lsm_fwd_workspace_size(&d, x.B, x.N, x.H, x.D, x.dtype);
+    void* wsp = w.get(need);
     check(lmoe_lsm_fwd(&d, x.B, x.N, x.H, x.D, x.dtype, x.q, x.k, x.v, gates.a_pre, gates.b_pre,
                        spec.mamba2_a_raw, initial_state ? initial_state->M : nullptr,
                        initial_state ? initial_state->z : nullptr, x.o,
                        final_state ? final_state->M : nullptr, final_state ? final_state->z : nullptr,
-                       w.get(need), w.size(), reinterpret_cast<lmoe_stream_t>(stream)));
+                       wsp, w.size(), reinterpret_cast<lmoe_stream_t>(stream)));
 }
 
 // sp_lsm_masked_rank (parallel.hpp:303-376): this rank's slice (chunk_range), one NCCL
@@ -136,10 +137,11 @@ inline void sp_lsm_masked_rank(void* nccl_comm, int rank, int world, const LsmVi
     Workspace& w = ws ? *ws : local;
     const lmoe_lsm_desc d = to_desc(spec, 64, check_device);
     const size_t need = lmoe_sp_lsm_fwd_workspace_size(&d, x_loc.B, x_loc.N, x_loc.H, x_loc.D, x_loc.dtype, world);
+    void* wsp = w.get(need);
     check(lmoe_sp_lsm_fwd(&d, x_loc.B, x_loc.N, x_loc.H, x_loc.D, x_loc.dtype, x_loc.q, x_loc.k, x_loc.v,
                           g_loc.a_pre, g_loc.b_pre, spec.mamba2_a_raw, x_loc.o,
                           final_state ? final_state->M : nullptr, final_state ? final_state->z : nullptr,
-                          nccl_comm, rank, world, w.get(need), w.size(),
+                          nccl_comm, rank, world, wsp, w.size(),
                           reinterpret_cast<lmoe_stream_t>(stream)));
 }
 
@@ -165,8 +167,9 @@ struct RoutingDecision {
 inline void route(const float* logits, int T, int E, int top_k, const RoutingDecision& out,
                   Workspace& ws, cudaStream_t stream = nullptr) {
     const size_t need = lmoe_moe_workspace_size(T, 64, 64, E, top_k > 0 ? top_k : 1);
+    void* wsp = ws.get(need);
     check(lmoe_moe_route(logits, T, E, top_k, out.expert_ids, out.gates, out.full_probs, out.counts,
-                         out.aux, ws.get(need), ws.size(), reinterpret_cast<lmoe_stream_t>(stream)));
+                         out.aux, wsp, ws.size(), reinterpret_cast<lmoe_stream_t>(stream)));
 }
 
 // MoeConfig / MoeLayer (moe.hpp:15-27, 106-149) with bf16 device weights in the reference
@@ -193,8 +196,9 @@ struct MoeLayer {
         config.validate();
         const MoeConfig& c = config;
         const size_t need = lmoe_moe_workspace_size(T, c.hidden, c.ffn_dim, c.num_experts, c.top_k);
+        void* wsp = ws.get(need);
         check(lmoe_moe_forward(T, c.hidden, c.ffn_dim, c.num_experts, c.top_k, x, router, w_gate, w_up,
-                               w_down, y, y_f32 ? 1 : 0, aux, nullptr, nullptr, nullptr, ws.get(need),
+                               w_down, y, y_f32 ? 1 : 0, aux, nullptr, nullptr, nullptr, wsp,
                                ws.size(), reinterpret_cast<lmoe_stream_t>(stream)));
     }
 };

@@ -1,31 +1,36 @@
 // lsm_combine.cu -- segment / rank prefix-combine kernels of the LSM forward.
+// log-decays come per (b,h,segment) either as one scalar (None / ConstScalar / TokenScalar)
+// or as a d_k vector (TokenVector: GLA / HGRN2 / RWKV6); `lw` is 1 or d_k, and the decay of
+// element (i, j) of the state uses log-decay entry i (diag(D) M, parallel.hpp:340-361).
 #include "lsm_fwd.cuh"
 #include "lsm_launch.h"
 
 namespace lmoe_dev {
 
 // ------------------------------------------------------------------------------------
-// Phase 2: decayed exclusive prefix over segments (and ranks, for SP)
-//   Min[s] = acc ; acc = exp(logD[s]) * acc + S[s]        per element of [M | z]
+// Phase 2: decayed exclusive prefix over segments
+//   Min[s] = acc ; acc = exp(logD[s][row]) * acc + S[s]        per element of [M | z]
 // ------------------------------------------------------------------------------------
 __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __restrict__ zS,
                                 const float* __restrict__ logD, const float* __restrict__ M0,
                                 const float* __restrict__ z0, float* __restrict__ Min,
                                 float* __restrict__ zin, float* __restrict__ Mfin,
                                 float* __restrict__ zfin, float* __restrict__ logDtot,
-                                int fin_stride, int nseg, int dk, int dv, int norm, int* err) {
+                                int fin_stride, int nseg, int dk, int dv, int norm, int lw, int* err) {
     const int bh = blockIdx.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int nm = dk * dv;
     const int total = nm + (norm ? dk : 0);
-    if (logDtot && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (logDtot && blockIdx.x == 0 && threadIdx.x < lw) {
         float t = 0.f;
-        for (int s = 0; s < nseg; ++s) t += logD[(size_t)bh * nseg + s];
-        logDtot[(size_t)bh * fin_stride] = t;
+        for (int s = 0; s < nseg; ++s) t += logD[((size_t)bh * nseg + s) * lw + threadIdx.x];
+        logDtot[(size_t)bh * fin_stride + threadIdx.x] = t;
     }
     if (e >= total) return;
     const bool isz = e >= nm;
     const int ee = isz ? e - nm : e;
+    const int row = isz ? ee : ee / dv;
+    const int li = lw == 1 ? 0 : row;
     const int stride = isz ? dk : nm;
     const float* src = isz ? zS : S;
     float* dst = isz ? zin : Min;
@@ -35,7 +40,7 @@ __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __rest
     const size_t base = (size_t)bh * nseg * stride + ee;
     for (int s = 0; s < nseg; ++s) {
         if (dst) dst[base + (size_t)s * stride] = acc;
-        acc = __expf(logD[(size_t)bh * nseg + s]) * acc + src[base + (size_t)s * stride];
+        acc = __expf(logD[((size_t)bh * nseg + s) * lw + li]) * acc + src[base + (size_t)s * stride];
     }
     if (!isfinite(acc)) atomicOr(&err[1], 1);
     float* fin = isz ? zfin : Mfin;
@@ -44,41 +49,40 @@ __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __rest
 }
 
 // LSM sequence parallelism: rank `rank` folds the gathered per-rank payloads
-// [world][BH][P] (P = dk*dv [+ dk] + 1: local state from zero, normaliser, total log decay)
+// [world][BH][P] (P = dk*dv [+ dk] + lw: local state from zero, normaliser, total log decay)
 // into its carried-in state -- the decayed exclusive prefix of sp_lsm_masked_rank
 // (parallel.hpp:340-361): acc_{i+1} = D_i acc_i + M_i over ranks i < rank.
 __global__ void sp_rank_combine(const float* __restrict__ gathered, int P, int BH, int rank,
-                                int dk, int dv, int norm, float* __restrict__ M0,
+                                int dk, int dv, int norm, int lw, float* __restrict__ M0,
                                 float* __restrict__ z0) {
     const int bh = blockIdx.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int nm = dk * dv;
     const int total = nm + (norm ? dk : 0);
     if (e >= total) return;
+    const int row = e < nm ? e / dv : e - nm;
+    const int li = lw == 1 ? 0 : row;
     float acc = 0.f;
     for (int i = 0; i < rank; ++i) {
         const float* pl = gathered + ((size_t)i * BH + bh) * P;
-        acc = __expf(pl[P - 1]) * acc + pl[e];
+        acc = __expf(pl[P - lw + li]) * acc + pl[e];
     }
     if (e < nm) M0[(size_t)bh * nm + e] = acc;
     else z0[(size_t)bh * dk + (e - nm)] = acc;
 }
 
-
-}  // namespace lmoe_dev
-
-namespace lmoe_dev {
 cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const float* zS,
                                const float* logD, const float* M0, const float* z0, float* Min,
                                float* zin, float* Mfin, float* zfin, float* logDtot, int fin_stride,
-                               int nseg, int dk, int dv, int norm, int* err) {
+                               int nseg, int dk, int dv, int norm, int lw, int* err) {
     lsm_seg_combine<<<grid, 256, 0, st>>>(S, zS, logD, M0, z0, Min, zin, Mfin, zfin, logDtot,
-                                          fin_stride, nseg, dk, dv, norm, err);
+                                          fin_stride, nseg, dk, dv, norm, lw, err);
     return cudaGetLastError();
 }
 cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,
-                                int rank, int dk, int dv, int norm, float* M0, float* z0) {
-    sp_rank_combine<<<grid, 256, 0, st>>>(gathered, P, BH, rank, dk, dv, norm, M0, z0);
+                                int rank, int dk, int dv, int norm, int lw, float* M0, float* z0) {
+    sp_rank_combine<<<grid, 256, 0, st>>>(gathered, P, BH, rank, dk, dv, norm, lw, M0, z0);
     return cudaGetLastError();
 }
+
 }  // namespace lmoe_dev

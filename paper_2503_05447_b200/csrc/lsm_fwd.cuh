@@ -39,7 +39,7 @@ constexpr int kBlockBytes = kC * 128;           // one SW128 column block of a t
 constexpr int kMathThreads = 256;               // 8 epilogue warps (output pass)
 constexpr float kSafeLogDecay = -80.f;          // e^{-G} stays finite in fp32 above this
 
-enum DecayMode { kDecayNone = 0, kDecayConst = 1, kDecayTokenScalar = 2 };
+enum DecayMode { kDecayNone = 0, kDecayConst = 1, kDecayTokenScalar = 2, kDecayTokenVector = 3 };
 
 struct LsmFwdParams {
     int B, N, H;
@@ -51,7 +51,7 @@ struct LsmFwdParams {
     const float* a_raw;  // [H]       Mamba2 static parameter
     float* Sseg;         // [B*H][nseg][dk][dv]
     float* zseg;         // [B*H][nseg][dk]
-    float* logDseg;      // [B*H][nseg]
+    float* logDseg;      // [B*H][nseg][lw]  (lw = 1, or d_k for TokenVector decays)
     const float* Min;    // [B*H][nseg][dk][dv]  (phase 3 input)
     const float* zin;    // [B*H][nseg][dk]
     void* o;             // [B, Nstride, H, D] output (phase 3), written from registers
@@ -132,9 +132,9 @@ __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __rest
                                 const float* __restrict__ z0, float* __restrict__ Min,
                                 float* __restrict__ zin, float* __restrict__ Mfin,
                                 float* __restrict__ zfin, float* __restrict__ logDtot,
-                                int fin_stride, int nseg, int dk, int dv, int norm, int* err);
+                                int fin_stride, int nseg, int dk, int dv, int norm, int lw, int* err);
 __global__ void sp_rank_combine(const float* __restrict__ gathered, int P, int BH, int rank,
-                                int dk, int dv, int norm, float* __restrict__ M0,
+                                int dk, int dv, int norm, int lw, float* __restrict__ M0,
                                 float* __restrict__ z0);
 
 }  // namespace lmoe_dev

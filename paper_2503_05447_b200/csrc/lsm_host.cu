@@ -46,6 +46,7 @@ int device_decay_mode(int inst) {
         case LMOE_BLA: case LMOE_REBASED: return lmoe_dev::kDecayNone;
         case LMOE_LIGHTNING: case LMOE_RETNET: return lmoe_dev::kDecayConst;
         case LMOE_MAMBA2: return lmoe_dev::kDecayTokenScalar;
+        case LMOE_GLA: case LMOE_HGRN2: case LMOE_RWKV6: return lmoe_dev::kDecayTokenVector;
         default: return -1;
     }
 }
@@ -84,7 +85,7 @@ static LsmPlan plan_lsm(int B, int N, int H, int D) {
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
     pl.off_S = take(heads_nseg * D * D * 4);
     pl.off_z = take(heads_nseg * D * 4);
-    pl.off_logD = take(heads_nseg * 4);
+    pl.off_logD = take(heads_nseg * D * 4);  // per-row log decay for TokenVector kinds
     pl.off_Min = take(heads_nseg * D * D * 4);
     pl.off_zin = take(heads_nseg * D * 4);
     pl.off_err = take(64);
@@ -132,10 +133,13 @@ struct LsmCall {
     uint8_t* ws;
     LsmPlan pl;
     cudaStream_t st;
+    const void* a_pre = nullptr;  // TokenVector gate pre-activations [B, N, H, D]
     std::vector<cudaEvent_t> ev;
     lmoe_dev::LsmFwdParams p{};
     lmoe_dev::LsmVariant var{};
     bool norm = false;
+    bool vec = false;
+    int lw = 1;  // log-decay entries per state: 1, or D for TokenVector kinds
 
     void mark() {
         if (!(d->flags & LMOE_FLAG_TIMING)) return;
@@ -154,7 +158,11 @@ struct LsmCall {
         var.decay = device_decay_mode(d->instance);
         var.fm = d->feature_map;
         var.norm = d->use_normalizer ? 1 : 0;
+        var.hgrn2 = d->instance == LMOE_HGRN2 ? 1 : 0;
         norm = var.norm != 0;
+        vec = var.decay == lmoe_dev::kDecayTokenVector;
+        lw = vec ? D : 1;
+        if (vec && !a_pre) throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd: TokenVector instances need a_pre");
         p.log_a = var.decay == lmoe_dev::kDecayConst ? logf(d->scalar_decay) : 0.f;
         p.b_pre = b_pre;
         p.a_raw = a_raw;
@@ -192,10 +200,18 @@ struct LsmCall {
     void state_pass() {
         const CUtensorMap tk = tmap<T>(k), tv = tmap<T>(v);
         mark();
-        if constexpr (sizeof(T) == 2)
-            LMOE_CUDA_CHECK(lmoe_dev::launch_state_pass_bf16(var, dim3(pl.nseg, H, B), st, tk, tv, p));
-        else
-            LMOE_CUDA_CHECK(lmoe_dev::launch_state_pass_f32(var, dim3(pl.nseg, H, B), st, tk, tv, p));
+        const dim3 grid(pl.nseg, H, B);
+        if (vec) {
+            const CUtensorMap ta = tmap<T>(a_pre);
+            if constexpr (sizeof(T) == 2)
+                LMOE_CUDA_CHECK(lmoe_dev::launch_state_pass_vec_bf16(var, grid, st, tk, tv, ta, p));
+            else
+                LMOE_CUDA_CHECK(lmoe_dev::launch_state_pass_vec_f32(var, grid, st, tk, tv, ta, p));
+        } else if constexpr (sizeof(T) == 2) {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_state_pass_bf16(var, grid, st, tk, tv, p));
+        } else {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_state_pass_f32(var, grid, st, tk, tv, p));
+        }
         ++g_launch_count;
     }
     // Segment prefix with carried-in state (M0, z0); writes per-segment M_in and the
@@ -208,26 +224,36 @@ struct LsmCall {
             dim3((nel + 255) / 256, B * H), st, p.Sseg, p.zseg, p.logDseg, M0, z0,
             write_min ? const_cast<float*>(p.Min) : nullptr,
             write_min ? const_cast<float*>(p.zin) : nullptr, Mfin, zfin, logDtot, fin_stride,
-            pl.nseg, D, D, norm ? 1 : 0, p.err));
+            pl.nseg, D, D, norm ? 1 : 0, lw, p.err));
         ++g_launch_count;
     }
     template <typename T>
     void output_pass() {
         const CUtensorMap tq = tmap<T>(q), tk = tmap<T>(k), tv = tmap<T>(v), to = tmap<T>(o);
         mark();
-        if constexpr (sizeof(T) == 2)
-            LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_bf16(var, dim3(pl.nseg, H, B), st, tq, tk, tv, to, p));
-        else
-            LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_f32(var, dim3(pl.nseg, H, B), st, tq, tk, tv, to, p));
+        const dim3 grid(pl.nseg, H, B);
+        if (vec) {
+            const CUtensorMap ta = tmap<T>(a_pre);
+            if constexpr (sizeof(T) == 2)
+                LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_vec_bf16(var, grid, st, tq, tk, tv, ta, p));
+            else
+                LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_vec_f32(var, grid, st, tq, tk, tv, ta, p));
+        } else if constexpr (sizeof(T) == 2) {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_bf16(var, grid, st, tq, tk, tv, to, p));
+        } else {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_f32(var, grid, st, tq, tk, tv, to, p));
+        }
         ++g_launch_count;
         mark();
     }
     void clear_err() { LMOE_CUDA_CHECK(cudaMemsetAsync(p.err, 0, 64, st)); }
     void check_err() {
         if (!(d->flags & LMOE_FLAG_CHECK)) return;
-        int err[2] = {0, 0};
+        int err[3] = {0, 0, 0};
         LMOE_CUDA_CHECK(cudaMemcpyAsync(err, p.err, sizeof(err), cudaMemcpyDeviceToHost, st));
         LMOE_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (err[2])  // TokenVector chunk whose half-chunk decay span leaves the fp32 range
+            throw Error(LMOE_ERR_NONFINITE, "non-finite output in div");
         if (err[0])
             throw Error(LMOE_ERR_DEGENERATE,
                         std::string("degenerate normalizer in instance ") + instance_name(d->instance));
@@ -248,8 +274,12 @@ static void run_local(LsmCall& c, const float* M0, const float* z0, float* M_out
     c.check_err();
 }
 
+// [M | z? | log D]: log D is a scalar, or a d_k vector for TokenVector kinds
+static int payload_lw(const lmoe_lsm_desc* d, int D) {
+    return device_decay_mode(d->instance) == lmoe_dev::kDecayTokenVector ? D : 1;
+}
 static size_t payload_floats(const lmoe_lsm_desc* d, int D) {
-    return (size_t)D * D + (d->use_normalizer ? D : 0) + 1;
+    return (size_t)D * D + (d->use_normalizer ? D : 0) + payload_lw(d, D);
 }
 
 struct SpWorkspace {
@@ -278,7 +308,7 @@ static void sp_phase_a(LsmCall& c, float* payload) {
     const int P = (int)payload_floats(c.d, c.D);
     c.state_pass<T>();
     c.combine(nullptr, nullptr, false, payload, c.norm ? payload + c.D * c.D : nullptr,
-              payload + P - 1, P);
+              payload + P - c.lw, P);
 }
 // Phase B (parallel.hpp:340-373): decayed exclusive prefix over ranks < rank, then the
 // output pass with the carried-in state.
@@ -290,7 +320,7 @@ static void sp_phase_b(LsmCall& c, const float* gathered, int rank, float* M0, f
     c.mark();
     LMOE_CUDA_CHECK(lmoe_dev::launch_rank_combine(dim3((nel + 255) / 256, c.B * c.H), c.st,
                                                   gathered, P, c.B * c.H, rank, c.D, c.D,
-                                                  c.norm ? 1 : 0, M0, z0));
+                                                  c.norm ? 1 : 0, c.lw, M0, z0));
     ++g_launch_count;
     c.combine(M0, c.norm ? z0 : nullptr, true, M_out, z_out, nullptr, 0);
     c.output_pass<T>();
@@ -347,10 +377,9 @@ extern "C" int lmoe_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
                             lmoe_stream_t stream) {
     return guarded([&]() {
         validate(desc, B, N, H, D, dtype, q, k, v, o);
-        (void)a_pre;
         LsmCall c{desc, B, N, N, H, D, dtype, q, k, v, b_pre, a_raw, o,
                   static_cast<uint8_t*>(workspace), plan_lsm(B, N, H, D),
-                  reinterpret_cast<cudaStream_t>(stream)};
+                  reinterpret_cast<cudaStream_t>(stream), a_pre};
         if (!workspace || workspace_bytes < c.pl.total)
             throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd: workspace too small (need " +
                                           std::to_string(c.pl.total) + " bytes)");
@@ -416,7 +445,7 @@ extern "C" int lmoe_sp_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N_local, in
                                           std::to_string(w.total) + " bytes)");
         uint8_t* ws = static_cast<uint8_t*>(workspace);
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-        LsmCall c{desc, B, N_local, N_local, H, D, dtype, q, k, v, b_pre, a_raw, o, ws, w.pl, st};
+        LsmCall c{desc, B, N_local, N_local, H, D, dtype, q, k, v, b_pre, a_raw, o, ws, w.pl, st, a_pre};
         c.setup();
         c.clear_err();
         float* payload = reinterpret_cast<float*>(ws + w.off_payload);
@@ -477,7 +506,8 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
             LsmCall c{desc, B, len, N, H, D, dtype,
                       static_cast<const uint8_t*>(q) + off, static_cast<const uint8_t*>(k) + off,
                       static_cast<const uint8_t*>(v) + off, b_pre ? b_pre + (size_t)r0 * H : nullptr,
-                      a_raw, static_cast<uint8_t*>(o) + off, ws, plan_lsm(B, len, H, D), st};
+                      a_raw, static_cast<uint8_t*>(o) + off, ws, plan_lsm(B, len, H, D), st,
+                      a_pre ? static_cast<const uint8_t*>(a_pre) + off : nullptr};
             c.setup();
             return c;
         };

@@ -12,6 +12,7 @@ struct LsmVariant {
     int decay;  // DecayMode
     int fm;     // 0 identity, 1 elu+1, 2 squared
     int norm;   // normaliser
+    int hgrn2;  // TokenVector with keff = 1 - a (HGRN2)
 };
 
 cudaError_t launch_state_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
@@ -31,7 +32,18 @@ namespace lmoe_dev {
 cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const float* zS,
                                const float* logD, const float* M0, const float* z0, float* Min,
                                float* zin, float* Mfin, float* zfin, float* logDtot, int fin_stride,
-                               int nseg, int dk, int dv, int norm, int* err);
+                               int nseg, int dk, int dv, int norm, int lw, int* err);
 cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,
-                                int rank, int dk, int dv, int norm, float* M0, float* z0);
+                                int rank, int dk, int dv, int norm, int lw, float* M0, float* z0);
+// TokenVector decays (GLA / HGRN2 / RWKV6): variant {decay = 3, fm, norm, hgrn2 in bit 8 of fm}
+cudaError_t launch_state_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
+                                       const CUtensorMap& val, const CUtensorMap& a, const LsmFwdParams& p);
+cudaError_t launch_output_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
+                                        const CUtensorMap& k, const CUtensorMap& val, const CUtensorMap& a,
+                                        const LsmFwdParams& p);
+cudaError_t launch_state_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
+                                      const CUtensorMap& val, const CUtensorMap& a, const LsmFwdParams& p);
+cudaError_t launch_output_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
+                                       const CUtensorMap& k, const CUtensorMap& val, const CUtensorMap& a,
+                                       const LsmFwdParams& p);
 }  // namespace lmoe_dev

@@ -1,0 +1,594 @@
+// lsm_vec_kernels.cuh -- TokenVector decays (GLA, HGRN2, RWKV6; lsm.hpp:64-85) on sm_100a.
+//
+// Decay per (token t, key column k): a_tk = sigmoid(a_pre[t, k]) (decay_vector_rows,
+// lsm.hpp:504-518); effective key phi(k) for GLA/RWKV6, 1 - a for HGRN2 (lsm.hpp:483-501).
+// Per chunk, G[t][k] = inclusive log-space cumsum of log a down each column (column-slab
+// scans by the math warps), and the pairwise factor e^{G_ik - G_jk} is folded into the
+// operands around a per-column midpoint reference r_k = G[63][k]:
+//     q~ = phi(q) e^{G - r},  k~ = keff e^{r - G}          (both finite while each
+//                                                           half-chunk column span < 80)
+//     S  = (q~ k~^T) . [j <= i]                             (no per-element factors)
+//     O  = P V + q~ (diag(e^r) M)                           (operand M' = diag(e^r) M)
+//     M' += k~^T V ;  M_next = diag(e^{G_end - r}) M'       (state resident in TMEM)
+// The state pass visits chunks last-to-first with one backward pass per column:
+//     w_jk = e^{L_jk} keff_jk,  L_jk = sum of log a over tokens after j up to the segment end.
+// A chunk whose half-chunk span exceeds the bound raises "non-finite output in div" -- the
+// reference's own message for its K/p form (lsm.hpp:576-577) in the same regime.
+#pragma once
+#include "lsm_kernels.cuh"
+
+namespace lmoe_dev {
+
+__device__ __forceinline__ float log_sigmoid(float x) { return -softplus_f(-x); }
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
+
+// element (row, col) of a [128 x 256 B] SW128 tile (two 128-B column blocks)
+template <typename T>
+__device__ __forceinline__ T* tile_elem(uint8_t* tile, int row, int col) {
+    using TT = TileTraits<T>;
+    const int blk = col / TT::EPB, cin = col % TT::EPB;
+    return reinterpret_cast<T*>(tile + blk * kBlockBytes + sw128_off(row, cin / TT::EPC) +
+                                (cin % TT::EPC) * sizeof(T));
+}
+template <typename T>
+__device__ __forceinline__ float ld_elem(uint8_t* tile, int row, int col) {
+    if constexpr (sizeof(T) == 2) return __bfloat162float(*tile_elem<T>(tile, row, col));
+    else return *tile_elem<T>(tile, row, col);
+}
+template <typename T>
+__device__ __forceinline__ void st_elem(uint8_t* tile, int row, int col, float v) {
+    if constexpr (sizeof(T) == 2) *tile_elem<T>(tile, row, col) = __float2bfloat16_rn(v);
+    else *tile_elem<T>(tile, row, col) = tf32r(v);
+}
+// fp32 transposed K-major tile [64 d rows x 128 tok]
+__device__ __forceinline__ float* tr_elem(uint8_t* tileT, int d, int tok) {
+    return reinterpret_cast<float*>(tileT + (tok >> 5) * 8192 + sw128_off(d, (tok & 31) >> 2) + ((tok & 3) << 2));
+}
+
+// ====================================================================================
+// Phase 1 (vector decay): warps 0 TMA, 1 MMA, 2-3 idle, 4-7 transform (thread = column)
+// ====================================================================================
+template <typename T, int FM, bool NORM, bool HG>
+__global__ void __launch_bounds__(kStatePassThreads, 1)
+    lsm_state_pass_vec(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                       const __grid_constant__ CUtensorMap tmA, LsmFwdParams p) {
+    using TT = TileTraits<T>;
+    constexpr int D = TT::D;
+    constexpr bool TR = TT::kTransposed;
+    constexpr int NST = TR ? 1 : 2;
+    constexpr int STAGE = 3 * kTileBytes;  // K | V | A
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if (smem_u32(smem) & 1023) __trap();
+    uint8_t* tiles = smem;
+    uint8_t* kT = tiles + NST * STAGE;
+    uint8_t* vT = kT + (TR ? kTileBytes : 0);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(vT + (TR ? kTileBytes : 0));
+    uint64_t* full = bars;          // [NST]
+    uint64_t* empty = bars + 2;     // [NST]
+    uint64_t* xf = bars + 4;
+    uint64_t* acc_full = bars + 5;
+    uint64_t* kt_free = bars + 6;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 7);
+
+    const int seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int bh = b * p.H + h;
+    const int t_begin = seg * p.seg_len;
+    const int t_end = min(p.N, t_begin + p.seg_len);
+    const int nchunks = (t_end - t_begin + kC - 1) / kC;
+    const int warp = warp_id(), lane = lane_id();
+    auto chunk_t0 = [&](int it) { return t_begin + (nchunks - 1 - it) * kC; };
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        mbar_init(xf, 128);
+        mbar_init(acc_full, 1);
+        mbar_init(kt_free, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<128>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmA);
+            for (int it = 0; it < nchunks; ++it) {
+                const int s = it % NST;
+                if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                const int t0 = chunk_t0(it);
+                uint8_t* st = tiles + s * STAGE;
+                mbar_expect_tx(&full[s], STAGE);
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) {
+                    tma_load_4d(st + blk * kBlockBytes, &tmK, &full[s], blk * TT::EPB, h, t0, b);
+                    tma_load_4d(st + kTileBytes + blk * kBlockBytes, &tmV, &full[s], blk * TT::EPB, h, t0, b);
+                    tma_load_4d(st + 2 * kTileBytes + blk * kBlockBytes, &tmA, &full[s], blk * TT::EPB, h, t0, b);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            for (int it = 0; it < nchunks; ++it) {
+                const int s = it % NST;
+                mbar_wait(&full[s], (it / NST) & 1);
+                mbar_wait(xf, it & 1);
+                tc_fence_after();
+                const uint32_t kt = smem_u32(tiles + s * STAGE);
+                const uint32_t vt = kt + kTileBytes;
+                if constexpr (!TR) {
+                    constexpr uint32_t idesc = umma_idesc(TT::FMT, 1, 1, 128, D);
+#pragma unroll
+                    for (int kk = 0; kk < kC / TT::KSTEP; ++kk)
+                        mma_ss_f16(tmem, umma_desc_sw128(kt + kk * TT::KSTEP * 128, kBlockBytes, 1024),
+                                   umma_desc_sw128(vt + kk * TT::KSTEP * 128, kBlockBytes, 1024), idesc,
+                                   (it > 0 || kk > 0) ? 1u : 0u);
+                } else {
+                    constexpr uint32_t idesc = umma_idesc(TT::FMT, 0, 0, 64, D);
+                    const uint32_t ka = smem_u32(kT), va = smem_u32(vT);
+#pragma unroll
+                    for (int kk = 0; kk < kC / TT::KSTEP; ++kk) {
+                        const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
+                        mma_ss_tf32(tmem, umma_desc_sw128(ka + off, 16, 1024), umma_desc_sw128(va + off, 16, 1024),
+                                    idesc, (it > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    mma_commit(kt_free);
+                }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(acc_full);
+        }
+    } else if (warp >= 4) {
+        const int tid = threadIdx.x - 128;  // column k (tid < D)
+        const int q = warp & 3;
+        float suffix = 0.f, zacc = 0.f;
+        for (int it = 0; it < nchunks; ++it) {
+            const int s = it % NST;
+            uint8_t* kt = tiles + s * STAGE;
+            uint8_t* vt = kt + kTileBytes;
+            uint8_t* at = kt + 2 * kTileBytes;
+            const int nvalid = min(kC, t_end - chunk_t0(it));
+            mbar_wait(&full[s], (it / NST) & 1);
+            if (TR && it >= 1) mbar_wait(kt_free, (it - 1) & 1);
+            if (tid < D) {
+                float L = suffix;  // log decay from the current row (exclusive) to segment end
+                for (int i = kC - 1; i >= 0; --i) {
+                    const bool valid = i < nvalid;
+                    const float a = ld_elem<T>(at, i, tid);
+                    float keff = 0.f;
+                    if (valid) keff = HG ? sigmoid_f(-a) : fmap_t<FM>(ld_elem<T>(kt, i, tid));
+                    const float kw = keff * __expf(L);
+                    if constexpr (!TR) st_elem<T>(kt, i, tid, kw);
+                    else {
+                        *tr_elem(kT, tid, i) = tf32r(kw);
+                        *tr_elem(vT, tid, i) = tf32r(ld_elem<T>(vt, i, tid));
+                    }
+                    if constexpr (NORM) zacc += kw;
+                    if (valid) L += log_sigmoid(a);
+                }
+                suffix = L;
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(xf);
+        }
+        mbar_wait(acc_full, 0);
+        tc_fence_after();
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const int row = TR ? q * 16 + lane : q * 32 + lane;
+        const bool own = TR ? lane < 16 : true;
+        float* dst = p.Sseg + (((size_t)bh * p.nseg + seg) * D + (own ? row : 0)) * D;
+#pragma unroll
+        for (int cb = 0; cb < D / 32; ++cb) {
+            uint32_t r[32];
+            tmem_ld32(tmem + lane_off + cb * 32, r);
+            tmem_wait_ld();
+            if (own) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(dst + cb * 32 + j) =
+                        make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                    __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+            }
+        }
+        if (tid < D) {
+            p.logDseg[((size_t)bh * p.nseg + seg) * D + tid] = suffix;
+            if constexpr (NORM) p.zseg[((size_t)bh * p.nseg + seg) * D + tid] = zacc;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<128>(tmem);
+}
+
+// ====================================================================================
+// Phase 3 (vector decay): warps 0 TMA, 1 MMA, 2-3 idle, 4-11 math (256 threads)
+// TMEM: S [0,128), O [128,256), M [256,384) (tf32: O [128,192), M [192,256) M=64 layout);
+// row partials (normaliser) in S columns 64.. (bf16) / [384,388) (tf32).
+// ====================================================================================
+template <typename T, int FM, bool NORM, bool HG>
+__global__ void __launch_bounds__(kOutputPassThreads, 1)
+    lsm_output_pass_vec(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmA,
+                        LsmFwdParams p) {
+    using TT = TileTraits<T>;
+    constexpr int D = TT::D;
+    constexpr bool kBF16 = sizeof(T) == 2;
+    constexpr bool TR = TT::kTransposed;
+    constexpr int DH = D / 2;
+    constexpr int NSLAB = kMathThreads / D;  // column slabs: 2 (bf16) / 4 (fp32)
+    constexpr int ROWS = kC / NSLAB;          // rows per slab
+    constexpr int STAGE = 4 * kTileBytes;     // Q | K | V | A
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if (smem_u32(smem) & 1023) __trap();
+    uint8_t* qt = smem;
+    uint8_t* kt = qt + kTileBytes;
+    uint8_t* vt = qt + 2 * kTileBytes;
+    uint8_t* at = qt + 3 * kTileBytes;
+    uint8_t* kT = qt + STAGE;
+    uint8_t* vT = kT + (TR ? kTileBytes : 0);
+    uint8_t* mop = vT + (TR ? kTileBytes : 0);
+    float* sTot = reinterpret_cast<float*>(mop + TT::MOP_BYTES);  // [NSLAB][D]
+    float* sR = sTot + NSLAB * D;                                   // [D]
+    float* sGe = sR + D;                                            // [D]
+    float* sZ = sGe + D;                                            // [D]
+    float* sZP = sZ + D;                                            // [D]  e^r z
+    float* sZC = sZP + D;                                           // [NSLAB][D]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sZC + NSLAB * D);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + 1;
+    uint64_t* xf = bars + 2;
+    uint64_t* s_full = bars + 3;
+    uint64_t* p_full = bars + 4;
+    uint64_t* mo_full = bars + 5;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 6);
+
+    const int seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int bh = b * p.H + h;
+    const int t_begin = seg * p.seg_len;
+    const int t_end = min(p.N, t_begin + p.seg_len);
+    const int nchunks = (t_end - t_begin + kC - 1) / kC;
+    const int warp = warp_id(), lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        mbar_init(full, 1);
+        mbar_init(empty, 1);
+        mbar_init(xf, kMathThreads);
+        mbar_init(s_full, 1);
+        mbar_init(p_full, kMathThreads);
+        mbar_init(mo_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+    const uint32_t tS = tmem, tO = tmem + 128, tM = tmem + (kBF16 ? 256 : 192);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmA);
+            for (int c = 0; c < nchunks; ++c) {
+                if (c >= 1) mbar_wait(empty, (c - 1) & 1);
+                const int t0 = t_begin + c * kC;
+                mbar_expect_tx(full, STAGE);
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) {
+                    tma_load_4d(qt + blk * kBlockBytes, &tmQ, full, blk * TT::EPB, h, t0, b);
+                    tma_load_4d(kt + blk * kBlockBytes, &tmK, full, blk * TT::EPB, h, t0, b);
+                    tma_load_4d(vt + blk * kBlockBytes, &tmV, full, blk * TT::EPB, h, t0, b);
+                    tma_load_4d(at + blk * kBlockBytes, &tmA, full, blk * TT::EPB, h, t0, b);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idS = umma_idesc(TT::FMT, 0, 0, 128, 128);
+            constexpr uint32_t idPV = umma_idesc(TT::FMT, 0, TR ? 0 : 1, 128, D);
+            constexpr uint32_t idQM = umma_idesc(TT::FMT, 0, TR ? 0 : 1, 128, D);
+            constexpr uint32_t idDM = TR ? umma_idesc(TT::FMT, 0, 0, 64, D) : umma_idesc(TT::FMT, 1, 1, 128, D);
+            const uint32_t qa = smem_u32(qt), ka = smem_u32(kt), va = smem_u32(vt);
+            const uint32_t mb = smem_u32(mop), kTa = smem_u32(kT), vTa = smem_u32(vT);
+            for (int c = 0; c < nchunks; ++c) {
+                mbar_wait(full, c & 1);
+                mbar_wait(xf, c & 1);
+                tc_fence_after();
+                // S = q~ k~^T ; O = q~ M' ; M' += k~^T V
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kBlockBytes + (kk & 3) * 32;
+                    const uint64_t a = umma_desc_sw128(qa + off, 16, 1024);
+                    if constexpr (kBF16) mma_ss_f16(tS, a, umma_desc_sw128(ka + off, 16, 1024), idS, kk > 0);
+                    else mma_ss_tf32(tS, a, umma_desc_sw128(ka + off, 16, 1024), idS, kk > 0);
+                }
+                mma_commit(s_full);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kBlockBytes + (kk & 3) * 32;
+                    const uint64_t a = umma_desc_sw128(qa + off, 16, 1024);
+                    if constexpr (!TR) mma_ss_f16(tO, a, umma_desc_sw128(mb + kk * TT::KSTEP * 128, D * 128, 1024), idQM, kk > 0);
+                    else mma_ss_tf32(tO, a, umma_desc_sw128(mb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idQM, kk > 0);
+                }
+#pragma unroll
+                for (int kk = 0; kk < kC / TT::KSTEP; ++kk) {
+                    if constexpr (!TR) {
+                        mma_ss_f16(tM, umma_desc_sw128(ka + kk * TT::KSTEP * 128, kBlockBytes, 1024),
+                                   umma_desc_sw128(va + kk * TT::KSTEP * 128, kBlockBytes, 1024), idDM, 1u);
+                    } else {
+                        const uint32_t off = (kk >> 2) * 8192 + (kk & 3) * 32;
+                        mma_ss_tf32(tM, umma_desc_sw128(kTa + off, 16, 1024), umma_desc_sw128(vTa + off, 16, 1024), idDM, 1u);
+                    }
+                }
+                mbar_wait(p_full, c & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < kC / TT::KSTEP; ++kk) {
+                    if constexpr (!TR)
+                        mma_ts_f16(tO, tS + kk * 8, umma_desc_sw128(va + kk * TT::KSTEP * 128, kBlockBytes, 1024), idPV, 1u);
+                    else
+                        mma_ts_tf32(tO, tS + kk * 8, umma_desc_sw128(vTa + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), idPV, 1u);
+                }
+                mma_commit(mo_full);
+                mma_commit(empty);
+            }
+        }
+    } else if (warp >= 4) {
+        const int tid = threadIdx.x - 128;  // 0..255
+        const int mw = warp - 4;
+        const int q = warp & 3, hh = mw >> 2;
+        const int row = q * 32 + lane;     // row mapping (S / O / P epilogues)
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const int srow = TR ? q * 16 + lane : row;  // state row (d_k index)
+        const bool sown = TR ? lane < 16 : true;
+        const int col = tid % D, slab = tid / D;    // column-slab mapping (scans, transforms)
+        T* const obase = reinterpret_cast<T*>(p.o);
+
+        // initial state: M_T <- M_in (fp32), z <- z_in
+        {
+            const float* src = p.Min + (((size_t)bh * p.nseg + seg) * D + (sown ? srow : 0)) * D + hh * DH;
+#pragma unroll
+            for (int cb = 0; cb < DH / 32; ++cb) {
+                uint32_t r[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(sown ? src[cb * 32 + j] : 0.f);
+                tmem_st32(tM + lane_off + hh * DH + cb * 32, r);
+            }
+            tmem_wait_st();
+            if constexpr (NORM) {
+                if (tid < D) sZ[tid] = p.zin[((size_t)bh * p.nseg + seg) * D + tid];
+            }
+        }
+        for (int c = 0; c < nchunks; ++c) {
+            const int t0 = t_begin + c * kC;
+            const int nvalid = min(kC, t_end - t0);
+            mbar_wait(full, c & 1);
+            // (1) column scans: G down each column of this slab's rows
+            float G[ROWS];
+            {
+                float run = 0.f;
+#pragma unroll
+                for (int ii = 0; ii < ROWS; ++ii) {
+                    const int i = slab * ROWS + ii;
+                    run += (i < nvalid) ? log_sigmoid(ld_elem<T>(at, i, col)) : 0.f;
+                    G[ii] = run;
+                }
+                sTot[slab * D + col] = run;
+            }
+            named_bar_sync(1, kMathThreads);
+            float off = 0.f, r = 0.f, ge = 0.f;
+#pragma unroll
+            for (int s2 = 0; s2 < NSLAB; ++s2) {
+                const float tv = sTot[s2 * D + col];
+                if (s2 < slab) off += tv;
+                if (s2 * ROWS <= 63) r += tv;  // inclusive G at row 63
+                ge += tv;
+            }
+            const float g0 = (slab == 0) ? G[0] : 0.f;
+            if (slab == 0) {
+                sR[col] = r;
+                sGe[col] = ge;
+                if (!((g0 - r) < -kSafeLogDecay && (r - ge) < -kSafeLogDecay)) atomicOr(&p.err[2], 1);
+            }
+            // (2) q~ = phi(q) e^{G - r}, k~ = keff e^{r - G} in place (tf32: also K~^T, V^T)
+            float zc = 0.f;
+#pragma unroll
+            for (int ii = 0; ii < ROWS; ++ii) {
+                const int i = slab * ROWS + ii;
+                const bool valid = i < nvalid;
+                const float e = __expf(G[ii] + off - r);
+                const float qv = valid ? fmap_t<FM>(ld_elem<T>(qt, i, col)) * e : 0.f;
+                float keff = 0.f;
+                if (valid) keff = HG ? sigmoid_f(-ld_elem<T>(at, i, col)) : fmap_t<FM>(ld_elem<T>(kt, i, col));
+                const float kv = valid ? keff / e : 0.f;
+                st_elem<T>(qt, i, col, qv);
+                st_elem<T>(kt, i, col, kv);
+                if constexpr (TR) {
+                    *tr_elem(kT, col, i) = tf32r(kv);
+                    *tr_elem(vT, col, i) = tf32r(ld_elem<T>(vt, i, col));
+                }
+                if constexpr (NORM) zc += kv;
+            }
+            if constexpr (NORM) sZC[slab * D + col] = zc;
+            named_bar_sync(1, kMathThreads);
+            // (3) state operand M' = diag(e^r) M  (and the TMEM copy), z' = e^r z
+            {
+                const float er = __expf(sR[srow < D ? srow : 0]);
+                float vals[DH];
+#pragma unroll
+                for (int cb = 0; cb < DH / 32; ++cb) {
+                    uint32_t rr[32];
+                    tmem_ld32(tM + lane_off + hh * DH + cb * 32, rr);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        vals[cb * 32 + j] = __uint_as_float(rr[j]) * er;
+                        rr[j] = __float_as_uint(vals[cb * 32 + j]);
+                    }
+                    tmem_st32(tM + lane_off + hh * DH + cb * 32, rr);
+                }
+                if (sown) {
+                    if constexpr (!TR) {
+                        uint8_t* dst = mop + hh * (D * 128);
+#pragma unroll
+                        for (int ch = 0; ch < 8; ++ch) {
+                            uint4 v;
+                            v.x = pack_bf16(vals[ch * 8 + 0], vals[ch * 8 + 1]);
+                            v.y = pack_bf16(vals[ch * 8 + 2], vals[ch * 8 + 3]);
+                            v.z = pack_bf16(vals[ch * 8 + 4], vals[ch * 8 + 5]);
+                            v.w = pack_bf16(vals[ch * 8 + 6], vals[ch * 8 + 7]);
+                            *reinterpret_cast<uint4*>(dst + sw128_off(srow, ch)) = v;
+                        }
+                    } else {
+                        uint8_t* base = mop + (srow >> 5) * 8192 + ((srow & 3) << 2);
+                        const int cch = (srow & 31) >> 2;
+#pragma unroll
+                        for (int j = 0; j < DH; ++j)
+                            *reinterpret_cast<float*>(base + sw128_off(hh * DH + j, cch)) = tf32r(vals[j]);
+                    }
+                }
+                if constexpr (NORM) {
+                    if (tid < D) sZP[tid] = __expf(sR[tid]) * sZ[tid];
+                }
+                tmem_wait_st();
+                fence_proxy_async_smem();
+                tc_fence_before();
+                if constexpr (NORM) named_bar_sync(1, kMathThreads);
+                mbar_arrive(xf);
+            }
+            // (4) P = S . mask  (+ row sums, q~ . z' for the normaliser)
+            mbar_wait(s_full, c & 1);
+            tc_fence_after();
+            {
+                uint32_t r0[32], r1[32];
+                tmem_ld32(tS + lane_off + hh * 64, r0);
+                tmem_ld32(tS + lane_off + hh * 64 + 32, r1);
+                tmem_wait_ld();
+                float rs = 0.f;
+#pragma unroll
+                for (int j = 0; j < 64; ++j) {
+                    const int cc = hh * 64 + j;
+                    float v = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
+                    v = (cc <= row) ? v : 0.f;
+                    if constexpr (TR) v = tf32r(v);
+                    rs += v;
+                    if (j < 32) r0[j] = __float_as_uint(v); else r1[j - 32] = __float_as_uint(v);
+                }
+                float qz = 0.f;
+                if constexpr (NORM) {
+#pragma unroll 8
+                    for (int j = 0; j < DH; ++j) qz += ld_elem<T>(qt, row, hh * DH + j) * sZP[hh * DH + j];
+                }
+                const uint32_t tpart = kBF16 ? tS + lane_off + 64 : tmem + 384 + lane_off;
+                if constexpr (kBF16) {
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        pk[j] = pack_bf16(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
+                        pk[16 + j] = pack_bf16(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]));
+                    }
+                    named_bar_sync(1, kMathThreads);
+                    tmem_st32(tS + lane_off + hh * 32, pk);
+                } else {
+                    tmem_st32(tS + lane_off + hh * 64, r0);
+                    tmem_st32(tS + lane_off + hh * 64 + 32, r1);
+                }
+                if constexpr (NORM) {
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart + hh),
+                                 "r"(__float_as_uint(rs)) : "memory");
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart + 2 + hh),
+                                 "r"(__float_as_uint(qz)) : "memory");
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(p_full);
+            }
+            // (5) state: M_next = diag(e^{G_end - r}) M'
+            mbar_wait(mo_full, c & 1);
+            tc_fence_after();
+            {
+                const int kr = srow < D ? srow : 0;
+                const float f = __expf(sGe[kr] - sR[kr]);
+#pragma unroll
+                for (int cb = 0; cb < DH / 32; ++cb) {
+                    uint32_t rr[32];
+                    tmem_ld32(tM + lane_off + hh * DH + cb * 32, rr);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) rr[j] = __float_as_uint(__uint_as_float(rr[j]) * f);
+                    tmem_st32(tM + lane_off + hh * DH + cb * 32, rr);
+                }
+                tmem_wait_st();
+                if constexpr (NORM) {
+                    if (tid < D) {
+                        float zs = 0.f;
+#pragma unroll
+                        for (int s2 = 0; s2 < NSLAB; ++s2) zs += sZC[s2 * D + tid];
+                        sZ[tid] = __expf(sGe[tid] - sR[tid]) * (sZP[tid] + zs);
+                    }
+                }
+            }
+            // (6) O epilogue -> global
+            {
+                float inv = 1.f;
+                if constexpr (NORM) {
+                    const uint32_t tpart = kBF16 ? tS + lane_off + 64 : tmem + 384 + lane_off;
+                    uint32_t pr[4];
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(pr[0]), "=r"(pr[1]), "=r"(pr[2]), "=r"(pr[3]) : "r"(tpart));
+                    tmem_wait_ld();
+                    const float den = __uint_as_float(pr[0]) + __uint_as_float(pr[1]) +
+                                      __uint_as_float(pr[2]) + __uint_as_float(pr[3]);
+                    if (fabsf(den) < 1e-12f && row < nvalid) atomicOr(&p.err[0], 1);
+                    inv = 1.f / den;
+                }
+                const bool vrow = row < nvalid;
+                T* dst = obase + (((size_t)b * p.Nstride + t0 + (vrow ? row : 0)) * p.H + h) * D + hh * DH;
+#pragma unroll
+                for (int cb = 0; cb < DH / 32; ++cb) {
+                    uint32_t rr[32];
+                    tmem_ld32(tO + lane_off + hh * DH + cb * 32, rr);
+                    tmem_wait_ld();
+                    if (vrow) {
+                        if constexpr (kBF16) {
+#pragma unroll
+                            for (int ch = 0; ch < 4; ++ch) {
+                                uint4 v;
+                                v.x = pack_bf16(__uint_as_float(rr[ch * 8 + 0]) * inv, __uint_as_float(rr[ch * 8 + 1]) * inv);
+                                v.y = pack_bf16(__uint_as_float(rr[ch * 8 + 2]) * inv, __uint_as_float(rr[ch * 8 + 3]) * inv);
+                                v.z = pack_bf16(__uint_as_float(rr[ch * 8 + 4]) * inv, __uint_as_float(rr[ch * 8 + 5]) * inv);
+                                v.w = pack_bf16(__uint_as_float(rr[ch * 8 + 6]) * inv, __uint_as_float(rr[ch * 8 + 7]) * inv);
+                                *reinterpret_cast<uint4*>(dst + cb * 32 + ch * 8) = v;
+                            }
+                        } else {
+#pragma unroll
+                            for (int ch = 0; ch < 8; ++ch)
+                                *reinterpret_cast<float4*>(dst + cb * 32 + ch * 4) =
+                                    make_float4(__uint_as_float(rr[ch * 4]) * inv, __uint_as_float(rr[ch * 4 + 1]) * inv,
+                                                __uint_as_float(rr[ch * 4 + 2]) * inv, __uint_as_float(rr[ch * 4 + 3]) * inv);
+                        }
+                    }
+                }
+                tc_fence_before();
+            }
+            named_bar_sync(1, kMathThreads);  // everyone done with this chunk's tiles and sZ
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+template <typename T>
+constexpr int output_pass_vec_smem() {
+    using TT = TileTraits<T>;
+    // + sTot, sR, sGe, sZ, sZP, sZC (8 x 128 floats) + 6 barriers + TMEM slot
+    return 4 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + TT::MOP_BYTES + 4096 + 128;
+}
+template <typename T>
+constexpr int state_pass_vec_smem() {
+    using TT = TileTraits<T>;
+    return (TT::kTransposed ? 1 : 2) * 3 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + 1024;
+}
+
+}  // namespace lmoe_dev

@@ -17,7 +17,7 @@ from conftest import load_golden, norm_rel_err
 pytestmark = pytest.mark.gpu
 
 TOL = {"f32": 1e-3, "bf16": 2e-2}
-DEVICE_INSTANCES = {0, 1, 2, 6, 13}  # BLA, Lightning, RetNet, Rebased, Mamba2
+DEVICE_INSTANCES = {0, 1, 2, 3, 6, 13, 14, 15}  # every separable kind (DecayKind None/Const/Token*)
 
 
 def _torch():
@@ -27,7 +27,7 @@ def _torch():
     return torch
 
 
-def _run(spec_d, q, k, v, b_pre=None, dtype="bf16", chunk=64, final=False):
+def _run(spec_d, q, k, v, b_pre=None, dtype="bf16", chunk=64, final=False, a_pre=None):
     """q,k,v numpy [B,N,H,D]; returns numpy o (f64) [+ final state]."""
     torch = _torch()
     import paper_2503_05447_b200 as pk
@@ -42,6 +42,8 @@ def _run(spec_d, q, k, v, b_pre=None, dtype="bf16", chunk=64, final=False):
     gates = None
     if b_pre is not None:
         gates = pk.LsmGates(b_pre=torch.tensor(np.ascontiguousarray(b_pre), dtype=torch.float32, device=dev))
+    if a_pre is not None:
+        gates = pk.LsmGates(a_pre=torch.tensor(np.ascontiguousarray(a_pre), dtype=torch.float32, device=dev).to(tdt))
     fs = pk.MemoryState() if final else None
     o = pk.lsm_forward_batched(Q, K, V, gates, spec, chunk, final_state=fs)
     torch.cuda.synchronize()
@@ -70,15 +72,17 @@ def test_golden_device_cases():
         dtype = "f32" if dd == 64 else "bf16"
         spec["mamba2_a_raw_h"] = [spec["mamba2_a_raw"]]
         b_pre = d.get(p + "/b_pre")
+        a_pre = d.get(p + "/a_pre")
         o, M, z = _run(spec, q[None, :, None], k[None, :, None], v[None, :, None],
                        None if b_pre is None else b_pre[None, :, None].astype(np.float64),
-                       dtype=dtype, chunk=int(d[p + "/chunk"][0]), final=True)
+                       dtype=dtype, chunk=int(d[p + "/chunk"][0]), final=True,
+                       a_pre=None if a_pre is None else a_pre[None, :, None].astype(np.float64))
         err = norm_rel_err(o[0, :, 0], d[p + "/o"])
         assert err < TOL[dtype], (p, err)
         errM = norm_rel_err(M[0, 0], d[p + "/M"])
         assert errM < TOL[dtype], (p, "M", errM)
         ran += 1
-    assert ran >= 6
+    assert ran >= 12
 
 
 @pytest.mark.parametrize("inst,fm,norm,dtype,N,H", [
@@ -91,6 +95,11 @@ def test_golden_device_cases():
     ("retnet", 0, 0, "f32", 515, 2),
     ("mamba2", 0, 0, "bf16", 1300, 2),
     ("mamba2", 0, 0, "f32", 640, 2),
+    ("gla", 0, 0, "bf16", 1000, 2),
+    ("gla", 0, 0, "f32", 600, 2),
+    ("gla", 1, 1, "bf16", 700, 2),
+    ("hgrn2", 0, 0, "bf16", 900, 2),
+    ("rwkv6", 0, 0, "f32", 515, 2),
 ])
 def test_random_vs_oracle(inst, fm, norm, dtype, N, H):
     rng = np.random.default_rng(zlib.crc32(repr((inst, fm, norm, dtype, N)).encode()))
@@ -107,10 +116,15 @@ def test_random_vs_oracle(inst, fm, norm, dtype, N, H):
         b_pre = rng.normal(-1.0, 1.0, (B, N, H)).astype(np.float32).astype(np.float64)
         a_raw = a_raw.astype(np.float32).astype(np.float64)
     spec["mamba2_a_raw_h"] = a_raw
-    o, M, z = _run(spec, q, k, v, b_pre, dtype=dtype, final=True)
+    a_pre = None
+    if inst in ("gla", "hgrn2", "rwkv6"):  # reference default gates N(0,1) (lsm.hpp:222-253)
+        a_pre = rng.normal(0, 1, (B, N, H, D))
+        a_pre = _bf16_round(a_pre) if dtype == "bf16" else a_pre.astype(np.float32).astype(np.float64)
+    o, M, z = _run(spec, q, k, v, b_pre, dtype=dtype, final=True, a_pre=a_pre)
     for h in range(H):
         sh = dict(spec, mamba2_a_raw=float(a_raw[h]))
         want, Mw, zw = oracle.lsm_chunked(sh, q[0, :, h], k[0, :, h], v[0, :, h],
+                                          a_pre=None if a_pre is None else a_pre[0, :, h],
                                           b_pre=None if b_pre is None else b_pre[0, :, h], chunk=64)
         err = norm_rel_err(o[0, :, h], want)
         assert err < TOL[dtype], (inst, h, err)
