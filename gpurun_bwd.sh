@@ -1,0 +1,4 @@
+#!/bin/bash
+python -c "from paper_2503_05447_b200 import _build; _build.build()" || exit 1
+timeout 600 python -m pytest tests/test_lsm_bwd_gpu.py -q 2>&1 | grep -E "Error|assert|passed|failed" | head -40
+timeout 600 python -m pytest tests/test_lsm_gpu.py -x -q 2>&1 | tail -3

@@ -87,6 +87,27 @@ int lmoe_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dty
                  void* o, float* M_out, float* z_out, void* workspace, size_t workspace_bytes,
                  lmoe_stream_t stream);
 
+/* ---------------------------------------------------------------------------------------
+ * LSM backward: the vector-Jacobian product the reference's tape computes through
+ * lsm_forward_chunked (tensor.hpp:1178-1215; ops of lsm.hpp:483-598), for every (b, h).
+ * Inputs as lmoe_lsm_fwd plus dO [B,N,H,D] and the optional final-state gradient dM_final
+ * [B,H,D,D] fp32 (NULL = 0).  Outputs (device, caller-owned):
+ *   dq, dk, dv : [B,N,H,D] dtype
+ *   db_pre     : [B,N,H] fp32 (Mamba2), da_raw : [H] fp32 (Mamba2, summed over batch)
+ *   da_pre     : [B,N,H,D] dtype (TokenVector kinds)
+ *   dM0        : [B,H,D,D] fp32 gradient of the initial state (may be NULL)
+ * No recomputation of the forward output is needed: the passes consume q, k, v, dO only.
+ * The normaliser path returns LMOE_ERR_UNSUPPORTED in this build.
+ * ------------------------------------------------------------------------------------- */
+size_t lmoe_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                                   lmoe_dtype dtype);
+int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
+                 const void* q, const void* k, const void* v, const void* a_pre,
+                 const float* b_pre, const float* a_raw, const float* M0, const void* dO,
+                 const float* dM_final, void* dq, void* dk, void* dv, void* da_pre,
+                 float* db_pre, float* da_raw, float* dM0, void* workspace,
+                 size_t workspace_bytes, lmoe_stream_t stream);
+
 /* Number of kernels one lmoe_lsm_fwd call launches (for launch accounting). */
 int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc);
 

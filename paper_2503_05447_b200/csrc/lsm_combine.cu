@@ -10,13 +10,16 @@ namespace lmoe_dev {
 // ------------------------------------------------------------------------------------
 // Phase 2: decayed exclusive prefix over segments
 //   Min[s] = acc ; acc = exp(logD[s][row]) * acc + S[s]        per element of [M | z]
+// rev = 1 (backward dM): the same recurrence over segments last-to-first, seeded with
+// dM_final; the value after segment 0 is dM0, the gradient of the initial state.
 // ------------------------------------------------------------------------------------
 __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __restrict__ zS,
                                 const float* __restrict__ logD, const float* __restrict__ M0,
                                 const float* __restrict__ z0, float* __restrict__ Min,
                                 float* __restrict__ zin, float* __restrict__ Mfin,
                                 float* __restrict__ zfin, float* __restrict__ logDtot,
-                                int fin_stride, int nseg, int dk, int dv, int norm, int lw, int* err) {
+                                int fin_stride, int nseg, int dk, int dv, int norm, int lw, int rev,
+                                int* err) {
     const int bh = blockIdx.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int nm = dk * dv;
@@ -38,7 +41,8 @@ __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __rest
     if (isz) { if (z0) acc = z0[(size_t)bh * dk + ee]; }
     else if (M0) acc = M0[(size_t)bh * nm + ee];
     const size_t base = (size_t)bh * nseg * stride + ee;
-    for (int s = 0; s < nseg; ++s) {
+    for (int i = 0; i < nseg; ++i) {
+        const int s = rev ? nseg - 1 - i : i;
         if (dst) dst[base + (size_t)s * stride] = acc;
         acc = __expf(logD[((size_t)bh * nseg + s) * lw + li]) * acc + src[base + (size_t)s * stride];
     }
@@ -74,9 +78,9 @@ __global__ void sp_rank_combine(const float* __restrict__ gathered, int P, int B
 cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const float* zS,
                                const float* logD, const float* M0, const float* z0, float* Min,
                                float* zin, float* Mfin, float* zfin, float* logDtot, int fin_stride,
-                               int nseg, int dk, int dv, int norm, int lw, int* err) {
+                               int nseg, int dk, int dv, int norm, int lw, int rev, int* err) {
     lsm_seg_combine<<<grid, 256, 0, st>>>(S, zS, logD, M0, z0, Min, zin, Mfin, zfin, logDtot,
-                                          fin_stride, nseg, dk, dv, norm, lw, err);
+                                          fin_stride, nseg, dk, dv, norm, lw, rev, err);
     return cudaGetLastError();
 }
 cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,

@@ -1,0 +1,303 @@
+// lsm_dgate.cu -- Mamba2 (TokenScalar) decay-gate gradients of the LSM backward.
+//
+// The gradient of the per-token log decay g_j (G = inclusive cumsum of g) is the sum over
+// all (query t, key s) pairs that straddle j:
+//     dg_j = sum_{s < j <= t} A_ts,   A_ts = (phi(q_t).keff_s) (dO_t.v_s) e^{G_t - G_s}
+// (with the initial / final states as extra keys / queries).  The telescoped form
+// sum_{t >= j} (phi(q_t).dphi(q_t) - keff_t.dkeff_t) cancels nearly equal totals, which
+// bf16 operand rounding cannot survive.  Here every term is a product of fp32 tensor-core
+// accumulators, evaluated per 128-token chunk c (one CTA, fully parallel):
+//     dg_j = C(j) + sum_{t in [j, end]} X_t + sum_{s in [start, j)} Y_s + e^{g_c} <M_c, dM_c>
+//   C(j)  within-chunk straddle: C(j) = sum_{i < j} (colsum_i - rowsum_i) of strictly
+//         lower A (S = phiQ phiK^T and dP = dO V^T on tcgen05, A in fp32 registers)
+//   X_t   = e^{G_t} phi(q_t) M_c dO_t^T       (Z = phiQ M_c on tcgen05)
+//   Y_s   = e^{g_c - G_s} keff_s dM_c v_s^T   (W = phiK dM_c on tcgen05)
+//   M_c   = state before chunk c (dq pass side output, M^T rows), dM_c = state gradient after
+//           chunk c (dk pass side output, dM^T rows): both [BH][nchunk][D][D] in T.
+// Then db_j = sigma(b_j) (dkf_j - softplus(a) dg_j) and da_raw += sigma(a) dg_j (-softplus(b_j))
+// (decay_vector_rows / effective_keys chain, lsm.hpp:483-518; oracle lmo_lsm_backward).
+#include "lsm_fwd.cuh"
+#include "lsm_launch.h"
+
+namespace lmoe_dev {
+namespace {
+
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x)); }
+
+// 32 consecutive elements [col0, col0 + 32) of `row` from an SW128 tile of two column
+// blocks (block stride blk_bytes).
+template <typename T>
+__device__ __forceinline__ void tile_row32(const uint8_t* tile, int blk_bytes, int row, int col0,
+                                           float (&out)[32]) {
+    using TT = TileTraits<T>;
+    const uint8_t* blk = tile + (col0 / TT::EPB) * blk_bytes;
+    const int ch0 = (col0 % TT::EPB) / TT::EPC;
+#pragma unroll
+    for (int c = 0; c < 32 / TT::EPC; ++c) {
+        const uint4 v = *reinterpret_cast<const uint4*>(blk + sw128_off(row, ch0 + c));
+        if constexpr (sizeof(T) == 2) {
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = unpack_bf16(w[i]);
+                out[c * 8 + 2 * i] = f.x;
+                out[c * 8 + 2 * i + 1] = f.y;
+            }
+        } else {
+            out[c * 4] = __uint_as_float(v.x); out[c * 4 + 1] = __uint_as_float(v.y);
+            out[c * 4 + 2] = __uint_as_float(v.z); out[c * 4 + 3] = __uint_as_float(v.w);
+        }
+    }
+}
+
+// 128-thread inclusive prefix sum (4 warps); `ws` holds 4 floats of shared scratch.
+__device__ __forceinline__ float block_incl_scan128(float x, float* ws) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    for (int i = 0; i < warp; ++i) x += ws[i];
+    return x;
+}
+__device__ __forceinline__ float block_sum128(float x, float* ws) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = x;
+    __syncthreads();
+    return ws[0] + ws[1] + ws[2] + ws[3];
+}
+
+template <typename T>
+struct DgateSmem {
+    static constexpr int D = TileTraits<T>::D;
+    static constexpr int kMT = D * D * (int)sizeof(T);  // state tile bytes
+    static constexpr int kQ = 0, kK = kTileBytes, kV = 2 * kTileBytes, kO = 3 * kTileBytes;
+    static constexpr int kM = 4 * kTileBytes, kDM = kM + kMT;
+    static constexpr int kMisc = kDM + kMT;  // sG, sKf, sX, sY, sR, scratch, barriers
+    static constexpr int kTotal = kMisc + 6 * 128 * 4 + 64;
+};
+
+}  // namespace
+
+template <typename T>
+__global__ void __launch_bounds__(128, 1)
+    lsm_mamba_dgate(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                    const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmDM,
+                    const float* __restrict__ b_pre, const float* __restrict__ a_raw,
+                    const float* __restrict__ dkf, float* __restrict__ db_pre, float* __restrict__ da_raw,
+                    int N, int H, int nchunk) {
+    using TT = TileTraits<T>;
+    using L = DgateSmem<T>;
+    constexpr int D = TT::D;
+    constexpr int MBLK = D * 128;  // column-block stride of a state tile
+    extern __shared__ __align__(1024) uint8_t smem[];
+    float* sG = reinterpret_cast<float*>(smem + L::kMisc);
+    float* sKf = sG + 128;
+    float* sX = sKf + 128;
+    float* sY = sX + 128;
+    float* sR = sY + 128;
+    float* ws = sR + 128;  // 128 floats scratch
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ws + 128);
+    uint64_t* mma_done = bar + 1;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bar + 2);
+
+    const int c = blockIdx.x, bh = blockIdx.y;
+    const int b = bh / H, h = bh % H;
+    const int t0 = c * kC;
+    const int nvalid = min(kC, N - t0);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(mma_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc<512>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+
+    if (tid == 0) {
+        mbar_expect_tx(bar, 4 * kTileBytes + 2 * L::kMT);
+        const int mrow = (bh * nchunk + c) * D;
+#pragma unroll
+        for (int blk = 0; blk < 2; ++blk) {
+            tma_load_4d(smem + L::kQ + blk * kBlockBytes, &tmQ, bar, blk * TT::EPB, h, t0, b);
+            tma_load_4d(smem + L::kK + blk * kBlockBytes, &tmK, bar, blk * TT::EPB, h, t0, b);
+            tma_load_4d(smem + L::kV + blk * kBlockBytes, &tmV, bar, blk * TT::EPB, h, t0, b);
+            tma_load_4d(smem + L::kO + blk * kBlockBytes, &tmO, bar, blk * TT::EPB, h, t0, b);
+            tma_load_2d(smem + L::kM + blk * MBLK, &tmM, bar, blk * TT::EPB, mrow);
+            tma_load_2d(smem + L::kDM + blk * MBLK, &tmDM, bar, blk * TT::EPB, mrow);
+        }
+    }
+    // gates while the tiles land: g_t = -softplus(b_t) softplus(a_h), kf_t = softplus(b_t)
+    const float spa = softplus_f(a_raw[h]);
+    float bv = 0.f, kf = 0.f, gl = 0.f;
+    if (tid < nvalid) {
+        bv = b_pre[((size_t)b * N + t0 + tid) * H + h];
+        kf = softplus_f(bv);
+        gl = -kf * spa;
+    }
+    const float G = block_incl_scan128(gl, ws);
+    sG[tid] = G;
+    sKf[tid] = kf;
+    if (tid == 0) {
+        mbar_wait(bar, 0);
+        tc_fence_after();
+        // S = phiQ phiK^T (cols 0..127), dP = dO V^T (128..255), Z = phiQ M_c (256..),
+        // W = phiK dM_c (384..): all operands K-major
+        constexpr uint32_t idSq = umma_idesc(TT::FMT, 0, 0, 128, 128);
+        constexpr uint32_t idSt = umma_idesc(TT::FMT, 0, 0, 128, D);
+        const uint32_t q = smem_u32(smem + L::kQ), k = smem_u32(smem + L::kK);
+        const uint32_t v = smem_u32(smem + L::kV), o = smem_u32(smem + L::kO);
+        const uint32_t m = smem_u32(smem + L::kM), dm = smem_u32(smem + L::kDM);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * kBlockBytes + (kk & 3) * 32;
+            const uint32_t moff = (kk >> 2) * MBLK + (kk & 3) * 32;
+            const uint32_t acc = kk > 0;
+            if constexpr (sizeof(T) == 2) {
+                mma_ss_f16(tmem, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024), idSq, acc);
+                mma_ss_f16(tmem + 128, umma_desc_sw128(o + off, 16, 1024), umma_desc_sw128(v + off, 16, 1024), idSq, acc);
+                mma_ss_f16(tmem + 256, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(m + moff, 16, 1024), idSt, acc);
+                mma_ss_f16(tmem + 384, umma_desc_sw128(k + off, 16, 1024), umma_desc_sw128(dm + moff, 16, 1024), idSt, acc);
+            } else {
+                mma_ss_tf32(tmem, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(k + off, 16, 1024), idSq, acc);
+                mma_ss_tf32(tmem + 128, umma_desc_sw128(o + off, 16, 1024), umma_desc_sw128(v + off, 16, 1024), idSq, acc);
+                mma_ss_tf32(tmem + 256, umma_desc_sw128(q + off, 16, 1024), umma_desc_sw128(m + moff, 16, 1024), idSt, acc);
+                mma_ss_tf32(tmem + 384, umma_desc_sw128(k + off, 16, 1024), umma_desc_sw128(dm + moff, 16, 1024), idSt, acc);
+            }
+        }
+        mma_commit(mma_done);
+    }
+    __syncthreads();  // sG / sKf visible
+    const float gend = sG[127];
+    // B_c partial: <M_c, dM_c> over this thread's slice of the (identically laid out) tiles
+    float bpart = 0.f;
+    {
+        constexpr int per = L::kMT / 128;
+        const uint8_t* pm = smem + L::kM + tid * per;
+        const uint8_t* pd = smem + L::kDM + tid * per;
+        mbar_wait(bar, 0);
+        for (int i = 0; i < per; i += 16) {
+            const uint4 a = *reinterpret_cast<const uint4*>(pm + i);
+            const uint4 d = *reinterpret_cast<const uint4*>(pd + i);
+            const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, dw[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if constexpr (sizeof(T) == 2) {
+                    const float2 fa = unpack_bf16(aw[e]), fd = unpack_bf16(dw[e]);
+                    bpart += fa.x * fd.x + fa.y * fd.y;
+                } else {
+                    bpart += __uint_as_float(aw[e]) * __uint_as_float(dw[e]);
+                }
+            }
+        }
+    }
+    mbar_wait(mma_done, 0);
+    tc_fence_after();
+    const uint32_t lo = (uint32_t)(warp * 32) << 16;
+    const int t = tid;  // TMEM lane == query row t
+    // X_t, Y_t from Z, W rows against dO / V rows (smem)
+    float xs = 0.f, ys = 0.f;
+#pragma unroll
+    for (int cb = 0; cb < D / 32; ++cb) {
+        uint32_t rz[32], rw[32];
+        tmem_ld32(tmem + 256 + lo + cb * 32, rz);
+        tmem_ld32(tmem + 384 + lo + cb * 32, rw);
+        tmem_wait_ld();
+        float vo[32], vv[32];
+        tile_row32<T>(smem + L::kO, kBlockBytes, t, cb * 32, vo);
+        tile_row32<T>(smem + L::kV, kBlockBytes, t, cb * 32, vv);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            xs += __uint_as_float(rz[j]) * vo[j];
+            ys += __uint_as_float(rw[j]) * vv[j];
+        }
+    }
+    const float Gt = sG[t];
+    const float X = t < nvalid ? __expf(Gt) * xs : 0.f;
+    const float Y = t < nvalid ? __expf(gend - Gt) * sKf[t] * ys : 0.f;
+    __syncthreads();  // all MMAs consumed Q/K (mma_done) and all threads past their tile reads
+    // strictly lower A_ts = S_ts kf_s dP_ts e^{G_t - G_s} (s < t): row sums here, rows to
+    // shared memory (XOR-swizzled by t) for the column sums
+    float* As = reinterpret_cast<float*>(smem + L::kQ);  // 128 x 128 fp32 over the Q, K tiles
+    float rsum = 0.f;
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tmem + lo + cb * 32, rs);
+        tmem_ld32(tmem + 128 + lo + cb * 32, rp);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int s = cb * 32 + j;
+            float a = 0.f;
+            if (s < t) a = __uint_as_float(rs[j]) * __uint_as_float(rp[j]) * sKf[s] * __expf(Gt - sG[s]);
+            rsum += a;
+            As[t * 128 + (s ^ (t & 31))] = a;
+        }
+    }
+    __syncthreads();
+    float csum = 0.f;  // column t: sum over rows r > t
+    for (int r = t + 1; r < 128; ++r) csum += As[r * 128 + (t ^ (r & 31))];
+    // dg_t = C(t) + sum_{u >= t} X_u + sum_{s < t} Y_s + e^{g_c} <M_c, dM_c>
+    const float Bc = __expf(gend) * block_sum128(bpart, ws);
+    const float dlt = csum - rsum;
+    const float Cin = block_incl_scan128(dlt, ws) - dlt;    // exclusive prefix
+    const float Xin = block_incl_scan128(X, ws);
+    const float Xtot = block_sum128(X, ws);
+    const float Xsuf = Xtot - Xin + X;
+    const float Yin = block_incl_scan128(Y, ws);
+    const float Ypre = Yin - Y;
+    const float dg = Cin + Xsuf + Ypre + Bc;
+    float dr = 0.f;
+    if (t < nvalid) {
+        const size_t row = ((size_t)b * N + t0 + t) * H + h;
+        db_pre[row] = sigm(bv) * (dkf[(size_t)bh * N + t0 + t] - spa * dg);
+        dr = dg * -kf;
+    }
+    dr = block_sum128(dr, ws);
+    if (tid == 0) atomicAdd(da_raw + h, dr * sigm(a_raw[h]));
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+template <typename T>
+static cudaError_t dgate_t(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                           const CUtensorMap& dO, const CUtensorMap& m, const CUtensorMap& dm,
+                           const float* b_pre, const float* a_raw, const float* dkf, float* db_pre,
+                           float* da_raw, int B, int N, int H, cudaStream_t st) {
+    static bool attr = false;
+    constexpr int smem = DgateSmem<T>::kTotal;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(lsm_mamba_dgate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int nchunk = (N + kC - 1) / kC;
+    cudaError_t e = cudaMemsetAsync(da_raw, 0, sizeof(float) * H, st);
+    if (e != cudaSuccess) return e;
+    lsm_mamba_dgate<T><<<dim3(nchunk, B * H), 128, smem, st>>>(q, k, v, dO, m, dm, b_pre, a_raw, dkf, db_pre,
+                                                                da_raw, N, H, nchunk);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mamba_dgate(bool bf16, const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                               const CUtensorMap& dO, const CUtensorMap& m, const CUtensorMap& dm,
+                               const float* b_pre, const float* a_raw, const float* dkf, float* db_pre,
+                               float* da_raw, int B, int N, int H, cudaStream_t st) {
+    return bf16 ? dgate_t<__nv_bfloat16>(q, k, v, dO, m, dm, b_pre, a_raw, dkf, db_pre, da_raw, B, N, H, st)
+                : dgate_t<float>(q, k, v, dO, m, dm, b_pre, a_raw, dkf, db_pre, da_raw, B, N, H, st);
+}
+
+}  // namespace lmoe_dev

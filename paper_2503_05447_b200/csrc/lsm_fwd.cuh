@@ -57,6 +57,13 @@ struct LsmFwdParams {
     void* o;             // [B, Nstride, H, D] output (phase 3), written from registers
     int* err;            // [0] degenerate normaliser, [1] non-finite state
     int order;           // phase-3 schedule: 0 = P epilogue first, 1 = transforms first
+    int out_f32;         // bf16 inputs, fp32 output rows (backward intermediates)
+    int rev_kfq;         // REV passes: scale output rows by kf_i = softplus(b_i) (Mamba2 keff query)
+    // backward side channel (Mamba2 gate gradients, lsm_dgate.cu): the state operand of every
+    // chunk (the state before it in forward order, the state gradient after it in REV order)
+    // written to mst [BH][nchunk_tot][D][D] in T
+    void* mst;
+    int nchunk_tot;
     unsigned long long* trace;  // optional clock64 trace of CTA (0,0,0) [64 chunks][16]
 };
 
@@ -120,10 +127,13 @@ constexpr int state_pass_smem() {
 constexpr int kStatePassThreads = 256;
 constexpr int kOutputPassThreads = 384;
 
-template <typename T, int DECAY, int FM, bool NORM>
+// REV = reverse-time pass of the backward (lsm_bwd.cuh): out_i = sum_{j >= i} e^{G_j - G_i}
+// (q'_i . k'_j) v'_j + e^{G_end - G_i} q'_i dM, chunks visited last-to-first, state carried
+// towards the sequence start (dM_{c-1} = e^{g(c)} dM_c + sum_j e^{G_j} k'_j^T v'_j).
+template <typename T, int DECAY, int FM, bool NORM, bool REV = false>
 __global__ void lsm_state_pass(const __grid_constant__ CUtensorMap tmK,
                                const __grid_constant__ CUtensorMap tmV, LsmFwdParams p);
-template <typename T, int DECAY, int FM, bool NORM>
+template <typename T, int DECAY, int FM, bool NORM, bool REV = false>
 __global__ void lsm_output_pass(const __grid_constant__ CUtensorMap tmQ,
                                 const __grid_constant__ CUtensorMap tmK,
                                 const __grid_constant__ CUtensorMap tmV, LsmFwdParams p);
@@ -132,7 +142,8 @@ __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __rest
                                 const float* __restrict__ z0, float* __restrict__ Min,
                                 float* __restrict__ zin, float* __restrict__ Mfin,
                                 float* __restrict__ zfin, float* __restrict__ logDtot,
-                                int fin_stride, int nseg, int dk, int dv, int norm, int lw, int* err);
+                                int fin_stride, int nseg, int dk, int dv, int norm, int lw, int rev,
+                                int* err);
 __global__ void sp_rank_combine(const float* __restrict__ gathered, int P, int BH, int rank,
                                 int dk, int dv, int norm, int lw, float* __restrict__ M0,
                                 float* __restrict__ z0);

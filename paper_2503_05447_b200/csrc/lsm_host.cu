@@ -217,14 +217,14 @@ struct LsmCall {
     // Segment prefix with carried-in state (M0, z0); writes per-segment M_in and the
     // inclusive total (Mfin/zfin with row stride fin_stride, and its total log decay).
     void combine(const float* M0, const float* z0, bool write_min, float* Mfin, float* zfin,
-                 float* logDtot, int fin_stride) {
+                 float* logDtot, int fin_stride, int rev = 0) {
         mark();
         const int nel = D * D + (norm ? D : 0);
         LMOE_CUDA_CHECK(lmoe_dev::launch_seg_combine(
             dim3((nel + 255) / 256, B * H), st, p.Sseg, p.zseg, p.logDseg, M0, z0,
             write_min ? const_cast<float*>(p.Min) : nullptr,
             write_min ? const_cast<float*>(p.zin) : nullptr, Mfin, zfin, logDtot, fin_stride,
-            pl.nseg, D, D, norm ? 1 : 0, lw, p.err));
+            pl.nseg, D, D, norm ? 1 : 0, lw, rev, p.err));
         ++g_launch_count;
     }
     template <typename T>
@@ -530,6 +530,153 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
             }
             if (last) c.check_err();
         }
+    });
+}
+
+// ------------------------------------------------------------------------------- backward
+// Three chunk passes, each a segment-parallel state pass + combine + output pass:
+//   dq pass  (forward order)  q'=dO, k'=v, v'=phi(k), M0' = M0^T    -> dphi(q) fp32, M_N^T
+//   dk pass  (REV)            q'=v,  k'=dO, v'=phi(q), dM' = dM_f^T -> dkeff fp32
+//   dv pass  (REV)            q'=keff, k'=phi(q), v'=dO, dM = dM_f  -> dv, dM0
+// then the chain rule (lsm_bwd_kernels.cu) and the Mamba2 gate gradients from the per-chunk
+// state snapshots of the dq / dk passes (lsm_dgate.cu).
+namespace lmoe_host {
+struct BwdPlan {
+    LsmPlan pl;
+    size_t off_dphq = 0, off_dkef = 0, off_phq = 0, off_phk = 0, off_M0T = 0, off_dMfT = 0,
+           off_MfinT = 0, off_dkf = 0, off_mst = 0, off_dmst = 0, total = 0;
+};
+static BwdPlan plan_bwd(const lmoe_lsm_desc* d, int B, int N, int H, int D, lmoe_dtype dt) {
+    BwdPlan w;
+    w.pl = plan_lsm(B, N, H, D);
+    const size_t act = (size_t)B * N * H * D, esz = dt == LMOE_BF16 ? 2 : 4;
+    const size_t BH = (size_t)B * H;
+    size_t off = align_up(w.pl.total, 256);
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    w.off_dphq = take(act * 4);
+    w.off_dkef = take(act * 4);
+    if (d && d->feature_map != 0) {
+        w.off_phq = take(act * esz);
+        w.off_phk = take(act * esz);
+    }
+    w.off_M0T = take(BH * D * D * 4);
+    w.off_dMfT = take(BH * D * D * 4);
+    w.off_MfinT = take(BH * D * D * 4);
+    w.off_dkf = take(BH * N * 4);
+    const size_t nchunk = (N + lmoe_dev::kC - 1) / lmoe_dev::kC;
+    if (d && device_decay_mode(d->instance) == lmoe_dev::kDecayTokenScalar) {
+        w.off_mst = take(BH * nchunk * D * D * esz);
+        w.off_dmst = take(BH * nchunk * D * D * esz);
+    }
+    w.total = off;
+    return w;
+}
+}  // namespace lmoe_host
+
+extern "C" size_t lmoe_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                                              lmoe_dtype dtype) {
+    if (!desc || B < 1 || N < 1 || H < 1 || D < 1) return 0;
+    return plan_bwd(desc, B, N, H, D, dtype).total;
+}
+
+extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
+                            const void* q, const void* k, const void* v, const void* a_pre,
+                            const float* b_pre, const float* a_raw, const float* M0, const void* dO,
+                            const float* dM_final, void* dq, void* dk, void* dv, void* da_pre,
+                            float* db_pre, float* da_raw, float* dM0, void* workspace,
+                            size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, B, N, H, D, dtype, q, k, v, dO);
+        (void)da_pre;
+        if (!dq || !dk || !dv) throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: null gradient tensor");
+        if (desc->use_normalizer)
+            throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_lsm_bwd: normalizer backward not in this build");
+        const int mode = device_decay_mode(desc->instance);
+        if (mode == lmoe_dev::kDecayTokenVector)
+            throw Error(LMOE_ERR_UNSUPPORTED, std::string("lmoe_lsm_bwd: instance ") +
+                                                  instance_name(desc->instance) + " has no device backward in this build");
+        const bool mamba = mode == lmoe_dev::kDecayTokenScalar;
+        if (mamba && (!db_pre || !da_raw)) throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: Mamba2 needs db_pre and da_raw");
+        const BwdPlan w = plan_bwd(desc, B, N, H, D, dtype);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: workspace too small (need " + std::to_string(w.total) + " bytes)");
+        uint8_t* ws = static_cast<uint8_t*>(workspace);
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const bool bf16 = dtype == LMOE_BF16;
+        const size_t act = (size_t)B * N * H * D;
+        const int BH = B * H;
+        auto F = [&](size_t off) { return reinterpret_cast<float*>(ws + off); };
+        // the chunk passes run with identity feature map and no normaliser
+        lmoe_lsm_desc dd = *desc;
+        dd.feature_map = 0;
+        dd.use_normalizer = 0;
+        const void* phq = q;
+        const void* phk = k;
+        if (desc->feature_map != 0) {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_apply_fmap(bf16, desc->feature_map, q, ws + w.off_phq, act, st));
+            LMOE_CUDA_CHECK(lmoe_dev::launch_apply_fmap(bf16, desc->feature_map, k, ws + w.off_phk, act, st));
+            g_launch_count += 2;
+            phq = ws + w.off_phq;
+            phk = ws + w.off_phk;
+        }
+        const float* M0T = nullptr;
+        if (M0) {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_transpose_states(M0, F(w.off_M0T), BH, D, st));
+            ++g_launch_count;
+            M0T = F(w.off_M0T);
+        }
+        const float* dMfT = nullptr;
+        if (dM_final) {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_transpose_states(dM_final, F(w.off_dMfT), BH, D, st));
+            ++g_launch_count;
+            dMfT = F(w.off_dMfT);
+        }
+        const int nchunk = (N + lmoe_dev::kC - 1) / lmoe_dev::kC;
+        // side: 1 / 2 = write the per-chunk state operands (dq pass: M_c^T, dk pass: dM_c^T)
+        auto pass = [&](const void* qq, const void* kk, const void* vv, void* oo, bool rev, bool out_f32,
+                        bool kfq, const float* init, float* fin, int side) {
+            LsmCall c{&dd, B, N, N, H, D, dtype, qq, kk, vv, b_pre, a_raw, oo, ws, w.pl, st, nullptr};
+            c.setup();
+            c.var.rev = rev ? 1 : 0;
+            c.p.out_f32 = out_f32 ? 1 : 0;
+            c.p.rev_kfq = kfq ? 1 : 0;
+            c.p.nchunk_tot = nchunk;
+            if (mamba && side == 1) c.p.mst = ws + w.off_mst;
+            if (mamba && side == 2) c.p.mst = ws + w.off_dmst;
+            c.clear_err();
+            if (bf16) c.state_pass<__nv_bfloat16>(); else c.state_pass<float>();
+            c.combine(init, nullptr, true, fin, nullptr, nullptr, 0, rev ? 1 : 0);
+            if (bf16) c.output_pass<__nv_bfloat16>(); else c.output_pass<float>();
+            c.finish_timing();
+            c.check_err();
+        };
+        float* dphq = F(w.off_dphq);
+        float* dkef = F(w.off_dkef);
+        pass(dO, v, phk, dphq, false, true, false, M0T, F(w.off_MfinT), 1);
+        pass(v, dO, phq, dkef, true, true, false, dMfT, nullptr, 2);
+        pass(phk, phq, dO, dv, true, false, mamba, dM_final, dM0, 0);
+        LMOE_CUDA_CHECK(lmoe_dev::launch_bwd_finish(bf16, desc->feature_map, mamba, q, k, dphq, dkef, b_pre, dq,
+                                                    dk, F(w.off_dkf), B, N, H, st));
+        ++g_launch_count;
+        if (mamba) {
+            LsmCall c{&dd, B, N, N, H, D, dtype, q, k, v, b_pre, a_raw, nullptr, ws, w.pl, st, nullptr};
+            const CUtensorMapDataType tdt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+            const int esz = bf16 ? 2 : 4, epb = 128 / esz;
+            const uint64_t srows = (uint64_t)BH * nchunk * D;
+            const CUtensorMap tm = make_tmap_2d(ws + w.off_mst, tdt, esz, D, srows, D, epb, D);
+            const CUtensorMap tdm = make_tmap_2d(ws + w.off_dmst, tdt, esz, D, srows, D, epb, D);
+            CUtensorMap tq, tk, tv, tdo;
+            if (bf16) {
+                tq = c.tmap<__nv_bfloat16>(phq); tk = c.tmap<__nv_bfloat16>(phk);
+                tv = c.tmap<__nv_bfloat16>(v); tdo = c.tmap<__nv_bfloat16>(dO);
+            } else {
+                tq = c.tmap<float>(phq); tk = c.tmap<float>(phk); tv = c.tmap<float>(v); tdo = c.tmap<float>(dO);
+            }
+            LMOE_CUDA_CHECK(lmoe_dev::launch_mamba_dgate(bf16, tq, tk, tv, tdo, tm, tdm, b_pre, a_raw, F(w.off_dkf),
+                                                         db_pre, da_raw, B, N, H, st));
+            ++g_launch_count;
+        }
+        if (desc->flags & LMOE_FLAG_CHECK) LMOE_CUDA_CHECK(cudaStreamSynchronize(st));
     });
 }
 

@@ -6,56 +6,59 @@
 namespace lmoe_dev {
 namespace {
 
-template <typename T, int DECAY, int FM, bool NORM>
+template <typename T, int DECAY, int FM, bool NORM, bool REV>
 cudaError_t sp_launch(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CUtensorMap& v,
                       const LsmFwdParams& p) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_state_pass<T, DECAY, FM, NORM>,
+        cudaError_t e = cudaFuncSetAttribute(lsm_state_pass<T, DECAY, FM, NORM, REV>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              state_pass_smem<T>());
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_state_pass<T, DECAY, FM, NORM><<<grid, kStatePassThreads, state_pass_smem<T>(), st>>>(k, v, p);
+    lsm_state_pass<T, DECAY, FM, NORM, REV><<<grid, kStatePassThreads, state_pass_smem<T>(), st>>>(k, v, p);
     return cudaGetLastError();
 }
 
-template <typename T, int DECAY, int FM, bool NORM>
+template <typename T, int DECAY, int FM, bool NORM, bool REV>
 cudaError_t op_launch(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& k,
                       const CUtensorMap& v, const CUtensorMap& o, const LsmFwdParams& p) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_output_pass<T, DECAY, FM, NORM>,
+        cudaError_t e = cudaFuncSetAttribute(lsm_output_pass<T, DECAY, FM, NORM, REV>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              output_pass_smem<T>());
         if (e != cudaSuccess) return e;
         attr = true;
     }
     (void)o;
-    lsm_output_pass<T, DECAY, FM, NORM><<<grid, kOutputPassThreads, output_pass_smem<T>(), st>>>(q, k, v, p);
+    lsm_output_pass<T, DECAY, FM, NORM, REV><<<grid, kOutputPassThreads, output_pass_smem<T>(), st>>>(q, k, v, p);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 #define LSM_VARIANTS(X, ...)                                                                  \
-    switch (v.decay * 100 + v.fm * 10 + v.norm) {                                             \
-        case 0: return X<LSM_T, 0, 0, false>(__VA_ARGS__);                                    \
-        case 1: return X<LSM_T, 0, 0, true>(__VA_ARGS__);                                     \
-        case 10: return X<LSM_T, 0, 1, false>(__VA_ARGS__);                                   \
-        case 11: return X<LSM_T, 0, 1, true>(__VA_ARGS__);                                    \
-        case 20: return X<LSM_T, 0, 2, false>(__VA_ARGS__);                                   \
-        case 21: return X<LSM_T, 0, 2, true>(__VA_ARGS__);                                    \
-        case 100: return X<LSM_T, 1, 0, false>(__VA_ARGS__);                                  \
-        case 101: return X<LSM_T, 1, 0, true>(__VA_ARGS__);                                   \
-        case 110: return X<LSM_T, 1, 1, false>(__VA_ARGS__);                                  \
-        case 111: return X<LSM_T, 1, 1, true>(__VA_ARGS__);                                   \
-        case 120: return X<LSM_T, 1, 2, false>(__VA_ARGS__);                                  \
-        case 121: return X<LSM_T, 1, 2, true>(__VA_ARGS__);                                   \
-        case 200: return X<LSM_T, 2, 0, false>(__VA_ARGS__);                                  \
-        case 210: return X<LSM_T, 2, 1, false>(__VA_ARGS__);                                  \
-        case 220: return X<LSM_T, 2, 2, false>(__VA_ARGS__);                                  \
+    switch (v.rev * 1000 + v.decay * 100 + v.fm * 10 + v.norm) {                              \
+        case 0: return X<LSM_T, 0, 0, false, false>(__VA_ARGS__);                                    \
+        case 1: return X<LSM_T, 0, 0, true, false>(__VA_ARGS__);                                     \
+        case 10: return X<LSM_T, 0, 1, false, false>(__VA_ARGS__);                                   \
+        case 11: return X<LSM_T, 0, 1, true, false>(__VA_ARGS__);                                    \
+        case 20: return X<LSM_T, 0, 2, false, false>(__VA_ARGS__);                                   \
+        case 21: return X<LSM_T, 0, 2, true, false>(__VA_ARGS__);                                    \
+        case 100: return X<LSM_T, 1, 0, false, false>(__VA_ARGS__);                                  \
+        case 101: return X<LSM_T, 1, 0, true, false>(__VA_ARGS__);                                   \
+        case 110: return X<LSM_T, 1, 1, false, false>(__VA_ARGS__);                                  \
+        case 111: return X<LSM_T, 1, 1, true, false>(__VA_ARGS__);                                   \
+        case 120: return X<LSM_T, 1, 2, false, false>(__VA_ARGS__);                                  \
+        case 121: return X<LSM_T, 1, 2, true, false>(__VA_ARGS__);                                   \
+        case 200: return X<LSM_T, 2, 0, false, false>(__VA_ARGS__);                                  \
+        case 210: return X<LSM_T, 2, 1, false, false>(__VA_ARGS__);                                  \
+        case 220: return X<LSM_T, 2, 2, false, false>(__VA_ARGS__);                                  \
+        case 1000: return X<LSM_T, 0, 0, false, true>(__VA_ARGS__);                           \
+        case 1100: return X<LSM_T, 1, 0, false, true>(__VA_ARGS__);                           \
+        case 1200: return X<LSM_T, 2, 0, false, true>(__VA_ARGS__);                           \
         default: return cudaErrorInvalidValue;                                                \
     }
 

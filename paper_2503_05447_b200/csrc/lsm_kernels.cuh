@@ -107,7 +107,7 @@ __device__ __forceinline__ void load_half_row_f32(const uint8_t* blk, int row, f
 // Phase 1: per-segment state S_seg = sum_j exp(L_j) keff_j v_j^T accumulated in TMEM.
 // warps: 0 TMA, 1 MMA, 2 decay, 3 idle, 4..7 transform (row owners, 128 threads)
 // ====================================================================================
-template <typename T, int DECAY, int FM, bool NORM>
+template <typename T, int DECAY, int FM, bool NORM, bool REV>
 __global__ void __launch_bounds__(kStatePassThreads, 1)
     lsm_state_pass(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                    LsmFwdParams p) {
@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *sTmem;
-    auto chunk_t0 = [&](int it) { return t_begin + (nchunks - 1 - it) * kC; };  // last first
+    // forward: last chunk first (weights e^{G_end - G_j} need no pre-pass); REV: first first
+    auto chunk_t0 = [&](int it) { return t_begin + (REV ? it : nchunks - 1 - it) * kC; };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     } else if (warp == 2) {
         // decay warp: per-token weights w_t = exp(L_t) kf_t, L_t = log decay from token t
         // (exclusive) to the segment end = (G_end - G_t) + decay of the later chunks.
+        // REV: w_t = exp(G_t + decay of the earlier chunks) (from the segment start), no kf.
         const float spa = (DECAY == kDecayTokenScalar) ? softplus_f(p.a_raw[h]) : 0.f;
         float suffix = 0.f;
         float bvA[4], bvB[4], bvC[4];
@@ -221,7 +223,8 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
             const float gend = chunk_scan<DECAY>(p, bvA, nval(it), spa, lane, la, kf);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                ringW[slot * 128 + lane * 4 + u] = __expf(gend - la[u] + suffix) * kf[u];
+                ringW[slot * 128 + lane * 4 + u] =
+                    REV ? __expf(la[u] + suffix) : __expf(gend - la[u] + suffix) * kf[u];
             suffix += gend;
             __syncwarp();
             mbar_arrive(&wfull[slot]);
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
 //              current S buffer's columns 64..67 once P (packed bf16) occupies 0..63.
 //      (tf32): S0, S1, O [256,320), M [320,384) (M=64 layout), partials [384,388).
 // ====================================================================================
-template <typename T, int DECAY, int FM, bool NORM>
+template <typename T, int DECAY, int FM, bool NORM, bool REV>
 __global__ void __launch_bounds__(kOutputPassThreads, 1)
     lsm_output_pass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, LsmFwdParams p) {
@@ -363,6 +366,8 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
     const int t_end = min(p.N, t_begin + p.seg_len);
     const int nchunks = (t_end - t_begin + kC - 1) / kC;
     const int warp = warp_id(), lane = lane_id();
+    // processing order: first-to-last, or last-to-first for the reverse-time (REV) passes
+    auto chunk_t0 = [&](int c) { return t_begin + (REV ? nchunks - 1 - c : c) * kC; };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             for (int c = 0; c < nchunks; ++c) {
                 const int s = c % NST;
                 if (c >= NST) mbar_wait(&empty[s], ((c / NST) - 1) & 1);
-                const int t0 = t_begin + c * kC;
+                const int t0 = chunk_t0(c);
                 uint8_t* st = tiles + s * 3 * kTileBytes;
                 mbar_expect_tx(&full[s], 3 * kTileBytes);
 #pragma unroll
@@ -505,12 +510,12 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
         //   ringS = {G_end, safe}
         const float spa = (DECAY == kDecayTokenScalar) ? softplus_f(p.a_raw[h]) : 0.f;
         float bvA[4], bvB[4], bvC[4];
-        auto nval = [&](int c) { return min(kC, t_end - (t_begin + c * kC)); };
-        load_gates<DECAY>(p, b, h, t_begin, nval(0), lane, bvA);
-        if (nchunks > 1) load_gates<DECAY>(p, b, h, t_begin + kC, nval(1), lane, bvB);
+        auto nval = [&](int c) { return min(kC, t_end - chunk_t0(c)); };
+        load_gates<DECAY>(p, b, h, chunk_t0(0), nval(0), lane, bvA);
+        if (nchunks > 1) load_gates<DECAY>(p, b, h, chunk_t0(1), nval(1), lane, bvB);
         for (int c = 0; c < nchunks; ++c) {
             const int slot = c & 1;
-            if (c + 2 < nchunks) load_gates<DECAY>(p, b, h, t_begin + (c + 2) * kC, nval(c + 2), lane, bvC);
+            if (c + 2 < nchunks) load_gates<DECAY>(p, b, h, chunk_t0(c + 2), nval(c + 2), lane, bvC);
             if (c >= 2) mbar_wait(&gfree[slot], ((c >> 1) - 1) & 1);
             float G[4], kf[4];
             const float gend = chunk_scan<DECAY>(p, bvA, nval(c), spa, lane, G, kf);
@@ -522,8 +527,11 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 ringG[slot * 128 + lane * 4 + u] = G[u];
-                ringF[slot * 128 + lane * 4 + u] =
-                    (DECAY != kDecayNone && safe) ? __expf(r - G[u]) * kf[u] : kf[u];
+                if constexpr (REV)  // column factor e^{G_j - r} of e^{G_j - G_i}; no key kf
+                    ringF[slot * 128 + lane * 4 + u] = (DECAY != kDecayNone && safe) ? __expf(G[u] - r) : 1.f;
+                else
+                    ringF[slot * 128 + lane * 4 + u] =
+                        (DECAY != kDecayNone && safe) ? __expf(r - G[u]) * kf[u] : kf[u];
             }
             if (lane == 0) {
                 ringS[slot * 4] = gend;
@@ -554,7 +562,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
         auto prep = [&](int c) {  // phi(Q), phi(K) [+ tf32 rounding] in place; zero rows past the end
             const int s = c % NST;
             mbar_wait(&full[s], (c / NST) & 1);
-            const int nvalid = min(kC, t_end - (t_begin + c * kC));
+            const int nvalid = min(kC, t_end - chunk_t0(c));
             const float sc = row < nvalid ? 1.f : 0.f;
             uint8_t* qt = tiles + s * 3 * kTileBytes;
             xform_half_row<T, FM, TR>(qt + hh * kBlockBytes, row, sc);
@@ -585,6 +593,26 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             }
         };
 
+        // backward side channel (see LsmFwdParams::mst): vals = this thread's DH state values
+        // of row srow, the operand of processing step cidx
+        auto state_hook = [&](const float* vals, int cidx) {
+            if (p.mst == nullptr || !sown) return;
+            const int cg = chunk_t0(cidx) / kC;
+            T* dst = reinterpret_cast<T*>(p.mst) + (((size_t)bh * p.nchunk_tot + cg) * D + srow) * D + hh * DH;
+#pragma unroll
+            for (int j = 0; j < DH; j += 8) {
+                if constexpr (kBF16) {
+                    uint4 w;
+                    w.x = pack_bf16(vals[j], vals[j + 1]); w.y = pack_bf16(vals[j + 2], vals[j + 3]);
+                    w.z = pack_bf16(vals[j + 4], vals[j + 5]); w.w = pack_bf16(vals[j + 6], vals[j + 7]);
+                    *reinterpret_cast<uint4*>(dst + j) = w;
+                } else {
+                    *reinterpret_cast<float4*>(dst + j) = make_float4(vals[j], vals[j + 1], vals[j + 2], vals[j + 3]);
+                    *reinterpret_cast<float4*>(dst + j + 4) = make_float4(vals[j + 4], vals[j + 5], vals[j + 6], vals[j + 7]);
+                }
+            }
+        };
+
         if constexpr (kPrep) prep(0);
         // initial state: operand M_0, TMEM M = e^{G_end(0)} M_0
         {
@@ -598,6 +626,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 vals[j] = v.x; vals[j + 1] = v.y; vals[j + 2] = v.z; vals[j + 3] = v.w;
             }
             write_state_operand(vals);
+            state_hook(vals, 0);
 #pragma unroll
             for (int cb = 0; cb < DH / 32; ++cb) {
                 uint32_t r[32];
@@ -617,8 +646,14 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
 
         for (int c = 0; c < nchunks; ++c) {
             const int s = c % NST, bb = c & 1, slot = c & 1;
-            const int t0 = t_begin + c * kC;
+            const int t0 = chunk_t0(c);
             const int nvalid = min(kC, t_end - t0);
+            // REV with Mamba2 keff queries (dv pass): kf_i = softplus(b_i) scales output row i
+            float qf = 1.f;
+            if constexpr (REV && DECAY == kDecayTokenScalar) {
+                if (p.rev_kfq && row < nvalid)
+                    qf = softplus_f(__ldg(p.b_pre + ((size_t)b * p.Nstride + t0 + row) * p.H + h));
+            }
             uint8_t* qt = tiles + s * 3 * kTileBytes;
             uint8_t* kt = qt + kTileBytes;
             mbar_wait(&gfull[slot], (c >> 1) & 1);
@@ -643,9 +678,12 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             float qz = 0.f;  // q~_i . z_in partial (normaliser)
             // (b) Q~ = phiQ e^{G_i}, K~ = phiK kf e^{G_end - G_i}  (row owners; fp32: K~^T)
             auto do_b = [&]() {
-                const float fq = (DECAY != kDecayNone) ? __expf(gi) : 1.f;
+                // forward: query cross factor e^{G_i}, key state factor e^{G_end - G_j} kf_j;
+                // REV: e^{G_end - G_i} and e^{G_j}
+                const float fq = (DECAY != kDecayNone) ? __expf(REV ? gend - gi : gi) : 1.f;
                 float fk = 1.f;
-                if constexpr (DECAY != kDecayNone)
+                if constexpr (DECAY != kDecayNone && REV) fk = __expf(gi);
+                if constexpr (DECAY != kDecayNone && !REV)
                     fk = safe ? __expf(gend - gref) * Fs[row] : __expf(gend - gi) * Fs[row];
                 uint8_t* qb = qt + hh * kBlockBytes;
                 if constexpr (DECAY != kDecayNone || NORM) {
@@ -717,7 +755,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 tmem_ld32(tS, r0);
                 tmem_ld32(tS + 32, r1);
                 tmem_wait_ld();
-                const float eq = (DECAY != kDecayNone && safe) ? __expf(gi - gref) : 1.f;
+                const float eq = (DECAY != kDecayNone && safe) ? __expf(REV ? gref - gi : gi - gref) : 1.f;
                 float rs = 0.f;
 #pragma unroll
                 for (int j = 0; j < 64; ++j) {
@@ -725,8 +763,9 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                     float v = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
                     float f;
                     if constexpr (DECAY == kDecayNone) f = 1.f;
+                    else if constexpr (REV) f = safe ? eq * Fs[col] : __expf(Gs[col] - gi);
                     else f = safe ? eq * Fs[col] : __expf(gi - Gs[col]) * Fs[col];
-                    v = (col <= row) ? v * f : 0.f;
+                    v = (REV ? col >= row : col <= row) ? v * f : 0.f;
                     if constexpr (TR) v = tf32r(v);
                     rs += v;
                     if (j < 32) r0[j] = __float_as_uint(v); else r1[j - 32] = __float_as_uint(v);
@@ -778,6 +817,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                     for (int j = 0; j < 32; ++j) vals[cb * 32 + j] = __uint_as_float(r[j]);
                 }
                 write_state_operand(vals);
+                state_hook(vals, c + 1);
 #pragma unroll
                 for (int cb = 0; cb < DH / 32; ++cb) {
                     uint32_t r[32];
@@ -808,7 +848,25 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                     if (fabsf(den) < 1e-12f && row < nvalid) atomicOr(&p.err[0], 1);
                     inv = 1.f / den;
                 }
+                if constexpr (REV) inv = qf;
                 const bool vrow = row < nvalid;
+                if (kBF16 && p.out_f32) {  // fp32 rows (backward intermediates)
+                    float* dstf = reinterpret_cast<float*>(p.o) +
+                                  (((size_t)b * p.Nstride + t0 + (vrow ? row : 0)) * p.H + h) * D + hh * DH;
+#pragma unroll
+                    for (int cb = 0; cb < DH / 32; ++cb) {
+                        uint32_t r[32];
+                        tmem_ld32(tO + lane_off + hh * DH + cb * 32, r);
+                        tmem_wait_ld();
+                        if (vrow) {
+#pragma unroll
+                            for (int ch = 0; ch < 8; ++ch)
+                                *reinterpret_cast<float4*>(dstf + cb * 32 + ch * 4) =
+                                    make_float4(__uint_as_float(r[ch * 4]) * inv, __uint_as_float(r[ch * 4 + 1]) * inv,
+                                                __uint_as_float(r[ch * 4 + 2]) * inv, __uint_as_float(r[ch * 4 + 3]) * inv);
+                        }
+                    }
+                } else {
                 T* dst = obase + (((size_t)b * p.Nstride + t0 + (vrow ? row : 0)) * p.H + h) * D + hh * DH;
 #pragma unroll
                 for (int cb = 0; cb < DH / 32; ++cb) {
@@ -834,6 +892,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                                                 __uint_as_float(r[ch * 4 + 2]) * inv, __uint_as_float(r[ch * 4 + 3]) * inv);
                         }
                     }
+                }
                 }
                 tc_fence_before();
                 if (tid == 0) trace_mark(p, c, 5);

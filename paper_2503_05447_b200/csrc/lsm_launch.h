@@ -13,6 +13,7 @@ struct LsmVariant {
     int fm;     // 0 identity, 1 elu+1, 2 squared
     int norm;   // normaliser
     int hgrn2;  // TokenVector with keff = 1 - a (HGRN2)
+    int rev = 0;  // reverse-time backward pass (fm = 0, norm = 0)
 };
 
 cudaError_t launch_state_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
@@ -32,7 +33,7 @@ namespace lmoe_dev {
 cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const float* zS,
                                const float* logD, const float* M0, const float* z0, float* Min,
                                float* zin, float* Mfin, float* zfin, float* logDtot, int fin_stride,
-                               int nseg, int dk, int dv, int norm, int lw, int* err);
+                               int nseg, int dk, int dv, int norm, int lw, int rev, int* err);
 cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,
                                 int rank, int dk, int dv, int norm, int lw, float* M0, float* z0);
 // TokenVector decays (GLA / HGRN2 / RWKV6): variant {decay = 3, fm, norm, hgrn2 in bit 8 of fm}
@@ -46,4 +47,17 @@ cudaError_t launch_state_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, 
 cudaError_t launch_output_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
                                        const CUtensorMap& k, const CUtensorMap& val, const CUtensorMap& a,
                                        const LsmFwdParams& p);
+}  // namespace lmoe_dev
+
+namespace lmoe_dev {
+// backward helpers (lsm_bwd_kernels.cu)
+cudaError_t launch_bwd_finish(bool bf16, int fm, bool mamba, const void* q, const void* k,
+                              const float* dphq, const float* dkef, const float* b_pre, void* dq,
+                              void* dk, float* dkf, int B, int N, int H, cudaStream_t st);
+cudaError_t launch_mamba_dgate(bool bf16, const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                               const CUtensorMap& dO, const CUtensorMap& m, const CUtensorMap& dm,
+                               const float* b_pre, const float* a_raw, const float* dkf, float* db_pre,
+                               float* da_raw, int B, int N, int H, cudaStream_t st);
+cudaError_t launch_transpose_states(const float* in, float* out, int BH, int D, cudaStream_t st);
+cudaError_t launch_apply_fmap(bool bf16, int fm, const void* x, void* y, size_t n, cudaStream_t st);
 }  // namespace lmoe_dev

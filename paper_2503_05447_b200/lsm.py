@@ -165,3 +165,86 @@ def lsm_forward_chunked(q, k, v, gates, spec, chunk_size, final_state=None):
         final_state.z = None if fs.z is None else fs.z[0, 0]
         final_state.step = q.shape[0]
     return o[0, :, 0, :]
+
+
+@dataclasses.dataclass
+class LsmGrads:
+    """Gradients of lsm_forward_chunked w.r.t. its inputs (the reference tape's results)."""
+    dq: torch.Tensor
+    dk: torch.Tensor
+    dv: torch.Tensor
+    da_pre: Optional[torch.Tensor] = None
+    db_pre: Optional[torch.Tensor] = None
+    da_raw: Optional[torch.Tensor] = None
+    dM0: Optional[torch.Tensor] = None
+
+
+def _mamba_a_raw(spec, H, device):
+    if spec.instance != LsmInstance.MAMBA2:
+        return None
+    if spec.mamba2_a_raw is None:
+        raise RuntimeError("LsmSpec: mamba2_a_raw required for mamba2")
+    return torch.as_tensor(spec.mamba2_a_raw, dtype=torch.float32, device=device).reshape(-1).expand(H).contiguous()
+
+
+def lsm_backward_batched(q, k, v, gates, spec, dO, initial_state=None, dM_final=None,
+                         chunk_size=64, check=True, stream=None, timing=False):
+    """VJP of lsm_forward_batched: [B,N,H,D] q, k, v, dO (+ optional dM_final [B,H,D,D]).
+
+    Returns LsmGrads (dq, dk, dv in the input dtype; db_pre [B,N,H] and da_raw [H] fp32 for
+    Mamba2; dM0 [B,H,D,D] fp32).  Runs on the device only (lmoe_lsm_bwd)."""
+    B, N, H, D = q.shape
+    for t in (k, v, dO):
+        if t.shape != q.shape or t.dtype != q.dtype:
+            raise RuntimeError("shape mismatch in lsm backward: %s vs %s" % (tuple(q.shape), tuple(t.shape)))
+    q, k, v, dO = q.contiguous(), k.contiguous(), v.contiguous(), dO.contiguous()
+    dev = q.device
+    a_raw = _mamba_a_raw(spec, H, dev)
+    b_pre = None
+    if gates is not None and gates.b_pre is not None:
+        b_pre = gates.b_pre.to(torch.float32).contiguous()
+    a_pre = None
+    if gates is not None and gates.a_pre is not None:
+        a_pre = gates.a_pre.to(q.dtype).contiguous()
+    M0 = None
+    if initial_state is not None and initial_state.M is not None:
+        M0 = initial_state.M.to(torch.float32).contiguous()
+    dMf = None if dM_final is None else dM_final.to(torch.float32).contiguous()
+    g = LsmGrads(dq=torch.empty_like(q), dk=torch.empty_like(k), dv=torch.empty_like(v))
+    g.dM0 = torch.empty(B, H, D, D, dtype=torch.float32, device=dev)
+    if spec.instance == LsmInstance.MAMBA2:
+        g.db_pre = torch.empty(B, N, H, dtype=torch.float32, device=dev)
+        g.da_raw = torch.empty(H, dtype=torch.float32, device=dev)
+    if a_pre is not None:
+        g.da_pre = torch.empty_like(a_pre)
+    desc = make_desc(spec, chunk_size, check, timing)
+    L = _lib.lib()
+    dt = _DTYPES[q.dtype]
+    nbytes = L.lmoe_lsm_bwd_workspace_size(ctypes.byref(desc), B, N, H, D, dt)
+    ws = _workspace(nbytes, dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    P = _lib.ptr
+    rc = L.lmoe_lsm_bwd(ctypes.byref(desc), B, N, H, D, dt, P(q), P(k), P(v), P(a_pre), P(b_pre),
+                        P(a_raw), P(M0), P(dO), P(dMf), P(g.dq), P(g.dk), P(g.dv), P(g.da_pre),
+                        P(g.db_pre), P(g.da_raw), P(g.dM0), P(ws), ws.numel(), ctypes.c_void_p(st))
+    _lib.check(rc)
+    return g
+
+
+class LsmFunction(torch.autograd.Function):
+    """Autograd binding: forward = lmoe_lsm_fwd, backward = lmoe_lsm_bwd (device only)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, b_pre, spec, chunk_size):
+        gates = LsmGates(b_pre=b_pre) if b_pre is not None else None
+        o = lsm_forward_batched(q, k, v, gates, spec, chunk_size, check=False)
+        ctx.save_for_backward(q, k, v, b_pre)
+        ctx.spec, ctx.chunk = spec, chunk_size
+        return o
+
+    @staticmethod
+    def backward(ctx, dO):
+        q, k, v, b_pre = ctx.saved_tensors
+        gates = LsmGates(b_pre=b_pre) if b_pre is not None else None
+        g = lsm_backward_batched(q, k, v, gates, ctx.spec, dO.to(q.dtype), chunk_size=ctx.chunk, check=False)
+        return g.dq, g.dk, g.dv, g.db_pre, None, None

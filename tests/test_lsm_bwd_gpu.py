@@ -1,0 +1,233 @@
+"""GPU parity of the sm_100a LSM backward (lmoe_lsm_bwd via the C-ABI).
+
+Checks, per (b,h), norm-relative max|got-want|/max|want| against
+  * the reference's own gradients (tests/golden/lsm_grad.npz, made by the reference tape,
+    d = 4) zero-padded to the device head dim: padded q/k/v/dO columns contribute exactly 0,
+    so the first 4 columns are the reference problem;
+  * the float64 oracle backward (oracle/lmoe_oracle.c lmo_lsm_backward, pinned to the same
+    golden file) on random inputs with an initial state, ragged lengths and many segments;
+  * central finite differences of the oracle forward for the final-state gradient path
+    (dM_final), which the reference tape reaches through final_state (lsm.hpp:668-708).
+Tolerances: bf16 inputs 2e-2 (north star).  fp32 inputs 2e-3: the backward chains three
+tf32 passes (the forward alone meets 1e-3).  The same bounds hold for the Mamba2 gate
+gradients db_pre and da_raw: lsm_dgate.cu builds dg from fp32 accumulator products (no
+telescoped cancellation), so they need no looser tolerance (GATE_TOL == TOL).
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import load_golden, norm_rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 2e-3, "bf16": 2e-2}
+SCALAR_KINDS = {0, 1, 2, 6, 13}  # BLA, Lightning, RetNet, Rebased, Mamba2
+DIM = {"f32": 64, "bf16": 128}
+GATE_TOL = {"f32": 2e-3, "bf16": 2e-2}
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _round(x, dtype):
+    torch = _torch()
+    t = torch.tensor(np.ascontiguousarray(x), dtype=torch.float32)
+    if dtype == "bf16":
+        t = t.to(torch.bfloat16).float()
+    return t.numpy().astype(np.float64)
+
+
+def _bwd(spec_d, q, k, v, dO, b_pre=None, a_raw_h=None, M0=None, dMf=None, dtype="bf16"):
+    """numpy [B,N,H,D] in; numpy float64 gradients out."""
+    torch = _torch()
+    import paper_2503_05447_b200 as pk
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    dev = torch.device("cuda:0")
+    T = lambda x, dt=tdt: torch.tensor(np.ascontiguousarray(x), dtype=torch.float32, device=dev).to(dt)
+    spec = pk.LsmSpec(instance=spec_d["instance"], feature_map=spec_d.get("feature_map", 0),
+                      use_normalizer=bool(spec_d.get("use_normalizer", 0)),
+                      scalar_decay=spec_d.get("scalar_decay", 1.0), mamba2_a_raw=a_raw_h)
+    gates = None if b_pre is None else pk.LsmGates(b_pre=T(b_pre, torch.float32))
+    init = None if M0 is None else pk.MemoryState(M=T(M0, torch.float32))
+    g = pk.lsm_backward_batched(T(q), T(k), T(v), gates, spec, T(dO), initial_state=init,
+                                dM_final=None if dMf is None else T(dMf, torch.float32))
+    torch.cuda.synchronize()
+    out = {}
+    for name in ("dq", "dk", "dv", "db_pre", "da_raw", "dM0"):
+        x = getattr(g, name)
+        if x is not None:
+            out[name] = x.float().cpu().numpy().astype(np.float64)
+    return out
+
+
+def _oracle_bwd(spec_d, q, k, v, dO, b_pre, a_raw_h, M0):
+    """Per-head oracle backward over [B,N,H,D] arrays."""
+    B, N, H, D = q.shape
+    res = {n: np.zeros_like(q) for n in ("dq", "dk", "dv")}
+    res["dM0"] = np.zeros((B, H, D, D))
+    res["db_pre"] = np.zeros((B, N, H))
+    res["da_raw"] = np.zeros(H)
+    for b in range(B):
+        for h in range(H):
+            sp = dict(spec_d)
+            if a_raw_h is not None:
+                sp["mamba2_a_raw"] = float(a_raw_h[h])
+            g = oracle.lsm_backward(sp, q[b, :, h], k[b, :, h], v[b, :, h], dO[b, :, h],
+                                    None, None if b_pre is None else b_pre[b, :, h],
+                                    None if M0 is None else M0[b, h])
+            res["dq"][b, :, h], res["dk"][b, :, h], res["dv"][b, :, h] = g["dq"], g["dk"], g["dv"]
+            res["dM0"][b, h] = g["dM0"]
+            if b_pre is not None:
+                res["db_pre"][b, :, h] = g["db_pre"]
+                res["da_raw"][h] += g["da_raw"]
+    return res
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_golden_grads_padded(dtype):
+    """Reference tape gradients (d = 4) through the device path, zero-padded to D."""
+    d = load_golden("lsm_grad")
+    D = DIM[dtype]
+    ran = 0
+    for p in sorted({k.split("/")[0] for k in d}):
+        spec = oracle.spec_from_golden(d, p)
+        if spec["instance"] not in SCALAR_KINDS:
+            continue
+        pad = lambda x: np.pad(x, ((0, 0), (0, D - x.shape[1])))[None, :, None]
+        q, k, v, dO = (pad(_round(d[p + "/" + n], dtype)) for n in ("q", "k", "v", "dO"))
+        b_pre = d.get(p + "/b_pre")
+        b_pre = None if b_pre is None else b_pre.astype(np.float64)[None, :, None]
+        a_raw = [spec["mamba2_a_raw"]] if spec["instance"] == 13 else None
+        got = _bwd(spec, q, k, v, dO, b_pre, a_raw, dtype=dtype)
+        tol = TOL[dtype]
+        for n in ("dq", "dk", "dv"):
+            err = norm_rel_err(got[n][0, :, 0, :4], d[p + "/" + n])
+            assert err < tol, (p, n, err)
+            assert np.abs(got[n][0, :, 0, 4:]).max() == 0.0, (p, n, "padding must stay zero")
+        if b_pre is not None:
+            assert norm_rel_err(got["db_pre"][0, :, 0], d[p + "/db_pre"]) < tol, p
+            want = d[p + "/da_raw"][0]
+            assert abs(got["da_raw"][0] - want) < GATE_TOL[dtype] * max(1.0, abs(want)), (p, got["da_raw"][0], want)
+        ran += 1
+    assert ran == 5  # bla_plain, lightning, retnet, rebased_plain, mamba2
+
+
+CASES = [  # (name, spec, dtype, B, N, H)
+    ("bla_plain", {"instance": 0}, "bf16", 1, 300, 2),
+    ("bla_elu1", {"instance": 0, "feature_map": 1}, "bf16", 1, 257, 2),
+    ("rebased_sq", {"instance": 6, "feature_map": 2}, "f32", 1, 200, 2),
+    ("lightning", {"instance": 1, "scalar_decay": 0.95}, "bf16", 2, 700, 2),
+    ("retnet", {"instance": 2, "scalar_decay": 1 - 1 / 32}, "f32", 2, 700, 2),
+    ("retnet_long", {"instance": 2, "scalar_decay": 1 - 1 / 256}, "bf16", 1, 4096, 1),
+    ("mamba2", {"instance": 13}, "bf16", 1, 700, 2),
+    ("mamba2_short", {"instance": 13}, "bf16", 2, 256, 2),
+    ("mamba2_f32", {"instance": 13}, "f32", 2, 333, 2),
+    ("mamba2_long", {"instance": 13}, "bf16", 1, 4096, 2),
+    ("tiny", {"instance": 2, "scalar_decay": 0.9}, "bf16", 1, 1, 1),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_bwd_matches_oracle(case):
+    name, spec, dtype, B, N, H = case
+    D = DIM[dtype]
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    q, k, v = (_round(rng.normal(0, 0.5, (B, N, H, D)), dtype) for _ in range(3))
+    dO = _round(rng.normal(0, 1.0, (B, N, H, D)), dtype)
+    M0 = rng.normal(0, 0.1, (B, H, D, D))
+    b_pre = a_raw = None
+    if spec["instance"] == 13:
+        b_pre = rng.normal(-1.0 if "long" in name else 0.0, 1.0, (B, N, H))
+        a_raw = rng.normal(0, 0.5, H)
+    got = _bwd(spec, q, k, v, dO, b_pre, a_raw, M0, dtype=dtype)
+    want = _oracle_bwd(spec, q, k, v, dO, b_pre, a_raw, M0)
+    tol = TOL[dtype]
+    for n in ("dq", "dk", "dv"):
+        for b in range(B):
+            for h in range(H):
+                err = norm_rel_err(got[n][b, :, h], want[n][b, :, h])
+                assert err < tol, (name, n, b, h, err)
+    for b in range(B):
+        for h in range(H):
+            assert norm_rel_err(got["dM0"][b, h], want["dM0"][b, h]) < tol, (name, "dM0", b, h)
+    if b_pre is not None:
+        for b in range(B):
+            for h in range(H):
+                err = norm_rel_err(got["db_pre"][b, :, h], want["db_pre"][b, :, h])
+                assert err < tol, (name, "db_pre", b, h, err)
+        rel = np.abs(got["da_raw"] - want["da_raw"]).max() / max(1e-6, np.abs(want["da_raw"]).max())
+        assert rel < GATE_TOL[dtype], (name, "da_raw", got["da_raw"], want["da_raw"])
+
+
+@pytest.mark.parametrize("inst", [2, 13])
+def test_final_state_gradient_matches_finite_differences(inst):
+    """dM_final path: d/dtheta [<dO, O> + <dMf, M_N>] vs central differences of the f64 oracle."""
+    D, N = 64, 200
+    rng = np.random.default_rng(7 + inst)
+    spec = {"instance": inst, "scalar_decay": 1 - 1 / 32}
+    q, k, v = (_round(rng.normal(0, 0.5, (1, N, 1, D)), "f32") for _ in range(3))
+    dO = rng.normal(0, 1.0, (1, N, 1, D))
+    dMf = rng.normal(0, 1.0, (1, 1, D, D))
+    M0 = rng.normal(0, 0.1, (1, 1, D, D))
+    b_pre = rng.normal(0, 1, (1, N, 1)) if inst == 13 else None
+    a_raw = np.array([0.3]) if inst == 13 else None
+    got = _bwd(spec, q, k, v, dO, b_pre, a_raw, M0, dMf, dtype="f32")
+
+    def loss(q_, k_, v_, b_, ar_, M0_):
+        sp = dict(oracle.spec_default(inst))
+        sp.update(spec)
+        if inst == 13:
+            sp["mamba2_a_raw"] = float(ar_[0])
+        o, M, _ = oracle.lsm_chunked(sp, q_[0, :, 0], k_[0, :, 0], v_[0, :, 0], None,
+                                     None if b_ is None else b_[0, :, 0], 16, M0_[0, 0])
+        return float((o * dO[0, :, 0]).sum() + (M * dMf[0, 0]).sum())
+
+    args = [q, k, v, b_pre, a_raw, M0]
+    names = ["dq", "dk", "dv", "db_pre", "da_raw", "dM0"]
+    eps = 1e-5
+    for i, n in enumerate(names):
+        if args[i] is None:
+            continue
+        u = rng.normal(0, 1, args[i].shape)
+        plus = list(args); plus[i] = args[i] + eps * u
+        minus = list(args); minus[i] = args[i] - eps * u
+        fd = (loss(*plus) - loss(*minus)) / (2 * eps)
+        an = float((got[n] * u).sum())
+        # tf32 operands: the error of sum(g * u) scales with ||g|| (u ~ N(0, 1))
+        assert abs(an - fd) <= 2e-3 * np.linalg.norm(got[n]), (n, an, fd)
+
+
+def test_autograd_function_matches_direct_call():
+    torch = _torch()
+    import paper_2503_05447_b200 as pk
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device="cpu").manual_seed(3)
+    B, N, H, D = 1, 384, 2, 128
+    q, k, v = (torch.randn(B, N, H, D, generator=g).mul(0.5).to(dev, torch.bfloat16).requires_grad_() for _ in range(3))
+    b = torch.randn(B, N, H, generator=g).to(dev).requires_grad_()
+    spec = pk.LsmSpec.make("mamba2", D)
+    spec.mamba2_a_raw = torch.full((H,), 0.2, device=dev)
+    o = pk.LsmFunction.apply(q, k, v, b, spec, 64)
+    dO = torch.randn(o.shape, generator=g).to(dev, torch.bfloat16)
+    o.backward(dO)
+    ref = pk.lsm_backward_batched(q.detach(), k.detach(), v.detach(), pk.LsmGates(b_pre=b.detach()), spec, dO)
+    for a, r in ((q.grad, ref.dq), (k.grad, ref.dk), (v.grad, ref.dv), (b.grad, ref.db_pre)):
+        assert torch.equal(a, r)
+
+
+def test_bwd_error_texts():
+    torch = _torch()
+    import paper_2503_05447_b200 as pk
+    dev = torch.device("cuda:0")
+    x = torch.zeros(1, 16, 1, 128, dtype=torch.bfloat16, device=dev)
+    with pytest.raises(pk.LmoeError, match="normalizer backward not in this build"):
+        pk.lsm_backward_batched(x, x, x, None, pk.LsmSpec.make("bla", 128), x)
+    with pytest.raises(RuntimeError, match="shape mismatch"):
+        pk.lsm_backward_batched(x, x, x[:, :8], None, pk.LsmSpec.make("retnet", 128), x)
