@@ -145,6 +145,41 @@ inline void sp_lsm_masked_rank(void* nccl_comm, int rank, int world, const LsmVi
                           reinterpret_cast<lmoe_stream_t>(stream)));
 }
 
+// sp_lsm_nomask_rank (parallel.hpp:282-297): O = phiQ . sum over ranks of phiK^T V, one gather.
+inline void sp_lsm_nomask_rank(void* nccl_comm, int rank, int world, const LsmView& x_loc, const LsmSpec& spec,
+                               Workspace* ws = nullptr, cudaStream_t stream = nullptr, bool check_device = true) {
+    Workspace local;
+    Workspace& w = ws ? *ws : local;
+    const lmoe_lsm_desc d = to_desc(spec, 64, check_device);
+    const size_t need = lmoe_sp_lsm_nomask_workspace_size(&d, x_loc.B, x_loc.N, x_loc.H, x_loc.D, x_loc.dtype, world);
+    void* wsp = w.get(need);
+    check(lmoe_sp_lsm_nomask_fwd(&d, x_loc.B, x_loc.N, x_loc.H, x_loc.D, x_loc.dtype, x_loc.q, x_loc.k, x_loc.v,
+                                 x_loc.o, nccl_comm, rank, world, wsp, w.size(),
+                                 reinterpret_cast<lmoe_stream_t>(stream)));
+}
+
+// Gradients of lsm_forward_chunked (the reference tape, tensor.hpp:1178-1215): device
+// buffers in the layouts of lmoe_lsm_bwd.
+struct LsmGrads {
+    void *dq = nullptr, *dk = nullptr, *dv = nullptr, *da_pre = nullptr;
+    float* db_pre = nullptr;  // [B, N, H]   Mamba2
+    float* da_raw = nullptr;  // [H]         Mamba2
+    float* dM0 = nullptr;     // [B, H, D, D]
+};
+inline void lsm_backward_chunked(const LsmView& x, const LsmGates& gates, const LsmSpec& spec, const void* dO,
+                                 const LsmGrads& g, const MemoryState* initial_state = nullptr,
+                                 const float* dM_final = nullptr, Workspace* ws = nullptr,
+                                 cudaStream_t stream = nullptr, bool check_device = true) {
+    Workspace local;
+    Workspace& w = ws ? *ws : local;
+    const lmoe_lsm_desc d = to_desc(spec, 64, check_device);
+    const size_t need = lmoe_lsm_bwd_workspace_size(&d, x.B, x.N, x.H, x.D, x.dtype);
+    void* wsp = w.get(need);
+    check(lmoe_lsm_bwd(&d, x.B, x.N, x.H, x.D, x.dtype, x.q, x.k, x.v, gates.a_pre, gates.b_pre, spec.mamba2_a_raw,
+                       initial_state ? initial_state->M : nullptr, dO, dM_final, g.dq, g.dk, g.dv, g.da_pre,
+                       g.db_pre, g.da_raw, g.dM0, wsp, w.size(), reinterpret_cast<lmoe_stream_t>(stream)));
+}
+
 // chunk_range (parallel.hpp:192-197)
 inline std::pair<int, int> chunk_range(int n, int t, int rank) {
     if (n < t) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");

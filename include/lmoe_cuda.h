@@ -88,6 +88,25 @@ int lmoe_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dty
                  lmoe_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Unmasked LSM sequence parallelism (paper Alg. 1).  Replaces sp_lsm_nomask_rank
+ * (parallel.hpp:282-297): O_t = phi(Q_t) . sum_i phi(K_i)^T V_i over ALL ranks, with one
+ * all-gather of exactly T * d_k * d_v fp32 elements per (b, h).  Undecayed instances only
+ * ("sp_forward_nomask: requires an undecayed instance"), no normaliser
+ * ("sp_forward_nomask: normalizer unsupported").  The loopback variant runs `world`
+ * virtual ranks over a full [B,N,H,D] sequence on one device (chunk_range slices).
+ * ------------------------------------------------------------------------------------- */
+size_t lmoe_sp_lsm_nomask_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local, int H,
+                                         int D, lmoe_dtype dtype, int world);
+int lmoe_sp_lsm_nomask_fwd(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
+                           lmoe_dtype dtype, const void* q, const void* k, const void* v, void* o,
+                           void* nccl_comm, int rank, int world, void* workspace,
+                           size_t workspace_bytes, lmoe_stream_t stream);
+int lmoe_sp_lsm_nomask_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                                    lmoe_dtype dtype, const void* q, const void* k, const void* v,
+                                    void* o, int world, void* workspace, size_t workspace_bytes,
+                                    lmoe_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * LSM backward: the vector-Jacobian product the reference's tape computes through
  * lsm_forward_chunked (tensor.hpp:1178-1215; ops of lsm.hpp:483-598), for every (b, h).
  * Inputs as lmoe_lsm_fwd plus dO [B,N,H,D] and the optional final-state gradient dM_final

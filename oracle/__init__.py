@@ -180,6 +180,16 @@ def sp_forward_masked(spec, q, k, v, world, a_pre=None, b_pre=None, rank_chunk=0
     return o
 
 
+def sp_forward_nomask(spec, q, k, v, world):
+    """sp_forward_nomask (parallel.hpp:391-403): non-causal O = phi(Q) sum_r phi(K_r)^T V_r."""
+    q, k, v = map(_f64, (q, k, v))
+    n, dk = q.shape
+    dv = v.shape[1]
+    o = np.zeros((n, dv))
+    _run(lib().lmo_sp_forward_nomask, ctypes.byref(_spec(spec)), n, dk, dv, world, _p(q), _p(k), _p(v), _p(o))
+    return o
+
+
 def sp_payload_width(spec, dv):
     sp = _spec(spec)
     return lib().lmo_sp_payload_width(ctypes.byref(sp), dv)

@@ -554,6 +554,42 @@ void lmo_sp_combine(const lmo_spec* s, int d_k, int d_v, int rank, const double*
     free(factor);
 }
 
+/* sp_forward_nomask (parallel.hpp:391-403) / sp_lsm_nomask_rank (:282-297) */
+int lmo_sp_forward_nomask(const lmo_spec* s, int n, int d_k, int d_v, int world,
+                          const double* q, const double* k, const double* v, double* o,
+                          char* err, int errlen) {
+    if (lmo_spec_validate(s, d_k, d_v, err, errlen)) return -1;
+    if (lmo_decay_kind(s->instance) != LMO_DK_NONE) {
+        set_err(err, errlen, "sp_forward_nomask: requires an undecayed instance");
+        return -1;
+    }
+    if (s->use_normalizer) { set_err(err, errlen, "sp_forward_nomask: normalizer unsupported"); return -1; }
+    if (world < 1 || n < world) { set_err(err, errlen, "chunk_range: need at least one row per rank"); return -1; }
+    const size_t dd = (size_t)d_k * d_v;
+    double* Mg = (double*)calloc(dd, sizeof(double));
+    double* Ml = (double*)malloc(sizeof(double) * dd);
+    /* per rank: m_local = phi(K_r)^T V_r, then m_global = all[0] + all[1] + ... (rank order) */
+    for (int r = 0; r < world; ++r) {
+        int r0, r1;
+        lmo_chunk_range(n, world, r, &r0, &r1);
+        memset(Ml, 0, sizeof(double) * dd);
+        for (int t = r0; t < r1; ++t)
+            for (int i = 0; i < d_k; ++i) {
+                const double pk = fmap(s->feature_map, k[(size_t)t * d_k + i]);
+                for (int j = 0; j < d_v; ++j) Ml[i * d_v + j] += pk * v[(size_t)t * d_v + j];
+            }
+        for (size_t e = 0; e < dd; ++e) Mg[e] += Ml[e];
+    }
+    for (int t = 0; t < n; ++t)
+        for (int j = 0; j < d_v; ++j) {
+            double acc = 0.0;
+            for (int i = 0; i < d_k; ++i) acc += fmap(s->feature_map, q[(size_t)t * d_k + i]) * Mg[i * d_v + j];
+            o[(size_t)t * d_v + j] = acc;
+        }
+    free(Mg); free(Ml);
+    return 0;
+}
+
 /* sp_forward_masked (parallel.hpp:405-418) / sp_lsm_masked_rank (:303-376) */
 int lmo_sp_forward_masked(const lmo_spec* s, int n, int d_k, int d_v, int world,
                           int rank_chunk, const double* q, const double* k, const double* v,

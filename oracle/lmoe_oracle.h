@@ -121,6 +121,15 @@ int lmo_sp_forward_masked(const lmo_spec* s, int n, int d_k, int d_v, int world,
                           char* err, int errlen);
 
 /*
+ * sp_forward_nomask (parallel.hpp:391-403) with sp_lsm_nomask_rank (:282-297): every
+ * rank's local phi(K)^T V is gathered and summed; O = phi(Q) . sum.  Returns -1 with the
+ * reference's texts for decayed instances or the normaliser.
+ */
+int lmo_sp_forward_nomask(const lmo_spec* s, int n, int d_k, int d_v, int world,
+                          const double* q, const double* k, const double* v, double* o,
+                          char* err, int errlen);
+
+/*
  * The per-rank pieces of the same algorithm, so a multi-process harness
  * (tests/test_sp_gloo.py) can run the exchange itself:
  *  payload  = [M | z? | D?] of the local slice from zero (d_k x pw, pw =

@@ -327,6 +327,28 @@ void golden_sp() {
         }
         ++ci;
     }
+    // unmasked SP, Alg. 1 (parallel.hpp:282-297, 391-403)
+    for (const char* tag : {"bla_plain", "rebased_plain"}) {
+        const Variant* var = nullptr;
+        for (const Variant& v : kVariants) if (std::string(v.tag) == tag) var = &v;
+        Rng rng(13500 + ci);
+        LsmSpec spec = make_spec(*var, d, rng);
+        const Tensor q = Tensor::randn({n, d}, rng, 0.5);
+        const Tensor k = Tensor::randn({n, d}, rng, 0.5);
+        const Tensor v = Tensor::randn({n, d}, rng, 0.5);
+        const std::string p = std::string("spn/") + tag;
+        emit_spec(p, spec);
+        emit(p + "/q", q);
+        emit(p + "/k", k);
+        emit(p + "/v", v);
+        for (int t : {1, 2, 4, 8}) {
+            RankGroup grp(t);
+            emit(p + "/o_t" + std::to_string(t), sp_forward_nomask(grp, q, k, v, spec));
+            emit_scalar(p + "/comm_elems_t" + std::to_string(t),
+                        (double)(grp.comm_log().empty() ? 0 : grp.comm_log()[0].elements));
+        }
+        ++ci;
+    }
     // attention with row offset + KV all-gather SP (attention.hpp:18-38, parallel.hpp:380-387)
     Rng rng(14000);
     const int na = 24;

@@ -75,6 +75,23 @@ __global__ void sp_rank_combine(const float* __restrict__ gathered, int P, int B
     else z0[(size_t)bh * dk + (e - nm)] = acc;
 }
 
+// Unmasked SP (parallel.hpp:293-296): M_global = sum over all ranks of the gathered
+// local states [world][BH][nm].
+__global__ void sp_sum_states(const float* __restrict__ gathered, int world, int BH, int nm,
+                              float* __restrict__ M) {
+    const int bh = blockIdx.y;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nm) return;
+    float acc = 0.f;
+    for (int i = 0; i < world; ++i) acc += gathered[((size_t)i * BH + bh) * nm + e];
+    M[(size_t)bh * nm + e] = acc;
+}
+
+cudaError_t launch_sum_states(const float* gathered, int world, int BH, int nm, float* M, cudaStream_t st) {
+    sp_sum_states<<<dim3((nm + 255) / 256, BH), 256, 0, st>>>(gathered, world, BH, nm, M);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const float* zS,
                                const float* logD, const float* M0, const float* z0, float* Min,
                                float* zin, float* Mfin, float* zfin, float* logDtot, int fin_stride,

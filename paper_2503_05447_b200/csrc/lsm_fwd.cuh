@@ -59,6 +59,8 @@ struct LsmFwdParams {
     int order;           // phase-3 schedule: 0 = P epilogue first, 1 = transforms first
     int out_f32;         // bf16 inputs, fp32 output rows (backward intermediates)
     int rev_kfq;         // REV passes: scale output rows by kf_i = softplus(b_i) (Mamba2 keff query)
+    int nomask;          // unmasked SP (sp_lsm_nomask_rank): O = phiQ M_in[bh], no intra term,
+                         // no state update; Min is [B*H][dk][dv] (shared by all segments)
     // backward side channel (Mamba2 gate gradients, lsm_dgate.cu): the state operand of every
     // chunk (the state before it in forward order, the state gradient after it in REV order)
     // written to mst [BH][nchunk_tot][D][D] in T

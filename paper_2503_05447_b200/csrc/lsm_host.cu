@@ -533,6 +533,119 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
     });
 }
 
+// ------------------------------------------------------------------ unmasked SP (Alg. 1)
+// sp_lsm_nomask_rank (parallel.hpp:282-297): local phiK^T V, ONE all-gather of the
+// T * d_k * d_v state elements per head, global sum, O = phiQ . sum.
+namespace lmoe_host {
+static void validate_nomask(const lmoe_lsm_desc* d) {
+    if (device_decay_mode(d->instance) != lmoe_dev::kDecayNone)
+        throw Error(LMOE_ERR_ARG, "sp_forward_nomask: requires an undecayed instance");
+    if (d->use_normalizer) throw Error(LMOE_ERR_ARG, "sp_forward_nomask: normalizer unsupported");
+}
+template <typename T>
+static void nomask_local_state(LsmCall& c, float* slot) {
+    c.state_pass<T>();
+    c.combine(nullptr, nullptr, false, slot, nullptr, nullptr, c.D * c.D);
+}
+template <typename T>
+static void nomask_output(LsmCall& c, const float* Mglobal) {
+    c.p.Min = Mglobal;
+    c.p.nomask = 1;
+    c.output_pass<T>();
+}
+}  // namespace lmoe_host
+
+extern "C" size_t lmoe_sp_lsm_nomask_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local, int H,
+                                                    int D, lmoe_dtype dtype, int world) {
+    return lmoe_sp_lsm_fwd_workspace_size(desc, B, N_local, H, D, dtype, world);
+}
+
+extern "C" int lmoe_sp_lsm_nomask_fwd(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
+                                      lmoe_dtype dtype, const void* q, const void* k, const void* v,
+                                      void* o, void* nccl_comm, int rank, int world, void* workspace,
+                                      size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, B, N_local, H, D, dtype, q, k, v, o);
+        validate_nomask(desc);
+        if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_nomask_fwd: bad rank");
+        if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_nomask_fwd: null communicator");
+        const SpWorkspace w = plan_sp(desc, B, N_local, H, D, world);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_nomask_fwd: workspace too small (need " +
+                                          std::to_string(w.total) + " bytes)");
+        uint8_t* ws = static_cast<uint8_t*>(workspace);
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        LsmCall c{desc, B, N_local, N_local, H, D, dtype, q, k, v, nullptr, nullptr, o, ws, w.pl, st, nullptr};
+        c.setup();
+        c.clear_err();
+        float* payload = reinterpret_cast<float*>(ws + w.off_payload);
+        float* gathered = reinterpret_cast<float*>(ws + w.off_gathered);
+        float* Mg = reinterpret_cast<float*>(ws + w.off_M0);
+        const size_t P = (size_t)B * H * D * D;
+        if (dtype == LMOE_BF16) nomask_local_state<__nv_bfloat16>(c, payload);
+        else nomask_local_state<float>(c, payload);
+        if (world > 1) {
+            NCCL_CHECK(ncclAllGather(payload, gathered, P, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
+        } else {
+            LMOE_CUDA_CHECK(cudaMemcpyAsync(gathered, payload, P * 4, cudaMemcpyDeviceToDevice, st));
+        }
+        g_last_gather_elements = (long long)world * (long long)P;
+        LMOE_CUDA_CHECK(lmoe_dev::launch_sum_states(gathered, world, B * H, D * D, Mg, st));
+        ++g_launch_count;
+        if (dtype == LMOE_BF16) nomask_output<__nv_bfloat16>(c, Mg);
+        else nomask_output<float>(c, Mg);
+        c.finish_timing();
+        c.check_err();
+    });
+}
+
+extern "C" int lmoe_sp_lsm_nomask_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                                               lmoe_dtype dtype, const void* q, const void* k, const void* v,
+                                               void* o, int world, void* workspace, size_t workspace_bytes,
+                                               lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, B, N, H, D, dtype, q, k, v, o);
+        validate_nomask(desc);
+        if (world < 1 || N < world) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");
+        const SpWorkspace w = plan_sp(desc, B, (N + world - 1) / world, H, D, world);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_nomask_fwd_loopback: workspace too small");
+        uint8_t* ws = static_cast<uint8_t*>(workspace);
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const size_t esz = dtype == LMOE_BF16 ? 2 : 4;
+        const size_t P = (size_t)B * H * D * D;
+        float* gathered = reinterpret_cast<float*>(ws + w.off_gathered);
+        float* Mg = reinterpret_cast<float*>(ws + w.off_M0);
+        auto slice_call = [&](int r) {
+            const int base = N / world, rem = N % world;  // chunk_range (parallel.hpp:192-197)
+            const int r0 = r * base + std::min(r, rem);
+            const int len = base + (r < rem ? 1 : 0);
+            const size_t off = (size_t)r0 * H * D * esz;
+            LsmCall c{desc, B, len, N, H, D, dtype,
+                      static_cast<const uint8_t*>(q) + off, static_cast<const uint8_t*>(k) + off,
+                      static_cast<const uint8_t*>(v) + off, nullptr, nullptr,
+                      static_cast<uint8_t*>(o) + off, ws, plan_lsm(B, len, H, D), st, nullptr};
+            c.setup();
+            return c;
+        };
+        slice_call(0).clear_err();
+        for (int r = 0; r < world; ++r) {
+            LsmCall c = slice_call(r);
+            if (dtype == LMOE_BF16) nomask_local_state<__nv_bfloat16>(c, gathered + r * P);
+            else nomask_local_state<float>(c, gathered + r * P);
+        }
+        g_last_gather_elements = (long long)world * (long long)P;
+        LMOE_CUDA_CHECK(lmoe_dev::launch_sum_states(gathered, world, B * H, D * D, Mg, st));
+        ++g_launch_count;
+        for (int r = 0; r < world; ++r) {
+            LsmCall c = slice_call(r);
+            if (dtype == LMOE_BF16) nomask_output<__nv_bfloat16>(c, Mg);
+            else nomask_output<float>(c, Mg);
+        }
+        slice_call(0).check_err();
+    });
+}
+
 // ------------------------------------------------------------------------------- backward
 // Three chunk passes, each a segment-parallel state pass + combine + output pass:
 //   dq pass  (forward order)  q'=dO, k'=v, v'=phi(k), M0' = M0^T    -> dphi(q) fp32, M_N^T

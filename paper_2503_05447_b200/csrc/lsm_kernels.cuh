@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                             mma_ss_tf32(tO, a, bd, idQM, acc);
                         }
                     }
+                    if (p.nomask) return;  // the state is the global sum, never updated
 #pragma unroll
                     for (int kk = 0; kk < kC / TT::KSTEP; ++kk) {
                         if constexpr (!TR) {
@@ -619,7 +620,8 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             mbar_wait(&gfull[0], 0);
             const float g0 = __expf(ringS[0]);
             float vals[DH];
-            const float* src = p.Min + (((size_t)bh * p.nseg + seg) * D + (sown ? srow : 0)) * D + hh * DH;
+            const size_t mslot = p.nomask ? (size_t)bh : (size_t)bh * p.nseg + seg;
+            const float* src = p.Min + (mslot * D + (sown ? srow : 0)) * D + hh * DH;
 #pragma unroll
             for (int j = 0; j < DH; j += 4) {
                 const float4 v = sown ? *reinterpret_cast<const float4*>(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -765,7 +767,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                     if constexpr (DECAY == kDecayNone) f = 1.f;
                     else if constexpr (REV) f = safe ? eq * Fs[col] : __expf(Gs[col] - gi);
                     else f = safe ? eq * Fs[col] : __expf(gi - Gs[col]) * Fs[col];
-                    v = (REV ? col >= row : col <= row) ? v * f : 0.f;
+                    v = (!p.nomask && (REV ? col >= row : col <= row)) ? v * f : 0.f;
                     if constexpr (TR) v = tf32r(v);
                     rs += v;
                     if (j < 32) r0[j] = __float_as_uint(v); else r1[j - 32] = __float_as_uint(v);

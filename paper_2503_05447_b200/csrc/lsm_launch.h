@@ -34,6 +34,7 @@ cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const
                                const float* logD, const float* M0, const float* z0, float* Min,
                                float* zin, float* Mfin, float* zfin, float* logDtot, int fin_stride,
                                int nseg, int dk, int dv, int norm, int lw, int rev, int* err);
+cudaError_t launch_sum_states(const float* gathered, int world, int BH, int nm, float* M, cudaStream_t st);
 cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,
                                 int rank, int dk, int dv, int norm, int lw, float* M0, float* z0);
 // TokenVector decays (GLA / HGRN2 / RWKV6): variant {decay = 3, fm, norm, hgrn2 in bit 8 of fm}

@@ -8,6 +8,7 @@
                                              all-heads state payload per call
   sp_forward_masked_loopback(q, ..., world)  the same algorithm with `world` virtual ranks on
                                              one device (device copies as the gather)
+  sp_lsm_nomask_rank / sp_forward_nomask_loopback   parallel.hpp:282-297, 391-403 (Alg. 1)
 torch.distributed is used only to ship the 128-byte NCCL unique id (bootstrap).
 """
 import ctypes
@@ -45,6 +46,12 @@ def _bind():
     L.lmoe_sp_lsm_fwd_loopback.restype = i
     L.lmoe_sp_lsm_fwd_loopback.argtypes = [P, i, i, i, i, i, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                            i, vp, sz, vp]
+    L.lmoe_sp_lsm_nomask_workspace_size.restype = sz
+    L.lmoe_sp_lsm_nomask_workspace_size.argtypes = [P, i, i, i, i, i, i]
+    L.lmoe_sp_lsm_nomask_fwd.restype = i
+    L.lmoe_sp_lsm_nomask_fwd.argtypes = [P, i, i, i, i, i, vp, vp, vp, vp, vp, i, i, vp, sz, vp]
+    L.lmoe_sp_lsm_nomask_fwd_loopback.restype = i
+    L.lmoe_sp_lsm_nomask_fwd_loopback.argtypes = [P, i, i, i, i, i, vp, vp, vp, vp, i, vp, sz, vp]
     L.lmoe_sp_last_gather_elements.restype = ctypes.c_longlong
     L.lmoe_nccl_unique_id.argtypes = [vp]
     L.lmoe_nccl_comm_init.argtypes = [ctypes.POINTER(vp), i, i, vp]
@@ -154,3 +161,37 @@ def last_gather_elements():
 def payload_floats(spec, B, H, D):
     desc = make_desc(spec, 64)
     return int(_bind().lmoe_sp_payload_floats(ctypes.byref(desc), B, H, D))
+
+
+def sp_lsm_nomask_rank(comm, q_loc, k_loc, v_loc, spec, out=None, check=True, stream=None):
+    """Unmasked SP (parallel.hpp:282-297): O = phi(Q_loc) . sum over ALL ranks of phi(K)^T V."""
+    L = _bind()
+    B, N, H, D = q_loc.shape
+    o = out if out is not None else torch.empty_like(q_loc)
+    desc = make_desc(spec, 64, check)
+    dt = _DTYPES[q_loc.dtype]
+    ws = _workspace(L.lmoe_sp_lsm_nomask_workspace_size(ctypes.byref(desc), B, N, H, D, dt, comm.world),
+                    q_loc.device)
+    st = stream if stream is not None else torch.cuda.current_stream(q_loc.device).cuda_stream
+    _lib.check(L.lmoe_sp_lsm_nomask_fwd(ctypes.byref(desc), B, N, H, D, dt, _lib.ptr(q_loc), _lib.ptr(k_loc),
+                                        _lib.ptr(v_loc), _lib.ptr(o), comm.handle, comm.rank, comm.world,
+                                        _lib.ptr(ws), ws.numel(), ctypes.c_void_p(st)))
+    return o
+
+
+def sp_forward_nomask_loopback(q, k, v, spec, world, check=True):
+    """sp_forward_nomask (parallel.hpp:391-403) with `world` virtual ranks on one device."""
+    L = _bind()
+    B, N, H, D = q.shape
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    o = torch.empty_like(q)
+    desc = make_desc(spec, 64, check)
+    dt = _DTYPES[q.dtype]
+    nb = L.lmoe_sp_lsm_nomask_workspace_size(ctypes.byref(desc), B, max(1, (N + world - 1) // world), H, D,
+                                             dt, world)
+    ws = _workspace(nb, q.device)
+    st = torch.cuda.current_stream(q.device).cuda_stream
+    _lib.check(L.lmoe_sp_lsm_nomask_fwd_loopback(ctypes.byref(desc), B, N, H, D, dt, _lib.ptr(q), _lib.ptr(k),
+                                                 _lib.ptr(v), _lib.ptr(o), world, _lib.ptr(ws), ws.numel(),
+                                                 ctypes.c_void_p(st)))
+    return o

@@ -211,3 +211,18 @@ def test_kat_prefix_sums():
     for r, want in ((0, 0.0), (1, 1.0), (2, 3.0)):
         M, _ = oracle.sp_combine(spec, states, r, 2)
         assert np.all(M == want)
+
+
+def test_sp_nomask_matches_reference():
+    """sp_forward_nomask (parallel.hpp:391-403) outputs and comm volume vs the reference."""
+    d = load_golden("spn")
+    for p in sorted({k.split("/")[0] for k in d}):
+        spec = oracle.spec_from_golden(d, p)
+        q, k, v = d[p + "/q"], d[p + "/k"], d[p + "/v"]
+        for t in (1, 2, 4, 8):
+            o = oracle.sp_forward_nomask(spec, q, k, v, t)
+            assert np.abs(o - d[p + "/o_t%d" % t]).max() < 1e-12, (p, t)
+            # one all-gather of T * d_k * d_v elements (parallel.hpp:279-281)
+            assert int(d[p + "/comm_elems_t%d" % t][0]) == t * q.shape[1] * v.shape[1]
+    with pytest.raises(oracle.OracleError, match="requires an undecayed instance"):
+        oracle.sp_forward_nomask(oracle.spec_default("retnet"), q, k, v, 2)

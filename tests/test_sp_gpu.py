@@ -78,3 +78,57 @@ def test_nccl_world1_matches_local():
     torch.cuda.synchronize()
     assert torch.equal(o, ref)
     assert sp.chunk_range(10, 3, 0) == (0, 4) and sp.chunk_range(10, 3, 2) == (7, 10)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_nomask_golden_padded(world):
+    """Unmasked SP (Alg. 1) against the reference's own outputs (tests/golden/spn.npz,
+    d = 4 zero-padded to the device head dim), and its T * d * d gather volume."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from conftest import load_golden
+    import paper_2503_05447_b200 as pk
+    from paper_2503_05447_b200 import sp
+    d = load_golden("spn")
+    for p in sorted({k.split("/")[0] for k in d}):
+        sd = oracle.spec_from_golden(d, p)
+        for dtype, D in ((torch.float32, 64), (torch.bfloat16, 128)):
+            pad = lambda x: torch.tensor(np.pad(x, ((0, 0), (0, D - x.shape[1]))), dtype=torch.float32,
+                                         device="cuda")[None, :, None].to(dtype)
+            q, k, v = (pad(d[p + "/" + n]) for n in "qkv")
+            spec = pk.LsmSpec(instance=sd["instance"], feature_map=sd["feature_map"])
+            o = sp.sp_forward_nomask_loopback(q, k, v, spec, world)
+            torch.cuda.synchronize()
+            got = o[0, :, 0, :4].double().cpu().numpy()
+            tol = 2e-2 if dtype == torch.bfloat16 else 1e-3
+            assert norm_rel_err(got, d[p + "/o_t%d" % world]) < tol, (p, world, dtype)
+            assert sp.last_gather_elements() == world * D * D
+
+
+@pytest.mark.parametrize("inst", ["bla_plain", "rebased_plain"])
+def test_nomask_vs_oracle_and_nccl_world1(inst):
+    torch, pk, q, k, v, spec, gates = _setup("bla", N=1500, H=2)
+    from paper_2503_05447_b200 import sp
+    spec = pk.LsmSpec(instance=0 if inst == "bla_plain" else 6, feature_map=0 if inst == "bla_plain" else 2)
+    sd = {"instance": spec.instance, "feature_map": spec.feature_map}
+    for world in (1, 3, 8):
+        o = sp.sp_forward_nomask_loopback(q, k, v, spec, world)
+        torch.cuda.synchronize()
+        for h in range(q.shape[2]):
+            want = oracle.sp_forward_nomask(sd, *(t[0, :, h].float().cpu().numpy() for t in (q, k, v)), world)
+            assert norm_rel_err(o[0, :, h].float().cpu().numpy(), want) < 2e-2, (inst, world, h)
+    comm = sp.NcclComm(0, 1)
+    o1 = sp.sp_lsm_nomask_rank(comm, q, k, v, spec)
+    o2 = sp.sp_forward_nomask_loopback(q, k, v, spec, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+
+
+def test_nomask_error_texts():
+    torch, pk, q, k, v, spec, gates = _setup("bla", N=256, H=1)
+    from paper_2503_05447_b200 import sp
+    with pytest.raises(pk.LmoeError, match="sp_forward_nomask: requires an undecayed instance"):
+        sp.sp_forward_nomask_loopback(q, k, v, pk.LsmSpec.make("retnet", 128), 2)
+    with pytest.raises(pk.LmoeError, match="sp_forward_nomask: normalizer unsupported"):
+        sp.sp_forward_nomask_loopback(q, k, v, pk.LsmSpec.make("bla", 128), 2)
