@@ -107,6 +107,24 @@ int lmoe_sp_lsm_nomask_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int
                                     lmoe_stream_t stream);
 
 /* ---------------------------------------------------------------------------------------
+ * Softmax attention (the hybrid model's "N" layers).  lmoe_attn_fwd replaces
+ * softmax_attention_parallel(q, k, v, causal = true, row_offset) (attention.hpp:18-38):
+ * query row i attends to keys j <= i + row_offset (row_offset >= Nk: no mask).
+ *   q [B, Nq, H, D], k / v [B, Nk, H, D], o [B, Nq, H, D]; bf16, D = 128.
+ * lmoe_sp_attn_fwd replaces sp_attention_rank (parallel.hpp:380-387): this rank's
+ * chunk_range slice of an N_total sequence; K and V are all-gathered (one NCCL group of the
+ * two all-gathers) and the local queries attend with row_offset = r0.
+ * ------------------------------------------------------------------------------------- */
+int lmoe_attn_fwd(int B, int Nq, int Nk, int H, int D, lmoe_dtype dtype, const void* q,
+                  const void* k, const void* v, void* o, int row_offset, lmoe_stream_t stream);
+size_t lmoe_sp_attn_workspace_size(int B, int N_total, int H, int D, lmoe_dtype dtype, int world);
+int lmoe_sp_attn_fwd(int B, int N_total, int H, int D, lmoe_dtype dtype, const void* q_loc,
+                     const void* k_loc, const void* v_loc, void* o_loc, void* nccl_comm, int rank,
+                     int world, void* workspace, size_t workspace_bytes, lmoe_stream_t stream);
+/* Elements moved by the last lmoe_sp_attn_fwd gathers (K and V, padded slices). */
+long long lmoe_sp_attn_last_gather_elements(void);
+
+/* ---------------------------------------------------------------------------------------
  * LSM backward: the vector-Jacobian product the reference's tape computes through
  * lsm_forward_chunked (tensor.hpp:1178-1215; ops of lsm.hpp:483-598), for every (b, h).
  * Inputs as lmoe_lsm_fwd plus dO [B,N,H,D] and the optional final-state gradient dM_final
