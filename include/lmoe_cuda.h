@@ -125,6 +125,58 @@ int lmoe_sp_attn_fwd(int B, int N_total, int H, int D, lmoe_dtype dtype, const v
 long long lmoe_sp_attn_last_gather_elements(void);
 
 /* ---------------------------------------------------------------------------------------
+ * Dense bf16 GEMM (tcgen05): C[M, N] = A[M, K] W[K, N]; A rows lda elements apart, W
+ * row-major (the reference's (in x out) weight layout, model.hpp:152-160), C bf16 or fp32
+ * (out_f32) with row stride ldc.  K % 64 == 0; N % 128 == 0 (bf16) / N % 64 == 0 (fp32).
+ * ------------------------------------------------------------------------------------- */
+size_t lmoe_gemm_workspace_size(int M);
+int lmoe_gemm(const void* A, int M, int K, int lda, const void* W, int N, void* C, int ldc, int out_f32,
+              void* workspace, size_t workspace_bytes, lmoe_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * One Linear-MoE block (Block, model.hpp:284-304, as model_forward / hybrid_sp_forward run
+ * it, model.hpp:374-405, parallel.hpp:477-506):
+ *   h = rms_norm(x, norm_mixer); x += mixer(h); h2 = rms_norm(x, norm_moe); x += MoE(h2)
+ * kind 'L': LsmMixer (q, k, v, gates = h W, per-head LSM, o W_o); with world > 1 the LSM is
+ * sp_lsm_masked_rank (one state all-gather).  kind 'N': AttentionMixer; with world > 1
+ * sp_attention_rank (K/V all-gather, row offset from chunk_range of N_total).
+ * x: fp32 residual stream [B, N_local, hidden], updated in place; aux: this block's
+ * load-balance loss (device scalar).  head_dim = hidden / heads = 128.
+ * ------------------------------------------------------------------------------------- */
+typedef struct lmoe_block_desc {
+    int kind;                 /* 'L' or 'N'                                            */
+    int hidden, heads;
+    int num_experts, top_k, ffn_dim;
+    float norm_eps;           /* ModelConfig::norm_eps                                 */
+    lmoe_lsm_desc lsm;        /* L blocks: the LsmSpec of every head                   */
+} lmoe_block_desc;
+typedef struct lmoe_block_weights {
+    const float* norm_mixer;  /* [hidden] fp32                                         */
+    const float* norm_moe;    /* [hidden] fp32                                         */
+    const void* w_qkv;        /* bf16 [hidden, 3 hidden] = [Wq | Wk | Wv], or
+                                 [hidden, 4 hidden] = [Wq | Wk | Wv | W_gate_a] for
+                                 TokenVector instances (GLA / HGRN2 / RWKV6)            */
+    const void* w_gate_b;     /* Mamba2: bf16 [hidden, 64], W_gate_b in columns < heads  */
+    const float* a_raw;       /* Mamba2: [heads] fp32                                   */
+    const void* wo;           /* bf16 [hidden, hidden]                                  */
+    const void* router;       /* bf16 [hidden, E]                                       */
+    const void* w_gate;       /* bf16 [E, hidden, ffn]                                  */
+    const void* w_up;         /* bf16 [E, hidden, ffn]                                  */
+    const void* w_down;       /* bf16 [E, ffn, hidden]                                  */
+} lmoe_block_weights;
+size_t lmoe_block_workspace_size(const lmoe_block_desc* desc, int B, int N_local, int N_total,
+                                 int world);
+int lmoe_block_fwd(const lmoe_block_desc* desc, const lmoe_block_weights* weights, int B,
+                   int N_local, int N_total, float* x, float* aux, void* nccl_comm, int rank,
+                   int world, void* workspace, size_t workspace_bytes, lmoe_stream_t stream);
+/* x[t] = embedding[tokens[t]] + pos_embedding[pos0 + t % n] (model.hpp:385-386), fp32 out */
+int lmoe_embed(const int* tokens, int rows, int n, int pos0, int hidden, const void* embedding,
+               const void* pos_embedding, float* x, lmoe_stream_t stream);
+/* out (bf16) = rms_norm(x, w, eps) (tensor.hpp:1164-1170) */
+int lmoe_rmsnorm(const float* x, int rows, int hidden, const float* w, float eps, void* out,
+                 lmoe_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
  * LSM backward: the vector-Jacobian product the reference's tape computes through
  * lsm_forward_chunked (tensor.hpp:1178-1215; ops of lsm.hpp:483-598), for every (b, h).
  * Inputs as lmoe_lsm_fwd plus dO [B,N,H,D] and the optional final-state gradient dM_final

@@ -25,6 +25,7 @@
 
 #include "lmoe/attention.hpp"
 #include "lmoe/lsm.hpp"
+#include "lmoe/model.hpp"
 #include "lmoe/moe.hpp"
 #include "lmoe/parallel.hpp"
 
@@ -369,6 +370,91 @@ void golden_sp() {
     }
 }
 
+// ---- hybrid model (model.hpp:284-405, parallel.hpp:477-506): tiny stacks whose weights are
+// rounded to bf16 IN PLACE before the run, so the device sees the identical parameters ----
+void golden_model() {
+    NoGradGuard ng;
+    struct MC { const char* tag; LsmInstance inst; const char* pattern; };
+    const MC cases[] = {{"mamba2_hybrid", LsmInstance::Mamba2, "LNL"}, {"gla", LsmInstance::GLA, "L"}};
+    int ci = 0;
+    for (const MC& c : cases) {
+        ModelConfig cfg;
+        cfg.hidden = 256;
+        cfg.ffn_dim = 128;
+        cfg.num_heads = 2;
+        cfg.num_layers = (int)std::string(c.pattern).size();
+        cfg.num_experts = 2;
+        cfg.num_active = 2;
+        cfg.vocab_size = 64;
+        cfg.instance = c.inst;
+        cfg.pattern = c.pattern;
+        cfg.max_seq_len = 256;
+        Rng rng(15000 + ci);
+        Model m = build_model(cfg, rng);
+        for (const Tensor& t : m.params()) {
+            auto& d = const_cast<std::vector<double>&>(t.data());
+            for (double& x : d) x = to_bf16(x);
+        }
+        const int n = 256;
+        std::vector<int> toks(n);
+        for (int i = 0; i < n; ++i) toks[i] = (int)(rng.uniform() * cfg.vocab_size) % cfg.vocab_size;
+        const PackedBatch batch = pack_sequences({toks});
+        const std::string p = std::string("model/") + c.tag;
+        emit_scalar(p + "/instance", (double)(int)c.inst);
+        emit_scalar(p + "/hidden", cfg.hidden);
+        emit_scalar(p + "/heads", cfg.num_heads);
+        emit_scalar(p + "/ffn", cfg.ffn_dim);
+        emit_scalar(p + "/experts", cfg.num_experts);
+        emit_scalar(p + "/top_k", cfg.num_active);
+        emit_scalar(p + "/eps", cfg.norm_eps);
+        emit_scalar(p + "/scalar_decay", m.blocks[0].kind == 'L' ? m.blocks[0].lsm.head_specs[0].scalar_decay : 1.0);
+        std::vector<double> kinds;
+        for (char k : std::string(c.pattern)) kinds.push_back(k == 'L' ? 1.0 : 0.0);
+        emit(p + "/is_lsm", {(int)kinds.size()}, kinds);
+        std::vector<double> tk(toks.begin(), toks.end());
+        emit(p + "/tokens", {n}, tk);
+        emit(p + "/embedding", m.embedding);
+        emit(p + "/pos_embedding", m.pos_embedding);
+        for (size_t b = 0; b < m.blocks.size(); ++b) {
+            const Block& blk = m.blocks[b];
+            const std::string q = p + "/b" + std::to_string(b);
+            emit(q + "/norm_mixer", blk.norm_mixer);
+            emit(q + "/norm_moe", blk.norm_moe);
+            if (blk.kind == 'L') {
+                emit(q + "/wq", blk.lsm.wq); emit(q + "/wk", blk.lsm.wk);
+                emit(q + "/wv", blk.lsm.wv); emit(q + "/wo", blk.lsm.wo);
+                emit(q + "/w_gate_a", blk.lsm.w_gate_a);
+                emit(q + "/w_gate_b", blk.lsm.w_gate_b);
+                std::vector<double> ar;
+                for (const auto& hs : blk.lsm.head_specs)
+                    ar.push_back(hs.mamba2_a_raw.defined() ? hs.mamba2_a_raw.item() : 0.0);
+                emit(q + "/a_raw", {(int)ar.size()}, ar);
+            } else {
+                emit(q + "/wq", blk.attn.wq); emit(q + "/wk", blk.attn.wk);
+                emit(q + "/wv", blk.attn.wv); emit(q + "/wo", blk.attn.wo);
+            }
+            emit(q + "/router", blk.moe.router);
+            std::vector<double> wg, wu, wd;
+            for (const auto& ex : blk.moe.experts) {
+                wg.insert(wg.end(), ex.w_gate.data().begin(), ex.w_gate.data().end());
+                wu.insert(wu.end(), ex.w_up.data().begin(), ex.w_up.data().end());
+                wd.insert(wd.end(), ex.w_down.data().begin(), ex.w_down.data().end());
+            }
+            emit(q + "/w_gate", {cfg.num_experts, cfg.hidden, cfg.ffn_dim}, wg);
+            emit(q + "/w_up", {cfg.num_experts, cfg.hidden, cfg.ffn_dim}, wu);
+            emit(q + "/w_down", {cfg.num_experts, cfg.ffn_dim, cfg.hidden}, wd);
+        }
+        emit(p + "/final_norm", m.final_norm);
+        emit(p + "/lm_head", m.lm_head);
+        const ForwardOut fo = model_forward(m, batch);
+        emit(p + "/logits", fo.logits);
+        emit_scalar(p + "/aux", fo.aux_loss.item());
+        RankGroup g2(2);
+        emit(p + "/logits_sp2", hybrid_sp_forward(g2, m, batch));
+        ++ci;
+    }
+}
+
 int cmd_golden(const char* path) {
     g_out = fopen(path, "wb");
     if (!g_out) return 2;
@@ -378,6 +464,7 @@ int cmd_golden(const char* path) {
     golden_route();
     golden_moe();
     golden_sp();
+    golden_model();
     fclose(g_out);
     return 0;
 }

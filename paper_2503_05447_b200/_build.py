@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["common.cu", "lsm_host.cu", "lsm_combine.cu", "lsm_bwd_kernels.cu", "lsm_dgate.cu", "lsm_inst_bf16.cu", "lsm_inst_f32.cu", "lsm_inst_vec.cu",
-           "moe_host.cu", "attn.cu"]
+           "moe_host.cu", "attn.cu", "block.cu"]
 LIBS = ["-lnccl"]
 
 

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "common.h"
+#include "internal.h"
 #include "lsm_fwd.cuh"
 
 namespace lmoe_dev {
@@ -261,11 +262,12 @@ static void attn_validate(int B, int Nq, int Nk, int H, int D, lmoe_dtype dt, co
     if (!q || !k || !v || !o) throw Error(LMOE_ERR_ARG, "lmoe_attn_fwd: null tensor");
 }
 
+// ldq / ldkv: elements per token row of q and of k, v (0: H * D)
 static void attn_launch(int B, int Nq, int Nk, int H, int D, int row_offset, const void* q, const void* k,
-                        const void* v, void* o, cudaStream_t st) {
-    const CUtensorMap tq = make_tmap_4d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nq, B, 64, kC);
-    const CUtensorMap tk = make_tmap_4d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC);
-    const CUtensorMap tv = make_tmap_4d(v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC);
+                        const void* v, void* o, cudaStream_t st, int ldq = 0, int ldkv = 0) {
+    const CUtensorMap tq = make_tmap_4d(q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nq, B, 64, kC, 0, ldq);
+    const CUtensorMap tk = make_tmap_4d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
+    const CUtensorMap tv = make_tmap_4d(v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
     AttnParams p{Nq, Nk, H, row_offset, 1.4426950408889634f / sqrtf((float)D), static_cast<__nv_bfloat16*>(o)};
     constexpr int smem = 5 * kTileBytes + 256;
     static bool attr = false;
@@ -279,6 +281,80 @@ static void attn_launch(int B, int Nq, int Nk, int H, int D, int row_offset, con
 }
 
 static long long g_attn_gather_elements = 0;
+
+void attn_core(int B, int Nq, int Nk, int H, int D, const void* q, const void* k, const void* v, int ld,
+               void* o, int row_offset, cudaStream_t st) {
+    attn_validate(B, Nq, Nk, H, D, LMOE_BF16, q, k, v, o);
+    attn_launch(B, Nq, Nk, H, D, row_offset, q, k, v, o, st, ld, ld);
+}
+
+size_t sp_attn_ws(int B, int N_total, int H, int D, int world) {
+    if (B < 1 || N_total < world || world < 1) return 0;
+    const size_t maxlen = (N_total + world - 1) / world;
+    const size_t row = (size_t)H * D * 2;
+    // gathered K, V (padded) + compact K, V
+    return 2 * align_up((size_t)world * B * maxlen * row, 256) + 2 * align_up((size_t)B * N_total * row, 256);
+}
+
+// sp_attention_rank (parallel.hpp:380-387) over strided local rows (ld elements; 0: H * D).
+void sp_attn_core(int B, int N_total, int H, int D, const void* q_loc, const void* k_loc, const void* v_loc,
+                  int ld, void* o_loc, void* nccl_comm, int rank, int world, void* workspace,
+                  size_t workspace_bytes, cudaStream_t st) {
+    if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_sp_attn_fwd: bad rank");
+    if (N_total < world) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");
+    const int base = N_total / world, rem = N_total % world;
+    const int r0 = rank * base + std::min(rank, rem);
+    const int len = base + (rank < rem ? 1 : 0);
+    attn_validate(B, len, N_total, H, D, LMOE_BF16, q_loc, k_loc, v_loc, o_loc);
+    if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_sp_attn_fwd: null communicator");
+    const size_t need = sp_attn_ws(B, N_total, H, D, world);
+    if (!workspace || workspace_bytes < need)
+        throw Error(LMOE_ERR_ARG, "lmoe_sp_attn_fwd: workspace too small (need " + std::to_string(need) + " bytes)");
+    const int maxlen = (N_total + world - 1) / world;
+    const size_t row = (size_t)H * D * 2;
+    const size_t src_pitch = (ld ? (size_t)ld : (size_t)H * D) * 2;
+    const size_t gbytes = align_up((size_t)world * B * maxlen * row, 256);
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    uint8_t* gk = ws;
+    uint8_t* gv = ws + gbytes;
+    uint8_t* ck = ws + 2 * gbytes;
+    uint8_t* cv = ck + align_up((size_t)B * N_total * row, 256);
+    const size_t send = (size_t)B * maxlen * row;  // bytes per rank (padded)
+    // this rank's slice at the front of a maxlen-row slot per batch row (strided -> dense rows)
+    const bool direct = B == 1 && rem == 0;  // gathered layout == global layout
+    uint8_t* dk = direct ? ck : gk;
+    uint8_t* dv = direct ? cv : gv;
+    for (int b = 0; b < B; ++b) {
+        LMOE_CUDA_CHECK(cudaMemcpy2DAsync(dk + ((size_t)rank * B + b) * maxlen * row, row,
+                                          static_cast<const uint8_t*>(k_loc) + (size_t)b * len * src_pitch,
+                                          src_pitch, row, len, cudaMemcpyDeviceToDevice, st));
+        LMOE_CUDA_CHECK(cudaMemcpy2DAsync(dv + ((size_t)rank * B + b) * maxlen * row, row,
+                                          static_cast<const uint8_t*>(v_loc) + (size_t)b * len * src_pitch,
+                                          src_pitch, row, len, cudaMemcpyDeviceToDevice, st));
+    }
+    if (world > 1) {
+        ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+        ncclResult_t r = ncclGroupStart();
+        if (r == ncclSuccess) r = ncclAllGather(dk + rank * send, dk, send, ncclUint8, comm, st);
+        if (r == ncclSuccess) r = ncclAllGather(dv + rank * send, dv, send, ncclUint8, comm, st);
+        ncclResult_t r2 = ncclGroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            throw Error(LMOE_ERR_NCCL, std::string("NCCL error: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+    }
+    g_attn_gather_elements = 2LL * world * (long long)B * maxlen * H * D;
+    if (!direct) {
+        const int rowvec = (int)(row / 16);
+        const size_t total = (size_t)B * N_total * rowvec;
+        const int grid = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
+        attn_compact_kv<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(gk), reinterpret_cast<uint4*>(ck),
+                                              world, B, N_total, maxlen, rowvec);
+        attn_compact_kv<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(gv), reinterpret_cast<uint4*>(cv),
+                                              world, B, N_total, maxlen, rowvec);
+        LMOE_CUDA_CHECK(cudaGetLastError());
+        g_launch_count += 2;
+    }
+    attn_launch(B, len, N_total, H, D, r0, q_loc, ck, cv, o_loc, st, ld, 0);
+}
 
 }  // namespace lmoe_host
 
@@ -297,11 +373,7 @@ extern "C" int lmoe_attn_fwd(int B, int Nq, int Nk, int H, int D, lmoe_dtype dty
 
 extern "C" size_t lmoe_sp_attn_workspace_size(int B, int N_total, int H, int D, lmoe_dtype dtype, int world) {
     (void)dtype;
-    if (B < 1 || N_total < world || world < 1) return 0;
-    const size_t maxlen = (N_total + world - 1) / world;
-    const size_t row = (size_t)H * D * 2;
-    // gathered K, V (padded) + compact K, V
-    return 2 * align_up((size_t)world * B * maxlen * row, 256) + 2 * align_up((size_t)B * N_total * row, 256);
+    return sp_attn_ws(B, N_total, H, D, world);
 }
 
 extern "C" long long lmoe_sp_attn_last_gather_elements(void) { return g_attn_gather_elements; }
@@ -314,59 +386,9 @@ extern "C" int lmoe_sp_attn_fwd(int B, int N_total, int H, int D, lmoe_dtype dty
                                 const void* k_loc, const void* v_loc, void* o_loc, void* nccl_comm, int rank,
                                 int world, void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
     return guarded([&]() {
-        if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_sp_attn_fwd: bad rank");
-        if (N_total < world) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");
-        const int base = N_total / world, rem = N_total % world;
-        const int r0 = rank * base + std::min(rank, rem);
-        const int len = base + (rank < rem ? 1 : 0);
-        attn_validate(B, len, N_total, H, D, dtype, q_loc, k_loc, v_loc, o_loc);
-        if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_sp_attn_fwd: null communicator");
-        const size_t need = lmoe_sp_attn_workspace_size(B, N_total, H, D, dtype, world);
-        if (!workspace || workspace_bytes < need)
-            throw Error(LMOE_ERR_ARG, "lmoe_sp_attn_fwd: workspace too small (need " + std::to_string(need) + " bytes)");
-        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-        const int maxlen = (N_total + world - 1) / world;
-        const size_t row = (size_t)H * D * 2;
-        const size_t gbytes = align_up((size_t)world * B * maxlen * row, 256);
-        uint8_t* ws = static_cast<uint8_t*>(workspace);
-        uint8_t* gk = ws;
-        uint8_t* gv = ws + gbytes;
-        uint8_t* ck = ws + 2 * gbytes;
-        uint8_t* cv = ck + align_up((size_t)B * N_total * row, 256);
-        const size_t send = (size_t)B * maxlen * row;  // bytes per rank (padded)
-        // padded send: this rank's slice at the front of a maxlen-row slot per batch row
-        const bool direct = B == 1 && rem == 0;  // gathered layout == global layout
-        uint8_t* dk = direct ? ck : gk;
-        uint8_t* dv = direct ? cv : gv;
-        for (int b = 0; b < B; ++b) {
-            LMOE_CUDA_CHECK(cudaMemcpyAsync(dk + ((size_t)rank * B + b) * maxlen * row,
-                                            static_cast<const uint8_t*>(k_loc) + (size_t)b * len * row, len * row,
-                                            cudaMemcpyDeviceToDevice, st));
-            LMOE_CUDA_CHECK(cudaMemcpyAsync(dv + ((size_t)rank * B + b) * maxlen * row,
-                                            static_cast<const uint8_t*>(v_loc) + (size_t)b * len * row, len * row,
-                                            cudaMemcpyDeviceToDevice, st));
-        }
-        if (world > 1) {
-            ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
-            ncclResult_t r = ncclGroupStart();
-            if (r == ncclSuccess) r = ncclAllGather(dk + rank * send, dk, send, ncclUint8, comm, st);
-            if (r == ncclSuccess) r = ncclAllGather(dv + rank * send, dv, send, ncclUint8, comm, st);
-            ncclResult_t r2 = ncclGroupEnd();
-            if (r != ncclSuccess || r2 != ncclSuccess)
-                throw Error(LMOE_ERR_NCCL, std::string("NCCL error: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
-        }
-        g_attn_gather_elements = 2LL * world * (long long)B * maxlen * H * D;
-        if (!direct) {
-            const int rowvec = (int)(row / 16);
-            const size_t total = (size_t)B * N_total * rowvec;
-            const int grid = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
-            attn_compact_kv<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(gk), reinterpret_cast<uint4*>(ck),
-                                                  world, B, N_total, maxlen, rowvec);
-            attn_compact_kv<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(gv), reinterpret_cast<uint4*>(cv),
-                                                  world, B, N_total, maxlen, rowvec);
-            LMOE_CUDA_CHECK(cudaGetLastError());
-            g_launch_count += 2;
-        }
-        attn_launch(B, len, N_total, H, D, r0, q_loc, ck, cv, o_loc, st);
+        if (dtype != LMOE_BF16 || D != 128)
+            throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_attn_fwd: supported (dtype, head_dim) is (bf16, 128)");
+        sp_attn_core(B, N_total, H, D, q_loc, k_loc, v_loc, 0, o_loc, nccl_comm, rank, world, workspace,
+                     workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
     });
 }

@@ -32,11 +32,12 @@ static PFN_encodeTiled encode_fn() {
 
 CUtensorMap make_tmap_4d(const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
                          uint64_t d1, uint64_t d2, uint64_t d3, uint32_t box0, uint32_t box2,
-                         uint64_t d2_stride) {
+                         uint64_t d2_stride, uint64_t row_stride) {
     CUtensorMap m;
     if (d2_stride == 0) d2_stride = d2;
+    if (row_stride == 0) row_stride = d0 * d1;
     cuuint64_t dims[4] = {d0, d1, d2, d3};
-    cuuint64_t strides[3] = {d0 * esize, d0 * d1 * esize, d0 * d1 * d2_stride * esize};
+    cuuint64_t strides[3] = {d0 * esize, row_stride * esize, row_stride * d2_stride * esize};
     cuuint32_t box[4] = {box0, 1, box2, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = encode_fn()(&m, dt, 4, const_cast<void*>(base), dims, strides, box, es,

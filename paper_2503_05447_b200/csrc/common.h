@@ -33,7 +33,8 @@ void set_last_error(const std::string& msg);
 // box {box0, 1, box2, 1}.
 CUtensorMap make_tmap_4d(const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
                          uint64_t d1, uint64_t d2, uint64_t d3, uint32_t box0, uint32_t box2,
-                         uint64_t d2_stride = 0 /* elements of dim 2 per dim-3 step; 0 = d2 */);
+                         uint64_t d2_stride = 0 /* elements of dim 2 per dim-3 step; 0 = d2 */,
+                         uint64_t row_stride = 0 /* elements per dim-2 step; 0 = d0 * d1 */);
 // 3-D row-major tensor [d2][d1][d0], SWIZZLE_128B, box {box0, box1, 1}.
 CUtensorMap make_tmap_3d(const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
                          uint64_t d1, uint64_t d2, uint32_t box0, uint32_t box1);

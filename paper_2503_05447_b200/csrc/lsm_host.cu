@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "common.h"
+#include "internal.h"
 #include "lsm_launch.h"
 
 namespace lmoe_host {
@@ -140,6 +141,7 @@ struct LsmCall {
     bool norm = false;
     bool vec = false;
     int lw = 1;  // log-decay entries per state: 1, or D for TokenVector kinds
+    int ld = 0;  // elements per token row of q, k, v, a_pre (0: H * D); o is always dense
 
     void mark() {
         if (!(d->flags & LMOE_FLAG_TIMING)) return;
@@ -193,7 +195,9 @@ struct LsmCall {
         using TT = lmoe_dev::TileTraits<T>;
         const CUtensorMapDataType tdt =
             sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-        return make_tmap_4d(base, tdt, sizeof(T), TT::D, H, N, B, TT::EPB, lmoe_dev::kC, Nstride);
+        const bool dense_out = base == o;
+        return make_tmap_4d(base, tdt, sizeof(T), TT::D, H, N, B, TT::EPB, lmoe_dev::kC, Nstride,
+                            dense_out ? 0 : ld);
     }
 
     template <typename T>
@@ -425,6 +429,56 @@ extern "C" int lmoe_nccl_comm_destroy(void* comm) {
     return guarded([&]() { NCCL_CHECK(ncclCommDestroy(static_cast<ncclComm_t>(comm))); });
 }
 
+namespace lmoe_host {
+size_t lsm_mixer_ws(const lmoe_lsm_desc* d, int B, int N, int H, int D, int world) {
+    return plan_sp(d, B, N, H, D, world).total;
+}
+
+void lsm_mixer_core(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D, lmoe_dtype dtype,
+                    const void* q, const void* k, const void* v, const void* a_pre, int ld, const float* b_pre,
+                    const float* a_raw, void* o, void* nccl_comm, int rank, int world, void* workspace,
+                    size_t workspace_bytes, cudaStream_t st, float* M_out, float* z_out) {
+    validate(desc, B, N_local, H, D, dtype, q, k, v, o);
+    if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: bad rank");
+    if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: null communicator");
+    const SpWorkspace w = plan_sp(desc, B, N_local, H, D, world);
+    if (!workspace || workspace_bytes < w.total)
+        throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: workspace too small (need " +
+                                      std::to_string(w.total) + " bytes)");
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    LsmCall c{desc, B, N_local, N_local, H, D, dtype, q, k, v, b_pre, a_raw, o, ws, w.pl, st, a_pre};
+    c.ld = ld;
+    c.setup();
+    c.clear_err();
+    float* payload = reinterpret_cast<float*>(ws + w.off_payload);
+    float* gathered = reinterpret_cast<float*>(ws + w.off_gathered);
+    float* M0 = reinterpret_cast<float*>(ws + w.off_M0);
+    float* z0 = reinterpret_cast<float*>(ws + w.off_z0);
+    const size_t P = (size_t)B * H * payload_floats(desc, D);
+    if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, payload);
+    else sp_phase_a<float>(c, payload);
+    c.mark();
+    if (world > 1) {
+        NCCL_CHECK(ncclAllGather(payload, gathered, P, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
+    } else {
+        LMOE_CUDA_CHECK(cudaMemcpyAsync(gathered, payload, P * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    g_last_gather_elements = (long long)world * (long long)P;
+    if (dtype == LMOE_BF16) sp_phase_b<__nv_bfloat16>(c, gathered, rank, M0, z0, M_out, z_out);
+    else sp_phase_b<float>(c, gathered, rank, M0, z0, M_out, z_out);
+    c.finish_timing();
+    c.check_err();
+}
+
+void lsm_mixer_core(const lmoe_lsm_desc* d, int B, int N, int H, int D, lmoe_dtype dt, const void* q,
+                    const void* k, const void* v, const void* a_pre, int ld, const float* b_pre,
+                    const float* a_raw, void* o, void* comm, int rank, int world, void* ws, size_t ws_bytes,
+                    cudaStream_t st) {
+    lsm_mixer_core(d, B, N, H, D, dt, q, k, v, a_pre, ld, b_pre, a_raw, o, comm, rank, world, ws, ws_bytes, st,
+                   nullptr, nullptr);
+}
+}  // namespace lmoe_host
+
 // sp_lsm_masked_rank (parallel.hpp:303-376) for this rank's contiguous slice
 // (chunk_range, parallel.hpp:192-197): local pass, ONE ncclAllGather of the all-heads
 // payload, decayed prefix over earlier ranks, output pass.
@@ -435,37 +489,8 @@ extern "C" int lmoe_sp_lsm_fwd(const lmoe_lsm_desc* desc, int B, int N_local, in
                                int world, void* workspace, size_t workspace_bytes,
                                lmoe_stream_t stream) {
     return guarded([&]() {
-        validate(desc, B, N_local, H, D, dtype, q, k, v, o);
-        (void)a_pre;
-        if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: bad rank");
-        if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: null communicator");
-        const SpWorkspace w = plan_sp(desc, B, N_local, H, D, world);
-        if (!workspace || workspace_bytes < w.total)
-            throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd: workspace too small (need " +
-                                          std::to_string(w.total) + " bytes)");
-        uint8_t* ws = static_cast<uint8_t*>(workspace);
-        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-        LsmCall c{desc, B, N_local, N_local, H, D, dtype, q, k, v, b_pre, a_raw, o, ws, w.pl, st, a_pre};
-        c.setup();
-        c.clear_err();
-        float* payload = reinterpret_cast<float*>(ws + w.off_payload);
-        float* gathered = reinterpret_cast<float*>(ws + w.off_gathered);
-        float* M0 = reinterpret_cast<float*>(ws + w.off_M0);
-        float* z0 = reinterpret_cast<float*>(ws + w.off_z0);
-        const size_t P = (size_t)B * H * payload_floats(desc, D);
-        if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, payload);
-        else sp_phase_a<float>(c, payload);
-        c.mark();
-        if (world > 1) {
-            NCCL_CHECK(ncclAllGather(payload, gathered, P, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
-        } else {
-            LMOE_CUDA_CHECK(cudaMemcpyAsync(gathered, payload, P * 4, cudaMemcpyDeviceToDevice, st));
-        }
-        g_last_gather_elements = (long long)world * (long long)P;
-        if (dtype == LMOE_BF16) sp_phase_b<__nv_bfloat16>(c, gathered, rank, M0, z0, M_out, z_out);
-        else sp_phase_b<float>(c, gathered, rank, M0, z0, M_out, z_out);
-        c.finish_timing();
-        c.check_err();
+        lsm_mixer_core(desc, B, N_local, H, D, dtype, q, k, v, a_pre, 0, b_pre, a_raw, o, nccl_comm, rank, world,
+                       workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), M_out, z_out);
     });
 }
 

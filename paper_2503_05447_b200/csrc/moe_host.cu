@@ -2,6 +2,7 @@
 #include <algorithm>
 
 #include "common.h"
+#include "internal.h"
 #include "moe_kernels.cu"  // kernels and their launches in one translation unit
 
 namespace lmoe_host {
@@ -90,6 +91,32 @@ static void check_route_args(int T, int E, int K) {
     if (K < 1 || K > E) throw Error(LMOE_ERR_ARG, "route: bad top_k");
     if (E > 64 || K > 8) throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_moe: device routing supports E <= 64, top_k <= 8");
     if (T < 1) throw Error(LMOE_ERR_ARG, "lmoe_moe: need T >= 1");
+}
+
+size_t dense_gemm_ws(int M) { return align_up((size_t)((M + 127) / 128 + 2) * 3 * 4 + 64, 256); }
+
+// Dense projection on the grouped tcgen05 GEMM with a single group (the LsmMixer /
+// AttentionMixer matmuls, model.hpp:232-246, 266-278, and the LM head).
+void dense_gemm(const void* A, int M, int K, int lda, const void* W, int N, void* C, int ldc, bool out_f32,
+                void* ws, cudaStream_t st) {
+    if (M < 1 || K < 64 || K % 64 != 0) throw Error(LMOE_ERR_UNSUPPORTED, "dense GEMM: need K % 64 == 0");
+    if (out_f32 ? N % 64 != 0 : N % 128 != 0)
+        throw Error(LMOE_ERR_UNSUPPORTED, "dense GEMM: need N % 128 == 0 (bf16 out) or N % 64 == 0 (fp32 out)");
+    constexpr CUtensorMapDataType BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    int* dt = static_cast<int*>(ws);
+    const int ntile = (M + 127) / 128;
+    int* dgroup = dt + 1;
+    int* drow0 = dgroup + ntile + 1;
+    int* dend = drow0 + ntile + 1;
+    dense_plan<<<1, 256, 0, st>>>(M, dt, dgroup, drow0, dend);
+    LMOE_CUDA_CHECK(cudaGetLastError());
+    ++g_launch_count;
+    lmoe_dev::GemmParams gp{dt, dgroup, drow0, dend, K, C, ldc};
+    const CUtensorMap ta = make_tmap_2d(A, BF, 2, K, M, lda, 64, 128);
+    const CUtensorMap tb = make_tmap_3d(W, BF, 2, N, K, 1, 64, 64);
+    if (out_f32) launch_gemm<64, lmoe_dev::kEpiF32>(ta, tb, tb, gp, ntile, N / 64, st);
+    else if (N % 256 == 0 && (size_t)ntile * (N / 256) >= (size_t)num_sms()) launch_gemm<256, lmoe_dev::kEpiBF16>(ta, tb, tb, gp, ntile, N / 256, st);
+    else launch_gemm<128, lmoe_dev::kEpiBF16>(ta, tb, tb, gp, ntile, N / 128, st);
 }
 
 }  // namespace lmoe_host
@@ -226,5 +253,18 @@ extern "C" int lmoe_moe_dispatch_read(int T, int hidden, int ffn, int E, int top
         if (slot_pos) LMOE_CUDA_CHECK(cudaMemcpyAsync(slot_pos, ws + w.slot_pos, rows * 4, cudaMemcpyDeviceToDevice, st));
         if (perm_token) LMOE_CUDA_CHECK(cudaMemcpyAsync(perm_token, ws + w.perm_token, rows * 4, cudaMemcpyDeviceToDevice, st));
         if (offsets) LMOE_CUDA_CHECK(cudaMemcpyAsync(offsets, ws + w.offsets, (E + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    });
+}
+
+extern "C" size_t lmoe_gemm_workspace_size(int M) { return M < 1 ? 0 : dense_gemm_ws(M); }
+
+// C[M, N] = A[M, K] W[K, N]: bf16 operands (A rows lda elements apart, W row-major as the
+// reference's (in x out) weights), fp32 accumulate, C bf16 or fp32 (out_f32) with row stride ldc.
+extern "C" int lmoe_gemm(const void* A, int M, int K, int lda, const void* W, int N, void* C, int ldc,
+                         int out_f32, void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        if (!A || !W || !C) throw Error(LMOE_ERR_ARG, "lmoe_gemm: null tensor");
+        if (!workspace || workspace_bytes < dense_gemm_ws(M)) throw Error(LMOE_ERR_ARG, "lmoe_gemm: workspace too small");
+        dense_gemm(A, M, K, lda, W, N, C, ldc, out_f32 != 0, workspace, reinterpret_cast<cudaStream_t>(stream));
     });
 }

@@ -19,8 +19,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
 
-# groups whose large arrays are stored as float32 (inputs are bf16-exact there)
-F32_GROUPS = {"lsm_dev"}
+# groups whose large arrays are stored as float32 (inputs are bf16-exact there); in "model"
+# only the parameters (rounded to bf16 by the driver), never the logits
+F32_GROUPS = {"lsm_dev", "model"}
 
 
 def read_records(path):
@@ -55,7 +56,7 @@ def main():
     groups = {}
     for name, arr in recs.items():
         g, rest = name.split("/", 1)
-        if g in F32_GROUPS and arr.size > 1:
+        if g in F32_GROUPS and arr.size > 1 and "logits" not in rest:
             arr = arr.astype(np.float32)
         groups.setdefault(g, {})[rest] = arr
     for g, d in groups.items():
