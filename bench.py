@@ -162,6 +162,77 @@ def run_reference(args, world, rank):
     print(json.dumps(line))
 
 
+def layer_bench(dev, steps=5, warmup=3):
+    """SURVEY 8(d) second number: LSM-layer tokens/s on cfg4 (A0.3B-2B Linear-MoE block:
+    hidden 1024, 8 heads x 128, GLA, FFN 896, 64 experts top-8; 8 documents x 8192 tokens)
+    through lmoe_block_fwd: RMSNorm, fused QKV+gate GEMM, LSM, W_o, RMSNorm, MoE, residuals."""
+    import torch
+    from paper_2503_05447_b200.lsm import LsmInstance
+    from paper_2503_05447_b200.model import Model, ModelConfig
+    cfg = ModelConfig(hidden=1024, ffn_dim=896, num_heads=8, num_experts=64, num_active=8, vocab_size=256,
+                      instance=LsmInstance.GLA, pattern="L", max_seq_len=8192)
+    m = Model.init(cfg, seed=0, device=str(dev))
+    B, N = 8, 8192
+    g = torch.Generator(device=dev).manual_seed(7)
+    x0 = torch.randn(B * N, cfg.hidden, device=dev, generator=g)
+    x = x0.clone()
+    for _ in range(warmup):
+        x.copy_(x0)
+        m.run_block(0, x, B, N)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        m.run_block(0, x, B, N)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    T, h, H, d, F, E, K = B * N, cfg.hidden, cfg.num_heads, 128, cfg.ffn_dim, cfg.num_experts, cfg.num_active
+    flops = T * (2 * h * 4 * h + 2 * h * h + 2 * h * E + 6 * K * h * F + H * (4 * d * d + 2 * 64 * d))
+    tflops_peak = 1373.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            tflops_peak = json.load(f)["bf16_tflops_sustained"]
+    except Exception:  # noqa: BLE001
+        pass
+    tf = flops / (ms / 1e3) / 1e12
+    return {"workload": "cfg4 A0.3B-2B Linear-MoE block (GLA LSM + 64-expert top-8 MoE), 8 x 8192 tokens",
+            "tokens_per_s": T / (ms / 1e3), "ms_per_step": ms, "steps": steps,
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": tflops_peak, "unit": "TFLOP/s",
+                         "frac": tf / tflops_peak, "flops_per_step": flops,
+                         "note": "GEMM + LSM flops per block; peak = MEASURED_PEAKS bf16_tflops_sustained"}}
+
+
+def backward_bench(dev, steps=3, warmup=2):
+    """LSM backward (lmoe_lsm_bwd) at the cfg3 shape on one GPU: Mamba2, N = 262144, 16 x 128."""
+    import torch
+    import paper_2503_05447_b200 as pk
+    g = torch.Generator(device=dev).manual_seed(11)
+    q, k, v, dO = (torch.randn(1, SEQ, HEADS, HEAD_DIM, device=dev, generator=g).mul_(0.5).to(torch.bfloat16)
+                   for _ in range(4))
+    gates = pk.LsmGates(b_pre=torch.randn(1, SEQ, HEADS, device=dev, generator=g))
+    spec = pk.LsmSpec.make("mamba2", HEAD_DIM)
+    spec.mamba2_a_raw = torch.randn(HEADS, device=dev, generator=g).mul_(0.5)
+    for _ in range(warmup):
+        pk.lsm_backward_batched(q, k, v, gates, spec, dO, check=False)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        pk.lsm_backward_batched(q, k, v, gates, spec, dO, check=False)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    hbm, _, _ = peaks()
+    # SURVEY 8(d): backward bytes per (token, head) = 4 d s_in + 3 d s_out + 2 g
+    alg = (4 * HEAD_DIM * 2 + 3 * HEAD_DIM * 2 + 2 * 4) * SEQ * HEADS
+    gbs = alg / (ms / 1e3) / 1e9
+    return {"workload": "cfg3 Mamba2 LSM backward (dq, dk, dv, db_pre, da_raw, dM0), N=262144, 16 x 128",
+            "tokens_per_s": SEQ / (ms / 1e3), "ms_per_step": ms, "steps": steps,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                         "note": "algorithmic bytes of the op / step time (three chunk passes + gate kernel)"}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -171,6 +242,7 @@ def main():
     ap.add_argument("--instance", default="mamba2", choices=["mamba2", "lightning", "retnet", "bla"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the layer / backward side numbers")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
@@ -288,6 +360,10 @@ def main():
 
     if rank == 0:
         cb = None
+        extra = {}
+        if world == 1 and not args.no_extra:
+            extra["layer"] = layer_bench(dev)
+            extra["backward"] = backward_bench(dev)
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(args.instance, SEQ, os.cpu_count() or 1, 20.0)
         line = {
@@ -315,6 +391,7 @@ def main():
                     "path": "pinned host -> H2D -> lmoe_sp_lsm_fwd (C-ABI) -> D2H"},
             "cpu_baseline": cb,
         }
+        line.update(extra)
         print(json.dumps(line))
     comm.close()
     if world > 1:

@@ -181,6 +181,25 @@ class Model:
         return _BlockWeights(P(b.norm_mixer), P(b.norm_moe), P(b.w_qkv), P(b.w_gate_b), P(b.a_raw), P(b.wo),
                              P(b.router), P(b.w_gate), P(b.w_up), P(b.w_down))
 
+    def run_block(self, i, x, B, N, comm=None, n_total=None, aux=None, stream=None):
+        """Block i on the fp32 residual stream x [B*N, hidden] in place (lmoe_block_fwd)."""
+        L = _bind()
+        b = self.blocks[i]
+        dev = x.device
+        world = comm.world if comm is not None else 1
+        rank = comm.rank if comm is not None else 0
+        n_total = n_total or N
+        st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        if aux is None:
+            aux = torch.zeros(1, dtype=torch.float32, device=dev)
+        d = self._desc(b.kind)
+        ws = _workspace(L.lmoe_block_workspace_size(ctypes.byref(d), B, N, n_total, world), dev)
+        w = self._weights(b)
+        _lib.check(L.lmoe_block_fwd(ctypes.byref(d), ctypes.byref(w), B, N, n_total, x.data_ptr(), aux.data_ptr(),
+                                    comm.handle if comm is not None else None, rank, world, ws.data_ptr(),
+                                    ws.numel(), st))
+        return aux
+
     def forward(self, tokens, comm=None, n_total=None, stream=None):
         """tokens: int [B, N] (B equal-length documents), or this rank's [1, N_local] slice of
         one n_total-token document when `comm` (sp.NcclComm) spans > 1 rank.
@@ -205,14 +224,8 @@ class Model:
         _lib.check(L.lmoe_embed(tok.data_ptr(), T, N, pos0, c.hidden, self.embedding.data_ptr(),
                                 self.pos_embedding.data_ptr(), x.data_ptr(), st))
         aux = torch.zeros(len(self.blocks), dtype=torch.float32, device=dev)
-        handle = comm.handle if comm is not None else None
-        for i, b in enumerate(self.blocks):
-            d = self._desc(b.kind)
-            nb = L.lmoe_block_workspace_size(ctypes.byref(d), B, N, n_total, world)
-            ws = _workspace(nb, dev)
-            w = self._weights(b)
-            _lib.check(L.lmoe_block_fwd(ctypes.byref(d), ctypes.byref(w), B, N, n_total, x.data_ptr(),
-                                        aux[i:].data_ptr(), handle, rank, world, ws.data_ptr(), ws.numel(), st))
+        for i in range(len(self.blocks)):
+            self.run_block(i, x, B, N, comm, n_total, aux[i:], st)
         h = torch.empty(T, c.hidden, dtype=BF16, device=dev)
         _lib.check(L.lmoe_rmsnorm(x.data_ptr(), T, c.hidden, self.final_norm.data_ptr(), c.norm_eps, h.data_ptr(), st))
         logits = torch.empty(T, c.vocab_size, dtype=torch.float32, device=dev)
