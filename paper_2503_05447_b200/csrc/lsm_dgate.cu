@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(128, 1)
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmDM,
                     const float* __restrict__ b_pre, const float* __restrict__ a_raw,
-                    const float* __restrict__ dkf, float* __restrict__ db_pre, float* __restrict__ da_raw,
-                    int N, int H, int nchunk) {
+                    const float* __restrict__ dkf, const T* __restrict__ dk, float* __restrict__ db_pre,
+                    float* __restrict__ da_raw, int N, int H, int nchunk) {
     using TT = TileTraits<T>;
     using L = DgateSmem<T>;
     constexpr int D = TT::D;
@@ -224,9 +224,41 @@ __global__ void __launch_bounds__(128, 1)
         }
     }
     const float Gt = sG[t];
+    // dkf_t = phi(k_t) . dkeff_t: given, or from dk = kf dkeff (identity feature map)
+    float dkf_t = 0.f;
+    if (t < nvalid) {
+        if (dkf != nullptr) {
+            dkf_t = dkf[(size_t)bh * N + t0 + t];
+        } else {
+            const T* dkr = dk + (((size_t)b * N + t0 + t) * H + h) * D;
+            float acc = 0.f;
+#pragma unroll
+            for (int cb = 0; cb < D / 32; ++cb) {
+                float vk[32];
+                tile_row32<T>(smem + L::kK, kBlockBytes, t, cb * 32, vk);
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                    if constexpr (sizeof(T) == 2) {
+                        const uint4 u = *reinterpret_cast<const uint4*>(dkr + cb * 32 + j);
+                        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 f = unpack_bf16(w[e]);
+                            acc += vk[j + 2 * e] * f.x + vk[j + 2 * e + 1] * f.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc += vk[j + e] * dkr[cb * 32 + j + e];
+                    }
+                }
+            }
+            dkf_t = acc / kf;
+        }
+    }
     const float X = t < nvalid ? __expf(Gt) * xs : 0.f;
     const float Y = t < nvalid ? __expf(gend - Gt) * sKf[t] * ys : 0.f;
     __syncthreads();  // all MMAs consumed Q/K (mma_done) and all threads past their tile reads
+    // (the K rows above are read before this barrier; As overwrites the Q / K tiles below)
     // strictly lower A_ts = S_ts kf_s dP_ts e^{G_t - G_s} (s < t): row sums here, rows to
     // shared memory (XOR-swizzled by t) for the column sums
     float* As = reinterpret_cast<float*>(smem + L::kQ);  // 128 x 128 fp32 over the Q, K tiles
@@ -262,7 +294,7 @@ __global__ void __launch_bounds__(128, 1)
     float dr = 0.f;
     if (t < nvalid) {
         const size_t row = ((size_t)b * N + t0 + t) * H + h;
-        db_pre[row] = sigm(bv) * (dkf[(size_t)bh * N + t0 + t] - spa * dg);
+        db_pre[row] = sigm(bv) * (dkf_t - spa * dg);
         dr = dg * -kf;
     }
     dr = block_sum128(dr, ws);
@@ -275,8 +307,8 @@ __global__ void __launch_bounds__(128, 1)
 template <typename T>
 static cudaError_t dgate_t(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                            const CUtensorMap& dO, const CUtensorMap& m, const CUtensorMap& dm,
-                           const float* b_pre, const float* a_raw, const float* dkf, float* db_pre,
-                           float* da_raw, int B, int N, int H, cudaStream_t st) {
+                           const float* b_pre, const float* a_raw, const float* dkf, const void* dk,
+                           float* db_pre, float* da_raw, int B, int N, int H, cudaStream_t st) {
     static bool attr = false;
     constexpr int smem = DgateSmem<T>::kTotal;
     if (!attr) {
@@ -287,17 +319,18 @@ static cudaError_t dgate_t(const CUtensorMap& q, const CUtensorMap& k, const CUt
     const int nchunk = (N + kC - 1) / kC;
     cudaError_t e = cudaMemsetAsync(da_raw, 0, sizeof(float) * H, st);
     if (e != cudaSuccess) return e;
-    lsm_mamba_dgate<T><<<dim3(nchunk, B * H), 128, smem, st>>>(q, k, v, dO, m, dm, b_pre, a_raw, dkf, db_pre,
-                                                                da_raw, N, H, nchunk);
+    lsm_mamba_dgate<T><<<dim3(nchunk, B * H), 128, smem, st>>>(q, k, v, dO, m, dm, b_pre, a_raw, dkf,
+                                                                static_cast<const T*>(dk), db_pre, da_raw, N, H,
+                                                                nchunk);
     return cudaGetLastError();
 }
 
 cudaError_t launch_mamba_dgate(bool bf16, const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                                const CUtensorMap& dO, const CUtensorMap& m, const CUtensorMap& dm,
-                               const float* b_pre, const float* a_raw, const float* dkf, float* db_pre,
-                               float* da_raw, int B, int N, int H, cudaStream_t st) {
-    return bf16 ? dgate_t<__nv_bfloat16>(q, k, v, dO, m, dm, b_pre, a_raw, dkf, db_pre, da_raw, B, N, H, st)
-                : dgate_t<float>(q, k, v, dO, m, dm, b_pre, a_raw, dkf, db_pre, da_raw, B, N, H, st);
+                               const float* b_pre, const float* a_raw, const float* dkf, const void* dk,
+                               float* db_pre, float* da_raw, int B, int N, int H, cudaStream_t st) {
+    return bf16 ? dgate_t<__nv_bfloat16>(q, k, v, dO, m, dm, b_pre, a_raw, dkf, dk, db_pre, da_raw, B, N, H, st)
+                : dgate_t<float>(q, k, v, dO, m, dm, b_pre, a_raw, dkf, dk, db_pre, da_raw, B, N, H, st);
 }
 
 }  // namespace lmoe_dev

@@ -138,7 +138,8 @@ __global__ void lsm_state_pass(const __grid_constant__ CUtensorMap tmK,
 template <typename T, int DECAY, int FM, bool NORM, bool REV = false>
 __global__ void lsm_output_pass(const __grid_constant__ CUtensorMap tmQ,
                                 const __grid_constant__ CUtensorMap tmK,
-                                const __grid_constant__ CUtensorMap tmV, LsmFwdParams p);
+                                const __grid_constant__ CUtensorMap tmV,
+                                const __grid_constant__ CUtensorMap tmO, LsmFwdParams p);
 __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __restrict__ zS,
                                 const float* __restrict__ logD, const float* __restrict__ M0,
                                 const float* __restrict__ z0, float* __restrict__ Min,

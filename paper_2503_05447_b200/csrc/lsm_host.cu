@@ -790,12 +790,18 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
         };
         float* dphq = F(w.off_dphq);
         float* dkef = F(w.off_dkef);
-        pass(dO, v, phk, dphq, false, true, false, M0T, F(w.off_MfinT), 1);
-        pass(v, dO, phq, dkef, true, true, false, dMfT, nullptr, 2);
+        // identity feature map: dq = dphi(q) and dk = kf dkeff come straight out of the dq / dk
+        // passes (the kf row scale of the REV epilogue), in the input dtype; otherwise fp32
+        // intermediates go through the chain-rule kernel
+        const bool direct = desc->feature_map == 0;
+        pass(dO, v, phk, direct ? dq : dphq, false, !direct, false, M0T, F(w.off_MfinT), 1);
+        pass(v, dO, phq, direct ? dk : dkef, true, !direct, direct && mamba, dMfT, nullptr, 2);
         pass(phk, phq, dO, dv, true, false, mamba, dM_final, dM0, 0);
-        LMOE_CUDA_CHECK(lmoe_dev::launch_bwd_finish(bf16, desc->feature_map, mamba, q, k, dphq, dkef, b_pre, dq,
-                                                    dk, F(w.off_dkf), B, N, H, st));
-        ++g_launch_count;
+        if (!direct) {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_bwd_finish(bf16, desc->feature_map, mamba, q, k, dphq, dkef, b_pre, dq,
+                                                        dk, F(w.off_dkf), B, N, H, st));
+            ++g_launch_count;
+        }
         if (mamba) {
             LsmCall c{&dd, B, N, N, H, D, dtype, q, k, v, b_pre, a_raw, nullptr, ws, w.pl, st, nullptr};
             const CUtensorMapDataType tdt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -810,7 +816,8 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
             } else {
                 tq = c.tmap<float>(phq); tk = c.tmap<float>(phk); tv = c.tmap<float>(v); tdo = c.tmap<float>(dO);
             }
-            LMOE_CUDA_CHECK(lmoe_dev::launch_mamba_dgate(bf16, tq, tk, tv, tdo, tm, tdm, b_pre, a_raw, F(w.off_dkf),
+            LMOE_CUDA_CHECK(lmoe_dev::launch_mamba_dgate(bf16, tq, tk, tv, tdo, tm, tdm, b_pre, a_raw,
+                                                         direct ? nullptr : F(w.off_dkf), direct ? dk : nullptr,
                                                          db_pre, da_raw, B, N, H, st));
             ++g_launch_count;
         }

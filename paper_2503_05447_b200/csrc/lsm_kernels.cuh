@@ -329,7 +329,8 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
 template <typename T, int DECAY, int FM, bool NORM, bool REV>
 __global__ void __launch_bounds__(kOutputPassThreads, 1)
     lsm_output_pass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, LsmFwdParams p) {
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                    LsmFwdParams p) {
     using TT = TileTraits<T>;
     constexpr int D = TT::D;
     constexpr bool kBF16 = sizeof(T) == 2;
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&empty[i], 2);  // MMA commit + the O epilogue (it stages O in the Q tile)
             mbar_init(&s_full[i], 1);
             mbar_init(&gfull[i], 32);
             mbar_init(&gfree[i], kMathThreads);
@@ -852,7 +853,35 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 }
                 if constexpr (REV) inv = qf;
                 const bool vrow = row < nvalid;
-                if (kBF16 && p.out_f32) {  // fp32 rows (backward intermediates)
+                if (kBF16 && !p.out_f32) {
+                    // bf16 O: stage this thread's half row in the (consumed) Q tile in the TMA
+                    // SW128 layout, then one thread bulk-stores the tile (rows >= N clipped)
+#pragma unroll
+                    for (int cb = 0; cb < DH / 32; ++cb) {
+                        uint32_t r[32];
+                        tmem_ld32(tO + lane_off + hh * DH + cb * 32, r);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int ch = 0; ch < 4; ++ch) {
+                            uint4 v;
+                            v.x = pack_bf16(__uint_as_float(r[ch * 8 + 0]) * inv, __uint_as_float(r[ch * 8 + 1]) * inv);
+                            v.y = pack_bf16(__uint_as_float(r[ch * 8 + 2]) * inv, __uint_as_float(r[ch * 8 + 3]) * inv);
+                            v.z = pack_bf16(__uint_as_float(r[ch * 8 + 4]) * inv, __uint_as_float(r[ch * 8 + 5]) * inv);
+                            v.w = pack_bf16(__uint_as_float(r[ch * 8 + 6]) * inv, __uint_as_float(r[ch * 8 + 7]) * inv);
+                            *reinterpret_cast<uint4*>(qt + hh * kBlockBytes + sw128_off(row, cb * 4 + ch)) = v;
+                        }
+                    }
+                    tc_fence_before();
+                    fence_proxy_async_smem();
+                    named_bar_sync(2, kMathThreads);
+                    if (tid == 0) {
+                        tma_store_4d(&tmO, qt, 0, h, t0, b);
+                        tma_store_4d(&tmO, qt + kBlockBytes, TT::EPB, h, t0, b);
+                        bulk_commit();
+                        bulk_wait_read0();
+                        mbar_arrive(&empty[s]);
+                    }
+                } else if (kBF16 && p.out_f32) {  // fp32 rows (backward intermediates)
                     float* dstf = reinterpret_cast<float*>(p.o) +
                                   (((size_t)b * p.Nstride + t0 + (vrow ? row : 0)) * p.H + h) * D + hh * DH;
 #pragma unroll
@@ -896,6 +925,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                     }
                 }
                 }
+                if (!(kBF16 && !p.out_f32) && tid == 0) mbar_arrive(&empty[s]);  // stage untouched
                 tc_fence_before();
                 if (tid == 0) trace_mark(p, c, 5);
             }

@@ -57,8 +57,8 @@ cudaError_t launch_bwd_finish(bool bf16, int fm, bool mamba, const void* q, cons
                               void* dk, float* dkf, int B, int N, int H, cudaStream_t st);
 cudaError_t launch_mamba_dgate(bool bf16, const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                                const CUtensorMap& dO, const CUtensorMap& m, const CUtensorMap& dm,
-                               const float* b_pre, const float* a_raw, const float* dkf, float* db_pre,
-                               float* da_raw, int B, int N, int H, cudaStream_t st);
+                               const float* b_pre, const float* a_raw, const float* dkf, const void* dk,
+                               float* db_pre, float* da_raw, int B, int N, int H, cudaStream_t st);
 cudaError_t launch_transpose_states(const float* in, float* out, int BH, int D, cudaStream_t st);
 cudaError_t launch_apply_fmap(bool bf16, int fm, const void* x, void* y, size_t n, cudaStream_t st);
 }  // namespace lmoe_dev
