@@ -90,6 +90,7 @@ struct TileTraits<__nv_bfloat16> {
     static constexpr int OUT_STAGES = 2;
     static constexpr int SP_STAGES = 3;
     static constexpr bool kTransposed = false;
+    static constexpr int NQ = 4;           // output-pass column groups: 16 math warps
 };
 template <>
 struct TileTraits<float> {
@@ -102,6 +103,7 @@ struct TileTraits<float> {
     static constexpr int OUT_STAGES = 1;
     static constexpr int SP_STAGES = 2;
     static constexpr bool kTransposed = true;  // K-major-only operands
+    static constexpr int NQ = 2;
 };
 
 __device__ __forceinline__ float softplus_f(float x) {
@@ -127,7 +129,10 @@ constexpr int state_pass_smem() {
     return TT::SP_STAGES * 2 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + 4096;
 }
 constexpr int kStatePassThreads = 256;
-constexpr int kOutputPassThreads = 384;
+constexpr int kOutputPassThreads = 384;  // TokenVector output pass (lsm_vec_kernels.cuh)
+// scalar-decay output pass: 4 control warps + NQ warpgroups of math warps
+template <typename T>
+constexpr int output_pass_threads() { return 128 + 128 * TileTraits<T>::NQ; }
 
 // REV = reverse-time pass of the backward (lsm_bwd.cuh): out_i = sum_{j >= i} e^{G_j - G_i}
 // (q'_i . k'_j) v'_j + e^{G_end - G_i} q'_i dM, chunks visited last-to-first, state carried

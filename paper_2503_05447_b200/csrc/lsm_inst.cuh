@@ -32,7 +32,7 @@ cudaError_t op_launch(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CU
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_output_pass<T, DECAY, FM, NORM, REV><<<grid, kOutputPassThreads, output_pass_smem<T>(), st>>>(q, k, v, o, p);
+    lsm_output_pass<T, DECAY, FM, NORM, REV><<<grid, output_pass_threads<T>(), output_pass_smem<T>(), st>>>(q, k, v, o, p);
     return cudaGetLastError();
 }
 

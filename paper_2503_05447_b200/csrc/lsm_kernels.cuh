@@ -85,6 +85,35 @@ __device__ __forceinline__ void xform_half_row(uint8_t* blk, int row, float scal
     }
 }
 
+// Row-owner transform of `ncols` columns starting at col0 of a two-block SW128 tile.
+template <typename T, int FM, bool RND>
+__device__ __forceinline__ void xform_row_part(uint8_t* tile, int row, int col0, int ncols, float scale) {
+    using TT = TileTraits<T>;
+    uint8_t* blk = tile + (col0 / TT::EPB) * kBlockBytes;
+    const int ch0 = (col0 % TT::EPB) / TT::EPC;
+#pragma unroll
+    for (int ch = 0; ch < ncols / TT::EPC; ++ch) {
+        uint4* ptr = reinterpret_cast<uint4*>(blk + sw128_off(row, ch0 + ch));
+        uint4 v = *ptr;
+        if constexpr (sizeof(T) == 2) {
+            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float2 f = unpack_bf16(w[i]);
+                w[i] = pack_bf16(fmap_t<FM>(f.x) * scale, fmap_t<FM>(f.y) * scale);
+            }
+        } else {
+            float* f = reinterpret_cast<float*>(&v);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float x = fmap_t<FM>(f[i]) * scale;
+                f[i] = RND ? tf32r(x) : x;
+            }
+        }
+        *ptr = v;
+    }
+}
+
 // fp32 only: write one token row's 32 values of column block `hb` (already scaled) into a
 // transposed K-major tile [64 d rows x 128 tok] (4 SW128 blocks of 32 tokens, 8 KB apart).
 __device__ __forceinline__ void store_transposed_f32(uint8_t* dstT, int tok, int hb,
@@ -327,7 +356,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
 //      (tf32): S0, S1, O [256,320), M [320,384) (M=64 layout), partials [384,388).
 // ====================================================================================
 template <typename T, int DECAY, int FM, bool NORM, bool REV>
-__global__ void __launch_bounds__(kOutputPassThreads, 1)
+__global__ void __launch_bounds__(output_pass_threads<T>(), 1)
     lsm_output_pass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     LsmFwdParams p) {
@@ -337,7 +366,11 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
     constexpr int NST = TT::OUT_STAGES;
     constexpr bool TR = TT::kTransposed;
     constexpr bool kPrep = FM != 0 || TR;  // phi and/or tf32 rounding before S
-    constexpr int DH = D / 2;              // d_v columns per math-warp half
+    constexpr int NQ = TT::NQ;             // column groups per row (math warpgroups)
+    constexpr int MT = 128 * NQ;           // math threads
+    constexpr int DH = D / NQ;             // d_v columns per math thread (O, M)
+    constexpr int KC = 128 / NQ;           // key columns per math thread (S, P)
+    static_assert(!TR || NQ == 2, "the tf32 transposed path is written for two column halves");
     extern __shared__ __align__(1024) uint8_t smem[];
     if (smem_u32(smem) & 1023) __trap();
     uint8_t* tiles = smem;                                 // NST x [Q | K | V]
@@ -376,13 +409,13 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             mbar_init(&empty[i], 2);  // MMA commit + the O epilogue (it stages O in the Q tile)
             mbar_init(&s_full[i], 1);
             mbar_init(&gfull[i], 32);
-            mbar_init(&gfree[i], kMathThreads);
+            mbar_init(&gfree[i], MT);
         }
-        mbar_init(p_full, kMathThreads);
-        mbar_init(xf2, kMathThreads);
-        mbar_init(m_ready, kMathThreads);
+        mbar_init(p_full, MT);
+        mbar_init(xf2, MT);
+        mbar_init(m_ready, MT);
         mbar_init(mo_full, 1);
-        mbar_init(xf1, kMathThreads);
+        mbar_init(xf1, MT);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(sTmem);
@@ -548,9 +581,9 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
     } else if (warp >= 4) {
         // ---------------- math warps ----------------------------------------------------
         const int mw = warp - 4;
-        const int tid = threadIdx.x - 128;  // 0..255
+        const int tid = threadIdx.x - 128;  // 0..MT-1
         const int q = warp & 3;             // TMEM lane quarter
-        const int hh = mw >> 2;             // column half
+        const int hh = mw >> 2;             // column group (0..NQ-1)
         const int row = q * 32 + lane;      // token row of S / O / Q / K tiles
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         // state rows: d_k index (M=128 layout for bf16, M=64 layout for tf32)
@@ -567,23 +600,24 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             const int nvalid = min(kC, t_end - chunk_t0(c));
             const float sc = row < nvalid ? 1.f : 0.f;
             uint8_t* qt = tiles + s * 3 * kTileBytes;
-            xform_half_row<T, FM, TR>(qt + hh * kBlockBytes, row, sc);
-            xform_half_row<T, FM, TR>(qt + kTileBytes + hh * kBlockBytes, row, sc);
+            xform_row_part<T, FM, TR>(qt, row, hh * DH, DH, sc);
+            xform_row_part<T, FM, TR>(qt + kTileBytes, row, hh * DH, DH, sc);
             fence_proxy_async_smem();
             mbar_arrive(xf1);
         };
         auto write_state_operand = [&](const float* vals) {  // DH values of row srow
             if (!sown) return;
             if constexpr (!TR) {
-                uint8_t* dst = mop + hh * (D * 128);
+                uint8_t* dst = mop + (hh * DH / TT::EPB) * (D * 128);
+                const int ch0 = (hh * DH % TT::EPB) / TT::EPC;
 #pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
+                for (int ch = 0; ch < DH / 8; ++ch) {
                     uint4 v;
                     v.x = pack_bf16(vals[ch * 8 + 0], vals[ch * 8 + 1]);
                     v.y = pack_bf16(vals[ch * 8 + 2], vals[ch * 8 + 3]);
                     v.z = pack_bf16(vals[ch * 8 + 4], vals[ch * 8 + 5]);
                     v.w = pack_bf16(vals[ch * 8 + 6], vals[ch * 8 + 7]);
-                    *reinterpret_cast<uint4*>(dst + sw128_off(srow, ch)) = v;
+                    *reinterpret_cast<uint4*>(dst + sw128_off(srow, ch0 + ch)) = v;
                 }
             } else {
                 // M^T K-major: element (d_v j, d_k i) -> block i/32, row j
@@ -639,7 +673,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             }
             if constexpr (NORM) {
                 if (tid < D) sZ[tid] = p.zin[((size_t)bh * p.nseg + seg) * D + tid];
-                named_bar_sync(1, kMathThreads);
+                named_bar_sync(1, MT);
             }
             tmem_wait_st();
             fence_proxy_async_smem();
@@ -688,11 +722,12 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 if constexpr (DECAY != kDecayNone && REV) fk = __expf(gi);
                 if constexpr (DECAY != kDecayNone && !REV)
                     fk = safe ? __expf(gend - gref) * Fs[row] : __expf(gend - gi) * Fs[row];
-                uint8_t* qb = qt + hh * kBlockBytes;
+                uint8_t* qb = qt + (hh * DH / TT::EPB) * kBlockBytes;
+                const int qch0 = (hh * DH % TT::EPB) / TT::EPC;
                 if constexpr (DECAY != kDecayNone || NORM) {
 #pragma unroll
-                    for (int ch = 0; ch < 8; ++ch) {
-                        uint4* ptr = reinterpret_cast<uint4*>(qb + sw128_off(row, ch));
+                    for (int ch = 0; ch < DH / TT::EPC; ++ch) {
+                        uint4* ptr = reinterpret_cast<uint4*>(qb + sw128_off(row, qch0 + ch));
                         uint4 v = *ptr;
                         if constexpr (kBF16) {
                             uint32_t* w = reinterpret_cast<uint32_t*>(&v);
@@ -700,7 +735,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                             for (int e = 0; e < 4; ++e) {
                                 float2 f = unpack_bf16(w[e]);
                                 f.x *= fq; f.y *= fq;
-                                if constexpr (NORM) qz += f.x * sZ[hh * 64 + ch * 8 + 2 * e] + f.y * sZ[hh * 64 + ch * 8 + 2 * e + 1];
+                                if constexpr (NORM) qz += f.x * sZ[hh * DH + ch * 8 + 2 * e] + f.y * sZ[hh * DH + ch * 8 + 2 * e + 1];
                                 w[e] = pack_bf16(f.x, f.y);
                             }
                         } else {
@@ -708,14 +743,14 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 f[e] = tf32r(f[e] * fq);
-                                if constexpr (NORM) qz += f[e] * sZ[hh * 32 + ch * 4 + e];
+                                if constexpr (NORM) qz += f[e] * sZ[hh * DH + ch * 4 + e];
                             }
                         }
                         if constexpr (DECAY != kDecayNone) *ptr = v;
                     }
                 }
                 if constexpr (!TR) {
-                    if constexpr (DECAY != kDecayNone) xform_half_row<T, 0, false>(kt + hh * kBlockBytes, row, fk);
+                    if constexpr (DECAY != kDecayNone) xform_row_part<T, 0, false>(kt, row, hh * DH, DH, fk);
                 } else {
                     float vals[32];
                     load_half_row_f32(kt + hh * kBlockBytes, row, vals);
@@ -726,11 +761,11 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 fence_proxy_async_smem();
                 if constexpr (NORM) {
                     if (p.order == 0) {  // P already occupies the S buffer: partial slot is free
-                        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart(c) + 2 + hh),
+                        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart(c) + NQ + hh),
                                      "r"(__float_as_uint(qz)) : "memory");
                         tmem_wait_st();
                     }
-                    named_bar_sync(1, kMathThreads);
+                    named_bar_sync(1, MT);
                     if (tid < D) {
                         if constexpr (!TR) {
                             const int blk = tid / TT::EPB, cin = tid % TT::EPB;
@@ -753,17 +788,17 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             };
             // (a) S -> P
             auto do_a = [&]() {
-                uint32_t r0[32], r1[32];
-                const uint32_t tS = tmem + bb * 128 + lane_off + hh * 64;
-                tmem_ld32(tS, r0);
-                tmem_ld32(tS + 32, r1);
+                uint32_t r[KC / 32][32];
+                const uint32_t tS = tmem + bb * 128 + lane_off + hh * KC;
+#pragma unroll
+                for (int i = 0; i < KC / 32; ++i) tmem_ld32(tS + i * 32, r[i]);
                 tmem_wait_ld();
                 const float eq = (DECAY != kDecayNone && safe) ? __expf(REV ? gref - gi : gi - gref) : 1.f;
                 float rs = 0.f;
 #pragma unroll
-                for (int j = 0; j < 64; ++j) {
-                    const int col = hh * 64 + j;
-                    float v = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
+                for (int j = 0; j < KC; ++j) {
+                    const int col = hh * KC + j;
+                    float v = __uint_as_float(r[j / 32][j % 32]);
                     float f;
                     if constexpr (DECAY == kDecayNone) f = 1.f;
                     else if constexpr (REV) f = safe ? eq * Fs[col] : __expf(Gs[col] - gi);
@@ -771,26 +806,29 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                     v = (!p.nomask && (REV ? col >= row : col <= row)) ? v * f : 0.f;
                     if constexpr (TR) v = tf32r(v);
                     rs += v;
-                    if (j < 32) r0[j] = __float_as_uint(v); else r1[j - 32] = __float_as_uint(v);
+                    r[j / 32][j % 32] = __float_as_uint(v);
                 }
                 if constexpr (kBF16) {
-                    uint32_t pk[32];
+                    uint32_t pk[KC / 2];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        pk[j] = pack_bf16(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
-                        pk[16 + j] = pack_bf16(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]));
+                    for (int j = 0; j < KC / 2; ++j)
+                        pk[j] = pack_bf16(__uint_as_float(r[(2 * j) / 32][(2 * j) % 32]),
+                                          __uint_as_float(r[(2 * j + 1) / 32][(2 * j + 1) % 32]));
+                    named_bar_sync(1, MT);  // all S reads done before P overwrites
+                    if constexpr (KC == 32) {
+                        tmem_st16(tmem + bb * 128 + lane_off + hh * 16, pk);
+                    } else {
+                        tmem_st32(tmem + bb * 128 + lane_off + hh * 32, pk);
                     }
-                    named_bar_sync(1, kMathThreads);  // all S reads done before P overwrites
-                    tmem_st32(tmem + bb * 128 + lane_off + hh * 32, pk);
                 } else {
-                    tmem_st32(tS, r0);
-                    tmem_st32(tS + 32, r1);
+#pragma unroll
+                    for (int i = 0; i < KC / 32; ++i) tmem_st32(tS + i * 32, r[i]);
                 }
                 if constexpr (NORM) {
                     asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart(c) + hh),
                                  "r"(__float_as_uint(rs)) : "memory");
                     if (p.order == 1)
-                        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart(c) + 2 + hh),
+                        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart(c) + NQ + hh),
                                      "r"(__float_as_uint(qz)) : "memory");
                 }
                 tmem_wait_st();
@@ -841,13 +879,14 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             {
                 float inv = 1.f;
                 if constexpr (NORM) {
-                    uint32_t pr[4];
-                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                                 : "=r"(pr[0]), "=r"(pr[1]), "=r"(pr[2]), "=r"(pr[3])
-                                 : "r"(tpart(c)));
-                    tmem_wait_ld();
-                    const float den = __uint_as_float(pr[0]) + __uint_as_float(pr[1]) +
-                                      __uint_as_float(pr[2]) + __uint_as_float(pr[3]);
+                    float den = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 2 * NQ; ++i) {
+                        uint32_t pr;
+                        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(pr) : "r"(tpart(c) + i));
+                        tmem_wait_ld();
+                        den += __uint_as_float(pr);
+                    }
                     if (fabsf(den) < 1e-12f && row < nvalid) atomicOr(&p.err[0], 1);
                     inv = 1.f / den;
                 }
@@ -868,12 +907,13 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                             v.y = pack_bf16(__uint_as_float(r[ch * 8 + 2]) * inv, __uint_as_float(r[ch * 8 + 3]) * inv);
                             v.z = pack_bf16(__uint_as_float(r[ch * 8 + 4]) * inv, __uint_as_float(r[ch * 8 + 5]) * inv);
                             v.w = pack_bf16(__uint_as_float(r[ch * 8 + 6]) * inv, __uint_as_float(r[ch * 8 + 7]) * inv);
-                            *reinterpret_cast<uint4*>(qt + hh * kBlockBytes + sw128_off(row, cb * 4 + ch)) = v;
+                            *reinterpret_cast<uint4*>(qt + (hh * DH / TT::EPB) * kBlockBytes +
+                                                      sw128_off(row, (hh * DH % TT::EPB) / TT::EPC + cb * 4 + ch)) = v;
                         }
                     }
                     tc_fence_before();
                     fence_proxy_async_smem();
-                    named_bar_sync(2, kMathThreads);
+                    named_bar_sync(2, MT);
                     if (tid == 0) {
                         tma_store_4d(&tmO, qt, 0, h, t0, b);
                         tma_store_4d(&tmO, qt + kBlockBytes, TT::EPB, h, t0, b);
