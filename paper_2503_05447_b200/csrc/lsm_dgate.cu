@@ -183,11 +183,12 @@ __global__ void __launch_bounds__(128, 1)
     // B_c partial: <M_c, dM_c> over this thread's slice of the (identically laid out) tiles
     float bpart = 0.f;
     {
-        constexpr int per = L::kMT / 128;
-        const uint8_t* pm = smem + L::kM + tid * per;
-        const uint8_t* pd = smem + L::kDM + tid * per;
+        // 16-byte slices interleaved across the threads (a warp reads 512 contiguous bytes)
+        const uint8_t* pm = smem + L::kM + tid * 16;
+        const uint8_t* pd = smem + L::kDM + tid * 16;
         mbar_wait(bar, 0);
-        for (int i = 0; i < per; i += 16) {
+#pragma unroll 4
+        for (int i = 0; i < L::kMT; i += 128 * 16) {
             const uint4 a = *reinterpret_cast<const uint4*>(pm + i);
             const uint4 d = *reinterpret_cast<const uint4*>(pd + i);
             const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, dw[4] = {d.x, d.y, d.z, d.w};
