@@ -115,8 +115,8 @@ def lsm_sequential(spec, q, k, v, a_pre=None, b_pre=None, M0=None, z0=None):
     return o, M, z
 
 
-def lsm_backward(spec, q, k, v, dO, a_pre=None, b_pre=None, M0=None):
-    q, k, v, a_pre, b_pre, M0, dO = map(_f64, (q, k, v, a_pre, b_pre, M0, dO))
+def lsm_backward(spec, q, k, v, dO, a_pre=None, b_pre=None, M0=None, dM_final=None):
+    q, k, v, a_pre, b_pre, M0, dO, dM_final = map(_f64, (q, k, v, a_pre, b_pre, M0, dO, dM_final))
     n, dk = q.shape
     dv = v.shape[1]
     dq, dkk, dvv = np.zeros((n, dk)), np.zeros((n, dk)), np.zeros((n, dv))
@@ -127,7 +127,7 @@ def lsm_backward(spec, q, k, v, dO, a_pre=None, b_pre=None, M0=None):
     sp = _spec(spec)
     _run(lib().lmo_lsm_backward, ctypes.byref(sp), n, dk, dv, _p(q), _p(k), _p(v), _p(a_pre),
          _p(b_pre), _p(M0), _p(dO), _p(dq), _p(dkk), _p(dvv), _p(da), _p(db), ctypes.byref(draw),
-         _p(dM0))
+         _p(dM0), _p(dM_final))
     return {"dq": dq, "dk": dkk, "dv": dvv, "da_pre": da, "db_pre": db, "da_raw": draw.value,
             "dM0": dM0}
 

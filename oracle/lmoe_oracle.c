@@ -301,13 +301,15 @@ int lmo_lsm_backward(const lmo_spec* s, int n, int d_k, int d_v, const double* q
                      const double* k, const double* v, const double* a_pre,
                      const double* b_pre, const double* M0, const double* dO, double* dq,
                      double* dk, double* dv, double* da_pre, double* db_pre, double* da_raw,
-                     double* dM0, char* err, int errlen) {
+                     double* dM0, const double* dM_final, char* err, int errlen) {
     if (lmo_spec_validate(s, d_k, d_v, err, errlen)) return -1;
     if (check_separable(s, err, errlen)) return -1;
     if (s->use_normalizer) { set_err(err, errlen, "oracle backward: normalizer not restated"); return -1; }
     const size_t dd = (size_t)d_k * d_v;
     double* Ms = (double*)malloc(sizeof(double) * dd * (size_t)(n + 1)); /* M_{-1..n-1} */
     double* dM = (double*)calloc(dd, sizeof(double));
+    /* loss gradient w.r.t. the returned final state (lsm_forward_chunked's final_state) */
+    if (dM_final) memcpy(dM, dM_final, sizeof(double) * dd);
     if (M0) memcpy(Ms, M0, sizeof(double) * dd); else memset(Ms, 0, sizeof(double) * dd);
     for (int t = 0; t < n; ++t)
         for (int i = 0; i < d_k; ++i) {

@@ -82,7 +82,8 @@ int lmo_lsm_backward(const lmo_spec* s, int n, int d_k, int d_v,
                      const double* a_pre, const double* b_pre, const double* M0,
                      const double* dO,
                      double* dq, double* dk, double* dv, double* da_pre, double* db_pre,
-                     double* da_raw, double* dM0, char* err, int errlen);
+                     double* da_raw, double* dM0, const double* dM_final /* NULL = 0 */,
+                     char* err, int errlen);
 
 /*
  * route (moe.hpp:58-85): ids (t x top_k, ascending per token), gates and probs

@@ -682,7 +682,7 @@ namespace lmoe_host {
 struct BwdPlan {
     LsmPlan pl;
     size_t off_dphq = 0, off_dkef = 0, off_phq = 0, off_phk = 0, off_M0T = 0, off_dMfT = 0,
-           off_MfinT = 0, off_dkf = 0, off_mst = 0, off_dmst = 0, total = 0;
+           off_MfinT = 0, off_dkf = 0, off_mst = 0, off_dmst = 0, off_bd = 0, total = 0;
 };
 static BwdPlan plan_bwd(const lmoe_lsm_desc* d, int B, int N, int H, int D, lmoe_dtype dt) {
     BwdPlan w;
@@ -706,8 +706,69 @@ static BwdPlan plan_bwd(const lmoe_lsm_desc* d, int B, int N, int H, int D, lmoe
         w.off_mst = take(BH * nchunk * D * D * esz);
         w.off_dmst = take(BH * nchunk * D * D * esz);
     }
+    if (d && device_decay_mode(d->instance) == lmoe_dev::kDecayTokenVector) {
+        // chunk-boundary states and adjoints (bf16) and their row dots, lsm_vec_bwd.cu
+        w.off_mst = take(BH * (nchunk + 1) * D * D * 2);
+        w.off_dmst = take(BH * (nchunk + 1) * D * D * 2);
+        w.off_bd = take(BH * (nchunk + 1) * D * 4);
+    }
     w.total = off;
     return w;
+}
+
+// TokenVector (GLA / HGRN2 / RWKV6) backward, bf16 / D = 128: chunk-boundary states and
+// adjoints by two carry passes, then one fully parallel fused kernel per chunk
+// (lsm_vec_bwd.cu).  q / k are the feature-mapped inputs; dq / dk receive d phi(q) and
+// d keff in fp32 when out_f32 (chain rule by the caller).
+static void vec_backward(const lmoe_lsm_desc& dd, const BwdPlan& w, int B, int N, int H, int D, const void* phq,
+                         const void* phk, const void* v, const void* a_pre, const void* dO, const float* M0,
+                         const float* dM_final, void* dq, void* dk, void* dv, void* da, float* dM0, bool out_f32,
+                         uint8_t* ws, cudaStream_t st) {
+    using bf = __nv_bfloat16;
+    const int nchunk = (N + lmoe_dev::kC - 1) / lmoe_dev::kC;
+    const bool hg = dd.instance == LMOE_HGRN2;
+    LsmCall c{&dd, B, N, N, H, D, LMOE_BF16, phq, phk, v, nullptr, nullptr, nullptr, ws, w.pl, st, a_pre};
+    c.setup();
+    c.clear_err();
+    lmoe_dev::VecBwdParams vp{};
+    vp.B = B; vp.N = N; vp.H = H;
+    vp.seg_len = w.pl.seg_len; vp.nseg = w.pl.nseg; vp.nchunk = nchunk;
+    vp.Min = c.p.Min;
+    vp.bd = reinterpret_cast<const float*>(ws + w.off_bd);
+    vp.dq = dq; vp.dk = dk;
+    vp.dv = static_cast<bf*>(dv);
+    vp.da = static_cast<bf*>(da);
+    vp.out_f32 = out_f32 ? 1 : 0;
+    vp.err = c.p.err;
+    bf* snapM = reinterpret_cast<bf*>(ws + w.off_mst);
+    bf* snapX = reinterpret_cast<bf*>(ws + w.off_dmst);
+    const CUtensorMap tq = c.tmap<bf>(phq), tk = c.tmap<bf>(phk), tv = c.tmap<bf>(v), tdo = c.tmap<bf>(dO),
+                      ta = c.tmap<bf>(a_pre);
+    const dim3 sgrid(w.pl.nseg, H, B);
+    // 1-2: states entering every chunk (forward)
+    c.state_pass<bf>();
+    c.combine(M0, nullptr, true, nullptr, nullptr, nullptr, 0);
+    vp.snap = snapM;
+    LMOE_CUDA_CHECK(lmoe_dev::launch_vec_carry(hg, false, sgrid, st, tk, tv, ta, vp));
+    // 3-4: adjoints leaving every chunk (reverse), dM0
+    LsmCall r = c;
+    r.k = phq;
+    r.v = dO;
+    r.var.rev = 1;
+    r.state_pass<bf>();
+    r.combine(dM_final, nullptr, true, dM0, nullptr, nullptr, 0, 1);
+    vp.snap = snapX;
+    LMOE_CUDA_CHECK(lmoe_dev::launch_vec_carry(false, true, sgrid, st, tq, tdo, ta, vp));
+    // 5: boundary terms of the gate gradient
+    const long long rows = (long long)B * H * (nchunk + 1) * D;
+    LMOE_CUDA_CHECK(lmoe_dev::launch_vec_boundary_dot(snapM, snapX, reinterpret_cast<float*>(ws + w.off_bd), rows, st));
+    // 6: fused chunk backward
+    const CUtensorMap tm[7] = {tq, tk, tv, tdo, ta,
+                               make_tmap_2d(snapM, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, rows, D, 64, 128),
+                               make_tmap_2d(snapX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, rows, D, 64, 128)};
+    LMOE_CUDA_CHECK(lmoe_dev::launch_vec_bwd_chunk(hg, dim3(nchunk, H, B), st, tm, vp));
+    g_launch_count += 4;
+    c.check_err();
 }
 }  // namespace lmoe_host
 
@@ -725,14 +786,16 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
                             size_t workspace_bytes, lmoe_stream_t stream) {
     return guarded([&]() {
         validate(desc, B, N, H, D, dtype, q, k, v, dO);
-        (void)da_pre;
         if (!dq || !dk || !dv) throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: null gradient tensor");
         if (desc->use_normalizer)
             throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_lsm_bwd: normalizer backward not in this build");
         const int mode = device_decay_mode(desc->instance);
-        if (mode == lmoe_dev::kDecayTokenVector)
-            throw Error(LMOE_ERR_UNSUPPORTED, std::string("lmoe_lsm_bwd: instance ") +
-                                                  instance_name(desc->instance) + " has no device backward in this build");
+        if (mode == lmoe_dev::kDecayTokenVector) {
+            if (dtype != LMOE_BF16)
+                throw Error(LMOE_ERR_UNSUPPORTED, std::string("lmoe_lsm_bwd: instance ") + instance_name(desc->instance) +
+                                                      " has a device backward for bf16 / head_dim 128 only");
+            if (!a_pre || !da_pre) throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: TokenVector instances need a_pre and da_pre");
+        }
         const bool mamba = mode == lmoe_dev::kDecayTokenScalar;
         if (mamba && (!db_pre || !da_raw)) throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: Mamba2 needs db_pre and da_raw");
         const BwdPlan w = plan_bwd(desc, B, N, H, D, dtype);
@@ -757,6 +820,21 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
             phq = ws + w.off_phq;
             phk = ws + w.off_phk;
         }
+        const int nchunk = (N + lmoe_dev::kC - 1) / lmoe_dev::kC;
+        float* dphq = F(w.off_dphq);
+        float* dkef = F(w.off_dkef);
+        const bool direct = desc->feature_map == 0;
+        if (mode == lmoe_dev::kDecayTokenVector) {
+            vec_backward(dd, w, B, N, H, D, phq, phk, v, a_pre, dO, M0, dM_final, direct ? dq : dphq,
+                         direct ? dk : dkef, dv, da_pre, dM0, !direct, ws, st);
+            if (!direct) {
+                LMOE_CUDA_CHECK(lmoe_dev::launch_bwd_finish(bf16, desc->feature_map, false, q, k, dphq, dkef, nullptr,
+                                                            dq, dk, F(w.off_dkf), B, N, H, st));
+                ++g_launch_count;
+            }
+            if (desc->flags & LMOE_FLAG_CHECK) LMOE_CUDA_CHECK(cudaStreamSynchronize(st));
+            return;
+        }
         const float* M0T = nullptr;
         if (M0) {
             LMOE_CUDA_CHECK(lmoe_dev::launch_transpose_states(M0, F(w.off_M0T), BH, D, st));
@@ -769,7 +847,6 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
             ++g_launch_count;
             dMfT = F(w.off_dMfT);
         }
-        const int nchunk = (N + lmoe_dev::kC - 1) / lmoe_dev::kC;
         // side: 1 / 2 = write the per-chunk state operands (dq pass: M_c^T, dk pass: dM_c^T)
         auto pass = [&](const void* qq, const void* kk, const void* vv, void* oo, bool rev, bool out_f32,
                         bool kfq, const float* init, float* fin, int side) {
@@ -788,12 +865,9 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
             c.finish_timing();
             c.check_err();
         };
-        float* dphq = F(w.off_dphq);
-        float* dkef = F(w.off_dkef);
         // identity feature map: dq = dphi(q) and dk = kf dkeff come straight out of the dq / dk
         // passes (the kf row scale of the REV epilogue), in the input dtype; otherwise fp32
         // intermediates go through the chain-rule kernel
-        const bool direct = desc->feature_map == 0;
         pass(dO, v, phk, direct ? dq : dphq, false, !direct, false, M0T, F(w.off_MfinT), 1);
         pass(v, dO, phq, direct ? dk : dkef, true, !direct, direct && mamba, dMfT, nullptr, 2);
         pass(phk, phq, dO, dv, true, false, mamba, dM_final, dM0, 0);

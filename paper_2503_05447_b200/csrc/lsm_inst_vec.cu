@@ -5,17 +5,17 @@
 namespace lmoe_dev {
 namespace {
 
-template <typename T, int FM, bool NORM, bool HG>
+template <typename T, int FM, bool NORM, bool HG, bool REV = false>
 cudaError_t spv(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& a,
                 const LsmFwdParams& p) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_state_pass_vec<T, FM, NORM, HG>,
+        cudaError_t e = cudaFuncSetAttribute(lsm_state_pass_vec<T, FM, NORM, HG, REV>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, state_pass_vec_smem<T>());
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_state_pass_vec<T, FM, NORM, HG><<<grid, kStatePassThreads, state_pass_vec_smem<T>(), st>>>(k, v, a, p);
+    lsm_state_pass_vec<T, FM, NORM, HG, REV><<<grid, kStatePassThreads, state_pass_vec_smem<T>(), st>>>(k, v, a, p);
     return cudaGetLastError();
 }
 
@@ -51,6 +51,8 @@ cudaError_t opv(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensor
 
 cudaError_t launch_state_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
                                        const CUtensorMap& val, const CUtensorMap& a, const LsmFwdParams& p) {
+    // backward adjoint states (lsm_vec_bwd.cu): feature map pre-applied, no normaliser
+    if (v.rev) return spv<__nv_bfloat16, 0, false, false, true>(grid, st, k, val, a, p);
     VEC_VARIANTS(spv, __nv_bfloat16, grid, st, k, val, a, p)
 }
 cudaError_t launch_output_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,

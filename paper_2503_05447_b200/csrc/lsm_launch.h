@@ -62,3 +62,26 @@ cudaError_t launch_mamba_dgate(bool bf16, const CUtensorMap& q, const CUtensorMa
 cudaError_t launch_transpose_states(const float* in, float* out, int BH, int D, cudaStream_t st);
 cudaError_t launch_apply_fmap(bool bf16, int fm, const void* x, void* y, size_t n, cudaStream_t st);
 }  // namespace lmoe_dev
+
+namespace lmoe_dev {
+// TokenVector backward (lsm_vec_bwd.cu), bf16 / head dim 128
+struct VecBwdParams {
+    int B, N, H;
+    int seg_len, nseg, nchunk;           // nchunk = ceil(N / 128) chunks of the whole sequence
+    const float* Min;                     // [BH][nseg][D][D] state entering each segment (carry)
+    __nv_bfloat16* snap;                  // carry output [BH][nchunk + 1][D][D]
+    const float* bd;                      // [BH][nchunk + 1][D] boundary dots
+    void* dq;                             // [B, N, H, D] bf16, or fp32 when out_f32
+    void* dk;
+    __nv_bfloat16* dv;
+    __nv_bfloat16* da;                    // [B, N, H, D]
+    int out_f32;                          // dq / dk as fp32 d phi(q) / d keff (feature-map chain rule)
+    int* err;                             // [2]: half-chunk decay span out of the fp32 range
+};
+cudaError_t launch_vec_carry(bool hgrn2, bool rev, dim3 grid, cudaStream_t st, const CUtensorMap& x1,
+                             const CUtensorMap& x2, const CUtensorMap& a, const VecBwdParams& p);
+cudaError_t launch_vec_boundary_dot(const void* M, const void* X, float* bd, long long rows, cudaStream_t st);
+// tm = {q, k, v, dO, a_pre, snapM, snapX}
+cudaError_t launch_vec_bwd_chunk(bool hgrn2, dim3 grid, cudaStream_t st, const CUtensorMap* tm,
+                                 const VecBwdParams& p);
+}  // namespace lmoe_dev

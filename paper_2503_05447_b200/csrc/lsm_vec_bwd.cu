@@ -1,0 +1,633 @@
+// lsm_vec_bwd.cu -- backward of the TokenVector-decay LSM (GLA / HGRN2 / RWKV6, lsm.hpp:64-85,
+// 483-518) on sm_100a, bf16 operands, head dim 128.
+//
+// The reference differentiates chunk_forward_separable (lsm.hpp:554-598) on its tape
+// (tensor.hpp:1178-1215).  Per key column c, with la_t = log sigmoid(a_t), G the inclusive
+// cumulative log decay and A_ts = q_t[c] keff_s[c] e^{G_t[c]-G_s[c]} (dO_t . v_s):
+//   dq_t   = dO_t M_t^T                       (M_t the state after token t)
+//   dkeff_s= v_s dM_s^T                        (dM_s = dL/dM_s, the adjoint state)
+//   dv_s   = sum_{t>=s} (q_t . e^{G_t-G_s} . keff_s) dO_t + keff_s-weighted dM_final
+//   dla_j  = sum_{t>=j} sum_{s<j} A_ts
+// Here the sequence is cut into 128-token chunks and every chunk is differentiated
+// independently, given the state before it (M_c) and the adjoint after it (X_{c+1}):
+//   1. lsm_state_pass_vec (forward) + segment combine      -> M at every segment start
+//   2. lsm_vec_carry<FWD>   per segment, chunk by chunk   -> snapM[c] = M before chunk c (bf16)
+//   3. lsm_state_pass_vec<REV> + reverse combine           -> X at every segment end, dM0
+//   4. lsm_vec_carry<REV>                                  -> snapX[c+1] = X after chunk c
+//   5. lsm_vec_boundary_dot                                -> bd[c][k] = <M_c[k,:], X_c[k,:]>
+//   6. lsm_vec_bwd_chunk    one CTA per chunk: dq, dk, dv, da_pre.
+// The gate gradient avoids the sequence-long cancellation of the telescoped identity
+// dla_j = sum_{t>=j} (q.dq - keff.dkeff)_t: inside a chunk [a, b) the same identity holds
+// with the sum stopped at the chunk end plus the exact boundary term
+//   dla_j = sum_{t in [j,b)} (q.dq - keff.dkeff)_t + <M_{b-1}[c,:], X_b[c,:]>,
+// so the cancellation spans at most 128 tokens.  Inside the chunk the pairwise decay is
+// folded into the operands around the midpoint r = G_63 (as in the forward,
+// lsm_vec_kernels.cuh): q~ = q e^{G-r}, k~ = keff e^{r-G}, and
+//   dq    = e^{G-r} . (dP_m k~ + dO (diag(e^r) M_c)^T)
+//   dkeff = e^{r-G} . (dP_m^T q~ + V (diag(e^{G_end-r}) X)^T)
+//   dv    = (S_m^T dO) + k~ (diag(e^{G_end-r}) X)
+// with dP_m = (dO V^T) . [s<=t], S_m = (q~ k~^T) . [s<=t]; and q.dq - keff.dkeff =
+// q~.dq' - k~.dk' needs no per-element factor.
+#include "lsm_launch.h"
+#include "lsm_vec_kernels.cuh"
+
+namespace lmoe_dev {
+
+
+// ====================================================================================
+// Carry pass: per (b,h,segment) the state is carried chunk by chunk in TMEM and written
+// out (bf16) at every chunk boundary.
+//   FWD: snap[c]   = M;  M <- diag(e^{G_end}) M + (keff . e^{G_end - G})^T V
+//   REV: snap[c+1] = X;  X <- diag(e^{G_end}) X + (q . e^{G})^T dO      (chunks last-to-first)
+// Every weight is <= 1, so no range restriction applies here.  Warps: 0 TMA, 1 MMA,
+// 4-7 thread = key column c = TMEM lane (state row) c.
+// ====================================================================================
+constexpr int kCarryThreads = 256;
+constexpr int kCarryStages = 2;
+constexpr int carry_smem() { return kCarryStages * 3 * kTileBytes + 1024; }
+
+template <bool HG, bool REV>
+__global__ void __launch_bounds__(kCarryThreads, 1)
+    lsm_vec_carry(const __grid_constant__ CUtensorMap tmX1, const __grid_constant__ CUtensorMap tmX2,
+                  const __grid_constant__ CUtensorMap tmA, VecBwdParams p) {
+    using T = __nv_bfloat16;
+    using TT = TileTraits<T>;
+    constexpr int D = TT::D;
+    constexpr int NST = kCarryStages;
+    constexpr int STAGE = 3 * kTileBytes;  // X1 | X2 | A
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if (smem_u32(smem) & 1023) __trap();
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+    uint64_t* full = bars;         // [NST]
+    uint64_t* empty = bars + NST;  // [NST]
+    uint64_t* xf = bars + 2 * NST;
+    uint64_t* acc = xf + 1;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(acc + 1);
+
+    const int seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int bh = b * p.H + h;
+    const int t_begin = seg * p.seg_len;
+    const int t_end = min(p.N, t_begin + p.seg_len);
+    const int nchunks = (t_end - t_begin + kC - 1) / kC;
+    const int c_first = t_begin / kC;
+    const int warp = warp_id(), lane = lane_id();
+    auto chunk_idx = [&](int it) { return c_first + (REV ? nchunks - 1 - it : it); };
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        mbar_init(xf, 128);
+        mbar_init(acc, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<128>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch(&tmX1); tma_prefetch(&tmX2); tma_prefetch(&tmA);
+            for (int it = 0; it < nchunks; ++it) {
+                const int s = it % NST;
+                if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                const int t0 = chunk_idx(it) * kC;
+                uint8_t* st = smem + s * STAGE;
+                mbar_expect_tx(&full[s], STAGE);
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) {
+                    tma_load_4d(st + blk * kBlockBytes, &tmX1, &full[s], blk * TT::EPB, h, t0, b);
+                    tma_load_4d(st + kTileBytes + blk * kBlockBytes, &tmX2, &full[s], blk * TT::EPB, h, t0, b);
+                    tma_load_4d(st + 2 * kTileBytes + blk * kBlockBytes, &tmA, &full[s], blk * TT::EPB, h, t0, b);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc(TT::FMT, 1, 1, 128, D);
+            for (int it = 0; it < nchunks; ++it) {
+                const int s = it % NST;
+                mbar_wait(&full[s], (it / NST) & 1);
+                mbar_wait(xf, it & 1);
+                tc_fence_after();
+                const uint32_t xa = smem_u32(smem + s * STAGE), xb = xa + kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < kC / TT::KSTEP; ++kk)
+                    mma_ss_f16(tmem, umma_desc_sw128(xa + kk * TT::KSTEP * 128, kBlockBytes, 1024),
+                               umma_desc_sw128(xb + kk * TT::KSTEP * 128, kBlockBytes, 1024), idesc, 1u);
+                mma_commit(&empty[s]);
+                mma_commit(acc);
+            }
+        }
+    } else if (warp >= 4) {
+        const int c = threadIdx.x - 128;  // key column == state row
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        // state entering this segment
+        {
+            const float* src = p.Min + (((size_t)bh * p.nseg + seg) * D + c) * D;
+#pragma unroll
+            for (int cb = 0; cb < D / 32; ++cb) {
+                uint32_t r[32];
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    const float4 f = *reinterpret_cast<const float4*>(src + cb * 32 + j);
+                    r[j] = __float_as_uint(f.x); r[j + 1] = __float_as_uint(f.y);
+                    r[j + 2] = __float_as_uint(f.z); r[j + 3] = __float_as_uint(f.w);
+                }
+                tmem_st32(tmem + lane_off + cb * 32, r);
+            }
+            tmem_wait_st();
+        }
+        auto snapshot = [&](int idx, float scale) {
+            // write row c of the TMEM state to snap[idx] (bf16) and rescale it in place
+            __nv_bfloat16* dst = p.snap + (((size_t)bh * (p.nchunk + 1) + idx) * D + c) * D;
+#pragma unroll
+            for (int cb = 0; cb < D / 32; ++cb) {
+                uint32_t r[32];
+                tmem_ld32(tmem + lane_off + cb * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                    uint4 u;
+                    u.x = pack_bf16(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+                    u.y = pack_bf16(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                    u.z = pack_bf16(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
+                    u.w = pack_bf16(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
+                    *reinterpret_cast<uint4*>(dst + cb * 32 + j) = u;
+                }
+                if (scale != 1.f) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * scale);
+                    tmem_st32(tmem + lane_off + cb * 32, r);
+                }
+            }
+            tmem_wait_st();
+        };
+        for (int it = 0; it < nchunks; ++it) {
+            const int s = it % NST;
+            const int ci = chunk_idx(it);
+            const int nvalid = min(kC, p.N - ci * kC);
+            uint8_t* x1 = smem + s * STAGE;
+            uint8_t* at = x1 + 2 * kTileBytes;
+            mbar_wait(&full[s], (it / NST) & 1);
+            // column c: log decays, chunk total, operand weights (in place in the X1 tile)
+            // FWD walks the column bottom-up (L = log decay after row i up to the chunk end),
+            // REV top-down (G = inclusive log decay from the chunk start); either ends at G_end
+            float gend = 0.f;
+            for (int ii = 0; ii < kC; ++ii) {
+                const int i = REV ? ii : kC - 1 - ii;
+                const bool valid = i < nvalid;
+                float x = 0.f;
+                if (valid) {
+                    const float a = ld_elem<T>(at, i, c);
+                    if constexpr (REV) {
+                        gend += log_sigmoid(a);
+                        x = ld_elem<T>(x1, i, c) * __expf(gend);
+                    } else {
+                        x = (HG ? sigmoid_f(-a) : ld_elem<T>(x1, i, c)) * __expf(gend);
+                        gend += log_sigmoid(a);
+                    }
+                }
+                st_elem<T>(x1, i, c, x);
+            }
+            // state: wait for the previous chunk's MMA, snapshot, decay by the chunk total
+            if (it > 0) mbar_wait(acc, (it - 1) & 1);
+            tc_fence_after();
+            snapshot(REV ? ci + 1 : ci, __expf(gend));
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(xf);
+        }
+        mbar_wait(acc, (nchunks - 1) & 1);
+        tc_fence_after();
+        if (REV ? seg == 0 : seg == p.nseg - 1) snapshot(REV ? 0 : p.nchunk, 1.f);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<128>(tmem);
+}
+
+// bd[row] = <M[row, :], X[row, :]> over rows of [BH][nchunk + 1][D] x [D] (one warp per row)
+__global__ void __launch_bounds__(256) lsm_vec_boundary_dot(const __nv_bfloat16* __restrict__ M,
+                                                            const __nv_bfloat16* __restrict__ X,
+                                                            float* __restrict__ bd, long long rows) {
+    const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const uint2 mu = *reinterpret_cast<const uint2*>(M + row * 128 + lane * 4);
+    const uint2 xu = *reinterpret_cast<const uint2*>(X + row * 128 + lane * 4);
+    const float2 m0 = unpack_bf16(mu.x), m1 = unpack_bf16(mu.y);
+    const float2 x0 = unpack_bf16(xu.x), x1 = unpack_bf16(xu.y);
+    float s = m0.x * x0.x + m0.y * x0.y + m1.x * x1.x + m1.y * x1.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if (lane == 0) bd[row] = s;
+}
+
+// ====================================================================================
+// Fused chunk backward: one CTA per (chunk, h, b).  Warps 0 TMA, 1 MMA, 4-11 math.
+// smem: Q | K | V | dO | A | M | X tiles (7 x 32 KB) + scan scratch.
+// TMEM (512 cols): [0,128) dP -> packed dP_m | [128,256) dP^T -> packed | [256,384) S^T ->
+// packed S_m^T | [384,512) dq' then dv;  dk' halves in [64,128) and [192,256) once the
+// packed operands have been written.
+// ====================================================================================
+constexpr int kVbThreads = 384;
+constexpr int vb_smem() { return 7 * kTileBytes + 2048 + 256; }
+
+// 8 consecutive bf16 of row `row`, columns [col8*8, col8*8+8) of a two-block SW128 tile
+__device__ __forceinline__ uint4* tile_chunk(uint8_t* tile, int row, int col8) {
+    return reinterpret_cast<uint4*>(tile + (col8 >> 3) * kBlockBytes + sw128_off(row, col8 & 7));
+}
+
+template <bool HG>
+__global__ void __launch_bounds__(kVbThreads, 1)
+    lsm_vec_bwd_chunk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                      const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
+                      const __grid_constant__ CUtensorMap tmX, VecBwdParams p) {
+    using T = __nv_bfloat16;
+    constexpr int D = 128;
+    constexpr int NM = 256;  // math threads
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if (smem_u32(smem) & 1023) __trap();
+    uint8_t* Qt = smem;
+    uint8_t* Kt = Qt + kTileBytes;
+    uint8_t* Vt = Qt + 2 * kTileBytes;
+    uint8_t* Ot = Qt + 3 * kTileBytes;  // dO
+    uint8_t* At = Qt + 4 * kTileBytes;  // a_pre -> e^{G-r} -> q~dq' - k~dk'
+    uint8_t* Mt = Qt + 5 * kTileBytes;
+    uint8_t* Xt = Qt + 6 * kTileBytes;
+    float* sTot = reinterpret_cast<float*>(Qt + 7 * kTileBytes);  // [2][128]
+    float* sR = sTot + 2 * D;
+    float* sGe = sR + D;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sGe + D);
+    uint64_t* full = bars;
+    uint64_t* xf = bars + 1;
+    uint64_t* s_full = bars + 2;
+    uint64_t* p_full = bars + 3;
+    uint64_t* dq_full = bars + 4;
+    uint64_t* dk_full = bars + 5;
+    uint64_t* dq_free = bars + 6;
+    uint64_t* dv_full = bars + 7;
+    uint64_t* q_free = bars + 8;
+    uint64_t* a_full = bars + 9;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 10);
+
+    const int ci = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int bh = b * p.H + h;
+    const int t0 = ci * kC;
+    const int nvalid = min(kC, p.N - t0);
+    const int warp = warp_id(), lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        mbar_init(full, 1);
+        mbar_init(xf, NM);
+        mbar_init(s_full, 1);
+        mbar_init(p_full, NM);
+        mbar_init(dq_full, 1);
+        mbar_init(dk_full, 1);
+        mbar_init(dq_free, NM);
+        mbar_init(dv_full, 1);
+        mbar_init(q_free, NM);
+        mbar_init(a_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+    const uint32_t T0 = tmem, T1 = tmem + 128, T2 = tmem + 256, T3 = tmem + 384;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmDO);
+            tma_prefetch(&tmA); tma_prefetch(&tmM); tma_prefetch(&tmX);
+            const int mrow = (bh * (p.nchunk + 1) + ci) * D;
+            const int xrow = (bh * (p.nchunk + 1) + ci + 1) * D;
+            mbar_expect_tx(full, 7 * kTileBytes);
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) {
+                const int c0 = blk * 64;
+                tma_load_4d(Qt + blk * kBlockBytes, &tmQ, full, c0, h, t0, b);
+                tma_load_4d(Kt + blk * kBlockBytes, &tmK, full, c0, h, t0, b);
+                tma_load_4d(Vt + blk * kBlockBytes, &tmV, full, c0, h, t0, b);
+                tma_load_4d(Ot + blk * kBlockBytes, &tmDO, full, c0, h, t0, b);
+                tma_load_4d(At + blk * kBlockBytes, &tmA, full, c0, h, t0, b);
+                tma_load_2d(Mt + blk * kBlockBytes, &tmM, full, c0, mrow);
+                tma_load_2d(Xt + blk * kBlockBytes, &tmX, full, c0, xrow);
+            }
+            // raw gates again for the gate-gradient scan, into the Q tile once it is consumed
+            mbar_wait(q_free, 0);
+            mbar_expect_tx(a_full, kTileBytes);
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) tma_load_4d(Qt + blk * kBlockBytes, &tmA, a_full, blk * 64, h, t0, b);
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idSS = umma_idesc(1, 0, 0, 128, 128);   // A K-major, B K-major
+            constexpr uint32_t idTS = umma_idesc(1, 0, 1, 128, 128);   // B MN-major
+            constexpr uint32_t idTSh = umma_idesc(1, 0, 1, 128, 64);
+            constexpr uint32_t idSSh = umma_idesc(1, 0, 0, 128, 64);
+            constexpr uint32_t idSM = umma_idesc(1, 0, 1, 128, 128);   // A K-major, B MN-major
+            const uint32_t q = smem_u32(Qt), k = smem_u32(Kt), v = smem_u32(Vt), o = smem_u32(Ot);
+            const uint32_t m = smem_u32(Mt), x = smem_u32(Xt);
+            auto kdesc = [](uint32_t base, int kk) {  // K-major operand, K slice kk of 16
+                return umma_desc_sw128(base + (kk >> 2) * kBlockBytes + (kk & 3) * 32, 16, 1024);
+            };
+            auto mdesc = [](uint32_t base, int kk) {  // MN-major operand, K rows [16kk, 16kk+16)
+                return umma_desc_sw128(base + kk * 16 * 128, kBlockBytes, 1024);
+            };
+            mbar_wait(full, 0);
+            mbar_wait(xf, 0);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_ss_f16(T0, kdesc(o, kk), kdesc(v, kk), idSS, kk > 0);  // dP
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_ss_f16(T1, kdesc(v, kk), kdesc(o, kk), idSS, kk > 0);  // dP^T
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_ss_f16(T2, kdesc(k, kk), kdesc(q, kk), idSS, kk > 0);  // S^T
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_ss_f16(T3, kdesc(o, kk), kdesc(m, kk), idSS, kk > 0);  // dO M'^T
+            mma_commit(s_full);
+            mbar_wait(p_full, 0);
+            tc_fence_after();
+            // dq' += dP_m k~
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_ts_f16(T3, T0 + kk * 8, mdesc(k, kk), idTS, 1u);
+            mma_commit(dq_full);
+            // dk' = dP_m^T q~ + V X'^T, two N = 64 halves
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const uint32_t dst = hf ? tmem + 192 : tmem + 64;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_ts_f16(dst, T1 + kk * 8, mdesc(q + hf * kBlockBytes, kk), idTSh, kk > 0);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) mma_ss_f16(dst, kdesc(v, kk), kdesc(x + hf * 8192, kk), idSSh, 1u);
+            }
+            mma_commit(dk_full);
+            // dv = S_m^T dO + k~ X'   (into [384,512) once dq' has been read)
+            mbar_wait(dq_free, 0);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_ts_f16(T3, T2 + kk * 8, mdesc(o, kk), idTS, kk > 0);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_ss_f16(T3, kdesc(k, kk), mdesc(x, kk), idSM, 1u);
+            mma_commit(dv_full);
+        }
+    } else if (warp >= 4) {
+        const int tid = threadIdx.x - 128;  // 0..255
+        // ---------------- (T) column scans and operand transforms (slab = tid / 128)
+        const int col = tid & 127, slab = tid >> 7;
+        mbar_wait(full, 0);
+        {
+            float G[64];
+            float run = 0.f;
+#pragma unroll
+            for (int ii = 0; ii < 64; ++ii) {
+                const int i = slab * 64 + ii;
+                run += (i < nvalid) ? log_sigmoid(ld_elem<T>(At, i, col)) : 0.f;
+                G[ii] = run;
+            }
+            sTot[slab * D + col] = run;
+            named_bar_sync(1, NM);
+            const float r = sTot[col];               // G at row 63 (inclusive)
+            const float ge = r + sTot[D + col];      // G at the chunk end
+            const float off = slab ? r : 0.f;
+            if (slab == 0) {
+                sR[col] = r;
+                sGe[col] = ge;
+                if (!((G[0] - r) < -kSafeLogDecay && (r - ge) < -kSafeLogDecay)) atomicOr(&p.err[2], 1);
+            }
+#pragma unroll
+            for (int ii = 0; ii < 64; ++ii) {
+                const int i = slab * 64 + ii;
+                const bool valid = i < nvalid;
+                const float e = __expf(G[ii] + off - r);
+                float qv = 0.f, kv = 0.f;
+                if (valid) {
+                    qv = ld_elem<T>(Qt, i, col) * e;
+                    const float keff = HG ? sigmoid_f(-ld_elem<T>(At, i, col)) : ld_elem<T>(Kt, i, col);
+                    kv = keff / e;
+                }
+                st_elem<T>(Qt, i, col, qv);
+                st_elem<T>(Kt, i, col, kv);
+                st_elem<T>(At, i, col, e);
+            }
+        }
+        named_bar_sync(1, NM);
+        {
+            // M' = diag(e^r) M_c, X' = diag(e^{G_end - r}) X_{c+1}: thread = (row, column block)
+            const int row = tid & 127, blk = tid >> 7;
+            xform_half_row<T, 0, false>(Mt + blk * kBlockBytes, row, __expf(sR[row]));
+            xform_half_row<T, 0, false>(Xt + blk * kBlockBytes, row, __expf(sGe[row] - sR[row]));
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(xf);
+
+        // ---------------- (E1) masks, packed bf16 operands in TMEM (row layout)
+        const int mw = warp - 4;
+        const int qd = warp & 3, hh = mw >> 2;
+        const int row = qd * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+        mbar_wait(s_full, 0);
+        tc_fence_after();
+        auto pack_masked = [&](uint32_t base, bool lower, uint32_t (&pk)[32]) {
+            uint32_t r0[32], r1[32];
+            tmem_ld32(base + lane_off + hh * 64, r0);
+            tmem_ld32(base + lane_off + hh * 64 + 32, r1);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int c0 = hh * 64 + 2 * j, c1 = c0 + 32;
+                // lower: keep col <= row (dP, rows t / cols s); else keep col >= row (transposed)
+                const bool k00 = lower ? c0 <= row : c0 >= row, k01 = lower ? c0 + 1 <= row : c0 + 1 >= row;
+                const bool k10 = lower ? c1 <= row : c1 >= row, k11 = lower ? c1 + 1 <= row : c1 + 1 >= row;
+                pk[j] = pack_bf16(k00 ? __uint_as_float(r0[2 * j]) : 0.f, k01 ? __uint_as_float(r0[2 * j + 1]) : 0.f);
+                pk[16 + j] = pack_bf16(k10 ? __uint_as_float(r1[2 * j]) : 0.f, k11 ? __uint_as_float(r1[2 * j + 1]) : 0.f);
+            }
+        };
+        {
+            uint32_t pa[32], pb[32];
+            pack_masked(T0, true, pa);
+            pack_masked(T1, false, pb);
+            named_bar_sync(1, NM);  // every fp32 read of these regions precedes the packed writes
+            tmem_st32(T0 + lane_off + hh * 32, pa);
+            tmem_st32(T1 + lane_off + hh * 32, pb);
+            pack_masked(T2, false, pa);
+            named_bar_sync(1, NM);
+            tmem_st32(T2 + lane_off + hh * 32, pa);
+            tmem_wait_st();
+        }
+        tc_fence_before();
+        mbar_arrive(p_full);
+
+        // ---------------- (E2) dq, dk and the gate integrand q~dq' - k~dk'
+        mbar_wait(dq_full, 0);
+        mbar_wait(dk_full, 0);
+        tc_fence_after();
+        {
+            const bool vrow = row < nvalid;
+            const size_t grow = (((size_t)b * p.N + t0 + (vrow ? row : 0)) * p.H + h) * D;
+#pragma unroll 1
+            for (int cb = 0; cb < 2; ++cb) {
+                const int cbase = hh * 64 + cb * 32;
+                uint32_t rq[32], rk[32];
+                tmem_ld32(T3 + lane_off + cbase, rq);
+                tmem_ld32(tmem + 64 + hh * 128 + cb * 32 + lane_off, rk);
+                tmem_wait_ld();
+                float dqv[32], dkv[32];
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    const int c8 = cbase / 8 + ch;
+                    const uint4 eu = *tile_chunk(At, row, c8);
+                    const uint4 qu = *tile_chunk(Qt, row, c8);
+                    const uint4 ku = *tile_chunk(Kt, row, c8);
+                    const uint32_t* ew = reinterpret_cast<const uint32_t*>(&eu);
+                    const uint32_t* qw = reinterpret_cast<const uint32_t*>(&qu);
+                    const uint32_t* kw = reinterpret_cast<const uint32_t*>(&ku);
+                    uint4 du, hu;
+                    uint32_t* dw = reinterpret_cast<uint32_t*>(&du);
+                    uint32_t* hw = reinterpret_cast<uint32_t*>(&hu);
+#pragma unroll
+                    for (int w2 = 0; w2 < 4; ++w2) {
+                        const float2 e = unpack_bf16(ew[w2]), qq = unpack_bf16(qw[w2]), kq = unpack_bf16(kw[w2]);
+                        const int j = ch * 8 + w2 * 2;
+                        const float q0 = __uint_as_float(rq[j]), q1 = __uint_as_float(rq[j + 1]);
+                        const float k0 = __uint_as_float(rk[j]), k1 = __uint_as_float(rk[j + 1]);
+                        dqv[j] = e.x * q0; dqv[j + 1] = e.y * q1;
+                        dkv[j] = HG ? 0.f : k0 / e.x; dkv[j + 1] = HG ? 0.f : k1 / e.y;
+                        dw[w2] = pack_bf16(qq.x * q0 - kq.x * k0, qq.y * q1 - kq.y * k1);
+                        if constexpr (HG) hw[w2] = pack_bf16(kq.x * k0, kq.y * k1);
+                    }
+                    *tile_chunk(At, row, c8) = du;              // own elements: no cross-thread hazard
+                    if constexpr (HG) *tile_chunk(Vt, row, c8) = hu;  // V is dead once dk' is done
+                }
+                if (vrow) {
+                    if (p.out_f32) {
+                        float* gq = static_cast<float*>(p.dq) + grow + cbase;
+                        float* gk = static_cast<float*>(p.dk) + grow + cbase;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            *reinterpret_cast<float4*>(gq + j) = make_float4(dqv[j], dqv[j + 1], dqv[j + 2], dqv[j + 3]);
+                            *reinterpret_cast<float4*>(gk + j) = make_float4(dkv[j], dkv[j + 1], dkv[j + 2], dkv[j + 3]);
+                        }
+                    } else {
+                        T* gq = static_cast<T*>(p.dq) + grow + cbase;
+                        T* gk = static_cast<T*>(p.dk) + grow + cbase;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            uint4 a, c;
+                            a.x = pack_bf16(dqv[j], dqv[j + 1]); a.y = pack_bf16(dqv[j + 2], dqv[j + 3]);
+                            a.z = pack_bf16(dqv[j + 4], dqv[j + 5]); a.w = pack_bf16(dqv[j + 6], dqv[j + 7]);
+                            c.x = pack_bf16(dkv[j], dkv[j + 1]); c.y = pack_bf16(dkv[j + 2], dkv[j + 3]);
+                            c.z = pack_bf16(dkv[j + 4], dkv[j + 5]); c.w = pack_bf16(dkv[j + 6], dkv[j + 7]);
+                            *reinterpret_cast<uint4*>(gq + j) = a;
+                            *reinterpret_cast<uint4*>(gk + j) = c;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(dq_free);
+            mbar_arrive(q_free);
+            // ---------------- (E3) dv
+            mbar_wait(dv_full, 0);
+            tc_fence_after();
+#pragma unroll 1
+            for (int cb = 0; cb < 2; ++cb) {
+                const int cbase = hh * 64 + cb * 32;
+                uint32_t rv[32];
+                tmem_ld32(T3 + lane_off + cbase, rv);
+                tmem_wait_ld();
+                if (vrow) {
+                    T* gv = p.dv + grow + cbase;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        uint4 a;
+                        a.x = pack_bf16(__uint_as_float(rv[j]), __uint_as_float(rv[j + 1]));
+                        a.y = pack_bf16(__uint_as_float(rv[j + 2]), __uint_as_float(rv[j + 3]));
+                        a.z = pack_bf16(__uint_as_float(rv[j + 4]), __uint_as_float(rv[j + 5]));
+                        a.w = pack_bf16(__uint_as_float(rv[j + 6]), __uint_as_float(rv[j + 7]));
+                        *reinterpret_cast<uint4*>(gv + j) = a;
+                    }
+                }
+            }
+            tc_fence_before();
+        }
+        named_bar_sync(1, NM);  // the integrand tile is complete
+
+        // ---------------- (S) gate gradient: reverse in-chunk scan + boundary term
+        mbar_wait(a_full, 0);
+        {
+            float tot = 0.f;
+            for (int ii = 0; ii < 64; ++ii) tot += ld_elem<T>(At, slab * 64 + ii, col);
+            sTot[slab * D + col] = tot;
+            named_bar_sync(1, NM);
+            float acc = p.bd[((size_t)bh * (p.nchunk + 1) + ci + 1) * D + col] + (slab == 0 ? sTot[D + col] : 0.f);
+            T* gda = p.da + ((size_t)b * p.N + t0) * p.H * D + (size_t)h * D + col;
+            for (int ii = 63; ii >= 0; --ii) {
+                const int i = slab * 64 + ii;
+                acc += ld_elem<T>(At, i, col);
+                if (i < nvalid) {
+                    const float sg = sigmoid_f(ld_elem<T>(Qt, i, col));
+                    float g = acc * (1.f - sg);
+                    if constexpr (HG) g -= ld_elem<T>(Vt, i, col) * sg;
+                    gda[(size_t)i * p.H * D] = __float2bfloat16_rn(g);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------------------------------------------- launchers
+template <bool HG, bool REV>
+static cudaError_t carry_t(dim3 grid, cudaStream_t st, const CUtensorMap& x1, const CUtensorMap& x2,
+                           const CUtensorMap& a, const VecBwdParams& p) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(lsm_vec_carry<HG, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             carry_smem());
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    lsm_vec_carry<HG, REV><<<grid, kCarryThreads, carry_smem(), st>>>(x1, x2, a, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vec_carry(bool hgrn2, bool rev, dim3 grid, cudaStream_t st, const CUtensorMap& x1,
+                             const CUtensorMap& x2, const CUtensorMap& a, const VecBwdParams& p) {
+    if (rev) return carry_t<false, true>(grid, st, x1, x2, a, p);
+    return hgrn2 ? carry_t<true, false>(grid, st, x1, x2, a, p) : carry_t<false, false>(grid, st, x1, x2, a, p);
+}
+
+cudaError_t launch_vec_boundary_dot(const void* M, const void* X, float* bd, long long rows, cudaStream_t st) {
+    lsm_vec_boundary_dot<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(M),
+                                                                      static_cast<const __nv_bfloat16*>(X), bd, rows);
+    return cudaGetLastError();
+}
+
+template <bool HG>
+static cudaError_t chunk_t(dim3 grid, cudaStream_t st, const CUtensorMap* tm, const VecBwdParams& p) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(lsm_vec_bwd_chunk<HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             vb_smem());
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    lsm_vec_bwd_chunk<HG><<<grid, kVbThreads, vb_smem(), st>>>(tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], tm[6], p);
+    return cudaGetLastError();
+}
+
+// tm = {q, k, v, dO, a_pre, snapM, snapX}
+cudaError_t launch_vec_bwd_chunk(bool hgrn2, dim3 grid, cudaStream_t st, const CUtensorMap* tm,
+                                 const VecBwdParams& p) {
+    return hgrn2 ? chunk_t<true>(grid, st, tm, p) : chunk_t<false>(grid, st, tm, p);
+}
+
+}  // namespace lmoe_dev

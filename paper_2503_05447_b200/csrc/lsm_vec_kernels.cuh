@@ -14,6 +14,9 @@
 //     w_jk = e^{L_jk} keff_jk,  L_jk = sum of log a over tokens after j up to the segment end.
 // A chunk whose half-chunk span exceeds the bound raises "non-finite output in div" -- the
 // reference's own message for its K/p form (lsm.hpp:576-577) in the same regime.
+// REV (backward adjoint states, lsm_vec_bwd.cu): the state pass visits chunks first-to-last
+// with w_jk = e^{P_jk}, P_jk = log decay from the segment start through token j (inclusive),
+// so S_seg = sum_j (phi(q_j) . w_j)^T dO_j is the segment's contribution to dM at its start.
 #pragma once
 #include "lsm_kernels.cuh"
 
@@ -48,7 +51,7 @@ __device__ __forceinline__ float* tr_elem(uint8_t* tileT, int d, int tok) {
 // ====================================================================================
 // Phase 1 (vector decay): warps 0 TMA, 1 MMA, 2-3 idle, 4-7 transform (thread = column)
 // ====================================================================================
-template <typename T, int FM, bool NORM, bool HG>
+template <typename T, int FM, bool NORM, bool HG, bool REV = false>
 __global__ void __launch_bounds__(kStatePassThreads, 1)
     lsm_state_pass_vec(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        const __grid_constant__ CUtensorMap tmA, LsmFwdParams p) {
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     const int t_end = min(p.N, t_begin + p.seg_len);
     const int nchunks = (t_end - t_begin + kC - 1) / kC;
     const int warp = warp_id(), lane = lane_id();
-    auto chunk_t0 = [&](int it) { return t_begin + (nchunks - 1 - it) * kC; };
+    auto chunk_t0 = [&](int it) { return t_begin + (REV ? it : nchunks - 1 - it) * kC; };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -151,7 +154,20 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
             const int nvalid = min(kC, t_end - chunk_t0(it));
             mbar_wait(&full[s], (it / NST) & 1);
             if (TR && it >= 1) mbar_wait(kt_free, (it - 1) & 1);
-            if (tid < D) {
+            if (REV && tid < D) {
+                float P = suffix;  // log decay from the segment start through the current row
+                for (int i = 0; i < kC; ++i) {
+                    const bool valid = i < nvalid;
+                    if (valid) P += log_sigmoid(ld_elem<T>(at, i, tid));
+                    const float x = valid ? fmap_t<FM>(ld_elem<T>(kt, i, tid)) * __expf(P) : 0.f;
+                    if constexpr (!TR) st_elem<T>(kt, i, tid, x);
+                    else {
+                        *tr_elem(kT, tid, i) = tf32r(x);
+                        *tr_elem(vT, tid, i) = tf32r(ld_elem<T>(vt, i, tid));
+                    }
+                }
+                suffix = P;
+            } else if (tid < D) {
                 float L = suffix;  // log decay from the current row (exclusive) to segment end
                 for (int i = kC - 1; i >= 0; --i) {
                     const bool valid = i < nvalid;

@@ -44,7 +44,7 @@ def _round(x, dtype):
     return t.numpy().astype(np.float64)
 
 
-def _bwd(spec_d, q, k, v, dO, b_pre=None, a_raw_h=None, M0=None, dMf=None, dtype="bf16"):
+def _bwd(spec_d, q, k, v, dO, b_pre=None, a_raw_h=None, M0=None, dMf=None, dtype="bf16", a_pre=None):
     """numpy [B,N,H,D] in; numpy float64 gradients out."""
     torch = _torch()
     import paper_2503_05447_b200 as pk
@@ -55,22 +55,24 @@ def _bwd(spec_d, q, k, v, dO, b_pre=None, a_raw_h=None, M0=None, dMf=None, dtype
                       use_normalizer=bool(spec_d.get("use_normalizer", 0)),
                       scalar_decay=spec_d.get("scalar_decay", 1.0), mamba2_a_raw=a_raw_h)
     gates = None if b_pre is None else pk.LsmGates(b_pre=T(b_pre, torch.float32))
+    if a_pre is not None:
+        gates = pk.LsmGates(a_pre=T(a_pre))
     init = None if M0 is None else pk.MemoryState(M=T(M0, torch.float32))
     g = pk.lsm_backward_batched(T(q), T(k), T(v), gates, spec, T(dO), initial_state=init,
                                 dM_final=None if dMf is None else T(dMf, torch.float32))
     torch.cuda.synchronize()
     out = {}
-    for name in ("dq", "dk", "dv", "db_pre", "da_raw", "dM0"):
+    for name in ("dq", "dk", "dv", "db_pre", "da_raw", "da_pre", "dM0"):
         x = getattr(g, name)
         if x is not None:
             out[name] = x.float().cpu().numpy().astype(np.float64)
     return out
 
 
-def _oracle_bwd(spec_d, q, k, v, dO, b_pre, a_raw_h, M0):
+def _oracle_bwd(spec_d, q, k, v, dO, b_pre, a_raw_h, M0, a_pre=None, dMf=None):
     """Per-head oracle backward over [B,N,H,D] arrays."""
     B, N, H, D = q.shape
-    res = {n: np.zeros_like(q) for n in ("dq", "dk", "dv")}
+    res = {n: np.zeros_like(q) for n in ("dq", "dk", "dv", "da_pre")}
     res["dM0"] = np.zeros((B, H, D, D))
     res["db_pre"] = np.zeros((B, N, H))
     res["da_raw"] = np.zeros(H)
@@ -80,9 +82,12 @@ def _oracle_bwd(spec_d, q, k, v, dO, b_pre, a_raw_h, M0):
             if a_raw_h is not None:
                 sp["mamba2_a_raw"] = float(a_raw_h[h])
             g = oracle.lsm_backward(sp, q[b, :, h], k[b, :, h], v[b, :, h], dO[b, :, h],
-                                    None, None if b_pre is None else b_pre[b, :, h],
-                                    None if M0 is None else M0[b, h])
+                                    None if a_pre is None else a_pre[b, :, h],
+                                    None if b_pre is None else b_pre[b, :, h],
+                                    None if M0 is None else M0[b, h],
+                                    None if dMf is None else dMf[b, h])
             res["dq"][b, :, h], res["dk"][b, :, h], res["dv"][b, :, h] = g["dq"], g["dk"], g["dv"]
+            res["da_pre"][b, :, h] = g["da_pre"]
             res["dM0"][b, h] = g["dM0"]
             if b_pre is not None:
                 res["db_pre"][b, :, h] = g["db_pre"]
@@ -231,3 +236,78 @@ def test_bwd_error_texts():
         pk.lsm_backward_batched(x, x, x, None, pk.LsmSpec.make("bla", 128), x)
     with pytest.raises(RuntimeError, match="shape mismatch"):
         pk.lsm_backward_batched(x, x, x[:, :8], None, pk.LsmSpec.make("retnet", 128), x)
+
+
+# ------------------------------------------------------------------ TokenVector (GLA / HGRN2 / RWKV6)
+VEC_KINDS = {3: "gla", 14: "hgrn2", 15: "rwkv6"}
+
+
+def test_golden_vector_grads_padded():
+    """Reference tape gradients of GLA / HGRN2 (d = 4, lsm_grad.npz) through lsm_vec_bwd.cu.
+    Padded key columns get a_pre = 0: their q / k / v / dO are 0, so they cannot reach the
+    first 4 columns (HGRN2's keff = 1 - sigmoid(0) only feeds state rows that q never reads)."""
+    d = load_golden("lsm_grad")
+    D = 128
+    ran = 0
+    for p in sorted({k.split("/")[0] for k in d}):
+        spec = oracle.spec_from_golden(d, p)
+        if spec["instance"] not in VEC_KINDS:
+            continue
+        pad = lambda x: np.pad(x, ((0, 0), (0, D - x.shape[1])))[None, :, None]
+        q, k, v, dO, a = (pad(_round(d[p + "/" + n], "bf16")) for n in ("q", "k", "v", "dO", "a_pre"))
+        got = _bwd(spec, q, k, v, dO, dtype="bf16", a_pre=a)
+        for n in ("dq", "dk", "dv", "da_pre"):
+            want = d[p + "/" + n]
+            g = got[n][0, :, 0, :4]
+            if np.abs(want).max() == 0:
+                assert np.abs(g).max() == 0, (p, n)
+                continue
+            err = norm_rel_err(g, want)
+            assert err < TOL["bf16"], (p, n, err)
+        ran += 1
+    assert ran == 3  # gla, hgrn2, rwkv6
+
+
+VCASES = [  # (name, spec, B, N, H, a_pre mean)
+    ("gla", {"instance": 3}, 1, 700, 2, 0.0),
+    ("gla_b2_ragged", {"instance": 3}, 2, 333, 2, 0.0),
+    ("gla_long_memory", {"instance": 3}, 1, 4096, 1, 4.0),
+    ("gla_elu1", {"instance": 3, "feature_map": 1}, 1, 520, 2, 1.0),
+    ("hgrn2", {"instance": 14}, 1, 700, 2, 1.0),
+    ("rwkv6", {"instance": 15}, 1, 1000, 2, 2.0),
+    ("gla_tiny", {"instance": 3}, 1, 1, 1, 0.0),
+]
+
+
+@pytest.mark.parametrize("case", VCASES, ids=[c[0] for c in VCASES])
+def test_vector_bwd_matches_oracle(case):
+    name, spec, B, N, H, amean = case
+    D = 128
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    q, k, v = (_round(rng.normal(0, 0.5, (B, N, H, D)), "bf16") for _ in range(3))
+    dO = _round(rng.normal(0, 1.0, (B, N, H, D)), "bf16")
+    a = _round(rng.normal(amean, 1.0 if amean == 0 else 0.5, (B, N, H, D)), "bf16")
+    M0 = rng.normal(0, 0.1, (B, H, D, D))
+    dMf = rng.normal(0, 0.1, (B, H, D, D))
+    got = _bwd(spec, q, k, v, dO, None, None, M0, dMf, dtype="bf16", a_pre=a)
+    want = _oracle_bwd(spec, q, k, v, dO, None, None, M0, a_pre=a, dMf=dMf)
+    for n in ("dq", "dk", "dv", "da_pre"):
+        for b in range(B):
+            for h in range(H):
+                if spec["instance"] == 14 and n == "dk":
+                    assert np.abs(got[n][b, :, h]).max() == 0  # HGRN2 keff = 1 - a ignores k
+                    continue
+                err = norm_rel_err(got[n][b, :, h], want[n][b, :, h])
+                assert err < TOL["bf16"], (name, n, b, h, err)
+    for b in range(B):
+        for h in range(H):
+            assert norm_rel_err(got["dM0"][b, h], want["dM0"][b, h]) < TOL["bf16"], (name, "dM0", b, h)
+
+
+def test_vector_bwd_f32_is_refused():
+    torch = _torch()
+    import paper_2503_05447_b200 as pk
+    dev = torch.device("cuda:0")
+    x = torch.zeros(1, 16, 1, 64, dtype=torch.float32, device=dev)
+    with pytest.raises(pk.LmoeError, match="bf16 / head_dim 128 only"):
+        pk.lsm_backward_batched(x, x, x, pk.LsmGates(a_pre=x), pk.LsmSpec.make("gla", 64), x)

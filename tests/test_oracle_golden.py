@@ -226,3 +226,29 @@ def test_sp_nomask_matches_reference():
             assert int(d[p + "/comm_elems_t%d" % t][0]) == t * q.shape[1] * v.shape[1]
     with pytest.raises(oracle.OracleError, match="requires an undecayed instance"):
         oracle.sp_forward_nomask(oracle.spec_default("retnet"), q, k, v, 2)
+
+
+def test_backward_final_state_gradient_matches_finite_differences():
+    """dM_final seeding of the oracle backward (the gradient the reference tape sends back
+    through lsm_forward_chunked's final_state, lsm.hpp:668-708) for a TokenVector kind."""
+    rng = np.random.default_rng(11)
+    n, d = 37, 5
+    sp = oracle.spec_default("gla")
+    q, k, v, a = (rng.normal(0, 0.5, (n, d)) for _ in range(4))
+    M0 = rng.normal(0, 0.3, (d, d))
+    dO = rng.normal(0, 1, (n, d))
+    dMf = rng.normal(0, 1, (d, d))
+    g = oracle.lsm_backward(sp, q, k, v, dO, a_pre=a, M0=M0, dM_final=dMf)
+
+    def loss(q_, k_, v_, a_, M0_):
+        o, M, _ = oracle.lsm_chunked(sp, q_, k_, v_, a_pre=a_, chunk=8, M0=M0_)
+        return float((o * dO).sum() + (M * dMf).sum())
+
+    args = [q, k, v, a, M0]
+    for i, name in enumerate(["dq", "dk", "dv", "da_pre", "dM0"]):
+        u = rng.normal(0, 1, args[i].shape)
+        plus = list(args); plus[i] = args[i] + 1e-6 * u
+        minus = list(args); minus[i] = args[i] - 1e-6 * u
+        fd = (loss(*plus) - loss(*minus)) / 2e-6
+        an = float((g[name] * u).sum())
+        assert abs(an - fd) < 1e-6 * max(1.0, abs(fd)), (name, an, fd)
