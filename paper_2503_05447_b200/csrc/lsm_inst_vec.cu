@@ -15,7 +15,7 @@ cudaError_t spv(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CUtensor
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_state_pass_vec<T, FM, NORM, HG, REV><<<grid, kStatePassThreads, state_pass_vec_smem<T>(), st>>>(k, v, a, p);
+    lsm_state_pass_vec<T, FM, NORM, HG, REV><<<grid, kStatePassVecThreads, state_pass_vec_smem<T>(), st>>>(k, v, a, p);
     return cudaGetLastError();
 }
 

@@ -30,6 +30,7 @@
 // q~.dq' - k~.dk' needs no per-element factor.
 #include "lsm_launch.h"
 #include "lsm_vec_kernels.cuh"
+#include "lsm_vec_scan.cuh"
 
 namespace lmoe_dev {
 
@@ -40,11 +41,11 @@ namespace lmoe_dev {
 //   FWD: snap[c]   = M;  M <- diag(e^{G_end}) M + (keff . e^{G_end - G})^T V
 //   REV: snap[c+1] = X;  X <- diag(e^{G_end}) X + (q . e^{G})^T dO      (chunks last-to-first)
 // Every weight is <= 1, so no range restriction applies here.  Warps: 0 TMA, 1 MMA,
-// 4-7 thread = key column c = TMEM lane (state row) c.
+// 4-11 transforms (2-D scan layout); warps 4-7 also own the TMEM state rows (row = key c).
 // ====================================================================================
-constexpr int kCarryThreads = 256;
+constexpr int kCarryThreads = 128 + kVecNT;
 constexpr int kCarryStages = 2;
-constexpr int carry_smem() { return kCarryStages * 3 * kTileBytes + 1024; }
+constexpr int carry_smem() { return kCarryStages * 3 * kTileBytes + (16 + 3) * 128 * 4 + 128; }
 
 template <bool HG, bool REV>
 __global__ void __launch_bounds__(kCarryThreads, 1)
@@ -57,7 +58,11 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
     constexpr int STAGE = 3 * kTileBytes;  // X1 | X2 | A
     extern __shared__ __align__(1024) uint8_t smem[];
     if (smem_u32(smem) & 1023) __trap();
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+    float* sTot = reinterpret_cast<float*>(smem + NST * STAGE);  // [16][D]
+    float* sR = sTot + 16 * D;
+    float* sGe = sR + D;
+    float* sG0 = sGe + D;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sG0 + D);
     uint64_t* full = bars;         // [NST]
     uint64_t* empty = bars + NST;  // [NST]
     uint64_t* xf = bars + 2 * NST;
@@ -75,7 +80,7 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        mbar_init(xf, 128);
+        mbar_init(xf, kVecNT);
         mbar_init(acc, 1);
         fence_barrier_init();
     }
@@ -120,10 +125,14 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int c = threadIdx.x - 128;  // key column == state row
+        using L = VecLayout<T>;
+        const int tid = threadIdx.x - 128;
+        const int cg = tid & 15, rg = tid >> 4;
+        const bool owner = warp < 8;  // TMEM state row c = tid
+        const int c = tid;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         // state entering this segment
-        {
+        if (owner) {
             const float* src = p.Min + (((size_t)bh * p.nseg + seg) * D + c) * D;
 #pragma unroll
             for (int cb = 0; cb < D / 32; ++cb) {
@@ -170,37 +179,44 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
             uint8_t* x1 = smem + s * STAGE;
             uint8_t* at = x1 + 2 * kTileBytes;
             mbar_wait(&full[s], (it / NST) & 1);
-            // column c: log decays, chunk total, operand weights (in place in the X1 tile)
-            // FWD walks the column bottom-up (L = log decay after row i up to the chunk end),
-            // REV top-down (G = inclusive log decay from the chunk start); either ends at G_end
-            float gend = 0.f;
-            for (int ii = 0; ii < kC; ++ii) {
-                const int i = REV ? ii : kC - 1 - ii;
-                const bool valid = i < nvalid;
-                float x = 0.f;
-                if (valid) {
-                    const float a = ld_elem<T>(at, i, c);
-                    if constexpr (REV) {
-                        gend += log_sigmoid(a);
-                        x = ld_elem<T>(x1, i, c) * __expf(gend);
-                    } else {
-                        x = (HG ? sigmoid_f(-a) : ld_elem<T>(x1, i, c)) * __expf(gend);
-                        gend += log_sigmoid(a);
-                    }
+            float G[L::R][L::EPC];
+            float nocarry = 0.f;
+            vec_log_scan<T>(at, nvalid, tid, G, sTot, sR, sGe, sG0, nullptr, nocarry);
+            // operand weights in place in the X1 tile: FWD e^{G_end - G} keff, REV e^{G} q
+#pragma unroll
+            for (int ii = 0; ii < L::R; ++ii) {
+                const int row = rg * L::R + ii;
+                const bool valid = row < nvalid;
+                float x[L::EPC], av[L::EPC];
+                ld_chunk<T>(x1, row, cg, x);
+                if constexpr (HG && !REV) ld_chunk<T>(at, row, cg, av);
+#pragma unroll
+                for (int j = 0; j < L::EPC; ++j) {
+                    float w;
+                    if constexpr (REV) w = __expf(G[ii][j]);
+                    else w = __expf(sGe[cg * L::EPC + j] - G[ii][j]);
+                    float xv;
+                    if constexpr (HG && !REV) xv = sigmoid_f(-av[j]);
+                    else xv = x[j];
+                    x[j] = valid ? xv * w : 0.f;
                 }
-                st_elem<T>(x1, i, c, x);
+                st_chunk<T>(x1, row, cg, x);
             }
             // state: wait for the previous chunk's MMA, snapshot, decay by the chunk total
-            if (it > 0) mbar_wait(acc, (it - 1) & 1);
-            tc_fence_after();
-            snapshot(REV ? ci + 1 : ci, __expf(gend));
+            if (owner) {
+                if (it > 0) mbar_wait(acc, (it - 1) & 1);
+                tc_fence_after();
+                snapshot(REV ? ci + 1 : ci, __expf(sGe[c]));
+            }
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(xf);
         }
-        mbar_wait(acc, (nchunks - 1) & 1);
-        tc_fence_after();
-        if (REV ? seg == 0 : seg == p.nseg - 1) snapshot(REV ? 0 : p.nchunk, 1.f);
+        if (owner) {
+            mbar_wait(acc, (nchunks - 1) & 1);
+            tc_fence_after();
+            if (REV ? seg == 0 : seg == p.nseg - 1) snapshot(REV ? 0 : p.nchunk, 1.f);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -226,13 +242,16 @@ __global__ void __launch_bounds__(256) lsm_vec_boundary_dot(const __nv_bfloat16*
 
 // ====================================================================================
 // Fused chunk backward: one CTA per (chunk, h, b).  Warps 0 TMA, 1 MMA, 4-11 math.
-// smem: Q | K | V | dO | A | M | X tiles (7 x 32 KB) + scan scratch.
+// smem: Q | K | V | dO | A | M | X tiles (7 x 32 KB).  The 2-D scan scratch of the gate
+// scan lives in the M tile region, so M and X are loaded once that scan is done (their
+// latency hides behind the operand transforms) and the region is reused by the final
+// gate-gradient scan once M' has been consumed.
 // TMEM (512 cols): [0,128) dP -> packed dP_m | [128,256) dP^T -> packed | [256,384) S^T ->
 // packed S_m^T | [384,512) dq' then dv;  dk' halves in [64,128) and [192,256) once the
 // packed operands have been written.
 // ====================================================================================
 constexpr int kVbThreads = 384;
-constexpr int vb_smem() { return 7 * kTileBytes + 2048 + 256; }
+constexpr int vb_smem() { return 7 * kTileBytes + 3 * 128 * 4 + 256; }
 
 // 8 consecutive bf16 of row `row`, columns [col8*8, col8*8+8) of a two-block SW128 tile
 __device__ __forceinline__ uint4* tile_chunk(uint8_t* tile, int row, int col8) {
@@ -257,10 +276,11 @@ __global__ void __launch_bounds__(kVbThreads, 1)
     uint8_t* At = Qt + 4 * kTileBytes;  // a_pre -> e^{G-r} -> q~dq' - k~dk'
     uint8_t* Mt = Qt + 5 * kTileBytes;
     uint8_t* Xt = Qt + 6 * kTileBytes;
-    float* sTot = reinterpret_cast<float*>(Qt + 7 * kTileBytes);  // [2][128]
-    float* sR = sTot + 2 * D;
+    float* sTot = reinterpret_cast<float*>(Mt);  // [16][128] scan scratch (M region, see above)
+    float* sR = reinterpret_cast<float*>(Qt + 7 * kTileBytes);
     float* sGe = sR + D;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sGe + D);
+    float* sG0 = sGe + D;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sG0 + D);
     uint64_t* full = bars;
     uint64_t* xf = bars + 1;
     uint64_t* s_full = bars + 2;
@@ -271,7 +291,9 @@ __global__ void __launch_bounds__(kVbThreads, 1)
     uint64_t* dv_full = bars + 7;
     uint64_t* q_free = bars + 8;
     uint64_t* a_full = bars + 9;
-    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* scan_done = bars + 10;
+    uint64_t* mx_full = bars + 11;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 12);
 
     const int ci = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int bh = b * p.H + h;
@@ -290,6 +312,8 @@ __global__ void __launch_bounds__(kVbThreads, 1)
         mbar_init(dv_full, 1);
         mbar_init(q_free, NM);
         mbar_init(a_full, 1);
+        mbar_init(scan_done, NM);
+        mbar_init(mx_full, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(sTmem);
@@ -305,18 +329,22 @@ __global__ void __launch_bounds__(kVbThreads, 1)
             tma_prefetch(&tmA); tma_prefetch(&tmM); tma_prefetch(&tmX);
             const int mrow = (bh * (p.nchunk + 1) + ci) * D;
             const int xrow = (bh * (p.nchunk + 1) + ci + 1) * D;
-            mbar_expect_tx(full, 7 * kTileBytes);
+            mbar_expect_tx(full, 5 * kTileBytes);
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) {
                 const int c0 = blk * 64;
+                tma_load_4d(At + blk * kBlockBytes, &tmA, full, c0, h, t0, b);
                 tma_load_4d(Qt + blk * kBlockBytes, &tmQ, full, c0, h, t0, b);
                 tma_load_4d(Kt + blk * kBlockBytes, &tmK, full, c0, h, t0, b);
                 tma_load_4d(Vt + blk * kBlockBytes, &tmV, full, c0, h, t0, b);
                 tma_load_4d(Ot + blk * kBlockBytes, &tmDO, full, c0, h, t0, b);
-                tma_load_4d(At + blk * kBlockBytes, &tmA, full, c0, h, t0, b);
-                tma_load_2d(Mt + blk * kBlockBytes, &tmM, full, c0, mrow);
-                tma_load_2d(Xt + blk * kBlockBytes, &tmX, full, c0, xrow);
             }
+            mbar_expect_tx(mx_full, 2 * kTileBytes);
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) tma_load_2d(Xt + blk * kBlockBytes, &tmX, mx_full, blk * 64, xrow);
+            mbar_wait(scan_done, 0);  // the scan scratch in the M region is dead
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) tma_load_2d(Mt + blk * kBlockBytes, &tmM, mx_full, blk * 64, mrow);
             // raw gates again for the gate-gradient scan, into the Q tile once it is consumed
             mbar_wait(q_free, 0);
             mbar_expect_tx(a_full, kTileBytes);
@@ -339,6 +367,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                 return umma_desc_sw128(base + kk * 16 * 128, kBlockBytes, 1024);
             };
             mbar_wait(full, 0);
+            mbar_wait(mx_full, 0);
             mbar_wait(xf, 0);
             tc_fence_after();
 #pragma unroll
@@ -378,45 +407,38 @@ __global__ void __launch_bounds__(kVbThreads, 1)
         }
     } else if (warp >= 4) {
         const int tid = threadIdx.x - 128;  // 0..255
-        // ---------------- (T) column scans and operand transforms (slab = tid / 128)
-        const int col = tid & 127, slab = tid >> 7;
+        // ---------------- (T) 2-D column scan, operand transforms, M' / X' row scales
+        using L = VecLayout<T>;
+        const int cg = tid & 15, rg = tid >> 4;
         mbar_wait(full, 0);
         {
-            float G[64];
-            float run = 0.f;
+            float G[L::R][L::EPC];
+            float nocarry = 0.f;
+            vec_log_scan<T>(At, nvalid, tid, G, sTot, sR, sGe, sG0, nullptr, nocarry);
+            mbar_arrive(scan_done);
+            if (tid < D && !vec_split_ok(sG0[tid], sR[tid], sGe[tid])) atomicOr(&p.err[2], 1);
 #pragma unroll
-            for (int ii = 0; ii < 64; ++ii) {
-                const int i = slab * 64 + ii;
-                run += (i < nvalid) ? log_sigmoid(ld_elem<T>(At, i, col)) : 0.f;
-                G[ii] = run;
-            }
-            sTot[slab * D + col] = run;
-            named_bar_sync(1, NM);
-            const float r = sTot[col];               // G at row 63 (inclusive)
-            const float ge = r + sTot[D + col];      // G at the chunk end
-            const float off = slab ? r : 0.f;
-            if (slab == 0) {
-                sR[col] = r;
-                sGe[col] = ge;
-                if (!((G[0] - r) < -kSafeLogDecay && (r - ge) < -kSafeLogDecay)) atomicOr(&p.err[2], 1);
-            }
-#pragma unroll
-            for (int ii = 0; ii < 64; ++ii) {
-                const int i = slab * 64 + ii;
+            for (int ii = 0; ii < L::R; ++ii) {
+                const int i = rg * L::R + ii;
                 const bool valid = i < nvalid;
-                const float e = __expf(G[ii] + off - r);
-                float qv = 0.f, kv = 0.f;
-                if (valid) {
-                    qv = ld_elem<T>(Qt, i, col) * e;
-                    const float keff = HG ? sigmoid_f(-ld_elem<T>(At, i, col)) : ld_elem<T>(Kt, i, col);
-                    kv = keff / e;
+                float xq[8], xk[8], xa[8];
+                ld_chunk<T>(Qt, i, cg, xq);
+                ld_chunk<T>(At, i, cg, xa);
+                if constexpr (!HG) ld_chunk<T>(Kt, i, cg, xk);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float e = __expf(G[ii][j] - sR[cg * 8 + j]);
+                    const float keff = HG ? sigmoid_f(-xa[j]) : xk[j];
+                    xq[j] = valid ? xq[j] * e : 0.f;
+                    xk[j] = valid ? keff / e : 0.f;
+                    xa[j] = e;
                 }
-                st_elem<T>(Qt, i, col, qv);
-                st_elem<T>(Kt, i, col, kv);
-                st_elem<T>(At, i, col, e);
+                st_chunk<T>(Qt, i, cg, xq);
+                st_chunk<T>(Kt, i, cg, xk);
+                st_chunk<T>(At, i, cg, xa);
             }
         }
-        named_bar_sync(1, NM);
+        mbar_wait(mx_full, 0);
         {
             // M' = diag(e^r) M_c, X' = diag(e^{G_end - r}) X_{c+1}: thread = (row, column block)
             const int row = tid & 127, blk = tid >> 7;
@@ -558,23 +580,55 @@ __global__ void __launch_bounds__(kVbThreads, 1)
         }
         named_bar_sync(1, NM);  // the integrand tile is complete
 
-        // ---------------- (S) gate gradient: reverse in-chunk scan + boundary term
+        // ---------------- (S) gate gradient: reverse in-chunk scan + boundary term (2-D layout;
+        // the M region is free since dq' consumed M')
         mbar_wait(a_full, 0);
         {
-            float tot = 0.f;
-            for (int ii = 0; ii < 64; ++ii) tot += ld_elem<T>(At, slab * 64 + ii, col);
-            sTot[slab * D + col] = tot;
+            float Dv[L::R][8];
+            float tot[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tot[j] = 0.f;
+#pragma unroll
+            for (int ii = 0; ii < L::R; ++ii) {
+                ld_chunk<T>(At, rg * L::R + ii, cg, Dv[ii]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) tot[j] += Dv[ii][j];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sTot[rg * D + cg * 8 + j] = tot[j];
             named_bar_sync(1, NM);
-            float acc = p.bd[((size_t)bh * (p.nchunk + 1) + ci + 1) * D + col] + (slab == 0 ? sTot[D + col] : 0.f);
-            T* gda = p.da + ((size_t)b * p.N + t0) * p.H * D + (size_t)h * D + col;
-            for (int ii = 63; ii >= 0; --ii) {
-                const int i = slab * 64 + ii;
-                acc += ld_elem<T>(At, i, col);
+            if (tid < D) {  // exclusive suffix over later row groups, seeded with the boundary term
+                float acc = p.bd[((size_t)bh * (p.nchunk + 1) + ci + 1) * D + tid];
+#pragma unroll
+                for (int g = L::RG - 1; g >= 0; --g) {
+                    const float v = sTot[g * D + tid];
+                    sTot[g * D + tid] = acc;
+                    acc += v;
+                }
+            }
+            named_bar_sync(1, NM);
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = sTot[rg * D + cg * 8 + j];
+            T* gda = p.da + (((size_t)b * p.N + t0) * p.H + h) * D + cg * 8;
+#pragma unroll
+            for (int ii = L::R - 1; ii >= 0; --ii) {
+                const int i = rg * L::R + ii;
+                float av[8], kd[8], g[8];
+                ld_chunk<T>(Qt, i, cg, av);  // raw a_pre (reloaded)
+                if constexpr (HG) ld_chunk<T>(Vt, i, cg, kd);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    acc[j] += Dv[ii][j];
+                    const float sg = sigmoid_f(av[j]);
+                    g[j] = acc[j] * (1.f - sg);
+                    if constexpr (HG) g[j] -= kd[j] * sg;
+                }
                 if (i < nvalid) {
-                    const float sg = sigmoid_f(ld_elem<T>(Qt, i, col));
-                    float g = acc * (1.f - sg);
-                    if constexpr (HG) g -= ld_elem<T>(Vt, i, col) * sg;
-                    gda[(size_t)i * p.H * D] = __float2bfloat16_rn(g);
+                    uint4 u;
+                    u.x = pack_bf16(g[0], g[1]); u.y = pack_bf16(g[2], g[3]);
+                    u.z = pack_bf16(g[4], g[5]); u.w = pack_bf16(g[6], g[7]);
+                    *reinterpret_cast<uint4*>(gda + (size_t)i * p.H * D) = u;
                 }
             }
         }

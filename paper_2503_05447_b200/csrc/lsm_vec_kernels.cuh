@@ -18,7 +18,7 @@
 // with w_jk = e^{P_jk}, P_jk = log decay from the segment start through token j (inclusive),
 // so S_seg = sum_j (phi(q_j) . w_j)^T dO_j is the segment's contribution to dM at its start.
 #pragma once
-#include "lsm_kernels.cuh"
+#include "lsm_vec_scan.cuh"
 
 namespace lmoe_dev {
 
@@ -49,14 +49,19 @@ __device__ __forceinline__ float* tr_elem(uint8_t* tileT, int d, int tok) {
 }
 
 // ====================================================================================
-// Phase 1 (vector decay): warps 0 TMA, 1 MMA, 2-3 idle, 4-7 transform (thread = column)
+// Phase 1 (vector decay): warps 0 TMA, 1 MMA, 2-3 idle, 4-11 transform (2-D layout,
+// lsm_vec_scan.cuh); warps 4-7 also drain the TMEM accumulator.
 // ====================================================================================
+constexpr int kStatePassVecThreads = 128 + kVecNT;
+
 template <typename T, int FM, bool NORM, bool HG, bool REV = false>
-__global__ void __launch_bounds__(kStatePassThreads, 1)
+__global__ void __launch_bounds__(kStatePassVecThreads, 1)
     lsm_state_pass_vec(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        const __grid_constant__ CUtensorMap tmA, LsmFwdParams p) {
     using TT = TileTraits<T>;
+    using L = VecLayout<T>;
     constexpr int D = TT::D;
+    constexpr int EPC = L::EPC;
     constexpr bool TR = TT::kTransposed;
     constexpr int NST = TR ? 1 : 2;
     constexpr int STAGE = 3 * kTileBytes;  // K | V | A
@@ -65,7 +70,13 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     uint8_t* tiles = smem;
     uint8_t* kT = tiles + NST * STAGE;
     uint8_t* vT = kT + (TR ? kTileBytes : 0);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(vT + (TR ? kTileBytes : 0));
+    float* sTot = reinterpret_cast<float*>(vT + (TR ? kTileBytes : 0));  // [RG][D]
+    float* sR = sTot + L::RG * D;
+    float* sGe = sR + D;
+    float* sG0 = sGe + D;
+    float* sCar = sG0 + D;
+    float* sZ = sCar + D;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sZ + D);
     uint64_t* full = bars;          // [NST]
     uint64_t* empty = bars + 2;     // [NST]
     uint64_t* xf = bars + 4;
@@ -83,7 +94,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        mbar_init(xf, 128);
+        mbar_init(xf, kVecNT);
         mbar_init(acc_full, 1);
         mbar_init(kt_free, 1);
         fence_barrier_init();
@@ -143,9 +154,14 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
             mma_commit(acc_full);
         }
     } else if (warp >= 4) {
-        const int tid = threadIdx.x - 128;  // column k (tid < D)
-        const int q = warp & 3;
-        float suffix = 0.f, zacc = 0.f;
+        const int tid = threadIdx.x - 128;
+        const int cg = tid & 15, rg = tid >> 4;
+        // carry: FWD the log decay of the later chunks of the segment (suffix), REV of the
+        // earlier ones (prefix); per column, held by threads tid < D
+        float carry = 0.f;
+        if constexpr (NORM) {
+            if (tid < D) sZ[tid] = 0.f;
+        }
         for (int it = 0; it < nchunks; ++it) {
             const int s = it % NST;
             uint8_t* kt = tiles + s * STAGE;
@@ -154,62 +170,74 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
             const int nvalid = min(kC, t_end - chunk_t0(it));
             mbar_wait(&full[s], (it / NST) & 1);
             if (TR && it >= 1) mbar_wait(kt_free, (it - 1) & 1);
-            if (REV && tid < D) {
-                float P = suffix;  // log decay from the segment start through the current row
-                for (int i = 0; i < kC; ++i) {
-                    const bool valid = i < nvalid;
-                    if (valid) P += log_sigmoid(ld_elem<T>(at, i, tid));
-                    const float x = valid ? fmap_t<FM>(ld_elem<T>(kt, i, tid)) * __expf(P) : 0.f;
-                    if constexpr (!TR) st_elem<T>(kt, i, tid, x);
-                    else {
-                        *tr_elem(kT, tid, i) = tf32r(x);
-                        *tr_elem(vT, tid, i) = tf32r(ld_elem<T>(vt, i, tid));
+            float G[L::R][EPC];
+            vec_log_scan<T>(at, nvalid, tid, G, sTot, sR, sGe, sG0, sCar, carry);
+            float zc[EPC];
+#pragma unroll
+            for (int j = 0; j < EPC; ++j) zc[j] = 0.f;
+#pragma unroll
+            for (int ii = 0; ii < L::R; ++ii) {
+                const int row = rg * L::R + ii;
+                const bool valid = row < nvalid;
+                float x[EPC], av[EPC];
+                ld_chunk<T>(kt, row, cg, x);
+                if constexpr (HG && !REV) ld_chunk<T>(at, row, cg, av);
+#pragma unroll
+                for (int j = 0; j < EPC; ++j) {
+                    const int c = cg * EPC + j;
+                    // REV: w = e^{prefix + G}; FWD: w = e^{(G_end - G) + suffix} (both <= 1)
+                    const float w = REV ? __expf(G[ii][j] + sCar[c]) : __expf(sGe[c] - G[ii][j] + sCar[c]);
+                    float keff;
+                    if constexpr (HG && !REV) keff = sigmoid_f(-av[j]);
+                    else keff = fmap_t<FM>(x[j]);
+                    x[j] = valid ? keff * w : 0.f;
+                    if constexpr (NORM) zc[j] += x[j];
+                }
+                if constexpr (!TR) {
+                    st_chunk<T>(kt, row, cg, x);
+                } else {
+                    float vv[EPC];
+                    ld_chunk<T>(vt, row, cg, vv);
+#pragma unroll
+                    for (int j = 0; j < EPC; ++j) {
+                        *tr_elem(kT, cg * EPC + j, row) = tf32r(x[j]);
+                        *tr_elem(vT, cg * EPC + j, row) = tf32r(vv[j]);
                     }
                 }
-                suffix = P;
-            } else if (tid < D) {
-                float L = suffix;  // log decay from the current row (exclusive) to segment end
-                for (int i = kC - 1; i >= 0; --i) {
-                    const bool valid = i < nvalid;
-                    const float a = ld_elem<T>(at, i, tid);
-                    float keff = 0.f;
-                    if (valid) keff = HG ? sigmoid_f(-a) : fmap_t<FM>(ld_elem<T>(kt, i, tid));
-                    const float kw = keff * __expf(L);
-                    if constexpr (!TR) st_elem<T>(kt, i, tid, kw);
-                    else {
-                        *tr_elem(kT, tid, i) = tf32r(kw);
-                        *tr_elem(vT, tid, i) = tf32r(ld_elem<T>(vt, i, tid));
-                    }
-                    if constexpr (NORM) zacc += kw;
-                    if (valid) L += log_sigmoid(a);
-                }
-                suffix = L;
+            }
+            if constexpr (NORM) {
+#pragma unroll
+                for (int j = 0; j < EPC; ++j) atomicAdd(&sZ[cg * EPC + j], zc[j]);
             }
             fence_proxy_async_smem();
             mbar_arrive(xf);
         }
         mbar_wait(acc_full, 0);
         tc_fence_after();
-        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const int row = TR ? q * 16 + lane : q * 32 + lane;
-        const bool own = TR ? lane < 16 : true;
-        float* dst = p.Sseg + (((size_t)bh * p.nseg + seg) * D + (own ? row : 0)) * D;
+        if (warp < 8) {
+            const int q = warp & 3;
+            const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+            const int row = TR ? q * 16 + lane : q * 32 + lane;
+            const bool own = TR ? lane < 16 : true;
+            float* dst = p.Sseg + (((size_t)bh * p.nseg + seg) * D + (own ? row : 0)) * D;
 #pragma unroll
-        for (int cb = 0; cb < D / 32; ++cb) {
-            uint32_t r[32];
-            tmem_ld32(tmem + lane_off + cb * 32, r);
-            tmem_wait_ld();
-            if (own) {
+            for (int cb = 0; cb < D / 32; ++cb) {
+                uint32_t r[32];
+                tmem_ld32(tmem + lane_off + cb * 32, r);
+                tmem_wait_ld();
+                if (own) {
 #pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    *reinterpret_cast<float4*>(dst + cb * 32 + j) =
-                        make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                    __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(dst + cb * 32 + j) =
+                            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                }
             }
         }
+        named_bar_sync(1, kVecNT);  // sZ complete
         if (tid < D) {
-            p.logDseg[((size_t)bh * p.nseg + seg) * D + tid] = suffix;
-            if constexpr (NORM) p.zseg[((size_t)bh * p.nseg + seg) * D + tid] = zacc;
+            p.logDseg[((size_t)bh * p.nseg + seg) * D + tid] = carry;
+            if constexpr (NORM) p.zseg[((size_t)bh * p.nseg + seg) * D + tid] = sZ[tid];
         }
     }
     tc_fence_before();
@@ -232,8 +260,8 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
     constexpr bool kBF16 = sizeof(T) == 2;
     constexpr bool TR = TT::kTransposed;
     constexpr int DH = D / 2;
-    constexpr int NSLAB = kMathThreads / D;  // column slabs: 2 (bf16) / 4 (fp32)
-    constexpr int ROWS = kC / NSLAB;          // rows per slab
+    using L = VecLayout<T>;
+    static_assert(kMathThreads == kVecNT, "2-D scan layout");
     constexpr int STAGE = 4 * kTileBytes;     // Q | K | V | A
     extern __shared__ __align__(1024) uint8_t smem[];
     if (smem_u32(smem) & 1023) __trap();
@@ -244,13 +272,14 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
     uint8_t* kT = qt + STAGE;
     uint8_t* vT = kT + (TR ? kTileBytes : 0);
     uint8_t* mop = vT + (TR ? kTileBytes : 0);
-    float* sTot = reinterpret_cast<float*>(mop + TT::MOP_BYTES);  // [NSLAB][D]
-    float* sR = sTot + NSLAB * D;                                   // [D]
+    float* sTot = reinterpret_cast<float*>(mop + TT::MOP_BYTES);  // [16][D] scan scratch
+    float* sR = sTot + 16 * D;                                      // [D]
     float* sGe = sR + D;                                            // [D]
-    float* sZ = sGe + D;                                            // [D]
+    float* sG0 = sGe + D;                                           // [D]
+    float* sZ = sG0 + D;                                            // [D]
     float* sZP = sZ + D;                                            // [D]  e^r z
-    float* sZC = sZP + D;                                           // [NSLAB][D]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sZC + NSLAB * D);
+    float* sZC = sZP + D;                                           // [D]  this chunk's colsum of k~
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sZC + D);
     uint64_t* full = bars;
     uint64_t* empty = bars + 1;
     uint64_t* xf = bars + 2;
@@ -357,7 +386,6 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const int srow = TR ? q * 16 + lane : row;  // state row (d_k index)
         const bool sown = TR ? lane < 16 : true;
-        const int col = tid % D, slab = tid / D;    // column-slab mapping (scans, transforms)
         T* const obase = reinterpret_cast<T*>(p.o);
 
         // initial state: M_T <- M_in (fp32), z <- z_in
@@ -372,60 +400,60 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             }
             tmem_wait_st();
             if constexpr (NORM) {
-                if (tid < D) sZ[tid] = p.zin[((size_t)bh * p.nseg + seg) * D + tid];
+                if (tid < D) {
+                    sZ[tid] = p.zin[((size_t)bh * p.nseg + seg) * D + tid];
+                    sZC[tid] = 0.f;
+                }
             }
         }
         for (int c = 0; c < nchunks; ++c) {
             const int t0 = t_begin + c * kC;
             const int nvalid = min(kC, t_end - t0);
             mbar_wait(full, c & 1);
-            // (1) column scans: G down each column of this slab's rows
-            float G[ROWS];
+            // (1)+(2) 2-D column scan (lsm_vec_scan.cuh), then in place q~ = phi(q) e^{G - r},
+            // k~ = keff e^{r - G} (tf32: also the K-major K~^T, V^T tiles)
             {
-                float run = 0.f;
+                float G[L::R][L::EPC];
+                float nocarry = 0.f;
+                vec_log_scan<T>(at, nvalid, tid, G, sTot, sR, sGe, sG0, nullptr, nocarry);
+                if (tid < D && !vec_split_ok(sG0[tid], sR[tid], sGe[tid])) atomicOr(&p.err[2], 1);
+                const int cg = tid & 15, rg = tid >> 4;
+                float zc[L::EPC];
 #pragma unroll
-                for (int ii = 0; ii < ROWS; ++ii) {
-                    const int i = slab * ROWS + ii;
-                    run += (i < nvalid) ? log_sigmoid(ld_elem<T>(at, i, col)) : 0.f;
-                    G[ii] = run;
+                for (int j = 0; j < L::EPC; ++j) zc[j] = 0.f;
+#pragma unroll
+                for (int ii = 0; ii < L::R; ++ii) {
+                    const int i = rg * L::R + ii;
+                    const bool valid = i < nvalid;
+                    float xq[L::EPC], xk[L::EPC], xa[L::EPC];
+                    ld_chunk<T>(qt, i, cg, xq);
+                    if constexpr (HG) ld_chunk<T>(at, i, cg, xa);
+                    else ld_chunk<T>(kt, i, cg, xk);
+#pragma unroll
+                    for (int j = 0; j < L::EPC; ++j) {
+                        const float e = __expf(G[ii][j] - sR[cg * L::EPC + j]);
+                        const float keff = HG ? sigmoid_f(-xa[j]) : fmap_t<FM>(xk[j]);
+                        xq[j] = valid ? fmap_t<FM>(xq[j]) * e : 0.f;
+                        xk[j] = valid ? keff / e : 0.f;
+                        if constexpr (NORM) zc[j] += xk[j];
+                    }
+                    st_chunk<T>(qt, i, cg, xq);
+                    st_chunk<T>(kt, i, cg, xk);
+                    if constexpr (TR) {
+                        float xv[L::EPC];
+                        ld_chunk<T>(vt, i, cg, xv);
+#pragma unroll
+                        for (int j = 0; j < L::EPC; ++j) {
+                            *tr_elem(kT, cg * L::EPC + j, i) = tf32r(xk[j]);
+                            *tr_elem(vT, cg * L::EPC + j, i) = tf32r(xv[j]);
+                        }
+                    }
                 }
-                sTot[slab * D + col] = run;
-            }
-            named_bar_sync(1, kMathThreads);
-            float off = 0.f, r = 0.f, ge = 0.f;
+                if constexpr (NORM) {
 #pragma unroll
-            for (int s2 = 0; s2 < NSLAB; ++s2) {
-                const float tv = sTot[s2 * D + col];
-                if (s2 < slab) off += tv;
-                if (s2 * ROWS <= 63) r += tv;  // inclusive G at row 63
-                ge += tv;
-            }
-            const float g0 = (slab == 0) ? G[0] : 0.f;
-            if (slab == 0) {
-                sR[col] = r;
-                sGe[col] = ge;
-                if (!((g0 - r) < -kSafeLogDecay && (r - ge) < -kSafeLogDecay)) atomicOr(&p.err[2], 1);
-            }
-            // (2) q~ = phi(q) e^{G - r}, k~ = keff e^{r - G} in place (tf32: also K~^T, V^T)
-            float zc = 0.f;
-#pragma unroll
-            for (int ii = 0; ii < ROWS; ++ii) {
-                const int i = slab * ROWS + ii;
-                const bool valid = i < nvalid;
-                const float e = __expf(G[ii] + off - r);
-                const float qv = valid ? fmap_t<FM>(ld_elem<T>(qt, i, col)) * e : 0.f;
-                float keff = 0.f;
-                if (valid) keff = HG ? sigmoid_f(-ld_elem<T>(at, i, col)) : fmap_t<FM>(ld_elem<T>(kt, i, col));
-                const float kv = valid ? keff / e : 0.f;
-                st_elem<T>(qt, i, col, qv);
-                st_elem<T>(kt, i, col, kv);
-                if constexpr (TR) {
-                    *tr_elem(kT, col, i) = tf32r(kv);
-                    *tr_elem(vT, col, i) = tf32r(ld_elem<T>(vt, i, col));
+                    for (int j = 0; j < L::EPC; ++j) atomicAdd(&sZC[cg * L::EPC + j], zc[j]);
                 }
-                if constexpr (NORM) zc += kv;
             }
-            if constexpr (NORM) sZC[slab * D + col] = zc;
             named_bar_sync(1, kMathThreads);
             // (3) state operand M' = diag(e^r) M  (and the TMEM copy), z' = e^r z
             {
@@ -537,10 +565,8 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 tmem_wait_st();
                 if constexpr (NORM) {
                     if (tid < D) {
-                        float zs = 0.f;
-#pragma unroll
-                        for (int s2 = 0; s2 < NSLAB; ++s2) zs += sZC[s2 * D + tid];
-                        sZ[tid] = __expf(sGe[tid] - sR[tid]) * (sZP[tid] + zs);
+                        sZ[tid] = __expf(sGe[tid] - sR[tid]) * (sZP[tid] + sZC[tid]);
+                        sZC[tid] = 0.f;
                     }
                 }
             }
@@ -598,13 +624,15 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
 template <typename T>
 constexpr int output_pass_vec_smem() {
     using TT = TileTraits<T>;
-    // + sTot, sR, sGe, sZ, sZP, sZC (8 x 128 floats) + 6 barriers + TMEM slot
-    return 4 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + TT::MOP_BYTES + 4096 + 128;
+    // + sTot [16][D], sR, sGe, sG0, sZ, sZP, sZC + 6 barriers + TMEM slot
+    return 4 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + TT::MOP_BYTES + (16 + 6) * TT::D * 4 + 128;
 }
 template <typename T>
 constexpr int state_pass_vec_smem() {
     using TT = TileTraits<T>;
-    return (TT::kTransposed ? 1 : 2) * 3 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + 1024;
+    // + sTot [16][D], sR, sGe, sG0, sCar, sZ, barriers
+    return (TT::kTransposed ? 1 : 2) * 3 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) +
+           (16 + 5) * TT::D * 4 + 128;
 }
 
 }  // namespace lmoe_dev
