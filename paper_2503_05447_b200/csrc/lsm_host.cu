@@ -740,6 +740,7 @@ static void vec_backward(const lmoe_lsm_desc& dd, const BwdPlan& w, int B, int N
     vp.da = static_cast<bf*>(da);
     vp.out_f32 = out_f32 ? 1 : 0;
     vp.err = c.p.err;
+    vp.trace = c.p.trace;
     bf* snapM = reinterpret_cast<bf*>(ws + w.off_mst);
     bf* snapX = reinterpret_cast<bf*>(ws + w.off_dmst);
     const CUtensorMap tq = c.tmap<bf>(phq), tk = c.tmap<bf>(phk), tv = c.tmap<bf>(v), tdo = c.tmap<bf>(dO),

@@ -77,6 +77,7 @@ struct VecBwdParams {
     __nv_bfloat16* da;                    // [B, N, H, D]
     int out_f32;                          // dq / dk as fp32 d phi(q) / d keff (feature-map chain rule)
     int* err;                             // [2]: half-chunk decay span out of the fp32 range
+    unsigned long long* trace;            // optional clock64 phase trace of one CTA [16 x 16]
 };
 cudaError_t launch_vec_carry(bool hgrn2, bool rev, dim3 grid, cudaStream_t st, const CUtensorMap& x1,
                              const CUtensorMap& x2, const CUtensorMap& a, const VecBwdParams& p);

@@ -184,21 +184,22 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
             vec_log_scan<T>(at, nvalid, tid, G, sTot, sR, sGe, sG0, nullptr, nocarry);
             // operand weights in place in the X1 tile: FWD e^{G_end - G} keff, REV e^{G} q
 #pragma unroll
+            float gev[L::EPC];
+#pragma unroll
+            for (int j = 0; j < L::EPC; ++j) gev[j] = REV ? 0.f : sGe[cg * L::EPC + j];
             for (int ii = 0; ii < L::R; ++ii) {
                 const int row = rg * L::R + ii;
-                const bool valid = row < nvalid;
+                const float vm = row < nvalid ? 1.f : 0.f;
                 float x[L::EPC], av[L::EPC];
                 ld_chunk<T>(x1, row, cg, x);
                 if constexpr (HG && !REV) ld_chunk<T>(at, row, cg, av);
 #pragma unroll
                 for (int j = 0; j < L::EPC; ++j) {
-                    float w;
-                    if constexpr (REV) w = __expf(G[ii][j]);
-                    else w = __expf(sGe[cg * L::EPC + j] - G[ii][j]);
+                    const float w = vm * fast_exp(REV ? G[ii][j] : gev[j] - G[ii][j]);
                     float xv;
-                    if constexpr (HG && !REV) xv = sigmoid_f(-av[j]);
+                    if constexpr (HG && !REV) xv = sigmoid_fast(-av[j]);
                     else xv = x[j];
-                    x[j] = valid ? xv * w : 0.f;
+                    x[j] = xv * w;
                 }
                 st_chunk<T>(x1, row, cg, x);
             }
@@ -251,6 +252,16 @@ __global__ void __launch_bounds__(256) lsm_vec_boundary_dot(const __nv_bfloat16*
 // packed operands have been written.
 // ====================================================================================
 constexpr int kVbThreads = 384;
+
+// developer trace (LMOE_TRACE): clock64 at phase `slot` of the CTA of chunk nchunk / 2, head 0;
+// row = warp role (0 TMA, 1 MMA, 2 math warp 4)
+__device__ __forceinline__ void vb_mark(const VecBwdParams& p, int role, int slot) {
+    if (p.trace != nullptr && blockIdx.x == p.nchunk / 2 && blockIdx.y == 0 && blockIdx.z == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[role * 16 + slot] = t;
+    }
+}
 constexpr int vb_smem() { return 7 * kTileBytes + 3 * 128 * 4 + 256; }
 
 // 8 consecutive bf16 of row `row`, columns [col8*8, col8*8+8) of a two-block SW128 tile
@@ -329,6 +340,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
             tma_prefetch(&tmA); tma_prefetch(&tmM); tma_prefetch(&tmX);
             const int mrow = (bh * (p.nchunk + 1) + ci) * D;
             const int xrow = (bh * (p.nchunk + 1) + ci + 1) * D;
+            vb_mark(p, 0, 0);
             mbar_expect_tx(full, 5 * kTileBytes);
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) {
@@ -343,10 +355,12 @@ __global__ void __launch_bounds__(kVbThreads, 1)
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) tma_load_2d(Xt + blk * kBlockBytes, &tmX, mx_full, blk * 64, xrow);
             mbar_wait(scan_done, 0);  // the scan scratch in the M region is dead
+            vb_mark(p, 0, 1);
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) tma_load_2d(Mt + blk * kBlockBytes, &tmM, mx_full, blk * 64, mrow);
             // raw gates again for the gate-gradient scan, into the Q tile once it is consumed
             mbar_wait(q_free, 0);
+            vb_mark(p, 0, 2);
             mbar_expect_tx(a_full, kTileBytes);
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) tma_load_4d(Qt + blk * kBlockBytes, &tmA, a_full, blk * 64, h, t0, b);
@@ -367,8 +381,11 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                 return umma_desc_sw128(base + kk * 16 * 128, kBlockBytes, 1024);
             };
             mbar_wait(full, 0);
+            vb_mark(p, 1, 0);
             mbar_wait(mx_full, 0);
+            vb_mark(p, 1, 1);
             mbar_wait(xf, 0);
+            vb_mark(p, 1, 2);
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) mma_ss_f16(T0, kdesc(o, kk), kdesc(v, kk), idSS, kk > 0);  // dP
@@ -380,6 +397,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
             for (int kk = 0; kk < 8; ++kk) mma_ss_f16(T3, kdesc(o, kk), kdesc(m, kk), idSS, kk > 0);  // dO M'^T
             mma_commit(s_full);
             mbar_wait(p_full, 0);
+            vb_mark(p, 1, 3);
             tc_fence_after();
             // dq' += dP_m k~
 #pragma unroll
@@ -398,6 +416,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
             mma_commit(dk_full);
             // dv = S_m^T dO + k~ X'   (into [384,512) once dq' has been read)
             mbar_wait(dq_free, 0);
+            vb_mark(p, 1, 4);
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) mma_ts_f16(T3, T2 + kk * 8, mdesc(o, kk), idTS, kk > 0);
@@ -411,26 +430,32 @@ __global__ void __launch_bounds__(kVbThreads, 1)
         using L = VecLayout<T>;
         const int cg = tid & 15, rg = tid >> 4;
         mbar_wait(full, 0);
+        if (threadIdx.x == 128) vb_mark(p, 2, 0);
         {
             float G[L::R][L::EPC];
             float nocarry = 0.f;
             vec_log_scan<T>(At, nvalid, tid, G, sTot, sR, sGe, sG0, nullptr, nocarry);
             mbar_arrive(scan_done);
+            if (threadIdx.x == 128) vb_mark(p, 2, 1);
             if (tid < D && !vec_split_ok(sG0[tid], sR[tid], sGe[tid])) atomicOr(&p.err[2], 1);
+            float rr[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) rr[j] = sR[cg * 8 + j];
 #pragma unroll
             for (int ii = 0; ii < L::R; ++ii) {
                 const int i = rg * L::R + ii;
-                const bool valid = i < nvalid;
+                const float vm = i < nvalid ? 1.f : 0.f;
                 float xq[8], xk[8], xa[8];
                 ld_chunk<T>(Qt, i, cg, xq);
                 ld_chunk<T>(At, i, cg, xa);
                 if constexpr (!HG) ld_chunk<T>(Kt, i, cg, xk);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float e = __expf(G[ii][j] - sR[cg * 8 + j]);
-                    const float keff = HG ? sigmoid_f(-xa[j]) : xk[j];
-                    xq[j] = valid ? xq[j] * e : 0.f;
-                    xk[j] = valid ? keff / e : 0.f;
+                    const float gr = G[ii][j] - rr[j];
+                    const float e = fast_exp(gr);
+                    const float keff = HG ? sigmoid_fast(-xa[j]) : xk[j];
+                    xq[j] = xq[j] * (vm * e);
+                    xk[j] = keff * (vm * fast_exp(-gr));
                     xa[j] = e;
                 }
                 st_chunk<T>(Qt, i, cg, xq);
@@ -438,7 +463,9 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                 st_chunk<T>(At, i, cg, xa);
             }
         }
+        if (threadIdx.x == 128) vb_mark(p, 2, 2);
         mbar_wait(mx_full, 0);
+        if (threadIdx.x == 128) vb_mark(p, 2, 3);
         {
             // M' = diag(e^r) M_c, X' = diag(e^{G_end - r}) X_{c+1}: thread = (row, column block)
             const int row = tid & 127, blk = tid >> 7;
@@ -454,6 +481,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
         const int row = qd * 32 + lane;
         const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
         mbar_wait(s_full, 0);
+        if (threadIdx.x == 128) vb_mark(p, 2, 4);
         tc_fence_after();
         auto pack_masked = [&](uint32_t base, bool lower, uint32_t (&pk)[32]) {
             uint32_t r0[32], r1[32];
@@ -486,8 +514,10 @@ __global__ void __launch_bounds__(kVbThreads, 1)
         mbar_arrive(p_full);
 
         // ---------------- (E2) dq, dk and the gate integrand q~dq' - k~dk'
+        if (threadIdx.x == 128) vb_mark(p, 2, 5);
         mbar_wait(dq_full, 0);
         mbar_wait(dk_full, 0);
+        if (threadIdx.x == 128) vb_mark(p, 2, 6);
         tc_fence_after();
         {
             const bool vrow = row < nvalid;
@@ -519,7 +549,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                         const float q0 = __uint_as_float(rq[j]), q1 = __uint_as_float(rq[j + 1]);
                         const float k0 = __uint_as_float(rk[j]), k1 = __uint_as_float(rk[j + 1]);
                         dqv[j] = e.x * q0; dqv[j + 1] = e.y * q1;
-                        dkv[j] = HG ? 0.f : k0 / e.x; dkv[j + 1] = HG ? 0.f : k1 / e.y;
+                        dkv[j] = HG ? 0.f : k0 * rcp_ftz(e.x); dkv[j + 1] = HG ? 0.f : k1 * rcp_ftz(e.y);
                         dw[w2] = pack_bf16(qq.x * q0 - kq.x * k0, qq.y * q1 - kq.y * k1);
                         if constexpr (HG) hw[w2] = pack_bf16(kq.x * k0, kq.y * k1);
                     }
@@ -554,8 +584,10 @@ __global__ void __launch_bounds__(kVbThreads, 1)
             tc_fence_before();
             mbar_arrive(dq_free);
             mbar_arrive(q_free);
+            if (threadIdx.x == 128) vb_mark(p, 2, 7);
             // ---------------- (E3) dv
             mbar_wait(dv_full, 0);
+            if (threadIdx.x == 128) vb_mark(p, 2, 8);
             tc_fence_after();
 #pragma unroll 1
             for (int cb = 0; cb < 2; ++cb) {
@@ -582,7 +614,9 @@ __global__ void __launch_bounds__(kVbThreads, 1)
 
         // ---------------- (S) gate gradient: reverse in-chunk scan + boundary term (2-D layout;
         // the M region is free since dq' consumed M')
+        if (threadIdx.x == 128) vb_mark(p, 2, 9);
         mbar_wait(a_full, 0);
+        if (threadIdx.x == 128) vb_mark(p, 2, 10);
         {
             float Dv[L::R][8];
             float tot[8];
@@ -620,7 +654,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     acc[j] += Dv[ii][j];
-                    const float sg = sigmoid_f(av[j]);
+                    const float sg = sigmoid_fast(av[j]);
                     g[j] = acc[j] * (1.f - sg);
                     if constexpr (HG) g[j] -= kd[j] * sg;
                 }
@@ -632,6 +666,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                 }
             }
         }
+        if (threadIdx.x == 128) vb_mark(p, 2, 11);
     }
     tc_fence_before();
     __syncthreads();

@@ -23,7 +23,7 @@
 namespace lmoe_dev {
 
 __device__ __forceinline__ float log_sigmoid(float x) { return -softplus_f(-x); }
-__device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
+__device__ __forceinline__ float sigmoid_f(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }  // exact-ish (outside hot loops)
 
 // element (row, col) of a [128 x 256 B] SW128 tile (two 128-B column blocks)
 template <typename T>
@@ -176,21 +176,23 @@ __global__ void __launch_bounds__(kStatePassVecThreads, 1)
 #pragma unroll
             for (int j = 0; j < EPC; ++j) zc[j] = 0.f;
 #pragma unroll
+            float base[EPC];  // REV: prefix; FWD: G_end + suffix
+#pragma unroll
+            for (int j = 0; j < EPC; ++j) base[j] = sCar[cg * EPC + j] + (REV ? 0.f : sGe[cg * EPC + j]);
             for (int ii = 0; ii < L::R; ++ii) {
                 const int row = rg * L::R + ii;
-                const bool valid = row < nvalid;
+                const float vm = row < nvalid ? 1.f : 0.f;
                 float x[EPC], av[EPC];
                 ld_chunk<T>(kt, row, cg, x);
                 if constexpr (HG && !REV) ld_chunk<T>(at, row, cg, av);
 #pragma unroll
                 for (int j = 0; j < EPC; ++j) {
-                    const int c = cg * EPC + j;
                     // REV: w = e^{prefix + G}; FWD: w = e^{(G_end - G) + suffix} (both <= 1)
-                    const float w = REV ? __expf(G[ii][j] + sCar[c]) : __expf(sGe[c] - G[ii][j] + sCar[c]);
+                    const float w = vm * fast_exp(REV ? base[j] + G[ii][j] : base[j] - G[ii][j]);
                     float keff;
-                    if constexpr (HG && !REV) keff = sigmoid_f(-av[j]);
+                    if constexpr (HG && !REV) keff = sigmoid_fast(-av[j]);
                     else keff = fmap_t<FM>(x[j]);
-                    x[j] = valid ? keff * w : 0.f;
+                    x[j] = keff * w;
                     if constexpr (NORM) zc[j] += x[j];
                 }
                 if constexpr (!TR) {
@@ -316,6 +318,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmA);
             for (int c = 0; c < nchunks; ++c) {
                 if (c >= 1) mbar_wait(empty, (c - 1) & 1);
+                trace_mark(p, c, 10);
                 const int t0 = t_begin + c * kC;
                 mbar_expect_tx(full, STAGE);
 #pragma unroll
@@ -410,31 +413,36 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             const int t0 = t_begin + c * kC;
             const int nvalid = min(kC, t_end - t0);
             mbar_wait(full, c & 1);
+            if (tid == 0) trace_mark(p, c, 0);
             // (1)+(2) 2-D column scan (lsm_vec_scan.cuh), then in place q~ = phi(q) e^{G - r},
             // k~ = keff e^{r - G} (tf32: also the K-major K~^T, V^T tiles)
             {
                 float G[L::R][L::EPC];
                 float nocarry = 0.f;
                 vec_log_scan<T>(at, nvalid, tid, G, sTot, sR, sGe, sG0, nullptr, nocarry);
+                if (tid == 0) trace_mark(p, c, 1);
                 if (tid < D && !vec_split_ok(sG0[tid], sR[tid], sGe[tid])) atomicOr(&p.err[2], 1);
                 const int cg = tid & 15, rg = tid >> 4;
                 float zc[L::EPC];
 #pragma unroll
                 for (int j = 0; j < L::EPC; ++j) zc[j] = 0.f;
+                float rr[L::EPC];
+#pragma unroll
+                for (int j = 0; j < L::EPC; ++j) rr[j] = sR[cg * L::EPC + j];
 #pragma unroll
                 for (int ii = 0; ii < L::R; ++ii) {
                     const int i = rg * L::R + ii;
-                    const bool valid = i < nvalid;
+                    const float vm = i < nvalid ? 1.f : 0.f;
                     float xq[L::EPC], xk[L::EPC], xa[L::EPC];
                     ld_chunk<T>(qt, i, cg, xq);
                     if constexpr (HG) ld_chunk<T>(at, i, cg, xa);
                     else ld_chunk<T>(kt, i, cg, xk);
 #pragma unroll
                     for (int j = 0; j < L::EPC; ++j) {
-                        const float e = __expf(G[ii][j] - sR[cg * L::EPC + j]);
-                        const float keff = HG ? sigmoid_f(-xa[j]) : fmap_t<FM>(xk[j]);
-                        xq[j] = valid ? fmap_t<FM>(xq[j]) * e : 0.f;
-                        xk[j] = valid ? keff / e : 0.f;
+                        const float gr = G[ii][j] - rr[j];
+                        const float keff = HG ? sigmoid_fast(-xa[j]) : fmap_t<FM>(xk[j]);
+                        xq[j] = fmap_t<FM>(xq[j]) * (vm * fast_exp(gr));
+                        xk[j] = keff * (vm * fast_exp(-gr));
                         if constexpr (NORM) zc[j] += xk[j];
                     }
                     st_chunk<T>(qt, i, cg, xq);
@@ -455,6 +463,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 }
             }
             named_bar_sync(1, kMathThreads);
+            if (tid == 0) trace_mark(p, c, 2);
             // (3) state operand M' = diag(e^r) M  (and the TMEM copy), z' = e^r z
             {
                 const float er = __expf(sR[srow < D ? srow : 0]);
@@ -500,8 +509,10 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 if constexpr (NORM) named_bar_sync(1, kMathThreads);
                 mbar_arrive(xf);
             }
+            if (tid == 0) trace_mark(p, c, 3);
             // (4) P = S . mask  (+ row sums, q~ . z' for the normaliser)
             mbar_wait(s_full, c & 1);
+            if (tid == 0) trace_mark(p, c, 4);
             tc_fence_after();
             {
                 uint32_t r0[32], r1[32];
@@ -547,8 +558,10 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 tc_fence_before();
                 mbar_arrive(p_full);
             }
+            if (tid == 0) trace_mark(p, c, 5);
             // (5) state: M_next = diag(e^{G_end - r}) M'
             mbar_wait(mo_full, c & 1);
+            if (tid == 0) trace_mark(p, c, 6);
             tc_fence_after();
             {
                 const int kr = srow < D ? srow : 0;
@@ -613,7 +626,9 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 }
                 tc_fence_before();
             }
+            if (tid == 0) trace_mark(p, c, 7);
             named_bar_sync(1, kMathThreads);  // everyone done with this chunk's tiles and sZ
+            if (tid == 0) trace_mark(p, c, 8);
         }
     }
     tc_fence_before();

@@ -14,11 +14,29 @@ namespace lmoe_dev {
 
 constexpr int kVecNT = 256;  // transform threads of every TokenVector kernel
 
-// log sigmoid(x) = min(x, 0) - log(1 + e^{-|x|}) with MUFU ex2 / lg2 (abs error ~1e-7, far
-// below the bf16 / tf32 operand rounding it feeds)
-__device__ __forceinline__ float log_sigmoid_fast(float x) {
-    return fminf(x, 0.f) - __logf(1.f + __expf(-fabsf(x)));
+// MUFU ex2 / lg2 / rcp without the denormal fix-ups of __expf / __logf (flush-to-zero)
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_exp(float x) { return ex2_ftz(x * 1.4426950408889634f); }
+// log sigmoid(x) = min(x, 0) - log(1 + e^{-|x|}) (abs error ~1e-7, far below the bf16 / tf32
+// operand rounding it feeds)
+__device__ __forceinline__ float log_sigmoid_fast(float x) {
+    return fminf(x, 0.f) - 0.6931471805599453f * lg2_ftz(1.f + ex2_ftz(-fabsf(x) * 1.4426950408889634f));
+}
+__device__ __forceinline__ float sigmoid_fast(float x) { return rcp_ftz(1.f + fast_exp(-x)); }
 
 template <typename T>
 struct VecLayout {
@@ -80,10 +98,10 @@ __device__ __forceinline__ void vec_log_scan(const uint8_t* at, int nvalid, int 
         const int row = rg * L::R + ii;
         float x[L::EPC];
         ld_chunk<T>(at, row, cg, x);
-        const bool valid = row < nvalid;
+        const float vm = row < nvalid ? 1.f : 0.f;  // branch-free: rows past the end add 0
 #pragma unroll
         for (int j = 0; j < L::EPC; ++j) {
-            run[j] += valid ? log_sigmoid_fast(x[j]) : 0.f;
+            run[j] = fmaf(log_sigmoid_fast(x[j]), vm, run[j]);
             G[ii][j] = run[j];
         }
     }
