@@ -764,9 +764,14 @@ static void vec_backward(const lmoe_lsm_desc& dd, const BwdPlan& w, int B, int N
     const long long rows = (long long)B * H * (nchunk + 1) * D;
     LMOE_CUDA_CHECK(lmoe_dev::launch_vec_boundary_dot(snapM, snapX, reinterpret_cast<float*>(ws + w.off_bd), rows, st));
     // 6: fused chunk backward
-    const CUtensorMap tm[7] = {tq, tk, tv, tdo, ta,
-                               make_tmap_2d(snapM, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, rows, D, 64, 128),
-                               make_tmap_2d(snapX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, rows, D, 64, 128)};
+    // bf16 outputs leave through TMA bulk stores (dq / dk only when not fp32 intermediates)
+    const CUtensorMap tm[11] = {tq, tk, tv, tdo, ta,
+                                make_tmap_2d(snapM, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, rows, D, 64, 128),
+                                make_tmap_2d(snapX, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, rows, D, 64, 128),
+                                out_f32 ? tq : c.tmap<bf>(dq), out_f32 ? tk : c.tmap<bf>(dk), c.tmap<bf>(dv),
+                                c.tmap<bf>(da)};
+    if (hg && !out_f32)  // HGRN2's effective key 1 - sigmoid(a) ignores k
+        LMOE_CUDA_CHECK(cudaMemsetAsync(dk, 0, (size_t)B * N * H * D * sizeof(bf), st));
     LMOE_CUDA_CHECK(lmoe_dev::launch_vec_bwd_chunk(hg, dim3(nchunk, H, B), st, tm, vp));
     g_launch_count += 4;
     c.check_err();

@@ -82,7 +82,7 @@ struct VecBwdParams {
 cudaError_t launch_vec_carry(bool hgrn2, bool rev, dim3 grid, cudaStream_t st, const CUtensorMap& x1,
                              const CUtensorMap& x2, const CUtensorMap& a, const VecBwdParams& p);
 cudaError_t launch_vec_boundary_dot(const void* M, const void* X, float* bd, long long rows, cudaStream_t st);
-// tm = {q, k, v, dO, a_pre, snapM, snapX}
+// tm = {q, k, v, dO, a_pre, snapM, snapX, dq, dk, dv, da} (dq / dk maps unused when out_f32)
 cudaError_t launch_vec_bwd_chunk(bool hgrn2, dim3 grid, cudaStream_t st, const CUtensorMap* tm,
                                  const VecBwdParams& p);
 }  // namespace lmoe_dev

@@ -274,7 +274,9 @@ __global__ void __launch_bounds__(kVbThreads, 1)
     lsm_vec_bwd_chunk(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                       const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmM,
-                      const __grid_constant__ CUtensorMap tmX, VecBwdParams p) {
+                      const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDQ,
+                      const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
+                      const __grid_constant__ CUtensorMap tmDA, VecBwdParams p) {
     using T = __nv_bfloat16;
     constexpr int D = 128;
     constexpr int NM = 256;  // math threads
@@ -358,12 +360,12 @@ __global__ void __launch_bounds__(kVbThreads, 1)
             vb_mark(p, 0, 1);
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) tma_load_2d(Mt + blk * kBlockBytes, &tmM, mx_full, blk * 64, mrow);
-            // raw gates again for the gate-gradient scan, into the Q tile once it is consumed
-            mbar_wait(q_free, 0);
+            // raw gates again for the gate-gradient scan, into the M region once dO M'^T is done
+            mbar_wait(s_full, 0);
             vb_mark(p, 0, 2);
             mbar_expect_tx(a_full, kTileBytes);
 #pragma unroll
-            for (int blk = 0; blk < 2; ++blk) tma_load_4d(Qt + blk * kBlockBytes, &tmA, a_full, blk * 64, h, t0, b);
+            for (int blk = 0; blk < 2; ++blk) tma_load_4d(Mt + blk * kBlockBytes, &tmA, a_full, blk * 64, h, t0, b);
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -513,12 +515,14 @@ __global__ void __launch_bounds__(kVbThreads, 1)
         tc_fence_before();
         mbar_arrive(p_full);
 
-        // ---------------- (E2) dq, dk and the gate integrand q~dq' - k~dk'
+        // ---------------- (E2) dq, dk and the gate integrand q~dq' - k~dk'.  bf16 dq / dk are
+        // staged in the dead q~ / V tiles (own elements only) and written with TMA bulk stores.
         if (threadIdx.x == 128) vb_mark(p, 2, 5);
         mbar_wait(dq_full, 0);
         mbar_wait(dk_full, 0);
         if (threadIdx.x == 128) vb_mark(p, 2, 6);
         tc_fence_after();
+        const bool f32out = p.out_f32 != 0;
         {
             const bool vrow = row < nvalid;
             const size_t grow = (((size_t)b * p.N + t0 + (vrow ? row : 0)) * p.H + h) * D;
@@ -539,9 +543,11 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                     const uint32_t* ew = reinterpret_cast<const uint32_t*>(&eu);
                     const uint32_t* qw = reinterpret_cast<const uint32_t*>(&qu);
                     const uint32_t* kw = reinterpret_cast<const uint32_t*>(&ku);
-                    uint4 du, hu;
+                    uint4 du, hu, qo, ko;
                     uint32_t* dw = reinterpret_cast<uint32_t*>(&du);
                     uint32_t* hw = reinterpret_cast<uint32_t*>(&hu);
+                    uint32_t* qow = reinterpret_cast<uint32_t*>(&qo);
+                    uint32_t* kow = reinterpret_cast<uint32_t*>(&ko);
 #pragma unroll
                     for (int w2 = 0; w2 < 4; ++w2) {
                         const float2 e = unpack_bf16(ew[w2]), qq = unpack_bf16(qw[w2]), kq = unpack_bf16(kw[w2]);
@@ -552,40 +558,41 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                         dkv[j] = HG ? 0.f : k0 * rcp_ftz(e.x); dkv[j + 1] = HG ? 0.f : k1 * rcp_ftz(e.y);
                         dw[w2] = pack_bf16(qq.x * q0 - kq.x * k0, qq.y * q1 - kq.y * k1);
                         if constexpr (HG) hw[w2] = pack_bf16(kq.x * k0, kq.y * k1);
+                        qow[w2] = pack_bf16(dqv[j], dqv[j + 1]);
+                        kow[w2] = pack_bf16(dkv[j], dkv[j + 1]);
                     }
-                    *tile_chunk(At, row, c8) = du;              // own elements: no cross-thread hazard
-                    if constexpr (HG) *tile_chunk(Vt, row, c8) = hu;  // V is dead once dk' is done
+                    *tile_chunk(At, row, c8) = du;  // own elements: no cross-thread hazard
+                    if constexpr (HG) {
+                        *tile_chunk(Vt, row, c8) = hu;  // V is dead once dk' is done
+                    } else if (!f32out) {
+                        *tile_chunk(Vt, row, c8) = ko;
+                    }
+                    if (!f32out) *tile_chunk(Qt, row, c8) = qo;
                 }
-                if (vrow) {
-                    if (p.out_f32) {
-                        float* gq = static_cast<float*>(p.dq) + grow + cbase;
-                        float* gk = static_cast<float*>(p.dk) + grow + cbase;
+                if (f32out && vrow) {
+                    float* gq = static_cast<float*>(p.dq) + grow + cbase;
+                    float* gk = static_cast<float*>(p.dk) + grow + cbase;
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
-                            *reinterpret_cast<float4*>(gq + j) = make_float4(dqv[j], dqv[j + 1], dqv[j + 2], dqv[j + 3]);
-                            *reinterpret_cast<float4*>(gk + j) = make_float4(dkv[j], dkv[j + 1], dkv[j + 2], dkv[j + 3]);
-                        }
-                    } else {
-                        T* gq = static_cast<T*>(p.dq) + grow + cbase;
-                        T* gk = static_cast<T*>(p.dk) + grow + cbase;
-#pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            uint4 a, c;
-                            a.x = pack_bf16(dqv[j], dqv[j + 1]); a.y = pack_bf16(dqv[j + 2], dqv[j + 3]);
-                            a.z = pack_bf16(dqv[j + 4], dqv[j + 5]); a.w = pack_bf16(dqv[j + 6], dqv[j + 7]);
-                            c.x = pack_bf16(dkv[j], dkv[j + 1]); c.y = pack_bf16(dkv[j + 2], dkv[j + 3]);
-                            c.z = pack_bf16(dkv[j + 4], dkv[j + 5]); c.w = pack_bf16(dkv[j + 6], dkv[j + 7]);
-                            *reinterpret_cast<uint4*>(gq + j) = a;
-                            *reinterpret_cast<uint4*>(gk + j) = c;
-                        }
+                    for (int j = 0; j < 32; j += 4) {
+                        *reinterpret_cast<float4*>(gq + j) = make_float4(dqv[j], dqv[j + 1], dqv[j + 2], dqv[j + 3]);
+                        *reinterpret_cast<float4*>(gk + j) = make_float4(dkv[j], dkv[j + 1], dkv[j + 2], dkv[j + 3]);
                     }
                 }
             }
             tc_fence_before();
             mbar_arrive(dq_free);
-            mbar_arrive(q_free);
+            fence_proxy_async_smem();
+            named_bar_sync(1, NM);
+            if (tid == 0 && !f32out) {
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) {
+                    tma_store_4d(&tmDQ, Qt + blk * kBlockBytes, blk * 64, h, t0, b);
+                    if constexpr (!HG) tma_store_4d(&tmDK, Vt + blk * kBlockBytes, blk * 64, h, t0, b);
+                }
+                bulk_commit();
+            }
             if (threadIdx.x == 128) vb_mark(p, 2, 7);
-            // ---------------- (E3) dv
+            // ---------------- (E3) dv, staged in the dead k~ tile (own elements)
             mbar_wait(dv_full, 0);
             if (threadIdx.x == 128) vb_mark(p, 2, 8);
             tc_fence_after();
@@ -595,29 +602,34 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                 uint32_t rv[32];
                 tmem_ld32(T3 + lane_off + cbase, rv);
                 tmem_wait_ld();
-                if (vrow) {
-                    T* gv = p.dv + grow + cbase;
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        uint4 a;
-                        a.x = pack_bf16(__uint_as_float(rv[j]), __uint_as_float(rv[j + 1]));
-                        a.y = pack_bf16(__uint_as_float(rv[j + 2]), __uint_as_float(rv[j + 3]));
-                        a.z = pack_bf16(__uint_as_float(rv[j + 4]), __uint_as_float(rv[j + 5]));
-                        a.w = pack_bf16(__uint_as_float(rv[j + 6]), __uint_as_float(rv[j + 7]));
-                        *reinterpret_cast<uint4*>(gv + j) = a;
-                    }
+                for (int ch = 0; ch < 4; ++ch) {
+                    uint4 a;
+                    const int j = ch * 8;
+                    a.x = pack_bf16(__uint_as_float(rv[j]), __uint_as_float(rv[j + 1]));
+                    a.y = pack_bf16(__uint_as_float(rv[j + 2]), __uint_as_float(rv[j + 3]));
+                    a.z = pack_bf16(__uint_as_float(rv[j + 4]), __uint_as_float(rv[j + 5]));
+                    a.w = pack_bf16(__uint_as_float(rv[j + 6]), __uint_as_float(rv[j + 7]));
+                    *tile_chunk(Kt, row, cbase / 8 + ch) = a;
                 }
             }
             tc_fence_before();
+            fence_proxy_async_smem();
         }
-        named_bar_sync(1, NM);  // the integrand tile is complete
+        named_bar_sync(1, NM);  // the integrand tile and the staged dv are complete
+        if (tid == 0) {
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) tma_store_4d(&tmDV, Kt + blk * kBlockBytes, blk * 64, h, t0, b);
+            bulk_commit();
+        }
 
         // ---------------- (S) gate gradient: reverse in-chunk scan + boundary term (2-D layout;
-        // the M region is free since dq' consumed M')
+        // scratch in the dead X region, raw gates reloaded into the M region, da staged in dO)
         if (threadIdx.x == 128) vb_mark(p, 2, 9);
         mbar_wait(a_full, 0);
         if (threadIdx.x == 128) vb_mark(p, 2, 10);
         {
+            float* sSc = reinterpret_cast<float*>(Xt);
             float Dv[L::R][8];
             float tot[8];
 #pragma unroll
@@ -629,27 +641,26 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                 for (int j = 0; j < 8; ++j) tot[j] += Dv[ii][j];
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) sTot[rg * D + cg * 8 + j] = tot[j];
+            for (int j = 0; j < 8; ++j) sSc[rg * D + cg * 8 + j] = tot[j];
             named_bar_sync(1, NM);
             if (tid < D) {  // exclusive suffix over later row groups, seeded with the boundary term
                 float acc = p.bd[((size_t)bh * (p.nchunk + 1) + ci + 1) * D + tid];
 #pragma unroll
                 for (int g = L::RG - 1; g >= 0; --g) {
-                    const float v = sTot[g * D + tid];
-                    sTot[g * D + tid] = acc;
+                    const float v = sSc[g * D + tid];
+                    sSc[g * D + tid] = acc;
                     acc += v;
                 }
             }
             named_bar_sync(1, NM);
             float acc[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = sTot[rg * D + cg * 8 + j];
-            T* gda = p.da + (((size_t)b * p.N + t0) * p.H + h) * D + cg * 8;
+            for (int j = 0; j < 8; ++j) acc[j] = sSc[rg * D + cg * 8 + j];
 #pragma unroll
             for (int ii = L::R - 1; ii >= 0; --ii) {
                 const int i = rg * L::R + ii;
                 float av[8], kd[8], g[8];
-                ld_chunk<T>(Qt, i, cg, av);  // raw a_pre (reloaded)
+                ld_chunk<T>(Mt, i, cg, av);  // raw a_pre (reloaded)
                 if constexpr (HG) ld_chunk<T>(Vt, i, cg, kd);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
@@ -658,12 +669,15 @@ __global__ void __launch_bounds__(kVbThreads, 1)
                     g[j] = acc[j] * (1.f - sg);
                     if constexpr (HG) g[j] -= kd[j] * sg;
                 }
-                if (i < nvalid) {
-                    uint4 u;
-                    u.x = pack_bf16(g[0], g[1]); u.y = pack_bf16(g[2], g[3]);
-                    u.z = pack_bf16(g[4], g[5]); u.w = pack_bf16(g[6], g[7]);
-                    *reinterpret_cast<uint4*>(gda + (size_t)i * p.H * D) = u;
-                }
+                st_chunk<T>(Ot, i, cg, g);
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1, NM);
+            if (tid == 0) {
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) tma_store_4d(&tmDA, Ot + blk * kBlockBytes, blk * 64, h, t0, b);
+                bulk_commit();
+                bulk_wait0();  // smem must outlive the bulk stores
             }
         }
         if (threadIdx.x == 128) vb_mark(p, 2, 11);
@@ -709,11 +723,12 @@ static cudaError_t chunk_t(dim3 grid, cudaStream_t st, const CUtensorMap* tm, co
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_vec_bwd_chunk<HG><<<grid, kVbThreads, vb_smem(), st>>>(tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], tm[6], p);
+    lsm_vec_bwd_chunk<HG><<<grid, kVbThreads, vb_smem(), st>>>(tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], tm[6], tm[7],
+                                                                tm[8], tm[9], tm[10], p);
     return cudaGetLastError();
 }
 
-// tm = {q, k, v, dO, a_pre, snapM, snapX}
+// tm = {q, k, v, dO, a_pre, snapM, snapX, dq, dk, dv, da}
 cudaError_t launch_vec_bwd_chunk(bool hgrn2, dim3 grid, cudaStream_t st, const CUtensorMap* tm,
                                  const VecBwdParams& p) {
     return hgrn2 ? chunk_t<true>(grid, st, tm, p) : chunk_t<false>(grid, st, tm, p);
