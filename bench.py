@@ -233,6 +233,57 @@ def backward_bench(dev, steps=3, warmup=2):
                          "note": "algorithmic bytes of the op / step time (three chunk passes + gate kernel)"}}
 
 
+def ncu_traffic(path=os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                   "r1_lsm_output_pass.ncu.txt")):
+    """dram read + write bytes per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/), or None when absent."""
+    try:
+        vals = {}
+        for line in open(path):
+            parts = line.split()
+            if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}[parts[2]]
+                vals[parts[0]] = float(parts[1]) * scale
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def gla_bench(dev, steps=3, warmup=2):
+    """TokenVector side numbers at the cfg3 shape (GLA, N = 262144, 16 x 128, a_pre ~ N(0, 1) as
+    the reference's gate default): forward (lmoe_lsm_fwd) and backward (lmoe_lsm_bwd: dq, dk, dv,
+    da_pre, dM0), each against the HBM roofline of its algorithmic bytes (SURVEY 8(d):
+    fwd 3 d s_in + d s_out + d s_gate = 1280 B, bwd 4 d s_in + 3 d s_out + 2 d s_gate = 2304 B
+    per (token, head))."""
+    import torch
+    import paper_2503_05447_b200 as pk
+    g = torch.Generator(device=dev).manual_seed(21)
+    q, k, v, dO, a = (torch.randn(1, SEQ, HEADS, HEAD_DIM, device=dev, generator=g).mul_(s).to(torch.bfloat16)
+                      for s in (0.5, 0.5, 0.5, 1.0, 1.0))
+    gates = pk.LsmGates(a_pre=a)
+    spec = pk.LsmSpec.make("gla", HEAD_DIM)
+    hbm, _, _ = peaks()
+    out = {}
+    for name, fn, per in (("forward", lambda: pk.lsm_forward_batched(q, k, v, gates, spec, 64, check=False), 1280),
+                          ("backward", lambda: pk.lsm_backward_batched(q, k, v, gates, spec, dO, check=False), 2304)):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / steps
+        gbs = per * SEQ * HEADS / (ms / 1e3) / 1e9
+        out[name] = {"tokens_per_s": SEQ / (ms / 1e3), "ms_per_step": ms, "steps": steps,
+                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                                  "alg_bytes_per_token_head": per}}
+    out["workload"] = "cfg3 GLA (TokenVector decay) LSM, N=262144, 16 x 128, bf16, a_pre ~ N(0,1)"
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -325,22 +376,40 @@ def main():
     dq, dk, dv, db = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(b_pre)
     dgates = pk.LsmGates(b_pre=db) if args.instance == "mamba2" else None
 
-    def e2e_step():
-        dq.copy_(hq, non_blocking=True)
-        dk.copy_(hk, non_blocking=True)
-        dv.copy_(hv, non_blocking=True)
-        if dgates is not None:
-            db.copy_(hb, non_blocking=True)
-        spm.sp_lsm_masked_rank(comm, dq, dk, dv, dgates, spec, 64, out=out, check=False,
-                               stream=stream.cuda_stream)
-        hout.copy_(out, non_blocking=True)
+    # Pipelined like a serving loop: step i+1's H2D (copy stream) overlaps step i's D2H (second
+    # copy stream; PCIe is full duplex), inputs / outputs double-buffered in HBM.
+    bufs = [(dq, dk, dv, db, dgates, out)]
+    q2, k2, v2, b2 = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), torch.empty_like(b_pre)
+    bufs.append((q2, k2, v2, b2, pk.LsmGates(b_pre=b2) if args.instance == "mamba2" else None, torch.empty_like(out)))
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    done = [torch.cuda.Event(), torch.cuda.Event()]  # output of slot j copied out
+    done[0].record(s_out)
+    done[1].record(s_out)
 
-    e2e_step()
+    def e2e_step(i):
+        xq, xk, xv, xb, xg, xo = bufs[i & 1]
+        s_in.wait_event(done[i & 1])  # slot free: its previous output has left the device
+        with torch.cuda.stream(s_in):
+            xq.copy_(hq, non_blocking=True)
+            xk.copy_(hk, non_blocking=True)
+            xv.copy_(hv, non_blocking=True)
+            if xg is not None:
+                xb.copy_(hb, non_blocking=True)
+        stream.wait_stream(s_in)
+        spm.sp_lsm_masked_rank(comm, xq, xk, xv, xg, spec, 64, out=xo, check=False,
+                               stream=stream.cuda_stream)
+        s_out.wait_stream(stream)
+        with torch.cuda.stream(s_out):
+            hout.copy_(xo, non_blocking=True)
+        done[i & 1].record(s_out)
+
+    e2e_step(0)
     barrier()
     e0.record(stream)
-    for _ in range(args.e2e_steps):
-        e2e_step()
-    e1.record(stream)
+    s_in.wait_stream(stream)  # the timed region starts before the first H2D
+    for i in range(args.e2e_steps):
+        e2e_step(i + 1)
+    e1.record(s_out)
     barrier()
     te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -364,6 +433,7 @@ def main():
         if world == 1 and not args.no_extra:
             extra["layer"] = layer_bench(dev)
             extra["backward"] = backward_bench(dev)
+            extra["gla"] = gla_bench(dev)
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(args.instance, SEQ, os.cpu_count() or 1, 20.0)
         line = {
@@ -378,7 +448,8 @@ def main():
                        "l2": "inputs 3 GiB > L2; no flush needed"},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_source": src,
+                         "frac": achieved / hbm, "traffic": ncu_traffic(), "peak_source": src,
+                         "traffic_source": "profiles/r1_lsm_output_pass.ncu.txt (ncu --set full, one launch)",
                          "kernel": "lsm_output_pass",
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_per_token_head": ALG_BYTES_TH[args.instance]},
@@ -388,7 +459,7 @@ def main():
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "path": "pinned host -> H2D -> lmoe_sp_lsm_fwd (C-ABI) -> D2H"},
+                    "path": "pinned host -> H2D -> lmoe_sp_lsm_fwd (C-ABI) -> D2H, H2D(i+1) overlapping D2H(i)"},
             "cpu_baseline": cb,
         }
         line.update(extra)
