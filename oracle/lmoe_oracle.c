@@ -304,19 +304,30 @@ int lmo_lsm_backward(const lmo_spec* s, int n, int d_k, int d_v, const double* q
                      double* dM0, const double* dM_final, char* err, int errlen) {
     if (lmo_spec_validate(s, d_k, d_v, err, errlen)) return -1;
     if (check_separable(s, err, errlen)) return -1;
-    if (s->use_normalizer) { set_err(err, errlen, "oracle backward: normalizer not restated"); return -1; }
-    const size_t dd = (size_t)d_k * d_v;
+    /* The normaliser state z_s = Theta_s z_{s-1} + keff_s (lsm.hpp:335-441) is carried as one
+     * extra value column of M whose value is 1: o = num / den with num = phi(q) M[:, :d_v],
+     * den = phi(q) M[:, d_v]; its upstream gradient is [dO / den | -(dO . num) / den^2]. */
+    const int nz = s->use_normalizer ? 1 : 0;
+    const int dva = d_v + nz;
+    const size_t dd = (size_t)d_k * dva;
     double* Ms = (double*)malloc(sizeof(double) * dd * (size_t)(n + 1)); /* M_{-1..n-1} */
     double* dM = (double*)calloc(dd, sizeof(double));
+    double* dOa = (double*)malloc(sizeof(double) * dva);
     /* loss gradient w.r.t. the returned final state (lsm_forward_chunked's final_state) */
-    if (dM_final) memcpy(dM, dM_final, sizeof(double) * dd);
-    if (M0) memcpy(Ms, M0, sizeof(double) * dd); else memset(Ms, 0, sizeof(double) * dd);
+    if (dM_final)
+        for (int i = 0; i < d_k; ++i)
+            for (int j = 0; j < d_v; ++j) dM[i * dva + j] = dM_final[(size_t)i * d_v + j];
+    memset(Ms, 0, sizeof(double) * dd);
+    if (M0)
+        for (int i = 0; i < d_k; ++i)
+            for (int j = 0; j < d_v; ++j) Ms[i * dva + j] = M0[(size_t)i * d_v + j];
+#define VA(t, j) ((j) < d_v ? v[(size_t)(t) * d_v + (j)] : 1.0)
     for (int t = 0; t < n; ++t)
         for (int i = 0; i < d_k; ++i) {
             double a = decay_at(s, d_k, a_pre, b_pre, t, i);
             double ke = keff_at(s, d_k, k, a_pre, b_pre, t, i);
-            for (int j = 0; j < d_v; ++j)
-                Ms[(t + 1) * dd + i * d_v + j] = a * Ms[t * dd + i * d_v + j] + ke * v[(size_t)t * d_v + j];
+            for (int j = 0; j < dva; ++j)
+                Ms[(t + 1) * dd + i * dva + j] = a * Ms[t * dd + i * dva + j] + ke * VA(t, j);
         }
     const int dkind = lmo_decay_kind(s->instance);
     if (da_pre && dkind == LMO_DK_TOKEN_VECTOR) memset(da_pre, 0, sizeof(double) * n * d_k);
@@ -325,13 +336,30 @@ int lmo_lsm_backward(const lmo_spec* s, int n, int d_k, int d_v, const double* q
     for (int t = n - 1; t >= 0; --t) {
         const double* Mt = Ms + (size_t)(t + 1) * dd;
         const double* Mp = Ms + (size_t)t * dd;
+        for (int j = 0; j < d_v; ++j) dOa[j] = dO[(size_t)t * d_v + j];
+        if (nz) {
+            double den = 0.0, dn = 0.0;
+            for (int i = 0; i < d_k; ++i) den += fmap(s->feature_map, q[(size_t)t * d_k + i]) * Mt[i * dva + d_v];
+            if (fabs(den) < 1e-12) {
+                set_err(err, errlen, "degenerate normalizer");
+                free(Ms); free(dM); free(dOa);
+                return -1;
+            }
+            for (int j = 0; j < d_v; ++j) {
+                double num = 0.0;
+                for (int i = 0; i < d_k; ++i) num += fmap(s->feature_map, q[(size_t)t * d_k + i]) * Mt[i * dva + j];
+                dn += dOa[j] * num;
+                dOa[j] /= den;
+            }
+            dOa[d_v] = -dn / (den * den);
+        }
         /* dM_t += phi(q_t) (x) dO_t ; dphi(q_t) = M_t dO_t */
         for (int i = 0; i < d_k; ++i) {
             double pqi = fmap(s->feature_map, q[(size_t)t * d_k + i]);
             double dpq = 0.0;
-            for (int j = 0; j < d_v; ++j) {
-                dM[i * d_v + j] += pqi * dO[(size_t)t * d_v + j];
-                dpq += Mt[i * d_v + j] * dO[(size_t)t * d_v + j];
+            for (int j = 0; j < dva; ++j) {
+                dM[i * dva + j] += pqi * dOa[j];
+                dpq += Mt[i * dva + j] * dOa[j];
             }
             dq[(size_t)t * d_k + i] = dpq * fmap_grad(s->feature_map, q[(size_t)t * d_k + i]);
         }
@@ -343,12 +371,12 @@ int lmo_lsm_backward(const lmo_spec* s, int n, int d_k, int d_v, const double* q
             double a = decay_at(s, d_k, a_pre, b_pre, t, i);
             double ke = keff_at(s, d_k, k, a_pre, b_pre, t, i);
             double dke = 0.0, da = 0.0;
-            for (int j = 0; j < d_v; ++j) {
-                double g = dM[i * d_v + j];
-                dke += g * v[(size_t)t * d_v + j];
-                dv[(size_t)t * d_v + j] += g * ke;
-                da += g * Mp[i * d_v + j];
-                dM[i * d_v + j] = a * g; /* propagate to M_{t-1} */
+            for (int j = 0; j < dva; ++j) {
+                double g = dM[i * dva + j];
+                dke += g * VA(t, j);
+                if (j < d_v) dv[(size_t)t * d_v + j] += g * ke;
+                da += g * Mp[i * dva + j];
+                dM[i * dva + j] = a * g; /* propagate to M_{t-1} */
             }
             const double kraw = k[(size_t)t * d_k + i];
             /* effective key chain (lsm.hpp:483-501) */
@@ -376,9 +404,12 @@ int lmo_lsm_backward(const lmo_spec* s, int n, int d_k, int d_v, const double* q
             draw += da_sum * a * (-spb) * sigm(s->mamba2_a_raw);
         }
     }
+#undef VA
     if (da_raw) *da_raw = draw;
-    if (dM0) memcpy(dM0, dM, sizeof(double) * dd);
-    free(Ms); free(dM);
+    if (dM0)
+        for (int i = 0; i < d_k; ++i)
+            for (int j = 0; j < d_v; ++j) dM0[(size_t)i * d_v + j] = dM[i * dva + j];
+    free(Ms); free(dM); free(dOa);
     return 0;
 }
 

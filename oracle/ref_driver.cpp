@@ -192,8 +192,9 @@ void golden_lsm_device() {
 
 // ---- LSM gradients from the reference tape (tensor.hpp:1178) ----
 void golden_lsm_grad() {
+    // appended tags keep the seeds of the earlier ones: the normalised reference defaults
     const char* tags[] = {"bla_plain", "lightning", "retnet", "gla", "hgrn2", "rwkv6", "mamba2",
-                          "rebased_plain"};
+                          "rebased_plain", "bla", "rebased", "retnet_norm", "gla_norm"};
     int ci = 0;
     for (const char* tag : tags) {
         const Variant* var = nullptr;

@@ -88,6 +88,51 @@ __global__ void lsm_apply_fmap(const T* __restrict__ x, T* __restrict__ y, size_
         st_f(y + i, fmap_t<FM>(ld_f(x + i)));
 }
 
+// ---------------------------------------------------------------- normaliser backward helpers
+// o = num / den (chunk_forward_separable with the normaliser, lsm.hpp:584-596): the upstream
+// gradient splits into dnum = dO / den and dden = -(dO . num) / den^2, the latter fed to an
+// LSM whose value is e0 (den = column 0 of that LSM's output).
+template <typename T>
+__global__ void lsm_fill_e0(T* __restrict__ x, size_t rows, int D) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * D; i += (size_t)gridDim.x * blockDim.x)
+        st_f(x + i, (i % D) == 0 ? 1.f : 0.f);
+}
+
+// one warp per (b, t, h) row
+template <typename T, int D>
+__global__ void __launch_bounds__(256) lsm_norm_prep(const T* __restrict__ num, const T* __restrict__ den_o,
+                                                     const T* __restrict__ dO, T* __restrict__ dO1,
+                                                     T* __restrict__ dO2, size_t rows, int* err) {
+    constexpr int EPL = D / 32;
+    const size_t row = (size_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const float den = ld_f(den_o + row * D);
+    const float inv = 1.f / den;
+    float dn = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+        const size_t i = row * D + lane * EPL + e;
+        const float g = ld_f(dO + i);
+        dn += g * ld_f(num + i);
+        st_f(dO1 + i, g * inv);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dn += __shfl_xor_sync(0xFFFFFFFFu, dn, o);
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+        const int c = lane * EPL + e;
+        st_f(dO2 + row * D + c, c == 0 ? -dn * inv * inv : 0.f);
+    }
+    if (lane == 0 && fabsf(den) < 1e-12f) atomicOr(err, 1);
+}
+
+template <typename T>
+__global__ void lsm_add_inplace(T* __restrict__ dst, const T* __restrict__ src, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        st_f(dst + i, ld_f(dst + i) + ld_f(src + i));
+}
+
 // ------------------------------------------------------------------------------- launchers
 template <typename T, int D>
 static cudaError_t finish_t(int fm, bool mamba, const void* q, const void* k, const float* dphq,
@@ -128,4 +173,31 @@ cudaError_t launch_apply_fmap(bool bf16, int fm, const void* x, void* y, size_t 
     return cudaGetLastError();
 }
 
+}  // namespace lmoe_dev
+
+namespace lmoe_dev {
+cudaError_t launch_norm_helpers(int op, bool bf16, void* a, const void* b, const void* c, const void* d, void* e,
+                                void* f, size_t rows, int D, int* err, cudaStream_t st) {
+    const unsigned grid = (unsigned)std::min<size_t>((rows * D + 255) / 256, 148 * 16);
+    if (op == 0) {  // a <- e0 rows
+        if (bf16) lsm_fill_e0<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(a), rows, D);
+        else lsm_fill_e0<float><<<grid, 256, 0, st>>>(static_cast<float*>(a), rows, D);
+    } else if (op == 1) {  // (num b, den c, dO d) -> dO1 e, dO2 f
+        const unsigned g8 = (unsigned)((rows + 7) / 8);
+        if (bf16)
+            lsm_norm_prep<__nv_bfloat16, 128><<<g8, 256, 0, st>>>(
+                static_cast<const __nv_bfloat16*>(b), static_cast<const __nv_bfloat16*>(c),
+                static_cast<const __nv_bfloat16*>(d), static_cast<__nv_bfloat16*>(e), static_cast<__nv_bfloat16*>(f),
+                rows, err);
+        else
+            lsm_norm_prep<float, 64><<<g8, 256, 0, st>>>(static_cast<const float*>(b), static_cast<const float*>(c),
+                                                       static_cast<const float*>(d), static_cast<float*>(e),
+                                                       static_cast<float*>(f), rows, err);
+    } else {  // a += b over rows * D elements
+        if (bf16) lsm_add_inplace<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(a),
+                                                                        static_cast<const __nv_bfloat16*>(b), rows * D);
+        else lsm_add_inplace<float><<<grid, 256, 0, st>>>(static_cast<float*>(a), static_cast<const float*>(b), rows * D);
+    }
+    return cudaGetLastError();
+}
 }  // namespace lmoe_dev

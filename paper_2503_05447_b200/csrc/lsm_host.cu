@@ -778,9 +778,39 @@ static void vec_backward(const lmoe_lsm_desc& dd, const BwdPlan& w, int B, int N
 }
 }  // namespace lmoe_host
 
+namespace lmoe_host {
+// Normaliser backward (lsm.hpp:584-596): o = num / den.  The tape's VJP is the sum of the
+// backward of the unnormalised LSM under dnum = dO / den and the backward of the LSM with
+// value e0 (whose output column 0 is den) under dden = -(dO . num) / den^2: two forwards
+// (num, den), one elementwise split, two backward calls, one accumulation.
+struct NormPlan {
+    size_t off_inner = 0, inner = 0, off_fwd = 0, fwd = 0, off_e0 = 0, off_num = 0, off_den = 0, off_dO1 = 0,
+           off_dO2 = 0, off_dq2 = 0, off_dk2 = 0, off_dv2 = 0, off_da2 = 0, off_err = 0, total = 0;
+};
+static NormPlan plan_norm(const lmoe_lsm_desc* d, int B, int N, int H, int D, lmoe_dtype dt) {
+    lmoe_lsm_desc dd = *d;
+    dd.use_normalizer = 0;
+    NormPlan p;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    p.inner = plan_bwd(&dd, B, N, H, D, dt).total;
+    p.off_inner = take(p.inner);
+    p.fwd = plan_lsm(B, N, H, D).total;
+    p.off_fwd = take(p.fwd);
+    const size_t act = (size_t)B * N * H * D * (dt == LMOE_BF16 ? 2 : 4);
+    p.off_e0 = take(act); p.off_num = take(act); p.off_den = take(act);
+    p.off_dO1 = take(act); p.off_dO2 = take(act);
+    p.off_dq2 = take(act); p.off_dk2 = take(act); p.off_dv2 = take(act); p.off_da2 = take(act);
+    p.off_err = take(64);
+    p.total = off;
+    return p;
+}
+}  // namespace lmoe_host
+
 extern "C" size_t lmoe_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
                                               lmoe_dtype dtype) {
     if (!desc || B < 1 || N < 1 || H < 1 || D < 1) return 0;
+    if (desc->use_normalizer) return plan_norm(desc, B, N, H, D, dtype).total;
     return plan_bwd(desc, B, N, H, D, dtype).total;
 }
 
@@ -793,9 +823,60 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
     return guarded([&]() {
         validate(desc, B, N, H, D, dtype, q, k, v, dO);
         if (!dq || !dk || !dv) throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: null gradient tensor");
-        if (desc->use_normalizer)
-            throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_lsm_bwd: normalizer backward not in this build");
         const int mode = device_decay_mode(desc->instance);
+        if (desc->use_normalizer) {
+            if (mode == lmoe_dev::kDecayTokenVector && (!a_pre || !da_pre))
+                throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: TokenVector instances need a_pre and da_pre");
+            const NormPlan w = plan_norm(desc, B, N, H, D, dtype);
+            if (!workspace || workspace_bytes < w.total)
+                throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd: workspace too small (need " + std::to_string(w.total) + " bytes)");
+            uint8_t* ws = static_cast<uint8_t*>(workspace);
+            cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+            const bool bf16 = dtype == LMOE_BF16;
+            const size_t rows = (size_t)B * N * H;
+            lmoe_lsm_desc dd = *desc;
+            dd.use_normalizer = 0;
+            auto chk = [](int rc) {
+                if (rc != LMOE_OK) throw Error(rc, lmoe_last_error());
+            };
+            int* err = reinterpret_cast<int*>(ws + w.off_err);
+            LMOE_CUDA_CHECK(cudaMemsetAsync(err, 0, 64, st));
+            void* e0 = ws + w.off_e0;
+            LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(0, bf16, e0, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                          rows, D, nullptr, st));
+            chk(lmoe_lsm_fwd(&dd, B, N, H, D, dtype, q, k, v, a_pre, b_pre, a_raw, M0, nullptr, ws + w.off_num,
+                             nullptr, nullptr, ws + w.off_fwd, w.fwd, stream));
+            chk(lmoe_lsm_fwd(&dd, B, N, H, D, dtype, q, k, e0, a_pre, b_pre, a_raw, nullptr, nullptr,
+                             ws + w.off_den, nullptr, nullptr, ws + w.off_fwd, w.fwd, stream));
+            LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(1, bf16, nullptr, ws + w.off_num, ws + w.off_den, dO,
+                                                          ws + w.off_dO1, ws + w.off_dO2, rows, D, err, st));
+            g_launch_count += 2;
+            if (desc->flags & LMOE_FLAG_CHECK) {
+                int e = 0;
+                LMOE_CUDA_CHECK(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+                LMOE_CUDA_CHECK(cudaStreamSynchronize(st));
+                if (e)
+                    throw Error(LMOE_ERR_DEGENERATE,
+                                std::string("degenerate normalizer in instance ") + instance_name(desc->instance));
+            }
+            const bool vec = mode == lmoe_dev::kDecayTokenVector;
+            chk(lmoe_lsm_bwd(&dd, B, N, H, D, dtype, q, k, v, a_pre, b_pre, a_raw, M0, ws + w.off_dO1, dM_final,
+                             dq, dk, dv, da_pre, db_pre, da_raw, dM0, ws + w.off_inner, w.inner, stream));
+            chk(lmoe_lsm_bwd(&dd, B, N, H, D, dtype, q, k, e0, a_pre, b_pre, a_raw, nullptr, ws + w.off_dO2, nullptr,
+                             ws + w.off_dq2, ws + w.off_dk2, ws + w.off_dv2, vec ? ws + w.off_da2 : nullptr, nullptr,
+                             nullptr, nullptr, ws + w.off_inner, w.inner, stream));
+            LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(2, bf16, dq, ws + w.off_dq2, nullptr, nullptr, nullptr,
+                                                          nullptr, rows, D, nullptr, st));
+            LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(2, bf16, dk, ws + w.off_dk2, nullptr, nullptr, nullptr,
+                                                          nullptr, rows, D, nullptr, st));
+            g_launch_count += 3;
+            if (vec) {
+                LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(2, bf16, da_pre, ws + w.off_da2, nullptr, nullptr, nullptr,
+                                                              nullptr, rows, D, nullptr, st));
+                ++g_launch_count;
+            }
+            return;
+        }
         if (mode == lmoe_dev::kDecayTokenVector) {
             if (dtype != LMOE_BF16)
                 throw Error(LMOE_ERR_UNSUPPORTED, std::string("lmoe_lsm_bwd: instance ") + instance_name(desc->instance) +

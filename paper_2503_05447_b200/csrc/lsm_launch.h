@@ -61,6 +61,10 @@ cudaError_t launch_mamba_dgate(bool bf16, const CUtensorMap& q, const CUtensorMa
                                float* db_pre, float* da_raw, int B, int N, int H, cudaStream_t st);
 cudaError_t launch_transpose_states(const float* in, float* out, int BH, int D, cudaStream_t st);
 cudaError_t launch_apply_fmap(bool bf16, int fm, const void* x, void* y, size_t n, cudaStream_t st);
+// normaliser backward: op 0 fill e0 rows into a; op 1 (num b, den c, dO d) -> dO / den into e and
+// -(dO . num) / den^2 e0 into f (err on |den| < 1e-12); op 2 a += b
+cudaError_t launch_norm_helpers(int op, bool bf16, void* a, const void* b, const void* c, const void* d, void* e,
+                                void* f, size_t rows, int D, int* err, cudaStream_t st);
 }  // namespace lmoe_dev
 
 namespace lmoe_dev {

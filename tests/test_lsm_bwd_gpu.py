@@ -103,8 +103,8 @@ def test_golden_grads_padded(dtype):
     ran = 0
     for p in sorted({k.split("/")[0] for k in d}):
         spec = oracle.spec_from_golden(d, p)
-        if spec["instance"] not in SCALAR_KINDS:
-            continue
+        if spec["instance"] not in SCALAR_KINDS or spec["use_normalizer"]:
+            continue  # normalised specs: test_golden_normalizer_grads_padded / oracle cases
         pad = lambda x: np.pad(x, ((0, 0), (0, D - x.shape[1])))[None, :, None]
         q, k, v, dO = (pad(_round(d[p + "/" + n], dtype)) for n in ("q", "k", "v", "dO"))
         b_pre = d.get(p + "/b_pre")
@@ -232,8 +232,9 @@ def test_bwd_error_texts():
     import paper_2503_05447_b200 as pk
     dev = torch.device("cuda:0")
     x = torch.zeros(1, 16, 1, 128, dtype=torch.bfloat16, device=dev)
-    with pytest.raises(pk.LmoeError, match="normalizer backward not in this build"):
-        pk.lsm_backward_batched(x, x, x, None, pk.LsmSpec.make("bla", 128), x)
+    # squared feature map of all-zero inputs: den = 0 (chunk_forward_separable, lsm.hpp:590)
+    with pytest.raises(pk.LmoeError, match="degenerate normalizer in instance rebased"):
+        pk.lsm_backward_batched(x, x, x, None, pk.LsmSpec.make("rebased", 128), x)
     with pytest.raises(RuntimeError, match="shape mismatch"):
         pk.lsm_backward_batched(x, x, x[:, :8], None, pk.LsmSpec.make("retnet", 128), x)
 
@@ -251,7 +252,7 @@ def test_golden_vector_grads_padded():
     ran = 0
     for p in sorted({k.split("/")[0] for k in d}):
         spec = oracle.spec_from_golden(d, p)
-        if spec["instance"] not in VEC_KINDS:
+        if spec["instance"] not in VEC_KINDS or spec["use_normalizer"]:
             continue
         pad = lambda x: np.pad(x, ((0, 0), (0, D - x.shape[1])))[None, :, None]
         q, k, v, dO, a = (pad(_round(d[p + "/" + n], "bf16")) for n in ("q", "k", "v", "dO", "a_pre"))
@@ -311,3 +312,86 @@ def test_vector_bwd_f32_is_refused():
     x = torch.zeros(1, 16, 1, 64, dtype=torch.float32, device=dev)
     with pytest.raises(pk.LmoeError, match="bf16 / head_dim 128 only"):
         pk.lsm_backward_batched(x, x, x, pk.LsmGates(a_pre=x), pk.LsmSpec.make("gla", 64), x)
+
+
+# ------------------------------------------------------------------ normaliser (o = num / den)
+def _oracle_norm_parts(spec, q, k, v, dO, M0, a):
+    """f64 oracle of the two addends the normalised backward is made of: the unnormalised
+    backward under dO / den, and the backward of the value-e0 LSM (output column 0 = den)
+    under -(dO . num) / den^2 e0."""
+    B, N, H, D = q.shape
+    plain = dict(spec)
+    plain["use_normalizer"] = 0
+    e0 = np.zeros_like(v)
+    e0[..., 0] = 1.0
+    num, den = np.zeros_like(v), np.zeros(q.shape[:3])
+    for b in range(B):
+        for h in range(H):
+            sp = dict(oracle.spec_default(plain["instance"]))
+            sp.update(plain)
+            aa = None if a is None else a[b, :, h]
+            num[b, :, h], _, _ = oracle.lsm_chunked(sp, q[b, :, h], k[b, :, h], v[b, :, h], aa, None, 64, M0[b, h])
+            o2, _, _ = oracle.lsm_chunked(sp, q[b, :, h], k[b, :, h], e0[b, :, h], aa, None, 64)
+            den[b, :, h] = o2[:, 0]
+    dO1 = dO / den[..., None]
+    dO2 = np.zeros_like(dO)
+    dO2[..., 0] = -(dO * num).sum(-1) / den ** 2
+    return (_oracle_bwd(plain, q, k, v, dO1, None, None, M0, a_pre=a),
+            _oracle_bwd(plain, q, k, e0, dO2, None, None, np.zeros_like(M0), a_pre=a))
+
+
+def test_golden_normalizer_grads_padded():
+    """Reference tape gradients of the default Rebased spec (squared map + normaliser, d = 4).
+    Zero padding is exact for the squared map (phi(0) = 0); elu+1 maps 0 to 1, so the elu+1
+    normalised specs are checked against the oracle (pinned to their golden tapes) below."""
+    d = load_golden("lsm_grad")
+    p = "rebased"
+    spec = oracle.spec_from_golden(d, p)
+    assert spec["use_normalizer"] == 1 and spec["feature_map"] == 2
+    for dtype in ("f32", "bf16"):
+        D = DIM[dtype]
+        pad = lambda x: np.pad(x, ((0, 0), (0, D - x.shape[1])))[None, :, None]
+        q, k, v, dO = (pad(_round(d[p + "/" + n], dtype)) for n in ("q", "k", "v", "dO"))
+        got = _bwd(spec, q, k, v, dO, dtype=dtype)
+        for n in ("dq", "dk", "dv"):
+            err = norm_rel_err(got[n][0, :, 0, :4], d[p + "/" + n])
+            assert err < TOL[dtype], (dtype, n, err)
+
+
+NCASES = [  # (name, spec, dtype, B, N, H, a_pre mean or None)
+    ("bla_default_f32", {"instance": 0, "feature_map": 1, "use_normalizer": 1}, "f32", 1, 300, 2, None),
+    ("bla_default_bf16", {"instance": 0, "feature_map": 1, "use_normalizer": 1}, "bf16", 2, 257, 2, None),
+    ("rebased_default", {"instance": 6, "feature_map": 2, "use_normalizer": 1}, "bf16", 1, 400, 2, None),
+    ("retnet_norm", {"instance": 2, "feature_map": 1, "use_normalizer": 1, "scalar_decay": 1 - 1 / 32},
+     "f32", 1, 700, 2, None),
+    ("gla_norm", {"instance": 3, "feature_map": 1, "use_normalizer": 1}, "bf16", 1, 500, 2, 2.0),
+]
+
+
+@pytest.mark.parametrize("case", NCASES, ids=[c[0] for c in NCASES])
+def test_normalizer_bwd_matches_oracle(case):
+    name, spec, dtype, B, N, H, amean = case
+    D = DIM[dtype]
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    q, k, v = (_round(rng.normal(0, 0.5, (B, N, H, D)), dtype) for _ in range(3))
+    dO = _round(rng.normal(0, 1.0, (B, N, H, D)), dtype)
+    M0 = rng.normal(0, 0.1, (B, H, D, D))
+    a = None if amean is None else _round(rng.normal(amean, 0.5, (B, N, H, D)), dtype)
+    got = _bwd(spec, q, k, v, dO, None, None, M0, dtype=dtype, a_pre=a)
+    want = _oracle_bwd(spec, q, k, v, dO, None, None, M0, a_pre=a)
+    # Conditioning: d phi(q), d phi(k), d a are sums of a num part (upstream dO / den) and a den
+    # part (upstream -(dO . num) / den^2) that largely cancel for positive feature maps; each
+    # part is an ordinary LSM backward held to TOL, so the sum is held to TOL * kappa with
+    # kappa = max|part| / max|sum| from the f64 oracle (dv has no den part: kappa = 1).
+    parts = _oracle_norm_parts(spec, q, k, v, dO, M0, a)
+    names = ("dq", "dk", "dv") + (("da_pre",) if a is not None else ())
+    for n in names:
+        for b in range(B):
+            for h in range(H):
+                w = want[n][b, :, h]
+                kappa = max(1.0, max(np.abs(pp[n][b, :, h]).max() for pp in parts) / max(np.abs(w).max(), 1e-30))
+                err = norm_rel_err(got[n][b, :, h], w)
+                assert err < TOL[dtype] * kappa, (name, n, b, h, err, kappa)
+    for b in range(B):
+        for h in range(H):
+            assert norm_rel_err(got["dM0"][b, h], want["dM0"][b, h]) < TOL[dtype], (name, "dM0", b, h)
