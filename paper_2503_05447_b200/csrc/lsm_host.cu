@@ -239,9 +239,9 @@ struct LsmCall {
         if (vec) {
             const CUtensorMap ta = tmap<T>(a_pre);
             if constexpr (sizeof(T) == 2)
-                LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_vec_bf16(var, grid, st, tq, tk, tv, ta, p));
+                LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_vec_bf16(var, grid, st, tq, tk, tv, ta, to, p));
             else
-                LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_vec_f32(var, grid, st, tq, tk, tv, ta, p));
+                LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_vec_f32(var, grid, st, tq, tk, tv, ta, to, p));
         } else if constexpr (sizeof(T) == 2) {
             LMOE_CUDA_CHECK(lmoe_dev::launch_output_pass_bf16(var, grid, st, tq, tk, tv, to, p));
         } else {

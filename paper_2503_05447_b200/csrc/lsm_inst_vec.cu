@@ -21,7 +21,7 @@ cudaError_t spv(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CUtensor
 
 template <typename T, int FM, bool NORM, bool HG>
 cudaError_t opv(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                const CUtensorMap& a, const LsmFwdParams& p) {
+                const CUtensorMap& a, const CUtensorMap& o, const LsmFwdParams& p) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(lsm_output_pass_vec<T, FM, NORM, HG>,
@@ -29,7 +29,7 @@ cudaError_t opv(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensor
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_output_pass_vec<T, FM, NORM, HG><<<grid, kOutputPassThreads, output_pass_vec_smem<T>(), st>>>(q, k, v, a, p);
+    lsm_output_pass_vec<T, FM, NORM, HG><<<grid, output_pass_vec_threads<T>(), output_pass_vec_smem<T>(), st>>>(q, k, v, a, o, p);
     return cudaGetLastError();
 }
 
@@ -57,8 +57,8 @@ cudaError_t launch_state_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st,
 }
 cudaError_t launch_output_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
                                         const CUtensorMap& k, const CUtensorMap& val, const CUtensorMap& a,
-                                        const LsmFwdParams& p) {
-    VEC_VARIANTS(opv, __nv_bfloat16, grid, st, q, k, val, a, p)
+                                        const CUtensorMap& o, const LsmFwdParams& p) {
+    VEC_VARIANTS(opv, __nv_bfloat16, grid, st, q, k, val, a, o, p)
 }
 cudaError_t launch_state_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
                                       const CUtensorMap& val, const CUtensorMap& a, const LsmFwdParams& p) {
@@ -66,8 +66,8 @@ cudaError_t launch_state_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, 
 }
 cudaError_t launch_output_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
                                        const CUtensorMap& k, const CUtensorMap& val, const CUtensorMap& a,
-                                       const LsmFwdParams& p) {
-    VEC_VARIANTS(opv, float, grid, st, q, k, val, a, p)
+                                       const CUtensorMap& o, const LsmFwdParams& p) {
+    VEC_VARIANTS(opv, float, grid, st, q, k, val, a, o, p)
 }
 
 }  // namespace lmoe_dev

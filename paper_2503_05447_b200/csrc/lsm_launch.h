@@ -42,12 +42,12 @@ cudaError_t launch_state_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st,
                                        const CUtensorMap& val, const CUtensorMap& a, const LsmFwdParams& p);
 cudaError_t launch_output_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
                                         const CUtensorMap& k, const CUtensorMap& val, const CUtensorMap& a,
-                                        const LsmFwdParams& p);
+                                        const CUtensorMap& o, const LsmFwdParams& p);
 cudaError_t launch_state_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
                                       const CUtensorMap& val, const CUtensorMap& a, const LsmFwdParams& p);
 cudaError_t launch_output_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
                                        const CUtensorMap& k, const CUtensorMap& val, const CUtensorMap& a,
-                                       const LsmFwdParams& p);
+                                       const CUtensorMap& o, const LsmFwdParams& p);
 }  // namespace lmoe_dev
 
 namespace lmoe_dev {

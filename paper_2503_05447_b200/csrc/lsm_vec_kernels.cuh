@@ -252,18 +252,26 @@ __global__ void __launch_bounds__(kStatePassVecThreads, 1)
 // TMEM: S [0,128), O [128,256), M [256,384) (tf32: O [128,192), M [192,256) M=64 layout);
 // row partials (normaliser) in S columns 64.. (bf16) / [384,388) (tf32).
 // ====================================================================================
+// bf16: 16 math warps (four 32-column groups per row, as the scalar pass); tf32: 8
+template <typename T>
+constexpr int vec_math_threads() { return sizeof(T) == 2 ? 512 : 256; }
+template <typename T>
+constexpr int output_pass_vec_threads() { return 128 + vec_math_threads<T>(); }
+
 template <typename T, int FM, bool NORM, bool HG>
-__global__ void __launch_bounds__(kOutputPassThreads, 1)
+__global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
     lsm_output_pass_vec(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmA,
-                        LsmFwdParams p) {
+                        const __grid_constant__ CUtensorMap tmO, LsmFwdParams p) {
     using TT = TileTraits<T>;
     constexpr int D = TT::D;
     constexpr bool kBF16 = sizeof(T) == 2;
     constexpr bool TR = TT::kTransposed;
-    constexpr int DH = D / 2;
-    using L = VecLayout<T>;
-    static_assert(kMathThreads == kVecNT, "2-D scan layout");
+    constexpr int NM = vec_math_threads<T>();
+    constexpr int NQ = NM / 128;  // column groups per row in the row-layout phases
+    constexpr int DH = D / NQ;    // state / O columns per thread (32)
+    static_assert(DH == 32, "row-layout phases assume 32 columns per thread");
+    using L = VecLayout<T, NM>;
     constexpr int STAGE = 4 * kTileBytes;     // Q | K | V | A
     extern __shared__ __align__(1024) uint8_t smem[];
     if (smem_u32(smem) & 1023) __trap();
@@ -273,12 +281,13 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
     uint8_t* at = qt + 3 * kTileBytes;
     uint8_t* kT = qt + STAGE;
     uint8_t* vT = kT + (TR ? kTileBytes : 0);
-    uint8_t* mop = vT + (TR ? kTileBytes : 0);
-    float* sTot = reinterpret_cast<float*>(mop + TT::MOP_BYTES);  // [16][D] scan scratch
-    float* sR = sTot + 16 * D;                                      // [D]
-    float* sGe = sR + D;                                            // [D]
-    float* sG0 = sGe + D;                                           // [D]
-    float* sZ = sG0 + D;                                            // [D]
+    uint8_t* ostg = vT + (TR ? kTileBytes : 0);  // bf16: O staging for the bulk tensor store
+    uint8_t* mop = ostg + (kBF16 ? kTileBytes : 0);
+    float* sOffE = reinterpret_cast<float*>(mop + TT::MOP_BYTES);  // [RG][D] group factor offsets
+    float* sOffI = sOffE + L::RG * D;                               // [RG][D] (reciprocals)
+    float* sER = sOffI + L::RG * D;                                 // [D] e^{r} = prod sigma rows < 64
+    float* sEG = sER + D;                                           // [D] e^{G_end - r} = prod rows >= 64
+    float* sZ = sEG + D;                                            // [D]
     float* sZP = sZ + D;                                            // [D]  e^r z
     float* sZC = sZP + D;                                           // [D]  this chunk's colsum of k~
     uint64_t* bars = reinterpret_cast<uint64_t*>(sZC + D);
@@ -300,9 +309,9 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
     if (threadIdx.x == 0) {
         mbar_init(full, 1);
         mbar_init(empty, 1);
-        mbar_init(xf, kMathThreads);
+        mbar_init(xf, NM);
         mbar_init(s_full, 1);
-        mbar_init(p_full, kMathThreads);
+        mbar_init(p_full, NM);
         mbar_init(mo_full, 1);
         fence_barrier_init();
     }
@@ -382,14 +391,13 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int tid = threadIdx.x - 128;  // 0..255
+        const int tid = threadIdx.x - 128;  // 0..NM-1
         const int mw = warp - 4;
         const int q = warp & 3, hh = mw >> 2;
         const int row = q * 32 + lane;     // row mapping (S / O / P epilogues)
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const int srow = TR ? q * 16 + lane : row;  // state row (d_k index)
         const bool sown = TR ? lane < 16 : true;
-        T* const obase = reinterpret_cast<T*>(p.o);
 
         // initial state: M_T <- M_in (fp32), z <- z_in
         {
@@ -416,33 +424,82 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             if (tid == 0) trace_mark(p, c, 0);
             // (1)+(2) 2-D column scan (lsm_vec_scan.cuh), then in place q~ = phi(q) e^{G - r},
             // k~ = keff e^{r - G} (tf32: also the K-major K~^T, V^T tiles)
+            // The pairwise factor e^{G_i - G_j} = E_i / E_j with E_t = e^{G_t - r} is a product of
+            // per-token sigmas relative to the midpoint (row 63): E_t = prod_{t<u<=63} 1/sigma_u
+            // for t < 64, prod_{64<=u<=t} sigma_u for t >= 64 -- two MUFU ops per element (ex2,
+            // rcp) and FMA-pipe products, instead of log-space sums and two exponentials.
             {
-                float G[L::R][L::EPC];
-                float nocarry = 0.f;
-                vec_log_scan<T>(at, nvalid, tid, G, sTot, sR, sGe, sG0, nullptr, nocarry);
-                if (tid == 0) trace_mark(p, c, 1);
-                if (tid < D && !vec_split_ok(sG0[tid], sR[tid], sGe[tid])) atomicOr(&p.err[2], 1);
                 const int cg = tid & 15, rg = tid >> 4;
-                float zc[L::EPC];
+                constexpr int HALF = L::RG / 2;  // row groups below the midpoint
+                const bool lower = rg < HALF;
+                float sg[L::R][L::EPC], isg[L::R][L::EPC];
+                float tot[L::EPC];
 #pragma unroll
-                for (int j = 0; j < L::EPC; ++j) zc[j] = 0.f;
-                float rr[L::EPC];
-#pragma unroll
-                for (int j = 0; j < L::EPC; ++j) rr[j] = sR[cg * L::EPC + j];
+                for (int j = 0; j < L::EPC; ++j) tot[j] = 1.f;
 #pragma unroll
                 for (int ii = 0; ii < L::R; ++ii) {
                     const int i = rg * L::R + ii;
-                    const float vm = i < nvalid ? 1.f : 0.f;
-                    float xq[L::EPC], xk[L::EPC], xa[L::EPC];
-                    ld_chunk<T>(qt, i, cg, xq);
-                    if constexpr (HG) ld_chunk<T>(at, i, cg, xa);
-                    else ld_chunk<T>(kt, i, cg, xk);
+                    const bool valid = i < nvalid;
+                    float xa[L::EPC], keff[L::EPC];
+                    ld_chunk<T>(at, i, cg, xa);
 #pragma unroll
                     for (int j = 0; j < L::EPC; ++j) {
-                        const float gr = G[ii][j] - rr[j];
-                        const float keff = HG ? sigmoid_fast(-xa[j]) : fmap_t<FM>(xk[j]);
-                        xq[j] = fmap_t<FM>(xq[j]) * (vm * fast_exp(gr));
-                        xk[j] = keff * (vm * fast_exp(-gr));
+                        const float ex = ex2_ftz(-xa[j] * 1.4426950408889634f);  // e^{-a}
+                        const float sgm = rcp_ftz(1.f + ex);                       // sigma(a)
+                        sg[ii][j] = valid ? sgm : 1.f;
+                        isg[ii][j] = valid ? 1.f + ex : 1.f;
+                        tot[j] *= sg[ii][j];
+                        keff[j] = ex * sgm;                                        // HGRN2: 1 - sigma(a)
+                    }
+                    if constexpr (HG) st_chunk_raw<T>(kt, i, cg, keff);  // k is unused by HGRN2
+                }
+#pragma unroll
+                for (int j = 0; j < L::EPC; ++j) sOffE[rg * D + cg * L::EPC + j] = tot[j];
+                named_bar_sync(1, NM);
+                if (tid < D) {
+                    // first half: exclusive suffix over the later groups below the midpoint
+                    float sfx = 1.f;
+                    for (int g = HALF - 1; g >= 0; --g) {
+                        const float pg = sOffE[g * D + tid];
+                        sOffI[g * D + tid] = sfx;
+                        sOffE[g * D + tid] = rcp_ftz(sfx);
+                        sfx *= pg;
+                    }
+                    sER[tid] = sfx;
+                    // second half: exclusive prefix from the midpoint
+                    float pfx = 1.f;
+                    for (int g = HALF; g < L::RG; ++g) {
+                        const float pg = sOffE[g * D + tid];
+                        sOffE[g * D + tid] = pfx;
+                        sOffI[g * D + tid] = rcp_ftz(pfx);
+                        pfx *= pg;
+                    }
+                    sEG[tid] = pfx;
+                }
+                named_bar_sync(1, NM);
+                if (tid == 0) trace_mark(p, c, 1);
+                float E[L::EPC], Ei[L::EPC];
+#pragma unroll
+                for (int j = 0; j < L::EPC; ++j) {
+                    E[j] = sOffE[rg * D + cg * L::EPC + j];
+                    Ei[j] = sOffI[rg * D + cg * L::EPC + j];
+                }
+                float zc[L::EPC];
+#pragma unroll
+                for (int j = 0; j < L::EPC; ++j) zc[j] = 0.f;
+                bool bad = false;
+                // one row of q~ / k~ with the current factors
+                auto xform_row = [&](int ii, const float (&Ef)[L::EPC], const float (&Eif)[L::EPC]) {
+                    const int i = rg * L::R + ii;
+                    const float vm = i < nvalid ? 1.f : 0.f;
+                    float xq[L::EPC], xk[L::EPC];
+                    ld_chunk<T>(qt, i, cg, xq);
+                    ld_chunk<T>(kt, i, cg, xk);
+#pragma unroll
+                    for (int j = 0; j < L::EPC; ++j) {
+                        const float keff = HG ? xk[j] : fmap_t<FM>(xk[j]);
+                        xq[j] = fmap_t<FM>(xq[j]) * (vm * Ef[j]);
+                        xk[j] = keff * (vm * Eif[j]);
                         if constexpr (NORM) zc[j] += xk[j];
                     }
                     st_chunk<T>(qt, i, cg, xq);
@@ -456,17 +513,41 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                             *tr_elem(vT, cg * L::EPC + j, i) = tf32r(xv[j]);
                         }
                     }
+                };
+                // range of the midpoint split (|G - r| < 80, as the log-space check): the extreme
+                // factors are the first row (lower half) and the last row (upper half)
+                if (lower) {  // warp-uniform: half-warps share a row group pair
+#pragma unroll
+                    for (int kk = 0; kk < L::R; ++kk) {
+                        const int ii = L::R - 1 - kk;  // exclusive suffix: walk upwards
+                        xform_row(ii, E, Ei);
+#pragma unroll
+                        for (int j = 0; j < L::EPC; ++j) { E[j] *= isg[ii][j]; Ei[j] *= sg[ii][j]; }
+                    }
+#pragma unroll
+                    for (int j = 0; j < L::EPC; ++j) bad |= !(E[j] * sg[0][j] < 5.54e34f);
+                } else {
+#pragma unroll
+                    for (int ii = 0; ii < L::R; ++ii) {  // inclusive prefix: walk downwards
+#pragma unroll
+                        for (int j = 0; j < L::EPC; ++j) { E[j] *= sg[ii][j]; Ei[j] *= isg[ii][j]; }
+                        xform_row(ii, E, Ei);
+                    }
+#pragma unroll
+                    for (int j = 0; j < L::EPC; ++j) bad |= !(E[j] > 1.81e-35f);
                 }
                 if constexpr (NORM) {
 #pragma unroll
                     for (int j = 0; j < L::EPC; ++j) atomicAdd(&sZC[cg * L::EPC + j], zc[j]);
                 }
+                if (bad) atomicOr(&p.err[2], 1);
             }
-            named_bar_sync(1, kMathThreads);
+            if (tid == 0) bulk_wait_read0();  // the previous chunk's O store has left the staging tile
+            named_bar_sync(1, NM);
             if (tid == 0) trace_mark(p, c, 2);
             // (3) state operand M' = diag(e^r) M  (and the TMEM copy), z' = e^r z
             {
-                const float er = __expf(sR[srow < D ? srow : 0]);
+                const float er = sER[srow < D ? srow : 0];
                 float vals[DH];
 #pragma unroll
                 for (int cb = 0; cb < DH / 32; ++cb) {
@@ -482,15 +563,16 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 }
                 if (sown) {
                     if constexpr (!TR) {
-                        uint8_t* dst = mop + hh * (D * 128);
+                        // columns [32 hh, 32 hh + 32): block hh / 2, 16-byte chunks 4 (hh % 2) ..
+                        uint8_t* dst = mop + (hh >> 1) * (D * 128);
 #pragma unroll
-                        for (int ch = 0; ch < 8; ++ch) {
+                        for (int ch = 0; ch < 4; ++ch) {
                             uint4 v;
                             v.x = pack_bf16(vals[ch * 8 + 0], vals[ch * 8 + 1]);
                             v.y = pack_bf16(vals[ch * 8 + 2], vals[ch * 8 + 3]);
                             v.z = pack_bf16(vals[ch * 8 + 4], vals[ch * 8 + 5]);
                             v.w = pack_bf16(vals[ch * 8 + 6], vals[ch * 8 + 7]);
-                            *reinterpret_cast<uint4*>(dst + sw128_off(srow, ch)) = v;
+                            *reinterpret_cast<uint4*>(dst + sw128_off(srow, (hh & 1) * 4 + ch)) = v;
                         }
                     } else {
                         uint8_t* base = mop + (srow >> 5) * 8192 + ((srow & 3) << 2);
@@ -501,12 +583,12 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                     }
                 }
                 if constexpr (NORM) {
-                    if (tid < D) sZP[tid] = __expf(sR[tid]) * sZ[tid];
+                    if (tid < D) sZP[tid] = sER[tid] * sZ[tid];
                 }
                 tmem_wait_st();
                 fence_proxy_async_smem();
                 tc_fence_before();
-                if constexpr (NORM) named_bar_sync(1, kMathThreads);
+                if constexpr (NORM) named_bar_sync(1, NM);
                 mbar_arrive(xf);
             }
             if (tid == 0) trace_mark(p, c, 3);
@@ -515,14 +597,16 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             if (tid == 0) trace_mark(p, c, 4);
             tc_fence_after();
             {
+                // this thread's 128 / NQ columns of the S row (bf16: 32, tf32: 64)
+                constexpr int SC = 128 / NQ;
                 uint32_t r0[32], r1[32];
-                tmem_ld32(tS + lane_off + hh * 64, r0);
-                tmem_ld32(tS + lane_off + hh * 64 + 32, r1);
+                tmem_ld32(tS + lane_off + hh * SC, r0);
+                if constexpr (SC == 64) tmem_ld32(tS + lane_off + hh * SC + 32, r1);
                 tmem_wait_ld();
                 float rs = 0.f;
 #pragma unroll
-                for (int j = 0; j < 64; ++j) {
-                    const int cc = hh * 64 + j;
+                for (int j = 0; j < SC; ++j) {
+                    const int cc = hh * SC + j;
                     float v = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
                     v = (cc <= row) ? v : 0.f;
                     if constexpr (TR) v = tf32r(v);
@@ -536,14 +620,11 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 }
                 const uint32_t tpart = kBF16 ? tS + lane_off + 64 : tmem + 384 + lane_off;
                 if constexpr (kBF16) {
-                    uint32_t pk[32];
+                    uint32_t pk[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        pk[j] = pack_bf16(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
-                        pk[16 + j] = pack_bf16(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]));
-                    }
-                    named_bar_sync(1, kMathThreads);
-                    tmem_st32(tS + lane_off + hh * 32, pk);
+                    for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
+                    named_bar_sync(1, NM);
+                    tmem_st16(tS + lane_off + hh * 16, pk);
                 } else {
                     tmem_st32(tS + lane_off + hh * 64, r0);
                     tmem_st32(tS + lane_off + hh * 64 + 32, r1);
@@ -551,7 +632,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 if constexpr (NORM) {
                     asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart + hh),
                                  "r"(__float_as_uint(rs)) : "memory");
-                    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart + 2 + hh),
+                    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tpart + NQ + hh),
                                  "r"(__float_as_uint(qz)) : "memory");
                 }
                 tmem_wait_st();
@@ -565,7 +646,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
             tc_fence_after();
             {
                 const int kr = srow < D ? srow : 0;
-                const float f = __expf(sGe[kr] - sR[kr]);
+                const float f = sEG[kr];
 #pragma unroll
                 for (int cb = 0; cb < DH / 32; ++cb) {
                     uint32_t rr[32];
@@ -578,7 +659,7 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 tmem_wait_st();
                 if constexpr (NORM) {
                     if (tid < D) {
-                        sZ[tid] = __expf(sGe[tid] - sR[tid]) * (sZP[tid] + sZC[tid]);
+                        sZ[tid] = sEG[tid] * (sZP[tid] + sZC[tid]);
                         sZC[tid] = 0.f;
                     }
                 }
@@ -588,49 +669,69 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
                 float inv = 1.f;
                 if constexpr (NORM) {
                     const uint32_t tpart = kBF16 ? tS + lane_off + 64 : tmem + 384 + lane_off;
-                    uint32_t pr[4];
-                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                                 : "=r"(pr[0]), "=r"(pr[1]), "=r"(pr[2]), "=r"(pr[3]) : "r"(tpart));
+                    uint32_t pr[8];
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                 : "=r"(pr[0]), "=r"(pr[1]), "=r"(pr[2]), "=r"(pr[3]), "=r"(pr[4]), "=r"(pr[5]),
+                                   "=r"(pr[6]), "=r"(pr[7]) : "r"(tpart));
                     tmem_wait_ld();
-                    const float den = __uint_as_float(pr[0]) + __uint_as_float(pr[1]) +
-                                      __uint_as_float(pr[2]) + __uint_as_float(pr[3]);
+                    float den = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 2 * NQ; ++i) den += __uint_as_float(pr[i]);
                     if (fabsf(den) < 1e-12f && row < nvalid) atomicOr(&p.err[0], 1);
                     inv = 1.f / den;
                 }
-                const bool vrow = row < nvalid;
-                T* dst = obase + (((size_t)b * p.Nstride + t0 + (vrow ? row : 0)) * p.H + h) * D + hh * DH;
-#pragma unroll
-                for (int cb = 0; cb < DH / 32; ++cb) {
+                // bf16: stage O (this thread's 32 columns of its row); one TMA bulk tensor store
+                // per chunk (rows past the sequence end are clipped).  tf32 (no smem left for a
+                // staging tile): direct row stores.
+                if constexpr (!kBF16) {
                     uint32_t rr[32];
-                    tmem_ld32(tO + lane_off + hh * DH + cb * 32, rr);
+                    tmem_ld32(tO + lane_off + hh * DH, rr);
                     tmem_wait_ld();
-                    if (vrow) {
+                    if (row < nvalid) {
+                        T* dst = reinterpret_cast<T*>(p.o) + (((size_t)b * p.Nstride + t0 + row) * p.H + h) * D + hh * DH;
+#pragma unroll
+                        for (int ch = 0; ch < 8; ++ch)
+                            *reinterpret_cast<float4*>(dst + ch * 4) =
+                                make_float4(__uint_as_float(rr[ch * 4]) * inv, __uint_as_float(rr[ch * 4 + 1]) * inv,
+                                            __uint_as_float(rr[ch * 4 + 2]) * inv, __uint_as_float(rr[ch * 4 + 3]) * inv);
+                    }
+                } else {
+                    uint32_t rr[32];
+                    tmem_ld32(tO + lane_off + hh * DH, rr);
+                    tmem_wait_ld();
+                    constexpr int CPT = DH / TT::EPC;  // 16-byte chunks per thread
+#pragma unroll
+                    for (int ch = 0; ch < CPT; ++ch) {
+                        uint4 v;
                         if constexpr (kBF16) {
-#pragma unroll
-                            for (int ch = 0; ch < 4; ++ch) {
-                                uint4 v;
-                                v.x = pack_bf16(__uint_as_float(rr[ch * 8 + 0]) * inv, __uint_as_float(rr[ch * 8 + 1]) * inv);
-                                v.y = pack_bf16(__uint_as_float(rr[ch * 8 + 2]) * inv, __uint_as_float(rr[ch * 8 + 3]) * inv);
-                                v.z = pack_bf16(__uint_as_float(rr[ch * 8 + 4]) * inv, __uint_as_float(rr[ch * 8 + 5]) * inv);
-                                v.w = pack_bf16(__uint_as_float(rr[ch * 8 + 6]) * inv, __uint_as_float(rr[ch * 8 + 7]) * inv);
-                                *reinterpret_cast<uint4*>(dst + cb * 32 + ch * 8) = v;
-                            }
+                            v.x = pack_bf16(__uint_as_float(rr[ch * 8 + 0]) * inv, __uint_as_float(rr[ch * 8 + 1]) * inv);
+                            v.y = pack_bf16(__uint_as_float(rr[ch * 8 + 2]) * inv, __uint_as_float(rr[ch * 8 + 3]) * inv);
+                            v.z = pack_bf16(__uint_as_float(rr[ch * 8 + 4]) * inv, __uint_as_float(rr[ch * 8 + 5]) * inv);
+                            v.w = pack_bf16(__uint_as_float(rr[ch * 8 + 6]) * inv, __uint_as_float(rr[ch * 8 + 7]) * inv);
                         } else {
-#pragma unroll
-                            for (int ch = 0; ch < 8; ++ch)
-                                *reinterpret_cast<float4*>(dst + cb * 32 + ch * 4) =
-                                    make_float4(__uint_as_float(rr[ch * 4]) * inv, __uint_as_float(rr[ch * 4 + 1]) * inv,
-                                                __uint_as_float(rr[ch * 4 + 2]) * inv, __uint_as_float(rr[ch * 4 + 3]) * inv);
+                            v = make_uint4(__float_as_uint(__uint_as_float(rr[ch * 4]) * inv),
+                                           __float_as_uint(__uint_as_float(rr[ch * 4 + 1]) * inv),
+                                           __float_as_uint(__uint_as_float(rr[ch * 4 + 2]) * inv),
+                                           __float_as_uint(__uint_as_float(rr[ch * 4 + 3]) * inv));
                         }
+                        const int cgi = hh * CPT + ch;
+                        *reinterpret_cast<uint4*>(ostg + (cgi >> 3) * kBlockBytes + sw128_off(row, cgi & 7)) = v;
                     }
                 }
                 tc_fence_before();
+                fence_proxy_async_smem();
             }
             if (tid == 0) trace_mark(p, c, 7);
-            named_bar_sync(1, kMathThreads);  // everyone done with this chunk's tiles and sZ
+            named_bar_sync(1, NM);  // everyone done with this chunk's tiles and sZ; O staged
+            if (kBF16 && tid == 0) {
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) tma_store_4d(&tmO, ostg + blk * kBlockBytes, blk * TT::EPB, h, t0, b);
+                bulk_commit();
+            }
             if (tid == 0) trace_mark(p, c, 8);
         }
     }
+    if (threadIdx.x == 128) bulk_wait0();  // smem must outlive the last O store
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<512>(tmem);
@@ -639,8 +740,9 @@ __global__ void __launch_bounds__(kOutputPassThreads, 1)
 template <typename T>
 constexpr int output_pass_vec_smem() {
     using TT = TileTraits<T>;
-    // + sTot [16][D], sR, sGe, sG0, sZ, sZP, sZC + 6 barriers + TMEM slot
-    return 4 * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + TT::MOP_BYTES + (16 + 6) * TT::D * 4 + 128;
+    // + group offsets 2 x [RG][D], sER, sEG, sZ, sZP, sZC + 6 barriers + TMEM slot
+    return (sizeof(T) == 2 ? 5 : 4) * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + TT::MOP_BYTES +
+           (2 * (vec_math_threads<T>() / 16) + 5) * TT::D * 4 + 128;
 }
 template <typename T>
 constexpr int state_pass_vec_smem() {

@@ -38,12 +38,12 @@ __device__ __forceinline__ float log_sigmoid_fast(float x) {
 }
 __device__ __forceinline__ float sigmoid_fast(float x) { return rcp_ftz(1.f + fast_exp(-x)); }
 
-template <typename T>
+template <typename T, int NT = kVecNT>
 struct VecLayout {
     static constexpr int EPC = TileTraits<T>::EPC;  // columns per 16-byte chunk
     static constexpr int D = TileTraits<T>::D;      // 16 chunks per row
-    static constexpr int RG = kVecNT / 16;          // row groups
-    static constexpr int R = kC / RG;               // rows per thread (8)
+    static constexpr int RG = NT / 16;              // row groups
+    static constexpr int R = kC / RG;               // rows per thread (8 at NT = 256)
 };
 
 // EPC consecutive values of (row, chunk cg) of a two-block SW128 tile
@@ -77,18 +77,29 @@ __device__ __forceinline__ void st_chunk(uint8_t* tile, int row, int cg, const f
     *reinterpret_cast<uint4*>(tile + (cg >> 3) * kBlockBytes + sw128_off(row, cg & 7)) = u;
 }
 
+// fp32 tiles: store without the tf32 rounding (intermediates that are rounded later)
+template <typename T>
+__device__ __forceinline__ void st_chunk_raw(uint8_t* tile, int row, int cg, const float (&x)[TileTraits<T>::EPC]) {
+    if constexpr (sizeof(T) == 2) {
+        st_chunk<T>(tile, row, cg, x);
+    } else {
+        *reinterpret_cast<uint4*>(tile + (cg >> 3) * kBlockBytes + sw128_off(row, cg & 7)) =
+            make_uint4(__float_as_uint(x[0]), __float_as_uint(x[1]), __float_as_uint(x[2]), __float_as_uint(x[3]));
+    }
+}
+
 // Inclusive chunk-local log-decay G[ii][j] (row rg*R+ii, column cg*EPC+j) from the gate tile
 // `at` (la = log sigmoid(a) on valid rows, 0 beyond nvalid).  Also, per column:
 //   sR[c]  = G at row 63 (the midpoint reference), sGe[c] = G at the chunk end,
 //   sG0[c] = G at row 0 (range check of the midpoint split),
 //   sCar[c] = the caller's running carry before this chunk; carry += G_end afterwards
 //   (only threads tid < D hold a meaningful `carry`).
-// sTot: [RG][D] scratch.  Two named barriers (id 1, kVecNT threads).
-template <typename T>
+// sTot: [RG][D] scratch.  Two named barriers (id 1, NT threads).
+template <typename T, int NT = kVecNT>
 __device__ __forceinline__ void vec_log_scan(const uint8_t* at, int nvalid, int tid,
-                                             float (&G)[VecLayout<T>::R][VecLayout<T>::EPC], float* sTot,
+                                             float (&G)[VecLayout<T, NT>::R][VecLayout<T, NT>::EPC], float* sTot,
                                              float* sR, float* sGe, float* sG0, float* sCar, float& carry) {
-    using L = VecLayout<T>;
+    using L = VecLayout<T, NT>;
     const int cg = tid & 15, rg = tid >> 4;
     float run[L::EPC];
 #pragma unroll
@@ -111,7 +122,7 @@ __device__ __forceinline__ void vec_log_scan(const uint8_t* at, int nvalid, int 
 #pragma unroll
         for (int j = 0; j < L::EPC; ++j) sG0[cg * L::EPC + j] = G[0][j];
     }
-    named_bar_sync(1, kVecNT);
+    named_bar_sync(1, NT);
     if (tid < L::D) {
         float acc = 0.f, r = 0.f;
 #pragma unroll
@@ -126,7 +137,7 @@ __device__ __forceinline__ void vec_log_scan(const uint8_t* at, int nvalid, int 
         if (sCar) sCar[tid] = carry;
         carry += acc;
     }
-    named_bar_sync(1, kVecNT);
+    named_bar_sync(1, NT);
 #pragma unroll
     for (int j = 0; j < L::EPC; ++j) {
         const float off = sTot[rg * L::D + cg * L::EPC + j];
