@@ -272,19 +272,20 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
     constexpr int DH = D / NQ;    // state / O columns per thread (32)
     static_assert(DH == 32, "row-layout phases assume 32 columns per thread");
     using L = VecLayout<T, NM>;
-    constexpr int STAGE = 4 * kTileBytes;     // Q | K | V | A
+    // Gate tiles are double-buffered for bf16 (the next one loads while this chunk runs, so
+    // its scan overlaps the Q / K / V loads); each gate buffer then holds its chunk's state
+    // operand M' (dead gate tile), freed by the QM GEMM.
+    constexpr int NAB = kBF16 ? 2 : 1;
     extern __shared__ __align__(1024) uint8_t smem[];
     if (smem_u32(smem) & 1023) __trap();
     uint8_t* qt = smem;
     uint8_t* kt = qt + kTileBytes;
     uint8_t* vt = qt + 2 * kTileBytes;
-    uint8_t* at = qt + 3 * kTileBytes;
-    uint8_t* kT = qt + STAGE;
+    uint8_t* abase = qt + 3 * kTileBytes;
+    uint8_t* kT = abase + NAB * kTileBytes;
     uint8_t* vT = kT + (TR ? kTileBytes : 0);
     uint8_t* ostg = vT + (TR ? kTileBytes : 0);  // bf16: O staging for the bulk tensor store
-    uint8_t* mop = ostg + (kBF16 ? kTileBytes : 0);
-    float* sOffE = reinterpret_cast<float*>(mop + TT::MOP_BYTES);  // [RG][D] group factor offsets
-    float* sOffI = sOffE + L::RG * D;                               // [RG][D] (reciprocals)
+    float* sOffI = reinterpret_cast<float*>(ostg + (kBF16 ? kTileBytes : 0));  // [RG][D] group factors
     float* sER = sOffI + L::RG * D;                                 // [D] e^{r} = prod sigma rows < 64
     float* sEG = sER + D;                                           // [D] e^{G_end - r} = prod rows >= 64
     float* sZ = sEG + D;                                            // [D]
@@ -297,7 +298,10 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
     uint64_t* s_full = bars + 3;
     uint64_t* p_full = bars + 4;
     uint64_t* mo_full = bars + 5;
-    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 6);
+    uint64_t* a_full = bars + 6;  // [NAB]
+    uint64_t* a_free = bars + 8;  // [NAB]
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 10);
+    auto abuf = [&](int c) { return abase + (c % NAB) * kTileBytes; };
 
     const int seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int bh = b * p.H + h;
@@ -313,6 +317,7 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
         mbar_init(s_full, 1);
         mbar_init(p_full, NM);
         mbar_init(mo_full, 1);
+        for (int i = 0; i < NAB; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_free[i], 1); }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(sTmem);
@@ -326,16 +331,21 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
         if (lane == 0) {
             tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmA);
             for (int c = 0; c < nchunks; ++c) {
+                const int t0 = t_begin + c * kC;
+                const int ab = c % NAB;
+                if (c >= NAB) mbar_wait(&a_free[ab], ((c / NAB) - 1) & 1);  // M'(c - NAB) consumed
+                mbar_expect_tx(&a_full[ab], kTileBytes);
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk)
+                    tma_load_4d(abuf(c) + blk * kBlockBytes, &tmA, &a_full[ab], blk * TT::EPB, h, t0, b);
                 if (c >= 1) mbar_wait(empty, (c - 1) & 1);
                 trace_mark(p, c, 10);
-                const int t0 = t_begin + c * kC;
-                mbar_expect_tx(full, STAGE);
+                mbar_expect_tx(full, 3 * kTileBytes);
 #pragma unroll
                 for (int blk = 0; blk < 2; ++blk) {
                     tma_load_4d(qt + blk * kBlockBytes, &tmQ, full, blk * TT::EPB, h, t0, b);
                     tma_load_4d(kt + blk * kBlockBytes, &tmK, full, blk * TT::EPB, h, t0, b);
                     tma_load_4d(vt + blk * kBlockBytes, &tmV, full, blk * TT::EPB, h, t0, b);
-                    tma_load_4d(at + blk * kBlockBytes, &tmA, full, blk * TT::EPB, h, t0, b);
                 }
             }
         }
@@ -346,8 +356,9 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
             constexpr uint32_t idQM = umma_idesc(TT::FMT, 0, TR ? 0 : 1, 128, D);
             constexpr uint32_t idDM = TR ? umma_idesc(TT::FMT, 0, 0, 64, D) : umma_idesc(TT::FMT, 1, 1, 128, D);
             const uint32_t qa = smem_u32(qt), ka = smem_u32(kt), va = smem_u32(vt);
-            const uint32_t mb = smem_u32(mop), kTa = smem_u32(kT), vTa = smem_u32(vT);
+            const uint32_t kTa = smem_u32(kT), vTa = smem_u32(vT);
             for (int c = 0; c < nchunks; ++c) {
+                const uint32_t mb = smem_u32(abuf(c));  // M' lives in this chunk's gate buffer
                 mbar_wait(full, c & 1);
                 mbar_wait(xf, c & 1);
                 tc_fence_after();
@@ -377,6 +388,7 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
                         mma_ss_tf32(tM, umma_desc_sw128(kTa + off, 16, 1024), umma_desc_sw128(vTa + off, 16, 1024), idDM, 1u);
                     }
                 }
+                mma_commit(&a_free[c % NAB]);
                 mbar_wait(p_full, c & 1);
                 tc_fence_after();
 #pragma unroll
@@ -420,7 +432,10 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
         for (int c = 0; c < nchunks; ++c) {
             const int t0 = t_begin + c * kC;
             const int nvalid = min(kC, t_end - t0);
-            mbar_wait(full, c & 1);
+            uint8_t* at = abuf(c);
+            uint8_t* mop = at;
+            mbar_wait(&a_full[c % NAB], (c / NAB) & 1);
+            if constexpr (HG) mbar_wait(full, c & 1);  // keff = 1 - sigma(a) is written into K
             if (tid == 0) trace_mark(p, c, 0);
             // (1)+(2) 2-D column scan (lsm_vec_scan.cuh), then in place q~ = phi(q) e^{G - r},
             // k~ = keff e^{r - G} (tf32: also the K-major K~^T, V^T tiles)
@@ -454,23 +469,22 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
                     if constexpr (HG) st_chunk_raw<T>(kt, i, cg, keff);  // k is unused by HGRN2
                 }
 #pragma unroll
-                for (int j = 0; j < L::EPC; ++j) sOffE[rg * D + cg * L::EPC + j] = tot[j];
+                for (int j = 0; j < L::EPC; ++j) sOffI[rg * D + cg * L::EPC + j] = tot[j];
                 named_bar_sync(1, NM);
                 if (tid < D) {
-                    // first half: exclusive suffix over the later groups below the midpoint
+                    // per group, the factor 1/E of the row just past it (Einv offsets):
+                    // first half, exclusive suffix of sigma over the later groups below the midpoint
                     float sfx = 1.f;
                     for (int g = HALF - 1; g >= 0; --g) {
-                        const float pg = sOffE[g * D + tid];
+                        const float pg = sOffI[g * D + tid];
                         sOffI[g * D + tid] = sfx;
-                        sOffE[g * D + tid] = rcp_ftz(sfx);
                         sfx *= pg;
                     }
                     sER[tid] = sfx;
-                    // second half: exclusive prefix from the midpoint
+                    // second half, 1 / (exclusive prefix of sigma from the midpoint)
                     float pfx = 1.f;
                     for (int g = HALF; g < L::RG; ++g) {
-                        const float pg = sOffE[g * D + tid];
-                        sOffE[g * D + tid] = pfx;
+                        const float pg = sOffI[g * D + tid];
                         sOffI[g * D + tid] = rcp_ftz(pfx);
                         pfx *= pg;
                     }
@@ -478,11 +492,12 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
                 }
                 named_bar_sync(1, NM);
                 if (tid == 0) trace_mark(p, c, 1);
+                if constexpr (!HG) mbar_wait(full, c & 1);
                 float E[L::EPC], Ei[L::EPC];
 #pragma unroll
                 for (int j = 0; j < L::EPC; ++j) {
-                    E[j] = sOffE[rg * D + cg * L::EPC + j];
                     Ei[j] = sOffI[rg * D + cg * L::EPC + j];
+                    E[j] = rcp_ftz(Ei[j]);
                 }
                 float zc[L::EPC];
 #pragma unroll
@@ -741,8 +756,10 @@ template <typename T>
 constexpr int output_pass_vec_smem() {
     using TT = TileTraits<T>;
     // + group offsets 2 x [RG][D], sER, sEG, sZ, sZP, sZC + 6 barriers + TMEM slot
-    return (sizeof(T) == 2 ? 5 : 4) * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) + TT::MOP_BYTES +
-           (2 * (vec_math_threads<T>() / 16) + 5) * TT::D * 4 + 128;
+    // Q | K | V | NAB gate / M' buffers (| tf32 K~^T, V^T) (| bf16 O staging) + group factors
+    // [RG][D] + sER, sEG, sZ, sZP, sZC + 10 barriers + TMEM slot
+    return (sizeof(T) == 2 ? 6 : 4) * kTileBytes + (TT::kTransposed ? 2 * kTileBytes : 0) +
+           ((vec_math_threads<T>() / 16) + 5) * TT::D * 4 + 128;
 }
 template <typename T>
 constexpr int state_pass_vec_smem() {
