@@ -79,14 +79,42 @@ struct DgateSmem {
     static constexpr int kMT = D * D * (int)sizeof(T);  // state tile bytes
     static constexpr int kQ = 0, kK = kTileBytes, kV = 2 * kTileBytes, kO = 3 * kTileBytes;
     static constexpr int kM = 4 * kTileBytes, kDM = kM + kMT;
-    static constexpr int kMisc = kDM + kMT;  // sG, sKf, sX, sY, sR, scratch, barriers
-    static constexpr int kTotal = kMisc + 6 * 128 * 4 + 64;
+    static constexpr int kMisc = kDM + kMT;  // sG, sKf, 5 x [2][128] partials, scratch, barriers
+    static constexpr int kTotal = kMisc + (2 + 5 * 4) * 128 * 4 + 32 * 4 + 64;
 };
 
 }  // namespace
 
+// kDgNH x 128 threads: warp w owns TMEM lane quadrant w % 4 (query rows) and column part
+// w / 4 of every row-wise phase; the 128-entry scans run on warps 0-3 (named barrier 1).
+constexpr int kDgNH = 4;
+constexpr int kDgThreads = 128 * kDgNH;
+
+// 128-thread inclusive prefix sum over warps 0-3 (named barrier 1); `ws` holds 4 floats
+__device__ __forceinline__ float scan128_w03(float x, float* ws) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    named_bar_sync(1, 128);
+    if (lane == 31) ws[warp] = x;
+    named_bar_sync(1, 128);
+    for (int i = 0; i < warp; ++i) x += ws[i];
+    return x;
+}
+__device__ __forceinline__ float sum128_w03(float x, float* ws) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    named_bar_sync(1, 128);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = x;
+    named_bar_sync(1, 128);
+    return ws[0] + ws[1] + ws[2] + ws[3];
+}
+
 template <typename T>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kDgThreads, 1)
     lsm_mamba_dgate(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmDM,
@@ -100,11 +128,14 @@ __global__ void __launch_bounds__(128, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     float* sG = reinterpret_cast<float*>(smem + L::kMisc);
     float* sKf = sG + 128;
-    float* sX = sKf + 128;
-    float* sY = sX + 128;
-    float* sR = sY + 128;
-    float* ws = sR + 128;  // 128 floats scratch
-    uint64_t* bar = reinterpret_cast<uint64_t*>(ws + 128);
+    constexpr int NH = kDgNH;
+    float* sX = sKf + 128;   // [NH][128] row-part partials: X, Y, row sums, column sums, dkf
+    float* sY = sX + NH * 128;
+    float* sR = sY + NH * 128;
+    float* sC = sR + NH * 128;
+    float* sF = sC + NH * 128;
+    float* ws = sF + NH * 128;  // 32 floats scratch
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ws + 32);
     uint64_t* mma_done = bar + 1;
     uint32_t* sTmem = reinterpret_cast<uint32_t*>(bar + 2);
 
@@ -113,6 +144,10 @@ __global__ void __launch_bounds__(128, 1)
     const int t0 = c * kC;
     const int nvalid = min(kC, N - t0);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int t = (warp & 3) * 32 + lane;  // TMEM lane == query row t
+    const int hc = warp >> 2;              // column part of the row-wise phases
+    constexpr int PW = D / NH;             // state columns per thread (bf16 32, tf32 16)
+    constexpr int SW = 128 / NH;           // S / dP columns (and A rows) per thread
 
     if (tid == 0) {
         mbar_init(bar, 1);
@@ -140,15 +175,39 @@ __global__ void __launch_bounds__(128, 1)
     }
     // gates while the tiles land: g_t = -softplus(b_t) softplus(a_h), kf_t = softplus(b_t)
     const float spa = softplus_f(a_raw[h]);
-    float bv = 0.f, kf = 0.f, gl = 0.f;
-    if (tid < nvalid) {
-        bv = b_pre[((size_t)b * N + t0 + tid) * H + h];
+    float bv = 0.f, kf = 0.f;
+    if (t < nvalid) {
+        bv = b_pre[((size_t)b * N + t0 + t) * H + h];
         kf = softplus_f(bv);
-        gl = -kf * spa;
     }
-    const float G = block_incl_scan128(gl, ws);
-    sG[tid] = G;
-    sKf[tid] = kf;
+    // dkf_t = phi(k_t) . dkeff_t: given, or from dk = kf dkeff (identity feature map); the
+    // global dk row is read before the tiles are needed (latency overlaps the TMA loads)
+    float dkrow[PW];
+    const bool dk_direct = dkf == nullptr;
+    if (dk_direct && t < nvalid) {
+        const T* dkr = dk + (((size_t)b * N + t0 + t) * H + h) * D + hc * PW;
+        if constexpr (sizeof(T) == 2) {
+#pragma unroll
+            for (int j = 0; j < PW; j += 8) {
+                const uint4 u = *reinterpret_cast<const uint4*>(dkr + j);
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = unpack_bf16(w[e]);
+                    dkrow[j + 2 * e] = f.x;
+                    dkrow[j + 2 * e + 1] = f.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < PW; ++j) dkrow[j] = dkr[j];
+        }
+    }
+    if (warp < 4) {
+        const float G = scan128_w03(t < nvalid ? -kf * spa : 0.f, ws);
+        sG[t] = G;
+        sKf[t] = kf;
+    }
     if (tid == 0) {
         mbar_wait(bar, 0);
         tc_fence_after();
@@ -180,15 +239,14 @@ __global__ void __launch_bounds__(128, 1)
     }
     __syncthreads();  // sG / sKf visible
     const float gend = sG[127];
-    // B_c partial: <M_c, dM_c> over this thread's slice of the (identically laid out) tiles
+    // B_c partial: <M_c, dM_c> over this thread's 16-byte slices of the (identically laid out) tiles
     float bpart = 0.f;
     {
-        // 16-byte slices interleaved across the threads (a warp reads 512 contiguous bytes)
         const uint8_t* pm = smem + L::kM + tid * 16;
         const uint8_t* pd = smem + L::kDM + tid * 16;
         mbar_wait(bar, 0);
 #pragma unroll 4
-        for (int i = 0; i < L::kMT; i += 128 * 16) {
+        for (int i = 0; i < L::kMT; i += kDgThreads * 16) {
             const uint4 a = *reinterpret_cast<const uint4*>(pm + i);
             const uint4 d = *reinterpret_cast<const uint4*>(pd + i);
             const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, dw[4] = {d.x, d.y, d.z, d.w};
@@ -203,103 +261,145 @@ __global__ void __launch_bounds__(128, 1)
             }
         }
     }
+    // dkf_t partial from this half of the K row
+    float dkf_part = 0.f;
+    if (dk_direct && t < nvalid) {
+        float vk[32];
+        tile_row32<T>(smem + L::kK, kBlockBytes, t, (hc * PW) & ~31, vk);
+#pragma unroll
+        for (int j = 0; j < PW; ++j) dkf_part += vk[j] * dkrow[j];
+        if (PW == 16 && (hc & 1)) {  // odd parts: the upper 16 of the 32 loaded columns
+            dkf_part = 0.f;
+#pragma unroll
+            for (int j = 0; j < PW; ++j) dkf_part += vk[(16 + j) & 31] * dkrow[j];
+        }
+    }
     mbar_wait(mma_done, 0);
     tc_fence_after();
-    const uint32_t lo = (uint32_t)(warp * 32) << 16;
-    const int t = tid;  // TMEM lane == query row t
-    // X_t, Y_t from Z, W rows against dO / V rows (smem)
+    const uint32_t lo = (uint32_t)((warp & 3) * 32) << 16;
+    // X_t, Y_t partials from this half of the Z, W rows against dO / V rows (smem)
     float xs = 0.f, ys = 0.f;
-#pragma unroll
-    for (int cb = 0; cb < D / 32; ++cb) {
+    {
+        static_assert(PW == 32 || PW == 16, "state columns per thread");
+        const int col = hc * PW;
         uint32_t rz[32], rw[32];
-        tmem_ld32(tmem + 256 + lo + cb * 32, rz);
-        tmem_ld32(tmem + 384 + lo + cb * 32, rw);
+        if constexpr (PW == 32) {
+            tmem_ld32(tmem + 256 + lo + col, rz);
+            tmem_ld32(tmem + 384 + lo + col, rw);
+        } else {
+            uint32_t z16[16], w16[16];
+            tmem_ld16(tmem + 256 + lo + col, z16);
+            tmem_ld16(tmem + 384 + lo + col, w16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) { rz[j] = z16[j]; rw[j] = w16[j]; }
+        }
         tmem_wait_ld();
         float vo[32], vv[32];
-        tile_row32<T>(smem + L::kO, kBlockBytes, t, cb * 32, vo);
-        tile_row32<T>(smem + L::kV, kBlockBytes, t, cb * 32, vv);
+        tile_row32<T>(smem + L::kO, kBlockBytes, t, col & ~31, vo);
+        tile_row32<T>(smem + L::kV, kBlockBytes, t, col & ~31, vv);
+        // static register indices (PW == 16: odd parts read the upper half of the 32 loaded)
+        if (PW == 32 || (hc & 1) == 0) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            xs += __uint_as_float(rz[j]) * vo[j];
-            ys += __uint_as_float(rw[j]) * vv[j];
-        }
-    }
-    const float Gt = sG[t];
-    // dkf_t = phi(k_t) . dkeff_t: given, or from dk = kf dkeff (identity feature map)
-    float dkf_t = 0.f;
-    if (t < nvalid) {
-        if (dkf != nullptr) {
-            dkf_t = dkf[(size_t)bh * N + t0 + t];
-        } else {
-            const T* dkr = dk + (((size_t)b * N + t0 + t) * H + h) * D;
-            float acc = 0.f;
-#pragma unroll
-            for (int cb = 0; cb < D / 32; ++cb) {
-                float vk[32];
-                tile_row32<T>(smem + L::kK, kBlockBytes, t, cb * 32, vk);
-#pragma unroll
-                for (int j = 0; j < 32; j += 8) {
-                    if constexpr (sizeof(T) == 2) {
-                        const uint4 u = *reinterpret_cast<const uint4*>(dkr + cb * 32 + j);
-                        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 f = unpack_bf16(w[e]);
-                            acc += vk[j + 2 * e] * f.x + vk[j + 2 * e + 1] * f.y;
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) acc += vk[j + e] * dkr[cb * 32 + j + e];
-                    }
-                }
+            for (int j = 0; j < PW; ++j) {
+                xs += __uint_as_float(rz[j]) * vo[j];
+                ys += __uint_as_float(rw[j]) * vv[j];
             }
-            dkf_t = acc / kf;
+        } else {
+#pragma unroll
+            for (int j = 0; j < PW; ++j) {
+                xs += __uint_as_float(rz[j]) * vo[(16 + j) & 31];
+                ys += __uint_as_float(rw[j]) * vv[(16 + j) & 31];
+            }
         }
     }
-    const float X = t < nvalid ? __expf(Gt) * xs : 0.f;
-    const float Y = t < nvalid ? __expf(gend - Gt) * sKf[t] * ys : 0.f;
+    sX[hc * 128 + t] = xs;
+    sY[hc * 128 + t] = ys;
+    sF[hc * 128 + t] = dkf_part;
+    const float Gt = sG[t];
     __syncthreads();  // all MMAs consumed Q/K (mma_done) and all threads past their tile reads
-    // (the K rows above are read before this barrier; As overwrites the Q / K tiles below)
-    // strictly lower A_ts = S_ts kf_s dP_ts e^{G_t - G_s} (s < t): row sums here, rows to
-    // shared memory (XOR-swizzled by t) for the column sums
+    // strictly lower A_ts = S_ts kf_s dP_ts e^{G_t - G_s} (s < t), this thread's 64 columns:
+    // row sums here, rows to shared memory (XOR-swizzled by t) for the column sums
     float* As = reinterpret_cast<float*>(smem + L::kQ);  // 128 x 128 fp32 over the Q, K tiles
     float rsum = 0.f;
 #pragma unroll
-    for (int cb = 0; cb < 4; ++cb) {
+    for (int cb = 0; cb < SW / 32; ++cb) {
+        const int s0 = hc * SW + cb * 32;
         uint32_t rs[32], rp[32];
-        tmem_ld32(tmem + lo + cb * 32, rs);
-        tmem_ld32(tmem + 128 + lo + cb * 32, rp);
+        tmem_ld32(tmem + lo + s0, rs);
+        tmem_ld32(tmem + 128 + lo + s0, rp);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            const int s = cb * 32 + j;
+            const int s = s0 + j;
             float a = 0.f;
             if (s < t) a = __uint_as_float(rs[j]) * __uint_as_float(rp[j]) * sKf[s] * __expf(Gt - sG[s]);
             rsum += a;
             As[t * 128 + (s ^ (t & 31))] = a;
         }
     }
+    sR[hc * 128 + t] = rsum;
     __syncthreads();
-    float csum = 0.f;  // column t: sum over rows r > t
-    for (int r = t + 1; r < 128; ++r) csum += As[r * 128 + (t ^ (r & 31))];
-    // dg_t = C(t) + sum_{u >= t} X_u + sum_{s < t} Y_s + e^{g_c} <M_c, dM_c>
-    const float Bc = __expf(gend) * block_sum128(bpart, ws);
-    const float dlt = csum - rsum;
-    const float Cin = block_incl_scan128(dlt, ws) - dlt;    // exclusive prefix
-    const float Xin = block_incl_scan128(X, ws);
-    const float Xtot = block_sum128(X, ws);
-    const float Xsuf = Xtot - Xin + X;
-    const float Yin = block_incl_scan128(Y, ws);
-    const float Ypre = Yin - Y;
-    const float dg = Cin + Xsuf + Ypre + Bc;
-    float dr = 0.f;
-    if (t < nvalid) {
-        const size_t row = ((size_t)b * N + t0 + t) * H + h;
-        db_pre[row] = sigm(bv) * (dkf_t - spa * dg);
-        dr = dg * -kf;
+    // column t over rows r > t, this thread's half of the rows; four independent accumulators
+    // so the shared-memory loads pipeline (rows r <= t are zero in the strictly lower A)
+    {
+        float c4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int rr = 0; rr < SW; rr += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = hc * SW + rr + u;
+                c4[u] += As[r * 128 + (t ^ (r & 31))];
+            }
+        }
+        sC[hc * 128 + t] = (c4[0] + c4[1]) + (c4[2] + c4[3]);
     }
-    dr = block_sum128(dr, ws);
-    if (tid == 0) atomicAdd(da_raw + h, dr * sigm(a_raw[h]));
+    __syncthreads();
+    if (warp < 4) {
+        float xsum = 0.f, ysum = 0.f, rs = 0.f, cs = 0.f;
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+            xsum += sX[i * 128 + t]; ysum += sY[i * 128 + t];
+            rs += sR[i * 128 + t]; cs += sC[i * 128 + t];
+        }
+        const float X = t < nvalid ? __expf(Gt) * xsum : 0.f;
+        const float Y = t < nvalid ? __expf(gend - Gt) * sKf[t] * ysum : 0.f;
+        // dg_t = C(t) + sum_{u >= t} X_u + sum_{s < t} Y_s + e^{g_c} <M_c, dM_c>
+        const float dlt = cs - rs;
+        const float Cin = scan128_w03(dlt, ws) - dlt;    // exclusive prefix
+        const float Xin = scan128_w03(X, ws);
+        const float Xtot = sum128_w03(X, ws);
+        const float Xsuf = Xtot - Xin + X;
+        const float Yin = scan128_w03(Y, ws);
+        const float Ypre = Yin - Y;
+        sX[t] = Cin + Xsuf + Ypre;  // dg without the boundary term
+    }
+    // boundary term over all 256 threads
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bpart += __shfl_xor_sync(0xFFFFFFFFu, bpart, o);
+    if (lane == 0) ws[8 + warp] = bpart;
+    __syncthreads();
+    if (warp < 4) {
+        float Bc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4 * NH; ++i) Bc += ws[8 + i];
+        Bc *= __expf(gend);
+        const float dg = sX[t] + Bc;
+        float dkf_t = 0.f;
+        if (t < nvalid) {
+            float f = 0.f;
+#pragma unroll
+            for (int i = 0; i < NH; ++i) f += sF[i * 128 + t];
+            dkf_t = dk_direct ? f / kf : dkf[(size_t)bh * N + t0 + t];
+        }
+        float dr = 0.f;
+        if (t < nvalid) {
+            const size_t row = ((size_t)b * N + t0 + t) * H + h;
+            db_pre[row] = sigm(bv) * (dkf_t - spa * dg);
+            dr = dg * -kf;
+        }
+        dr = sum128_w03(dr, ws);
+        if (tid == 0) atomicAdd(da_raw + h, dr * sigm(a_raw[h]));
+    }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<512>(tmem);
@@ -320,7 +420,7 @@ static cudaError_t dgate_t(const CUtensorMap& q, const CUtensorMap& k, const CUt
     const int nchunk = (N + kC - 1) / kC;
     cudaError_t e = cudaMemsetAsync(da_raw, 0, sizeof(float) * H, st);
     if (e != cudaSuccess) return e;
-    lsm_mamba_dgate<T><<<dim3(nchunk, B * H), 128, smem, st>>>(q, k, v, dO, m, dm, b_pre, a_raw, dkf,
+    lsm_mamba_dgate<T><<<dim3(nchunk, B * H), kDgThreads, smem, st>>>(q, k, v, dO, m, dm, b_pre, a_raw, dkf,
                                                                 static_cast<const T*>(dk), db_pre, da_raw, N, H,
                                                                 nchunk);
     return cudaGetLastError();
