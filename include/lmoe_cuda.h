@@ -185,8 +185,9 @@ int lmoe_rmsnorm(const float* x, int rows, int hidden, const float* w, float eps
  *   db_pre     : [B,N,H] fp32 (Mamba2), da_raw : [H] fp32 (Mamba2, summed over batch)
  *   da_pre     : [B,N,H,D] dtype (TokenVector kinds)
  *   dM0        : [B,H,D,D] fp32 gradient of the initial state (may be NULL)
- * No recomputation of the forward output is needed: the passes consume q, k, v, dO only.
- * The normaliser path returns LMOE_ERR_UNSUPPORTED in this build.
+ * No recomputation of the forward output is needed: the passes consume q, k, v, dO only
+ * (the normaliser composes two unnormalised backwards and two forwards for num / den).
+ * TokenVector kinds: bf16 / head_dim 128 only.
  * ------------------------------------------------------------------------------------- */
 size_t lmoe_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
                                    lmoe_dtype dtype);
@@ -234,6 +235,30 @@ int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int
                              const void* a_pre, const float* b_pre, const float* a_raw, void* o,
                              float* M_out, float* z_out, int world, void* workspace,
                              size_t workspace_bytes, lmoe_stream_t stream);
+/* LSM sequence-parallel BACKWARD of lmoe_sp_lsm_fwd for this rank's slice (SURVEY 8(f) rank
+ * 1; the reference differentiates sp_lsm_masked_rank on its tape across the rank threads).
+ * Two all-gathers of B*H*(D*D + lw) fp32 per rank: the forward payload again (the rank's
+ * initial state), and the reverse-time payload [X | log D] (X = the adjoint at the slice
+ * start from the slice's own queries); a suffix combine over later ranks gives the adjoint
+ * entering the slice end, and the local backward (lmoe_lsm_bwd with M0 and dM_final) is then
+ * exact for the slice.  Outputs as lmoe_lsm_bwd for the slice; da_raw is this rank's
+ * contribution (the sum over ranks is the full gradient); dM0 is meaningful on rank 0.
+ * No normaliser in this build. */
+size_t lmoe_sp_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
+                                      lmoe_dtype dtype, int world);
+int lmoe_sp_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D, lmoe_dtype dtype,
+                    const void* q, const void* k, const void* v, const void* a_pre, const float* b_pre,
+                    const float* a_raw, const void* dO, void* dq, void* dk, void* dv, void* da_pre,
+                    float* db_pre, float* da_raw, float* dM0, void* nccl_comm, int rank, int world,
+                    void* workspace, size_t workspace_bytes, lmoe_stream_t stream);
+/* The same with `world` virtual ranks on one device over the full sequence (B == 1). */
+size_t lmoe_sp_lsm_bwd_loopback_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                                               lmoe_dtype dtype, int world);
+int lmoe_sp_lsm_bwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
+                             const void* q, const void* k, const void* v, const void* a_pre,
+                             const float* b_pre, const float* a_raw, const void* dO, void* dq, void* dk,
+                             void* dv, void* da_pre, float* db_pre, float* da_raw, float* dM0, int world,
+                             void* workspace, size_t workspace_bytes, lmoe_stream_t stream);
 /* Elements moved by the last SP gather (RankGroup::comm_log accounting, parallel.hpp:87-93). */
 long long lmoe_sp_last_gather_elements(void);
 /* NCCL bootstrap: rank 0 creates the 128-byte id, the caller distributes it. */

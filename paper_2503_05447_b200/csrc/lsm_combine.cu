@@ -75,6 +75,30 @@ __global__ void sp_rank_combine(const float* __restrict__ gathered, int P, int B
     else z0[(size_t)bh * dk + (e - nm)] = acc;
 }
 
+// SP backward: the adjoint state entering the END of rank `rank`'s slice from the queries of
+// later ranks, from the gathered reverse-time payloads [X_i | log D_i] (X_i = the adjoint at
+// the start of slice i from its own queries): acc = D_i acc + X_i over i = world-1 .. rank+1.
+__global__ void sp_rank_combine_rev(const float* __restrict__ gathered, int P, int BH, int rank, int world,
+                                    int dk, int dv, int lw, float* __restrict__ X) {
+    const int bh = blockIdx.y;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nm = dk * dv;
+    if (e >= nm) return;
+    const int li = lw == 1 ? 0 : e / dv;
+    float acc = 0.f;
+    for (int i = world - 1; i > rank; --i) {
+        const float* pl = gathered + ((size_t)i * BH + bh) * P;
+        acc = __expf(pl[P - lw + li]) * acc + pl[e];
+    }
+    X[(size_t)bh * nm + e] = acc;
+}
+
+cudaError_t launch_rank_combine_rev(const float* gathered, int P, int BH, int rank, int world, int dk, int dv,
+                                    int lw, float* X, cudaStream_t st) {
+    sp_rank_combine_rev<<<dim3((dk * dv + 255) / 256, BH), 256, 0, st>>>(gathered, P, BH, rank, world, dk, dv, lw, X);
+    return cudaGetLastError();
+}
+
 // Unmasked SP (parallel.hpp:293-296): M_global = sum over all ranks of the gathered
 // local states [world][BH][nm].
 __global__ void sp_sum_states(const float* __restrict__ gathered, int world, int BH, int nm,

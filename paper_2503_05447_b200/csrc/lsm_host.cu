@@ -994,3 +994,201 @@ extern "C" int lmoe_debug_trace_read(unsigned long long* out) {
         LMOE_CUDA_CHECK(cudaMemcpy(out, g_trace, 64 * 16 * 8, cudaMemcpyDeviceToHost));
     });
 }
+
+// ------------------------------------------------------------------- SP backward (8(f) rank 1)
+namespace lmoe_host {
+struct SpBwdPlan {
+    SpWorkspace f;  // forward payload, gather, M0
+    size_t off_bpay = 0, off_bgath = 0, off_Xin = 0, off_phq = 0, off_dar = 0, off_bws = 0, bws = 0, total = 0;
+};
+static size_t bwd_payload_floats(const lmoe_lsm_desc* d, int D) { return (size_t)D * D + payload_lw(d, D); }
+
+static SpBwdPlan plan_sp_bwd(const lmoe_lsm_desc* d, int B, int N_local, int H, int D, lmoe_dtype dt, int world) {
+    SpBwdPlan p;
+    p.f = plan_sp(d, B, N_local, H, D, world);
+    size_t off = align_up(p.f.total, 256);
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    const size_t BH = (size_t)B * H, P = BH * bwd_payload_floats(d, D);
+    p.off_bpay = take(P * 4);
+    p.off_bgath = take((size_t)world * P * 4);
+    p.off_Xin = take(BH * D * D * 4);
+    if (d->feature_map != 0) p.off_phq = take((size_t)B * N_local * H * D * (dt == LMOE_BF16 ? 2 : 4));
+    p.off_dar = take((size_t)H * 4);
+    p.bws = plan_bwd(d, B, N_local, H, D, dt).total;
+    p.off_bws = take(p.bws);
+    p.total = off;
+    return p;
+}
+
+static void check_sp_bwd_args(const lmoe_lsm_desc* d) {
+    if (d->use_normalizer)
+        throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_sp_lsm_bwd: normalizer SP backward not in this build");
+}
+
+// One slice: writes the forward payload [M | log D] (from zero) and the reverse-time payload
+// [X | log D] (X = sum_t (phi(q_t) e^{P_t})^T dO_t, P_t = decay from the slice start through t).
+template <typename T>
+static void sp_bwd_payloads(const lmoe_lsm_desc* d, int B, int n, int Nstride, int H, int D, lmoe_dtype dt,
+                            const void* q, const void* k, const void* v, const void* a_pre, const float* b_pre,
+                            const float* a_raw, const void* dO, uint8_t* ws, const SpBwdPlan& w, float* fpay,
+                            float* bpay, cudaStream_t st) {
+    LsmCall c{d, B, n, Nstride, H, D, dt, q, k, v, b_pre, a_raw, nullptr, ws, plan_lsm(B, n, H, D), st, a_pre};
+    c.setup();
+    sp_phase_a<T>(c, fpay);
+    // reverse pass over (phi(q), dO): identity map (phi applied beforehand), no normaliser
+    lmoe_lsm_desc dd = *d;
+    dd.feature_map = 0;
+    dd.use_normalizer = 0;
+    const void* phq = q;
+    if (d->feature_map != 0) {
+        LMOE_CUDA_CHECK(lmoe_dev::launch_apply_fmap(dt == LMOE_BF16, d->feature_map, q, ws + w.off_phq,
+                                                    (size_t)B * n * H * D, st));  // B == 1 or dense
+        ++g_launch_count;
+        phq = ws + w.off_phq;
+    }
+    LsmCall r{&dd, B, n, Nstride, H, D, dt, q, phq, dO, b_pre, a_raw, nullptr, ws, plan_lsm(B, n, H, D), st, a_pre};
+    r.setup();
+    r.var.rev = 1;
+    const int P = (int)bwd_payload_floats(d, D);
+    r.state_pass<T>();
+    r.combine(nullptr, nullptr, false, bpay, nullptr, bpay + P - r.lw, P, 1);
+}
+}  // namespace lmoe_host
+
+extern "C" size_t lmoe_sp_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
+                                                 lmoe_dtype dtype, int world) {
+    if (!desc || B < 1 || N_local < 1 || H < 1 || D < 1 || world < 1) return 0;
+    return plan_sp_bwd(desc, B, N_local, H, D, dtype, world).total;
+}
+
+extern "C" int lmoe_sp_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D, lmoe_dtype dtype,
+                               const void* q, const void* k, const void* v, const void* a_pre, const float* b_pre,
+                               const float* a_raw, const void* dO, void* dq, void* dk, void* dv, void* da_pre,
+                               float* db_pre, float* da_raw, float* dM0, void* nccl_comm, int rank, int world,
+                               void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, B, N_local, H, D, dtype, q, k, v, dO);
+        check_sp_bwd_args(desc);
+        if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd: bad rank");
+        if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd: null communicator");
+        const SpBwdPlan w = plan_sp_bwd(desc, B, N_local, H, D, dtype, world);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd: workspace too small (need " + std::to_string(w.total) + " bytes)");
+        uint8_t* ws = static_cast<uint8_t*>(workspace);
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const int BH = B * H;
+        const size_t Pf = (size_t)BH * payload_floats(desc, D), Pb = (size_t)BH * bwd_payload_floats(desc, D);
+        float* fpay = reinterpret_cast<float*>(ws + w.f.off_payload);
+        float* fgath = reinterpret_cast<float*>(ws + w.f.off_gathered);
+        float* bpay = reinterpret_cast<float*>(ws + w.off_bpay);
+        float* bgath = reinterpret_cast<float*>(ws + w.off_bgath);
+        float* M0 = reinterpret_cast<float*>(ws + w.f.off_M0);
+        float* Xin = reinterpret_cast<float*>(ws + w.off_Xin);
+        if (dtype == LMOE_BF16)
+            sp_bwd_payloads<__nv_bfloat16>(desc, B, N_local, N_local, H, D, dtype, q, k, v, a_pre, b_pre, a_raw, dO,
+                                           ws, w, fpay, bpay, st);
+        else
+            sp_bwd_payloads<float>(desc, B, N_local, N_local, H, D, dtype, q, k, v, a_pre, b_pre, a_raw, dO, ws, w,
+                                   fpay, bpay, st);
+        if (world > 1) {
+            NCCL_CHECK(ncclGroupStart());
+            NCCL_CHECK(ncclAllGather(fpay, fgath, Pf, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
+            NCCL_CHECK(ncclAllGather(bpay, bgath, Pb, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
+            NCCL_CHECK(ncclGroupEnd());
+        } else {
+            LMOE_CUDA_CHECK(cudaMemcpyAsync(fgath, fpay, Pf * 4, cudaMemcpyDeviceToDevice, st));
+            LMOE_CUDA_CHECK(cudaMemcpyAsync(bgath, bpay, Pb * 4, cudaMemcpyDeviceToDevice, st));
+        }
+        g_last_gather_elements = (long long)world * (long long)(Pf + Pb);
+        const int lw = payload_lw(desc, D);
+        LMOE_CUDA_CHECK(lmoe_dev::launch_rank_combine(dim3((D * D + 255) / 256, BH), st, fgath,
+                                                      (int)payload_floats(desc, D), BH, rank, D, D, 0, lw, M0,
+                                                      nullptr));
+        LMOE_CUDA_CHECK(lmoe_dev::launch_rank_combine_rev(bgath, (int)bwd_payload_floats(desc, D), BH, rank, world,
+                                                          D, D, lw, Xin, st));
+        g_launch_count += 2;
+        const int rc = lmoe_lsm_bwd(desc, B, N_local, H, D, dtype, q, k, v, a_pre, b_pre, a_raw, M0, dO, Xin, dq,
+                                    dk, dv, da_pre, db_pre, da_raw, dM0, ws + w.off_bws, w.bws, stream);
+        if (rc != LMOE_OK) throw Error(rc, lmoe_last_error());
+    });
+}
+
+extern "C" size_t lmoe_sp_lsm_bwd_loopback_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                                                          lmoe_dtype dtype, int world) {
+    if (!desc || world < 1 || N < world) return 0;
+    return plan_sp_bwd(desc, B, (N + world - 1) / world, H, D, dtype, world).total;
+}
+
+extern "C" int lmoe_sp_lsm_bwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
+                                        const void* q, const void* k, const void* v, const void* a_pre,
+                                        const float* b_pre, const float* a_raw, const void* dO, void* dq, void* dk,
+                                        void* dv, void* da_pre, float* db_pre, float* da_raw, float* dM0, int world,
+                                        void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, B, N, H, D, dtype, q, k, v, dO);
+        check_sp_bwd_args(desc);
+        if (B != 1) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd_loopback: B == 1 (rank slices are contiguous rows)");
+        if (world < 1 || N < world) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");
+        const SpBwdPlan w = plan_sp_bwd(desc, B, (N + world - 1) / world, H, D, dtype, world);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd_loopback: workspace too small");
+        uint8_t* ws = static_cast<uint8_t*>(workspace);
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        const bool bf16 = dtype == LMOE_BF16;
+        const size_t esz = bf16 ? 2 : 4;
+        const int BH = B * H;
+        const size_t Pf = (size_t)BH * payload_floats(desc, D), Pb = (size_t)BH * bwd_payload_floats(desc, D);
+        float* fgath = reinterpret_cast<float*>(ws + w.f.off_gathered);
+        float* bgath = reinterpret_cast<float*>(ws + w.off_bgath);
+        float* M0 = reinterpret_cast<float*>(ws + w.f.off_M0);
+        float* Xin = reinterpret_cast<float*>(ws + w.off_Xin);
+        float* dar = reinterpret_cast<float*>(ws + w.off_dar);
+        auto slice = [&](int r, int& r0, int& len) {  // chunk_range (parallel.hpp:192-197)
+            const int base = N / world, rem = N % world;
+            r0 = r * base + std::min(r, rem);
+            len = base + (r < rem ? 1 : 0);
+        };
+        auto at = [&](const void* p, int r0, size_t e) -> const void* {
+            return p ? static_cast<const uint8_t*>(p) + (size_t)r0 * H * D * e : nullptr;
+        };
+        auto atw = [&](void* p, int r0, size_t e) -> void* {
+            return p ? static_cast<uint8_t*>(p) + (size_t)r0 * H * D * e : nullptr;
+        };
+        for (int r = 0; r < world; ++r) {
+            int r0, len;
+            slice(r, r0, len);
+            const float* bp = b_pre ? b_pre + (size_t)r0 * H : nullptr;
+            if (bf16)
+                sp_bwd_payloads<__nv_bfloat16>(desc, B, len, len, H, D, dtype, at(q, r0, esz), at(k, r0, esz),
+                                               at(v, r0, esz), at(a_pre, r0, esz), bp, a_raw, at(dO, r0, esz), ws, w,
+                                               fgath + r * Pf, bgath + r * Pb, st);
+            else
+                sp_bwd_payloads<float>(desc, B, len, len, H, D, dtype, at(q, r0, esz), at(k, r0, esz),
+                                       at(v, r0, esz), at(a_pre, r0, esz), bp, a_raw, at(dO, r0, esz), ws, w,
+                                       fgath + r * Pf, bgath + r * Pb, st);
+        }
+        g_last_gather_elements = (long long)world * (long long)(Pf + Pb);
+        const int lw = payload_lw(desc, D);
+        if (da_raw) LMOE_CUDA_CHECK(cudaMemsetAsync(da_raw, 0, (size_t)H * 4, st));
+        for (int r = 0; r < world; ++r) {
+            int r0, len;
+            slice(r, r0, len);
+            LMOE_CUDA_CHECK(lmoe_dev::launch_rank_combine(dim3((D * D + 255) / 256, BH), st, fgath,
+                                                          (int)payload_floats(desc, D), BH, r, D, D, 0, lw, M0,
+                                                          nullptr));
+            LMOE_CUDA_CHECK(lmoe_dev::launch_rank_combine_rev(bgath, (int)bwd_payload_floats(desc, D), BH, r, world,
+                                                              D, D, lw, Xin, st));
+            g_launch_count += 2;
+            const int rc = lmoe_lsm_bwd(desc, B, len, H, D, dtype, at(q, r0, esz), at(k, r0, esz), at(v, r0, esz),
+                                        at(a_pre, r0, esz), b_pre ? b_pre + (size_t)r0 * H : nullptr, a_raw, M0,
+                                        at(dO, r0, esz), Xin, atw(dq, r0, esz), atw(dk, r0, esz), atw(dv, r0, esz),
+                                        atw(da_pre, r0, esz), db_pre ? db_pre + (size_t)r0 * H : nullptr,
+                                        da_raw ? dar : nullptr, r == 0 ? dM0 : nullptr, ws + w.off_bws, w.bws,
+                                        stream);
+            if (rc != LMOE_OK) throw Error(rc, lmoe_last_error());
+            if (da_raw)
+                LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(2, false, da_raw, dar, nullptr, nullptr, nullptr, nullptr,
+                                                              1, H, nullptr, st));
+        }
+    });
+}

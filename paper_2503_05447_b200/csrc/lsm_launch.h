@@ -37,6 +37,8 @@ cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const
 cudaError_t launch_sum_states(const float* gathered, int world, int BH, int nm, float* M, cudaStream_t st);
 cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,
                                 int rank, int dk, int dv, int norm, int lw, float* M0, float* z0);
+cudaError_t launch_rank_combine_rev(const float* gathered, int P, int BH, int rank, int world, int dk, int dv,
+                                    int lw, float* X, cudaStream_t st);
 // TokenVector decays (GLA / HGRN2 / RWKV6): variant {decay = 3, fm, norm, hgrn2 in bit 8 of fm}
 cudaError_t launch_state_pass_vec_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
                                        const CUtensorMap& val, const CUtensorMap& a, const LsmFwdParams& p);

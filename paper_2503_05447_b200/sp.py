@@ -16,7 +16,7 @@ import ctypes
 import torch
 
 from . import _lib
-from .lsm import LsmInstance, _DTYPES, _workspace, make_desc
+from .lsm import LsmGrads, LsmInstance, _DTYPES, _workspace, make_desc
 
 
 def chunk_range(n, t, rank):
@@ -52,6 +52,14 @@ def _bind():
     L.lmoe_sp_lsm_nomask_fwd.argtypes = [P, i, i, i, i, i, vp, vp, vp, vp, vp, i, i, vp, sz, vp]
     L.lmoe_sp_lsm_nomask_fwd_loopback.restype = i
     L.lmoe_sp_lsm_nomask_fwd_loopback.argtypes = [P, i, i, i, i, i, vp, vp, vp, vp, i, vp, sz, vp]
+    L.lmoe_sp_lsm_bwd_workspace_size.restype = sz
+    L.lmoe_sp_lsm_bwd_workspace_size.argtypes = [P, i, i, i, i, i, i]
+    L.lmoe_sp_lsm_bwd.restype = i
+    L.lmoe_sp_lsm_bwd.argtypes = [P, i, i, i, i, i] + [vp] * 15 + [i, i, vp, sz, vp]
+    L.lmoe_sp_lsm_bwd_loopback_workspace_size.restype = sz
+    L.lmoe_sp_lsm_bwd_loopback_workspace_size.argtypes = [P, i, i, i, i, i, i]
+    L.lmoe_sp_lsm_bwd_loopback.restype = i
+    L.lmoe_sp_lsm_bwd_loopback.argtypes = [P, i, i, i, i, i] + [vp] * 14 + [i, vp, sz, vp]
     L.lmoe_sp_last_gather_elements.restype = ctypes.c_longlong
     L.lmoe_nccl_unique_id.argtypes = [vp]
     L.lmoe_nccl_comm_init.argtypes = [ctypes.POINTER(vp), i, i, vp]
@@ -101,6 +109,25 @@ def _common(q, gates, spec):
     return B, N, H, D, a_raw, b_pre
 
 
+def _a_pre(q, gates):
+    """TokenVector gate pre-activations in the input dtype, or None."""
+    if gates is None or gates.a_pre is None:
+        return None
+    return gates.a_pre.to(q.dtype).contiguous()
+
+
+def _grads_like(q, gates, spec):
+    B, N, H, D = q.shape
+    g = LsmGrads(dq=torch.empty_like(q), dk=torch.empty_like(q), dv=torch.empty_like(q))
+    g.dM0 = torch.zeros(B, H, D, D, dtype=torch.float32, device=q.device)
+    if spec.instance == LsmInstance.MAMBA2:
+        g.db_pre = torch.empty(B, N, H, dtype=torch.float32, device=q.device)
+        g.da_raw = torch.empty(H, dtype=torch.float32, device=q.device)
+    if gates is not None and gates.a_pre is not None:
+        g.da_pre = torch.empty_like(q)
+    return g
+
+
 def sp_lsm_masked_rank(comm, q_loc, k_loc, v_loc, gates_loc, spec, chunk_size=64,
                        final_state=None, out=None, check=True, timing=False, stream=None):
     """This rank's output for its contiguous slice [B, N_loc, H, D] (parallel.hpp:303-376)."""
@@ -118,7 +145,7 @@ def sp_lsm_masked_rank(comm, q_loc, k_loc, v_loc, gates_loc, spec, chunk_size=64
             z_out = torch.empty(B, H, D, dtype=torch.float32, device=q_loc.device)
     st = stream if stream is not None else torch.cuda.current_stream(q_loc.device).cuda_stream
     rc = L.lmoe_sp_lsm_fwd(ctypes.byref(desc), B, N, H, D, dt, _lib.ptr(q_loc), _lib.ptr(k_loc),
-                           _lib.ptr(v_loc), None, _lib.ptr(b_pre), _lib.ptr(a_raw), _lib.ptr(o),
+                           _lib.ptr(v_loc), _lib.ptr(_a_pre(q_loc, gates_loc)), _lib.ptr(b_pre), _lib.ptr(a_raw), _lib.ptr(o),
                            _lib.ptr(M_out), _lib.ptr(z_out), comm.handle, comm.rank, comm.world,
                            _lib.ptr(ws), ws.numel(), ctypes.c_void_p(st))
     _lib.check(rc)
@@ -144,13 +171,54 @@ def sp_forward_masked_loopback(q, k, v, gates, spec, world, chunk_size=64, final
             z_out = torch.empty(B, H, D, dtype=torch.float32, device=q.device)
     st = torch.cuda.current_stream(q.device).cuda_stream
     rc = L.lmoe_sp_lsm_fwd_loopback(ctypes.byref(desc), B, N, H, D, dt, _lib.ptr(q), _lib.ptr(k),
-                                    _lib.ptr(v), None, _lib.ptr(b_pre), _lib.ptr(a_raw),
+                                    _lib.ptr(v), _lib.ptr(_a_pre(q, gates)), _lib.ptr(b_pre), _lib.ptr(a_raw),
                                     _lib.ptr(o), _lib.ptr(M_out), _lib.ptr(z_out), world,
                                     _lib.ptr(ws), ws.numel(), ctypes.c_void_p(st))
     _lib.check(rc)
     if final_state is not None:
         final_state.M, final_state.z = M_out, z_out
     return o
+
+
+def sp_lsm_backward_rank(comm, q_loc, k_loc, v_loc, gates_loc, spec, dO_loc, chunk_size=64, check=True,
+                         stream=None):
+    """VJP of sp_lsm_masked_rank for this rank's slice (lmoe_sp_lsm_bwd): two all-gathers
+    (forward payload, reverse-time payload), then the exact local backward.  Returns LsmGrads;
+    da_raw is this rank's contribution (sum over ranks = the full gradient)."""
+    L = _bind()
+    B, N, H, D, a_raw, b_pre = _common(q_loc, gates_loc, spec)
+    g = _grads_like(q_loc, gates_loc, spec)
+    desc = make_desc(spec, chunk_size, check)
+    dt = _DTYPES[q_loc.dtype]
+    nbytes = L.lmoe_sp_lsm_bwd_workspace_size(ctypes.byref(desc), B, N, H, D, dt, comm.world)
+    ws = _workspace(nbytes, q_loc.device)
+    st = stream if stream is not None else torch.cuda.current_stream(q_loc.device).cuda_stream
+    P = _lib.ptr
+    rc = L.lmoe_sp_lsm_bwd(ctypes.byref(desc), B, N, H, D, dt, P(q_loc), P(k_loc), P(v_loc),
+                           P(_a_pre(q_loc, gates_loc)), P(b_pre), P(a_raw), P(dO_loc.contiguous()), P(g.dq),
+                           P(g.dk), P(g.dv), P(g.da_pre), P(g.db_pre), P(g.da_raw), P(g.dM0), comm.handle,
+                           comm.rank, comm.world, P(ws), ws.numel(), ctypes.c_void_p(st))
+    _lib.check(rc)
+    return g
+
+
+def sp_backward_masked_loopback(q, k, v, gates, spec, dO, world, chunk_size=64, check=True):
+    """The SP backward with `world` virtual ranks on one device over the full sequence (B == 1)."""
+    L = _bind()
+    B, N, H, D, a_raw, b_pre = _common(q, gates, spec)
+    g = _grads_like(q, gates, spec)
+    desc = make_desc(spec, chunk_size, check)
+    dt = _DTYPES[q.dtype]
+    nbytes = L.lmoe_sp_lsm_bwd_loopback_workspace_size(ctypes.byref(desc), B, N, H, D, dt, world)
+    ws = _workspace(nbytes, q.device)
+    st = torch.cuda.current_stream(q.device).cuda_stream
+    P = _lib.ptr
+    rc = L.lmoe_sp_lsm_bwd_loopback(ctypes.byref(desc), B, N, H, D, dt, P(q), P(k), P(v), P(_a_pre(q, gates)),
+                                    P(b_pre), P(a_raw), P(dO.contiguous()), P(g.dq), P(g.dk), P(g.dv),
+                                    P(g.da_pre), P(g.db_pre), P(g.da_raw), P(g.dM0), world, P(ws), ws.numel(),
+                                    ctypes.c_void_p(st))
+    _lib.check(rc)
+    return g
 
 
 def last_gather_elements():

@@ -132,3 +132,90 @@ def test_nomask_error_texts():
         sp.sp_forward_nomask_loopback(q, k, v, pk.LsmSpec.make("retnet", 128), 2)
     with pytest.raises(pk.LmoeError, match="sp_forward_nomask: normalizer unsupported"):
         sp.sp_forward_nomask_loopback(q, k, v, pk.LsmSpec.make("bla", 128), 2)
+
+
+# ------------------------------------------------------------------ SP backward (8(f) rank 1)
+def _gla_setup(N=1100, H=2, D=128, seed=3):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_05447_b200 as pk
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q, k, v = (torch.randn(1, N, H, D, device="cuda", generator=g).mul_(0.5).to(torch.bfloat16) for _ in range(3))
+    a = torch.randn(1, N, H, D, device="cuda", generator=g).mul_(0.5).add_(3.0).to(torch.bfloat16)
+    return torch, pk, q, k, v, pk.LsmSpec.make("gla", D), pk.LsmGates(a_pre=a)
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).abs().max() / b.float().abs().max()).item()
+
+
+@pytest.mark.parametrize("inst", ["bla_plain", "retnet", "mamba2", "gla"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sp_backward_rank_invariance(inst, world):
+    """The SP backward of every virtual rank, stitched together, equals the single-device
+    backward of the whole sequence (exact algorithm; agreement to bf16 rounding)."""
+    if inst == "gla":
+        torch, pk, q, k, v, spec, gates = _gla_setup()
+    else:
+        torch, pk, q, k, v, spec, gates = _setup("bla" if inst == "bla_plain" else inst)
+        if inst == "bla_plain":
+            spec = pk.LsmSpec(instance=pk.LsmInstance.BLA, feature_map=0, use_normalizer=False)
+    from paper_2503_05447_b200 import sp
+    g = torch.Generator(device="cuda").manual_seed(11)
+    dO = torch.randn(q.shape, device="cuda", generator=g).to(torch.bfloat16)
+    ref = pk.lsm_backward_batched(q, k, v, gates, spec, dO)
+    got = sp.sp_backward_masked_loopback(q, k, v, gates, spec, dO, world)
+    torch.cuda.synchronize()
+    for n in ("dq", "dk", "dv", "db_pre", "da_pre", "dM0"):
+        r, o = getattr(ref, n), getattr(got, n)
+        if r is None:
+            continue
+        # TokenVector gate gradients pass through bf16 chunk-boundary state snapshots whose
+        # values differ with the segmentation: the bf16 gradient bound (north star) applies
+        tol = 2e-2 if n == "da_pre" else 1e-2
+        assert _rel(o, r) < tol, (inst, world, n, _rel(o, r))
+    if ref.da_raw is not None:
+        assert _rel(got.da_raw, ref.da_raw) < 1e-2, (inst, world, "da_raw")
+    # two all-gathers: forward payload (d*d + 1) and reverse payload (d*d + lw)
+    D = q.shape[-1]
+    lw = D if inst == "gla" else 1
+    assert sp.last_gather_elements() == world * q.shape[2] * ((D * D + lw) * 2)
+
+
+def test_sp_backward_vs_oracle():
+    """Loopback SP backward (world 4, Mamba2 long memory) against the float64 oracle backward."""
+    torch, pk, q, k, v, spec, gates = _setup("mamba2", N=900, H=2)
+    from paper_2503_05447_b200 import sp
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dO = torch.randn(q.shape, device="cuda", generator=g).to(torch.bfloat16)
+    got = sp.sp_backward_masked_loopback(q, k, v, gates, spec, dO, 4)
+    torch.cuda.synchronize()
+    dar = np.zeros(2)
+    for h in range(2):
+        sd = oracle.spec_default("mamba2")
+        sd["mamba2_a_raw"] = float(spec.mamba2_a_raw[h])
+        w = oracle.lsm_backward(sd, *(t[0, :, h].float().cpu().numpy() for t in (q, k, v, dO)),
+                                None, gates.b_pre[0, :, h].cpu().numpy())
+        for n in ("dq", "dk", "dv"):
+            assert norm_rel_err(getattr(got, n)[0, :, h].float().cpu().numpy(), w[n]) < 2e-2, (n, h)
+        assert norm_rel_err(got.db_pre[0, :, h].cpu().numpy(), w["db_pre"]) < 2e-2
+        dar[h] = w["da_raw"]
+    assert np.abs(got.da_raw.cpu().numpy() - dar).max() / np.abs(dar).max() < 2e-2
+
+
+def test_sp_backward_nccl_world1_and_gla_forward():
+    """NCCL entry point at world 1 equals the local backward; TokenVector SP forward (a_pre
+    through the Python mirror) equals the single-device forward."""
+    torch, pk, q, k, v, spec, gates = _gla_setup(N=700)
+    from paper_2503_05447_b200 import sp
+    dO = torch.randn(q.shape, device="cuda").to(torch.bfloat16)
+    comm = sp.NcclComm(0, 1)
+    got = sp.sp_lsm_backward_rank(comm, q, k, v, gates, spec, dO)
+    ref = pk.lsm_backward_batched(q, k, v, gates, spec, dO)
+    torch.cuda.synchronize()
+    for n in ("dq", "dk", "dv", "da_pre"):
+        assert _rel(getattr(got, n), getattr(ref, n)) < 1e-2, n
+    o = sp.sp_forward_masked_loopback(q, k, v, gates, spec, 4)
+    o_ref = pk.lsm_forward_batched(q, k, v, gates, spec, 64)
+    assert _rel(o, o_ref) < 1e-2
