@@ -6,6 +6,7 @@
 //   reference (CPU, lmoe::)                    this header (B200, lmoe::cuda::)
 //   lsm_forward_chunked   lsm.hpp:668          lsm_forward_chunked(view, gates, spec, chunk, &fs)
 //   sp_lsm_masked_rank    parallel.hpp:303     sp_lsm_masked_rank(comm, view, gates, spec, &fs)
+//   (its tape VJP)                             sp_lsm_masked_rank_backward(comm, ..., dO, grads)
 //   route                 moe.hpp:58           route(logits, T, E, top_k)
 //   MoeLayer::forward     moe.hpp:133          MoeLayer::forward(x, T, y)
 //   std::runtime_error(msg)                    lmoe::cuda::Error (a std::runtime_error) with the
@@ -178,6 +179,24 @@ inline void lsm_backward_chunked(const LsmView& x, const LsmGates& gates, const 
     check(lmoe_lsm_bwd(&d, x.B, x.N, x.H, x.D, x.dtype, x.q, x.k, x.v, gates.a_pre, gates.b_pre, spec.mamba2_a_raw,
                        initial_state ? initial_state->M : nullptr, dO, dM_final, g.dq, g.dk, g.dv, g.da_pre,
                        g.db_pre, g.da_raw, g.dM0, wsp, w.size(), reinterpret_cast<lmoe_stream_t>(stream)));
+}
+
+// Backward of sp_lsm_masked_rank for this rank's slice: two all-gathers (forward and
+// reverse-time payloads), suffix combine over later ranks, exact local backward.  da_raw is
+// this rank's contribution; dM0 is meaningful on rank 0.
+inline void sp_lsm_masked_rank_backward(void* nccl_comm, int rank, int world, const LsmView& x_loc,
+                                        const LsmGates& g_loc, const LsmSpec& spec, const void* dO_loc,
+                                        const LsmGrads& g, Workspace* ws = nullptr, cudaStream_t stream = nullptr,
+                                        bool check_device = true) {
+    Workspace local;
+    Workspace& w = ws ? *ws : local;
+    const lmoe_lsm_desc d = to_desc(spec, 64, check_device);
+    const size_t need = lmoe_sp_lsm_bwd_workspace_size(&d, x_loc.B, x_loc.N, x_loc.H, x_loc.D, x_loc.dtype, world);
+    void* wsp = w.get(need);
+    check(lmoe_sp_lsm_bwd(&d, x_loc.B, x_loc.N, x_loc.H, x_loc.D, x_loc.dtype, x_loc.q, x_loc.k, x_loc.v,
+                          g_loc.a_pre, g_loc.b_pre, spec.mamba2_a_raw, dO_loc, g.dq, g.dk, g.dv, g.da_pre, g.db_pre,
+                          g.da_raw, g.dM0, nccl_comm, rank, world, wsp, w.size(),
+                          reinterpret_cast<lmoe_stream_t>(stream)));
 }
 
 // chunk_range (parallel.hpp:192-197)

@@ -32,9 +32,9 @@ def _sources():
 
 def _deps():
     out = []
-    for d in (CSRC, os.path.join(ROOT, "include")):
+    for d in (CSRC, os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "cpp")):
         for r, _, fs in os.walk(d):
-            out += [os.path.join(r, f) for f in fs if f.endswith((".cu", ".cuh", ".h", ".hpp"))]
+            out += [os.path.join(r, f) for f in fs if f.endswith((".cu", ".cuh", ".h", ".hpp", ".cpp"))]
     return out
 
 

@@ -67,7 +67,52 @@ int main() {
     } catch (const Error& e) {
         text_ok = std::string(e.what()) == "LsmSpec: normalizer unsupported for instance mamba2";
     }
-    std::printf("cpp api: norm-rel err %.3e (tol 1e-3), error text %s\n", worst, text_ok ? "ok" : "MISMATCH");
+    // backward through the drop-in API: lsm_backward_chunked (the tape's VJP) with dO = 1 /
+    // N-scaled random, dv checked against dv_s = sum_{t >= s} a^{t-s} (q_t . k_s) dO_t, and the
+    // SP backward at world 1 (sp_lsm_masked_rank_backward) equal to it
+    std::vector<float> gO(N * H * D);
+    for (auto& x : gO) x = nd(gen);
+    float *ddO, *gq, *gk, *gv, *sq, *sk, *sv;
+    for (float** p : {&ddO, &gq, &gk, &gv, &sq, &sk, &sv}) cudaMalloc(p, bytes);
+    cudaMemcpy(ddO, gO.data(), bytes, cudaMemcpyHostToDevice);
+    double worst_bwd = 1.0, worst_sp = 1.0;
+    try {
+        LsmGrads g;
+        g.dq = gq; g.dk = gk; g.dv = gv;
+        lsm_backward_chunked(x, LsmGates{}, spec, ddO, g);
+        LsmGrads gs;
+        gs.dq = sq; gs.dk = sk; gs.dv = sv;
+        sp_lsm_masked_rank_backward(nullptr, 0, 1, x, LsmGates{}, spec, ddO, gs);
+        std::vector<float> hv(N * H * D), hs(N * H * D);
+        cudaMemcpy(hv.data(), gv, bytes, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hs.data(), sv, bytes, cudaMemcpyDeviceToHost);
+        worst_bwd = worst_sp = 0.0;
+        for (int h = 0; h < H; ++h) {
+            double maxref = 0.0, maxerr = 0.0, maxsp = 0.0;
+            for (int s0 = 0; s0 < N; s0 += 7) {  // every 7th row keeps the host reference cheap
+                std::vector<double> acc(D, 0.0);
+                double w = 1.0;
+                for (int t = s0; t < N; ++t, w *= spec.scalar_decay) {
+                    double qk = 0.0;
+                    for (int i = 0; i < D; ++i) qk += (double)q[(t * H + h) * D + i] * k[(s0 * H + h) * D + i];
+                    for (int j = 0; j < D; ++j) acc[j] += w * qk * gO[(t * H + h) * D + j];
+                }
+                for (int j = 0; j < D; ++j) {
+                    const size_t e = (size_t)(s0 * H + h) * D + j;
+                    maxref = std::fmax(maxref, std::fabs(acc[j]));
+                    maxerr = std::fmax(maxerr, std::fabs(acc[j] - hv[e]));
+                    maxsp = std::fmax(maxsp, std::fabs((double)hs[e] - hv[e]));
+                }
+            }
+            worst_bwd = std::fmax(worst_bwd, maxerr / maxref);
+            worst_sp = std::fmax(worst_sp, maxsp / maxref);
+        }
+    } catch (const Error& e) {
+        std::printf("backward error: %s\n", e.what());
+    }
+    std::printf("cpp api: norm-rel err %.3e (tol 1e-3), error text %s, backward dv %.3e (tol 2e-3), "
+                "SP world-1 vs local %.3e\n", worst, text_ok ? "ok" : "MISMATCH", worst_bwd, worst_sp);
     cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(dM);
-    return (worst < 1e-3 && text_ok) ? 0 : 1;
+    for (float* p : {ddO, gq, gk, gv, sq, sk, sv}) cudaFree(p);
+    return (worst < 1e-3 && text_ok && worst_bwd < 2e-3 && worst_sp < 1e-5) ? 0 : 1;
 }
