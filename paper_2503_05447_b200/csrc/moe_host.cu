@@ -53,8 +53,12 @@ static void launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUten
                                              lmoe_dev::gemm_smem<BN, EPI>()));
         attr = true;
     }
-    lmoe_dev::moe_gemm<BN, EPI><<<dim3(ntiles_n, max_tiles), lmoe_dev::kGemmThreads,
-                                  lmoe_dev::gemm_smem<BN, EPI>(), st>>>(a, b0, b1, gp);
+    // persistent: one CTA per SM (or fewer when the tile list is short) walks the tile list
+    lmoe_dev::GemmParams g = gp;
+    g.ntn = ntiles_n;
+    const long long upper = (long long)max_tiles * ntiles_n;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(num_sms(), upper));
+    lmoe_dev::moe_gemm<BN, EPI><<<grid, lmoe_dev::kGemmThreads, lmoe_dev::gemm_smem<BN, EPI>(), st>>>(a, b0, b1, g);
     LMOE_CUDA_CHECK(cudaGetLastError());
     ++g_launch_count;
 }

@@ -16,6 +16,10 @@ namespace lmoe_dev {
 
 // ====================================================================================
 // Grouped GEMM  C[rows of group g] = A[rows] (K-major, bf16) x B_g (MN-major [K][N], bf16)
+// Persistent: one CTA per SM walks the (128-row M tile, BN-column N tile) list, M-major so
+// the CTAs running at once share A tiles in L2.  The smem ring runs continuously across
+// tiles; the TMEM accumulator is double-buffered so the epilogue of tile i overlaps the
+// MMAs of tile i+1.
 // warps: 0 TMA producer, 1 MMA issuer, 2..5 epilogue (one thread per output row)
 // ====================================================================================
 template <int BN, int EPI>
@@ -27,28 +31,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr int B_BYTES = 64 * 2 * BN;                     // 64 K rows x BN cols (bf16)
     constexpr int STAGE = A_BYTES + NB * B_BYTES;
     constexpr int NST = gemm_stages<BN, EPI>();
-    constexpr uint32_t TCOLS = (NB * BN <= 128) ? 128 : (NB * BN <= 256 ? 256 : 512);
+    constexpr uint32_t ACOLS = NB * BN;                      // accumulator columns per buffer
+    constexpr uint32_t TCOLS = 2 * ACOLS;                    // two buffers (128 / 256 / 512)
     extern __shared__ __align__(1024) uint8_t smem[];
     if (smem_u32(smem) & 1023) __trap();
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
     uint64_t* full = bars;             // [NST]
     uint64_t* empty = bars + NST;      // [NST]
-    uint64_t* acc_full = bars + 2 * NST;
-    uint32_t* sTmem = reinterpret_cast<uint32_t*>(acc_full + 1);
+    uint64_t* acc_full = bars + 2 * NST;   // [2]
+    uint64_t* acc_empty = acc_full + 2;    // [2]
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
-    // blockIdx.x walks the N tiles of one 128-row M tile so they share the A tile in L2
-    const int tile = blockIdx.y;
-    if (tile >= *p.num_tiles) return;
-    const int g = p.tile_group[tile];
-    const int row0 = p.tile_row0[tile];
-    const int rows_left = p.group_end[g] - row0;  // valid rows of this tile (<= 128)
-    const int n0 = blockIdx.x * BN;
+    const int total = *p.num_tiles * p.ntn;
     const int kblocks = p.K / 64;
     const int warp = warp_id(), lane = lane_id();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        mbar_init(acc_full, 1);
+        for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 128); }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<TCOLS>(sTmem);
@@ -62,99 +62,121 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tma_prefetch(&tmA);
             tma_prefetch(&tmB0);
             if (NB == 2) tma_prefetch(&tmB1);
-            for (int kb = 0; kb < kblocks; ++kb) {
-                const int s = kb % NST;
-                if (kb >= NST) mbar_wait(&empty[s], ((kb / NST) - 1) & 1);
-                uint8_t* st = smem + s * STAGE;
-                mbar_expect_tx(&full[s], STAGE);
-                tma_load_2d(st, &tmA, &full[s], kb * 64, row0);
+            int it = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int mt = t / p.ntn, n0 = (t % p.ntn) * BN;
+                const int g = p.tile_group[mt], row0 = p.tile_row0[mt];
+                for (int kb = 0; kb < kblocks; ++kb, ++it) {
+                    const int s = it % NST;
+                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    uint8_t* st = smem + s * STAGE;
+                    mbar_expect_tx(&full[s], STAGE);
+                    tma_load_2d(st, &tmA, &full[s], kb * 64, row0);
 #pragma unroll
-                for (int nb = 0; nb < BN / 64; ++nb) {
-                    tma_load_3d(st + A_BYTES + nb * 8192, &tmB0, &full[s], n0 + nb * 64, kb * 64, g);
-                    if constexpr (NB == 2)
-                        tma_load_3d(st + A_BYTES + B_BYTES + nb * 8192, &tmB1, &full[s], n0 + nb * 64, kb * 64, g);
+                    for (int nb = 0; nb < BN / 64; ++nb) {
+                        tma_load_3d(st + A_BYTES + nb * 8192, &tmB0, &full[s], n0 + nb * 64, kb * 64, g);
+                        if constexpr (NB == 2)
+                            tma_load_3d(st + A_BYTES + B_BYTES + nb * 8192, &tmB1, &full[s], n0 + nb * 64, kb * 64, g);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc(1, 0, 1, 128, BN);
-            for (int kb = 0; kb < kblocks; ++kb) {
-                const int s = kb % NST;
-                mbar_wait(&full[s], (kb / NST) & 1);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+                const int buf = lt & 1;
+                if (lt >= 2) mbar_wait(&acc_empty[buf], ((lt >> 1) - 1) & 1);  // epilogue drained it
                 tc_fence_after();
-                const uint32_t a0 = smem_u32(smem + s * STAGE);
-                const uint32_t b0 = a0 + A_BYTES;
+                const uint32_t acc_t = tmem + buf * ACOLS;
+                for (int kb = 0; kb < kblocks; ++kb, ++it) {
+                    const int s = it % NST;
+                    mbar_wait(&full[s], (it / NST) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + s * STAGE);
+                    const uint32_t b0 = a0 + A_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t ad = umma_desc_sw128(a0 + kk * 32, 16, 1024);
-                    const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-                    mma_ss_f16(tmem, ad, umma_desc_sw128(b0 + kk * 2048, 8192, 1024), idesc, acc);
-                    if constexpr (NB == 2)
-                        mma_ss_f16(tmem + BN, ad, umma_desc_sw128(b0 + B_BYTES + kk * 2048, 8192, 1024),
-                                   idesc, acc);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t ad = umma_desc_sw128(a0 + kk * 32, 16, 1024);
+                        const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+                        mma_ss_f16(acc_t, ad, umma_desc_sw128(b0 + kk * 2048, 8192, 1024), idesc, acc);
+                        if constexpr (NB == 2)
+                            mma_ss_f16(acc_t + BN, ad, umma_desc_sw128(b0 + B_BYTES + kk * 2048, 8192, 1024),
+                                       idesc, acc);
+                    }
+                    mma_commit(&empty[s]);
                 }
-                mma_commit(&empty[s]);
+                mma_commit(&acc_full[buf]);
             }
-            mma_commit(acc_full);
         }
     } else {
         // epilogue: thread (quarter q, lane) owns output row q*32 + lane of the tile
         const int q = warp & 3;
         const int r = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        mbar_wait(acc_full, 0);
-        tc_fence_after();
-        const bool valid = r < rows_left;
-        const size_t grow = (size_t)row0 + (valid ? r : 0);
+        int lt = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+            const int buf = lt & 1;
+            const int mt = t / p.ntn, n0 = (t % p.ntn) * BN;
+            const int row0 = p.tile_row0[mt];
+            const int rows_left = p.group_end[p.tile_group[mt]] - row0;  // valid rows (<= 128)
+            mbar_wait(&acc_full[buf], (lt >> 1) & 1);
+            tc_fence_after();
+            const uint32_t acc_t = tmem + buf * ACOLS;
+            const bool valid = r < rows_left;
+            const size_t grow = (size_t)row0 + (valid ? r : 0);
 #pragma unroll 1
-        for (int cb = 0; cb < BN; cb += 32) {
-            uint32_t a[32];
-            tmem_ld32(tmem + lane_off + cb, a);
-            if constexpr (EPI == kEpiSwiGLU) {
-                uint32_t u[32];
-                tmem_ld32(tmem + lane_off + BN + cb, u);
-                tmem_wait_ld();
-                if (valid) {
-                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + n0 + cb;
+            for (int cb = 0; cb < BN; cb += 32) {
+                uint32_t a[32];
+                tmem_ld32(acc_t + lane_off + cb, a);
+                if constexpr (EPI == kEpiSwiGLU) {
+                    uint32_t u[32];
+                    tmem_ld32(acc_t + lane_off + BN + cb, u);
+                    tmem_wait_ld();
+                    if (valid) {
+                        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + n0 + cb;
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        uint4 v;
-                        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+                        for (int j = 0; j < 32; j += 8) {
+                            uint4 v;
+                            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float g0 = __uint_as_float(a[j + 2 * e]), g1 = __uint_as_float(a[j + 2 * e + 1]);
-                            const float u0 = __uint_as_float(u[j + 2 * e]), u1 = __uint_as_float(u[j + 2 * e + 1]);
-                            w[e] = pack_bf16(silu_f(g0) * u0, silu_f(g1) * u1);
+                            for (int e = 0; e < 4; ++e) {
+                                const float g0 = __uint_as_float(a[j + 2 * e]), g1 = __uint_as_float(a[j + 2 * e + 1]);
+                                const float u0 = __uint_as_float(u[j + 2 * e]), u1 = __uint_as_float(u[j + 2 * e + 1]);
+                                w[e] = pack_bf16(silu_f(g0) * u0, silu_f(g1) * u1);
+                            }
+                            *reinterpret_cast<uint4*>(dst + j) = v;
                         }
-                        *reinterpret_cast<uint4*>(dst + j) = v;
                     }
-                }
-            } else if constexpr (EPI == kEpiBF16) {
-                tmem_wait_ld();
-                if (valid) {
-                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + n0 + cb;
+                } else if constexpr (EPI == kEpiBF16) {
+                    tmem_wait_ld();
+                    if (valid) {
+                        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.C) + grow * p.ldc + n0 + cb;
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        uint4 v;
-                        v.x = pack_bf16(__uint_as_float(a[j]), __uint_as_float(a[j + 1]));
-                        v.y = pack_bf16(__uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
-                        v.z = pack_bf16(__uint_as_float(a[j + 4]), __uint_as_float(a[j + 5]));
-                        v.w = pack_bf16(__uint_as_float(a[j + 6]), __uint_as_float(a[j + 7]));
-                        *reinterpret_cast<uint4*>(dst + j) = v;
+                        for (int j = 0; j < 32; j += 8) {
+                            uint4 v;
+                            v.x = pack_bf16(__uint_as_float(a[j]), __uint_as_float(a[j + 1]));
+                            v.y = pack_bf16(__uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
+                            v.z = pack_bf16(__uint_as_float(a[j + 4]), __uint_as_float(a[j + 5]));
+                            v.w = pack_bf16(__uint_as_float(a[j + 6]), __uint_as_float(a[j + 7]));
+                            *reinterpret_cast<uint4*>(dst + j) = v;
+                        }
                     }
-                }
-            } else {  // fp32
-                tmem_wait_ld();
-                if (valid) {
-                    float* dst = reinterpret_cast<float*>(p.C) + grow * p.ldc + n0 + cb;
+                } else {  // fp32
+                    tmem_wait_ld();
+                    if (valid) {
+                        float* dst = reinterpret_cast<float*>(p.C) + grow * p.ldc + n0 + cb;
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        *reinterpret_cast<float4*>(dst + j) =
-                            make_float4(__uint_as_float(a[j]), __uint_as_float(a[j + 1]),
-                                        __uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + j) =
+                                make_float4(__uint_as_float(a[j]), __uint_as_float(a[j + 1]),
+                                            __uint_as_float(a[j + 2]), __uint_as_float(a[j + 3]));
+                    }
                 }
             }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[buf]);
         }
     }
     tc_fence_before();

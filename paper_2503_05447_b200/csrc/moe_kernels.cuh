@@ -15,6 +15,7 @@ struct GemmParams {
     int K;                  // reduction length (multiple of 64)
     void* C;                // output rows (same row index space as A)
     int ldc;                // elements per output row
+    int ntn = 1;            // N tiles per M tile (set by the launcher)
 };
 
 template <int BN, int EPI>
@@ -27,7 +28,7 @@ constexpr int gemm_stages() {
 }
 template <int BN, int EPI>
 constexpr int gemm_smem() {
-    return gemm_stages<BN, EPI>() * gemm_stage_bytes<BN, EPI>() + 256;
+    return gemm_stages<BN, EPI>() * gemm_stage_bytes<BN, EPI>() + 512;
 }
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.f + __expf(-x)); }
