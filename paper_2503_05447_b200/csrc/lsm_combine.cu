@@ -41,10 +41,25 @@ __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __rest
     if (isz) { if (z0) acc = z0[(size_t)bh * dk + ee]; }
     else if (M0) acc = M0[(size_t)bh * nm + ee];
     const size_t base = (size_t)bh * nseg * stride + ee;
-    for (int i = 0; i < nseg; ++i) {
-        const int s = rev ? nseg - 1 - i : i;
-        if (dst) dst[base + (size_t)s * stride] = acc;
-        acc = __expf(logD[((size_t)bh * nseg + s) * lw + li]) * acc + src[base + (size_t)s * stride];
+    // the loads do not depend on the running prefix: fetch 8 segments ahead of the recurrence
+    for (int i0 = 0; i0 < nseg; i0 += 8) {
+        float sv[8], dv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u;
+            const int s = rev ? nseg - 1 - i : i;
+            sv[u] = i < nseg ? src[base + (size_t)s * stride] : 0.f;
+            dv[u] = i < nseg ? __expf(logD[((size_t)bh * nseg + s) * lw + li]) : 1.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u;
+            if (i < nseg) {
+                const int s = rev ? nseg - 1 - i : i;
+                if (dst) dst[base + (size_t)s * stride] = acc;
+                acc = dv[u] * acc + sv[u];
+            }
+        }
     }
     if (!isfinite(acc)) atomicOr(&err[1], 1);
     float* fin = isz ? zfin : Mfin;

@@ -57,29 +57,29 @@ struct LsmPlan {
     size_t off_S = 0, off_z = 0, off_logD = 0, off_Min = 0, off_zin = 0, off_err = 0, total = 0;
 };
 
-// Segment length: a multiple of the 128-token tile chosen so the B*H*nseg CTAs of the
-// segment-parallel passes fill whole waves of the SMs (one CTA per SM).
+// Segment length: a multiple of the 128-token tile.  The B*H*nseg CTAs of the
+// segment-parallel passes run one per SM; a pass costs about waves x (chunks per segment +
+// a per-CTA fixed cost: prologue, pipeline fill and drain, ~2 chunks), so short slices
+// (sequence parallelism) prefer one wave of longer segments over several waves of short ones.
 static LsmPlan plan_lsm(int B, int N, int H, int D) {
     LsmPlan pl;
     const int C = lmoe_dev::kC;
     const int chunks = (N + C - 1) / C;
     const long long heads = (long long)B * H;
     const int sms = num_sms();
-    double best = -1.0;
-    for (int waves = 1; waves <= 12; ++waves) {
-        long long target = (long long)sms * waves;
-        int seg_chunks = (int)std::max<long long>(1, (heads * chunks + target - 1) / target);
-        seg_chunks = std::min(seg_chunks, chunks);
-        int nseg = (chunks + seg_chunks - 1) / seg_chunks;
-        long long ctas = heads * nseg;
-        long long w = (ctas + sms - 1) / sms;
-        double eff = (double)(heads * chunks) / (double)(w * sms * seg_chunks);
-        double score = eff - 0.002 * waves;  // fuller waves first, then fewer segments
-        if (score > best) {
-            best = score;
+    constexpr double kFixedChunks = 2.0;
+    double best = 1e300;
+    for (int nseg = 1; nseg <= chunks; ++nseg) {
+        const int seg_chunks = (chunks + nseg - 1) / nseg;
+        if ((chunks + seg_chunks - 1) / seg_chunks != nseg) continue;  // same as a smaller nseg
+        const long long w = (heads * nseg + sms - 1) / sms;
+        const double cost = (double)w * (seg_chunks + kFixedChunks);
+        if (cost < best - 1e-9) {
+            best = cost;
             pl.seg_len = seg_chunks * C;
             pl.nseg = nseg;
         }
+        if (w > 16) break;
     }
     const size_t heads_nseg = (size_t)heads * pl.nseg;
     size_t off = 0;

@@ -1,0 +1,35 @@
+"""Per-rank step time of the cfg3 SP forward at the slice lengths of T = 1, 2, 4, 8 ranks
+(world 1 on one GPU: everything but the all-gather), to bound strong-scaling efficiency."""
+import torch
+
+import paper_2503_05447_b200 as pk
+from paper_2503_05447_b200 import sp
+
+H, D = 16, 128
+comm = sp.NcclComm(0, 1)
+for inst in ("mamba2", "gla"):
+    base = None
+    for T in (1, 2, 4, 8):
+        n = 262144 // T
+        g = torch.Generator(device="cuda").manual_seed(0)
+        q, k, v = (torch.randn(1, n, H, D, device="cuda", generator=g).mul_(0.5).bfloat16() for _ in range(3))
+        spec = pk.LsmSpec.make(inst, D)
+        if inst == "mamba2":
+            spec.mamba2_a_raw = torch.randn(H, device="cuda", generator=g).mul_(0.5)
+            gates = pk.LsmGates(b_pre=torch.randn(1, n, H, device="cuda", generator=g))
+        else:
+            gates = pk.LsmGates(a_pre=torch.randn(1, n, H, D, device="cuda", generator=g).bfloat16())
+        out = torch.empty_like(q)
+        for _ in range(3):
+            sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        base = base or ms
+        print("%s T=%d slice=%d: %.3f ms per rank step; ideal %.3f; efficiency bound %.1f%%"
+              % (inst, T, n, ms, base / T, 100 * base / (T * ms)))
