@@ -45,6 +45,7 @@ CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dt, int esize, ui
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+
 int num_sms();
 
 template <typename F>

@@ -20,6 +20,8 @@ __global__ void lsm_seg_combine(const float* __restrict__ S, const float* __rest
                                 float* __restrict__ zfin, float* __restrict__ logDtot,
                                 int fin_stride, int nseg, int dk, int dv, int norm, int lw, int rev,
                                 int* err) {
+    pdl_wait();
+    pdl_trigger();
     const int bh = blockIdx.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int nm = dk * dv;
@@ -90,6 +92,62 @@ __global__ void sp_rank_combine(const float* __restrict__ gathered, int P, int B
     else z0[(size_t)bh * dk + (e - nm)] = acc;
 }
 
+// SP phase B in one kernel: the decayed prefix over earlier ranks (sp_rank_combine) seeds the
+// decayed exclusive prefix over this rank's segments (lsm_seg_combine): Min per segment and
+// the rank's final state.
+__global__ void sp_rank_seg_combine(const float* __restrict__ gathered, int P, int BH, int rank,
+                                    const float* __restrict__ S, const float* __restrict__ zS,
+                                    const float* __restrict__ logD, float* __restrict__ Min,
+                                    float* __restrict__ zin, float* __restrict__ Mfin, float* __restrict__ zfin,
+                                    int nseg, int dk, int dv, int norm, int lw) {
+    pdl_wait();
+    pdl_trigger();
+    const int bh = blockIdx.y;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nm = dk * dv;
+    const int total = nm + (norm ? dk : 0);
+    if (e >= total) return;
+    const bool isz = e >= nm;
+    const int ee = isz ? e - nm : e;
+    const int row = isz ? ee : ee / dv;
+    const int li = lw == 1 ? 0 : row;
+    float acc = 0.f;
+    for (int i = 0; i < rank; ++i) {
+        const float* pl = gathered + ((size_t)i * BH + bh) * P;
+        acc = __expf(pl[P - lw + li]) * acc + pl[e];
+    }
+    const int stride = isz ? dk : nm;
+    const float* src = isz ? zS : S;
+    float* dst = isz ? zin : Min;
+    const size_t base = (size_t)bh * nseg * stride + ee;
+    for (int i0 = 0; i0 < nseg; i0 += 8) {
+        float sv[8], dvv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u;
+            sv[u] = i < nseg ? src[base + (size_t)i * stride] : 0.f;
+            dvv[u] = i < nseg ? __expf(logD[((size_t)bh * nseg + i) * lw + li]) : 1.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (i0 + u < nseg) {
+                dst[base + (size_t)(i0 + u) * stride] = acc;
+                acc = dvv[u] * acc + sv[u];
+            }
+        }
+    }
+    float* fin = isz ? zfin : Mfin;
+    if (fin) fin[(size_t)bh * (isz ? dk : nm) + ee] = acc;
+}
+
+cudaError_t launch_rank_seg_combine(const float* gathered, int P, int BH, int rank, const float* S, const float* zS,
+                                    const float* logD, float* Min, float* zin, float* Mfin, float* zfin, int nseg,
+                                    int dk, int dv, int norm, int lw, cudaStream_t st) {
+    const int nel = dk * dv + (norm ? dk : 0);
+    return launch_pdl(sp_rank_seg_combine, dim3((nel + 255) / 256, BH), dim3(256), 0, st, gathered, P, BH, rank, S,
+                      zS, logD, Min, zin, Mfin, zfin, nseg, dk, dv, norm, lw);
+}
+
 // SP backward: the adjoint state entering the END of rank `rank`'s slice from the queries of
 // later ranks, from the gathered reverse-time payloads [X_i | log D_i] (X_i = the adjoint at
 // the start of slice i from its own queries): acc = D_i acc + X_i over i = world-1 .. rank+1.
@@ -135,9 +193,8 @@ cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const
                                const float* logD, const float* M0, const float* z0, float* Min,
                                float* zin, float* Mfin, float* zfin, float* logDtot, int fin_stride,
                                int nseg, int dk, int dv, int norm, int lw, int rev, int* err) {
-    lsm_seg_combine<<<grid, 256, 0, st>>>(S, zS, logD, M0, z0, Min, zin, Mfin, zfin, logDtot,
-                                          fin_stride, nseg, dk, dv, norm, lw, rev, err);
-    return cudaGetLastError();
+    return launch_pdl(lsm_seg_combine, grid, dim3(256), 0, st, S, zS, logD, M0, z0, Min, zin, Mfin, zfin, logDtot,
+                      fin_stride, nseg, dk, dv, norm, lw, rev, err);
 }
 cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,
                                 int rank, int dk, int dv, int norm, int lw, float* M0, float* z0) {

@@ -69,6 +69,18 @@ struct LsmFwdParams {
     unsigned long long* trace;  // optional clock64 trace of CTA (0,0,0) [64 chunks][16]
 };
 
+// per-CTA globaltimer at kernel start (after the prologue) and end, slots after the 64 x 16
+// chunk trace: [cta][2] for up to 2048 CTAs
+__device__ __forceinline__ void trace_cta(const LsmFwdParams& p, int which) {
+    if (p.trace != nullptr && threadIdx.x == 0) {
+        const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        if (cta < 2048) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.trace[64 * 16 + cta * 2 + which] = t;
+        }
+    }
+}
 __device__ __forceinline__ void trace_mark(const LsmFwdParams& p, int c, int slot) {
     if (p.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && c < 64) {
         unsigned long long t;

@@ -181,8 +181,8 @@ struct LsmCall {
         p.trace = nullptr;
         if (getenv("LMOE_TRACE")) {
             if (!g_trace) {
-                LMOE_CUDA_CHECK(cudaMalloc(&g_trace, 64 * 16 * 8));
-                LMOE_CUDA_CHECK(cudaMemset(g_trace, 0, 64 * 16 * 8));
+                LMOE_CUDA_CHECK(cudaMalloc(&g_trace, (64 * 16 + 4096) * 8));
+                LMOE_CUDA_CHECK(cudaMemset(g_trace, 0, (64 * 16 + 4096) * 8));
             }
             p.trace = g_trace;
         }
@@ -320,13 +320,14 @@ template <typename T>
 static void sp_phase_b(LsmCall& c, const float* gathered, int rank, float* M0, float* z0,
                        float* M_out, float* z_out) {
     const int P = (int)payload_floats(c.d, c.D);
-    const int nel = c.D * c.D + (c.norm ? c.D : 0);
+    (void)M0; (void)z0;
+    c.mark();  // rank-combine phase (fused with the segment combine below)
     c.mark();
-    LMOE_CUDA_CHECK(lmoe_dev::launch_rank_combine(dim3((nel + 255) / 256, c.B * c.H), c.st,
-                                                  gathered, P, c.B * c.H, rank, c.D, c.D,
-                                                  c.norm ? 1 : 0, c.lw, M0, z0));
+    LMOE_CUDA_CHECK(lmoe_dev::launch_rank_seg_combine(gathered, P, c.B * c.H, rank, c.p.Sseg, c.p.zseg, c.p.logDseg,
+                                                      const_cast<float*>(c.p.Min), const_cast<float*>(c.p.zin),
+                                                      M_out, z_out, c.pl.nseg, c.D, c.D, c.norm ? 1 : 0, c.lw,
+                                                      c.st));
     ++g_launch_count;
-    c.combine(M0, c.norm ? z0 : nullptr, true, M_out, z_out, nullptr, 0);
     c.output_pass<T>();
 }
 
@@ -991,7 +992,7 @@ extern "C" int lmoe_debug_trace_read(unsigned long long* out) {
     return guarded([&]() {
         if (!g_trace) throw Error(LMOE_ERR_ARG, "no trace (set LMOE_TRACE)");
         LMOE_CUDA_CHECK(cudaDeviceSynchronize());
-        LMOE_CUDA_CHECK(cudaMemcpy(out, g_trace, 64 * 16 * 8, cudaMemcpyDeviceToHost));
+        LMOE_CUDA_CHECK(cudaMemcpy(out, g_trace, (64 * 16 + 4096) * 8, cudaMemcpyDeviceToHost));
     });
 }
 

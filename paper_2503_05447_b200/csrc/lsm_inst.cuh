@@ -17,8 +17,8 @@ cudaError_t sp_launch(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CU
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_state_pass<T, DECAY, FM, NORM, REV><<<grid, kStatePassThreads, state_pass_smem<T>(), st>>>(k, v, p);
-    return cudaGetLastError();
+    return launch_pdl(lsm_state_pass<T, DECAY, FM, NORM, REV>, grid, dim3(kStatePassThreads), state_pass_smem<T>(),
+                      st, k, v, p);
 }
 
 template <typename T, int DECAY, int FM, bool NORM, bool REV>
@@ -32,8 +32,8 @@ cudaError_t op_launch(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CU
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_output_pass<T, DECAY, FM, NORM, REV><<<grid, output_pass_threads<T>(), output_pass_smem<T>(), st>>>(q, k, v, o, p);
-    return cudaGetLastError();
+    return launch_pdl(lsm_output_pass<T, DECAY, FM, NORM, REV>, grid, dim3(output_pass_threads<T>()),
+                      output_pass_smem<T>(), st, q, k, v, o, p);
 }
 
 }  // namespace

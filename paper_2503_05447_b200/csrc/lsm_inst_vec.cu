@@ -15,8 +15,8 @@ cudaError_t spv(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CUtensor
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_state_pass_vec<T, FM, NORM, HG, REV><<<grid, kStatePassVecThreads, state_pass_vec_smem<T>(), st>>>(k, v, a, p);
-    return cudaGetLastError();
+    return launch_pdl(lsm_state_pass_vec<T, FM, NORM, HG, REV>, grid, dim3(kStatePassVecThreads),
+                      state_pass_vec_smem<T>(), st, k, v, a, p);
 }
 
 template <typename T, int FM, bool NORM, bool HG>
@@ -29,8 +29,8 @@ cudaError_t opv(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensor
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    lsm_output_pass_vec<T, FM, NORM, HG><<<grid, output_pass_vec_threads<T>(), output_pass_vec_smem<T>(), st>>>(q, k, v, a, o, p);
-    return cudaGetLastError();
+    return launch_pdl(lsm_output_pass_vec<T, FM, NORM, HG>, grid, dim3(output_pass_vec_threads<T>()),
+                      output_pass_vec_smem<T>(), st, q, k, v, a, o, p);
 }
 
 }  // namespace

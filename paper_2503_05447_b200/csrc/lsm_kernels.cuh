@@ -181,6 +181,8 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *sTmem;
+    pdl_wait();  // predecessor's outputs (segment states / prefixes) are visible from here
+    pdl_trigger();
     // forward: last chunk first (weights e^{G_end - G_j} need no pre-pass); REV: first first
     auto chunk_t0 = [&](int it) { return t_begin + (REV ? it : nchunks - 1 - it) * kC; };
 
@@ -423,6 +425,9 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *sTmem;
+    trace_cta(p, 0);
+    pdl_wait();  // predecessor's outputs (segment states / prefixes) are visible from here
+    pdl_trigger();
     const uint32_t tO = tmem + 256;
     const uint32_t tM = tmem + (kBF16 ? 384 : 320);
 
@@ -974,6 +979,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
     }
     tc_fence_before();
     __syncthreads();
+    trace_cta(p, 1);
     if (warp == 1) tmem_dealloc<512>(tmem);
 }
 

@@ -4,9 +4,28 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "lsm_fwd.cuh"
 
 namespace lmoe_dev {
+// Launch with programmatic stream serialization (PDL; see ptx.cuh pdl_wait / pdl_trigger).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 
 struct LsmVariant {
     int decay;  // DecayMode
@@ -37,6 +56,9 @@ cudaError_t launch_seg_combine(dim3 grid, cudaStream_t st, const float* S, const
 cudaError_t launch_sum_states(const float* gathered, int world, int BH, int nm, float* M, cudaStream_t st);
 cudaError_t launch_rank_combine(dim3 grid, cudaStream_t st, const float* gathered, int P, int BH,
                                 int rank, int dk, int dv, int norm, int lw, float* M0, float* z0);
+cudaError_t launch_rank_seg_combine(const float* gathered, int P, int BH, int rank, const float* S, const float* zS,
+                                    const float* logD, float* Min, float* zin, float* Mfin, float* zfin, int nseg,
+                                    int dk, int dv, int norm, int lw, cudaStream_t st);
 cudaError_t launch_rank_combine_rev(const float* gathered, int P, int BH, int rank, int world, int dk, int dv,
                                     int lw, float* X, cudaStream_t st);
 // TokenVector decays (GLA / HGRN2 / RWKV6): variant {decay = 3, fm, norm, hgrn2 in bit 8 of fm}

@@ -104,6 +104,8 @@ __global__ void __launch_bounds__(kStatePassVecThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *sTmem;
+    pdl_wait();  // predecessor's outputs (segment states / prefixes) are visible from here
+    pdl_trigger();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -325,6 +327,8 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *sTmem;
+    pdl_wait();  // predecessor's outputs (segment states / prefixes) are visible from here
+    pdl_trigger();
     const uint32_t tS = tmem, tO = tmem + 128, tM = tmem + (kBF16 ? 256 : 192);
 
     if (warp == 0) {

@@ -52,6 +52,15 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of one chain are launched with programmatic stream serialization: a kernel's
+// prologue overlaps its predecessor's tail; pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible (no-op without PDL); pdl_trigger() lets the next
+// kernel of the stream start launching.  Every kernel waits before it triggers, so data
+// produced two kernels back is complete too.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2503_05447_b200 as pk
 from paper_2503_05447_b200 import _lib
-N, H, D = 262144, 16, 128
+N, H, D = int(os.environ.get("N", 262144)), 16, 128
 g = torch.Generator(device="cuda").manual_seed(0)
 q, k, v = (torch.randn(1, N, H, D, device="cuda", generator=g).mul_(0.5).to(torch.bfloat16) for _ in range(3))
 spec = pk.LsmSpec.make(os.environ.get("INST", "mamba2"), D)
