@@ -294,6 +294,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the layer / backward side numbers")
+    ap.add_argument("--no-graph", action="store_true", help="time direct calls instead of a CUDA-graph replay")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
@@ -327,7 +328,7 @@ def main():
     spec.mamba2_a_raw = torch.randn(HEADS, device=dev, generator=g).mul_(0.5)
     gates = pk.LsmGates(b_pre=b_pre) if args.instance == "mamba2" else None
     out = torch.empty_like(q)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # a side stream (CUDA-graph capture needs a non-default stream)
 
     def step(timing=False):
         spm.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False,
@@ -338,10 +339,29 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(args.warmup):
-        step()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
     barrier()
     _lib.timing_read(8)  # drop warm-up timings
+
+    # The step (kernels + the NCCL all-gather) is captured once as a CUDA graph and replayed:
+    # the timed region is then free of host submission gaps.  --no-graph times direct calls.
+    graph, per_step = None, None
+    if not args.no_graph:
+        try:
+            n0 = pk.launch_count()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step()
+            per_step = pk.launch_count() - n0
+            graph = g
+            graph.replay()
+            barrier()
+        except Exception as exc:  # noqa: BLE001 -- capture unsupported here: time direct calls
+            print("bench: CUDA graph capture failed (%s); timing direct calls" % exc, file=sys.stderr)
+            graph = None
+            barrier()
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -350,13 +370,23 @@ def main():
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        step(timing=True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
     e1.record(stream)
     barrier()
-    launches = pk.launch_count() - launches0
+    launches = per_step * args.steps if graph is not None else pk.launch_count() - launches0
     ms_total = e0.elapsed_time(e1)
     clk = clocks.stop()
+    # per-phase device times (roofline of the dominant kernel): the same step with CUDA events
+    # between its kernels, outside the timed region
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step(timing=True)
+    barrier()
     calls, phase_ms = _lib.timing_read(8)
     # phases of lmoe_sp_lsm_fwd: 0 state pass, 1 local combine, 2 all-gather,
     # 3 rank combine, 4 segment combine, 5 output pass
@@ -424,8 +454,8 @@ def main():
     alg_bytes = ALG_BYTES_TH[args.instance] * units
     achieved = alg_bytes / (out_pass_ms / 1e3) / 1e9
     step_alg = ALG_BYTES_TH[args.instance] * units / (ms_step / 1e3) / 1e9
-    phase_names = ["state_pass", "local_combine", "all_gather", "rank_combine", "seg_combine",
-                   "output_pass"]
+    phase_names = ["state_pass", "local_combine", "all_gather", "rank_combine(fused into next)",
+                   "rank_seg_combine", "output_pass"]
 
     if rank == 0:
         cb = None
@@ -445,6 +475,7 @@ def main():
                                    % args.instance,
                        "seq_len": SEQ, "heads": HEADS, "head_dim": HEAD_DIM, "batch": 1,
                        "tokens_per_rank": n_loc, "parallelism": "sp%d" % world,
+                       "timed": "CUDA-graph replay of the step" if graph is not None else "direct calls",
                        "l2": "inputs 3 GiB > L2; no flush needed"},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
