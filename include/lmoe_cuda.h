@@ -169,6 +169,13 @@ size_t lmoe_block_workspace_size(const lmoe_block_desc* desc, int B, int N_local
 int lmoe_block_fwd(const lmoe_block_desc* desc, const lmoe_block_weights* weights, int B,
                    int N_local, int N_total, float* x, float* aux, void* nccl_comm, int rank,
                    int world, void* workspace, size_t workspace_bytes, lmoe_stream_t stream);
+/* One block over packed documents (model_forward, model.hpp:374-405): norms, projections and
+ * the MoE over all T rows; the mixer (LSM or causal attention) per document of cu_seqlens
+ * (HOST array, 0 .. T).  x: fp32 [T, hidden] residual stream, updated in place. */
+size_t lmoe_block_varlen_workspace_size(const lmoe_block_desc* desc, int T, const int* cu_seqlens, int n_docs);
+int lmoe_block_fwd_varlen(const lmoe_block_desc* desc, const lmoe_block_weights* weights, int T,
+                          const int* cu_seqlens, int n_docs, float* x, float* aux, void* workspace,
+                          size_t workspace_bytes, lmoe_stream_t stream);
 /* x[t] = embedding[tokens[t]] + pos_embedding[pos0 + t % n] (model.hpp:385-386), fp32 out */
 int lmoe_embed(const int* tokens, int rows, int n, int pos0, int hidden, const void* embedding,
                const void* pos_embedding, float* x, lmoe_stream_t stream);
@@ -197,6 +204,24 @@ int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dty
                  const float* dM_final, void* dq, void* dk, void* dv, void* da_pre,
                  float* db_pre, float* da_raw, float* dM0, void* workspace,
                  size_t workspace_bytes, lmoe_stream_t stream);
+
+/* Packed documents (PackedBatch, model.hpp:86-121; model_forward runs the mixer per document,
+ * model.hpp:374-405): q, k, v, ... are [1, T, H, D] with document i in rows
+ * [cu_seqlens[i], cu_seqlens[i+1]) (HOST array, 0 .. T, strictly ascending); the state is
+ * zero at every document start.  M_out: [n_docs, H, D, D] final states (may be NULL).
+ * backward: da_raw sums over documents (workspace from the size query with backward = 1,
+ * plus H floats when da_raw is requested). */
+size_t lmoe_lsm_varlen_workspace_size(const lmoe_lsm_desc* desc, int T, const int* cu_seqlens, int n_docs,
+                                      int H, int D, lmoe_dtype dtype, int backward);
+int lmoe_lsm_fwd_varlen(const lmoe_lsm_desc* desc, int T, const int* cu_seqlens, int n_docs, int H, int D,
+                        lmoe_dtype dtype, const void* q, const void* k, const void* v, const void* a_pre,
+                        const float* b_pre, const float* a_raw, void* o, float* M_out, void* workspace,
+                        size_t workspace_bytes, lmoe_stream_t stream);
+int lmoe_lsm_bwd_varlen(const lmoe_lsm_desc* desc, int T, const int* cu_seqlens, int n_docs, int H, int D,
+                        lmoe_dtype dtype, const void* q, const void* k, const void* v, const void* a_pre,
+                        const float* b_pre, const float* a_raw, const void* dO, void* dq, void* dk, void* dv,
+                        void* da_pre, float* db_pre, float* da_raw, void* workspace, size_t workspace_bytes,
+                        lmoe_stream_t stream);
 
 /* Number of kernels one lmoe_lsm_fwd call launches (for launch accounting). */
 int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc);

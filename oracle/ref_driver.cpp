@@ -452,6 +452,16 @@ void golden_model() {
         emit_scalar(p + "/aux", fo.aux_loss.item());
         RankGroup g2(2);
         emit(p + "/logits_sp2", hybrid_sp_forward(g2, m, batch));
+        // packed documents (model.hpp:86-121, 374-405): the mixer runs per document, positions
+        // restart at each boundary; the MoE sees all tokens
+        const std::vector<int> d0(toks.begin(), toks.begin() + 100), d1(toks.begin() + 100, toks.begin() + 137),
+            d2(toks.begin() + 137, toks.end());
+        const PackedBatch packed = pack_sequences({d0, d1, d2});
+        std::vector<double> bounds(packed.boundaries.begin(), packed.boundaries.end());
+        emit(p + "/packed_bounds", {(int)bounds.size()}, bounds);
+        const ForwardOut fp = model_forward(m, packed);
+        emit(p + "/packed_logits", fp.logits);
+        emit_scalar(p + "/packed_aux", fp.aux_loss.item());
         ++ci;
     }
 }

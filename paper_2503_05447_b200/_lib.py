@@ -54,6 +54,12 @@ def lib():
     L.lmoe_lsm_bwd_workspace_size.argtypes = [ctypes.POINTER(LsmDesc), i, i, i, i, i]
     L.lmoe_lsm_bwd.restype = i
     L.lmoe_lsm_bwd.argtypes = [ctypes.POINTER(LsmDesc), i, i, i, i, i] + [vp] * 17 + [sz, vp]
+    L.lmoe_lsm_varlen_workspace_size.restype = sz
+    L.lmoe_lsm_varlen_workspace_size.argtypes = [ctypes.POINTER(LsmDesc), i, vp, i, i, i, i, i]
+    L.lmoe_lsm_fwd_varlen.restype = i
+    L.lmoe_lsm_fwd_varlen.argtypes = [ctypes.POINTER(LsmDesc), i, vp, i, i, i, i] + [vp] * 9 + [sz, vp]
+    L.lmoe_lsm_bwd_varlen.restype = i
+    L.lmoe_lsm_bwd_varlen.argtypes = [ctypes.POINTER(LsmDesc), i, vp, i, i, i, i] + [vp] * 14 + [sz, vp]
     L.lmoe_timing_read.restype = i
     L.lmoe_timing_read.argtypes = [ctypes.POINTER(ctypes.c_float), i]
     _lib = L

@@ -153,17 +153,11 @@ extern "C" size_t lmoe_block_workspace_size(const lmoe_block_desc* desc, int B, 
     return plan_block(desc, B, N_local, N_total, world).total;
 }
 
-extern "C" int lmoe_block_fwd(const lmoe_block_desc* d, const lmoe_block_weights* wt, int B, int N_local,
-                              int N_total, float* x, float* aux, void* nccl_comm, int rank, int world,
-                              void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
-    return guarded([&]() {
-        block_validate(d);
-        if (!wt || !x) throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: null weights or activations");
-        if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: bad rank");
-        if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: null communicator");
-        const BlockWs w = plan_block(d, B, N_local, N_total, world);
-        if (!workspace || workspace_bytes < w.total)
-            throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: workspace too small (need " + std::to_string(w.total) + " bytes)");
+namespace lmoe_host {
+// One block; cu != nullptr: packed documents (B = 1, N_local = T), the mixer per document.
+static void block_core(const lmoe_block_desc* d, const lmoe_block_weights* wt, int B, int N_local, int N_total,
+                       float* x, float* aux, void* nccl_comm, int rank, int world, const BlockWs& w,
+                       void* workspace, lmoe_stream_t stream, const int* cu, int n_docs) {
         uint8_t* ws = static_cast<uint8_t*>(workspace);
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         const int T = B * N_local, hid = d->hidden, H = d->heads, D = 128;
@@ -188,9 +182,28 @@ extern "C" int lmoe_block_fwd(const lmoe_block_desc* d, const lmoe_block_weights
                 ++g_launch_count;
                 b_pre = reinterpret_cast<const float*>(ws + w.bpre);
             }
-            lsm_mixer_core(&d->lsm, B, N_local, H, D, LMOE_BF16, qkv, qkv + col, qkv + 2 * col,
-                           mode == 3 ? qkv + 3 * col : nullptr, w.nc, b_pre, wt->a_raw, o, nccl_comm, rank, world,
-                           ws + w.mixer, w.mixer_bytes, st);
+            if (cu) {
+                for (int i = 0; i < n_docs; ++i) {
+                    const size_t r0 = (size_t)cu[i];
+                    uint8_t* qd = qkv + r0 * w.nc * 2;
+                    lsm_mixer_core(&d->lsm, 1, cu[i + 1] - cu[i], H, D, LMOE_BF16, qd, qd + col, qd + 2 * col,
+                                   mode == 3 ? qd + 3 * col : nullptr, w.nc, b_pre ? b_pre + r0 * H : nullptr,
+                                   wt->a_raw, static_cast<uint8_t*>(o) + r0 * hid * 2, nullptr, 0, 1, ws + w.mixer,
+                                   w.mixer_bytes, st);
+                }
+            } else {
+                lsm_mixer_core(&d->lsm, B, N_local, H, D, LMOE_BF16, qkv, qkv + col, qkv + 2 * col,
+                               mode == 3 ? qkv + 3 * col : nullptr, w.nc, b_pre, wt->a_raw, o, nccl_comm, rank,
+                               world, ws + w.mixer, w.mixer_bytes, st);
+            }
+        } else if (cu) {
+            for (int i = 0; i < n_docs; ++i) {
+                const size_t r0 = (size_t)cu[i];
+                const int len = cu[i + 1] - cu[i];
+                uint8_t* qd = qkv + r0 * w.nc * 2;
+                attn_core(1, len, len, H, D, qd, qd + col, qd + 2 * col, w.nc, static_cast<uint8_t*>(o) + r0 * hid * 2,
+                          0, st);
+            }
         } else if (world == 1) {
             attn_core(B, N_local, N_local, H, D, qkv, qkv + col, qkv + 2 * col, w.nc, o, 0, st);
         } else {
@@ -206,6 +219,61 @@ extern "C" int lmoe_block_fwd(const lmoe_block_desc* d, const lmoe_block_weights
                                         ws + w.moe, w.moe_bytes, stream);
         if (rc != LMOE_OK) throw Error(rc, lmoe_last_error());
         add_rmsnorm(x, ws + w.y, true, nullptr, 0.f, nullptr, T, hid, st);
+}
+}  // namespace lmoe_host
+
+extern "C" int lmoe_block_fwd(const lmoe_block_desc* d, const lmoe_block_weights* wt, int B, int N_local,
+                              int N_total, float* x, float* aux, void* nccl_comm, int rank, int world,
+                              void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        block_validate(d);
+        if (!wt || !x) throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: null weights or activations");
+        if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: bad rank");
+        if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: null communicator");
+        const BlockWs w = plan_block(d, B, N_local, N_total, world);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: workspace too small (need " + std::to_string(w.total) + " bytes)");
+        block_core(d, wt, B, N_local, N_total, x, aux, nccl_comm, rank, world, w, workspace, stream, nullptr, 0);
+    });
+}
+
+namespace lmoe_host {
+static BlockWs plan_block_varlen(const lmoe_block_desc* d, int T, const int* cu, int n_docs) {
+    BlockWs w = plan_block(d, 1, T, T, 1);
+    size_t mix = 0;  // the mixer workspace of the longest document (attention needs none)
+    for (int i = 0; i < n_docs; ++i)
+        if (d->kind == 'L') mix = std::max(mix, lsm_mixer_ws(&d->lsm, 1, cu[i + 1] - cu[i], d->heads, 128, 1));
+    if (mix > w.mixer_bytes) {
+        w.total += align_up(mix - w.mixer_bytes, 256);
+        w.moe += align_up(mix - w.mixer_bytes, 256);
+        w.mixer_bytes = mix;
+    }
+    return w;
+}
+}  // namespace lmoe_host
+
+extern "C" size_t lmoe_block_varlen_workspace_size(const lmoe_block_desc* desc, int T, const int* cu_seqlens,
+                                                   int n_docs) {
+    if (!desc || T < 1 || !cu_seqlens || n_docs < 1) return 0;
+    return plan_block_varlen(desc, T, cu_seqlens, n_docs).total;
+}
+
+extern "C" int lmoe_block_fwd_varlen(const lmoe_block_desc* d, const lmoe_block_weights* wt, int T,
+                                     const int* cu_seqlens, int n_docs, float* x, float* aux, void* workspace,
+                                     size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        block_validate(d);
+        if (!wt || !x) throw Error(LMOE_ERR_ARG, "lmoe_block_fwd: null weights or activations");
+        if (!cu_seqlens || n_docs < 1 || cu_seqlens[0] != 0 || cu_seqlens[n_docs] != T)
+            throw Error(LMOE_ERR_ARG, "PackedBatch: boundaries must run from 0 to total length");
+        for (int i = 1; i <= n_docs; ++i)
+            if (cu_seqlens[i] <= cu_seqlens[i - 1])
+                throw Error(LMOE_ERR_ARG, "PackedBatch: boundaries must be strictly ascending");
+        const BlockWs w = plan_block_varlen(d, T, cu_seqlens, n_docs);
+        if (!workspace || workspace_bytes < w.total)
+            throw Error(LMOE_ERR_ARG, "lmoe_block_fwd_varlen: workspace too small (need " + std::to_string(w.total) +
+                                          " bytes)");
+        block_core(d, wt, 1, T, T, x, aux, nullptr, 0, 1, w, workspace, stream, cu_seqlens, n_docs);
     });
 }
 

@@ -1193,3 +1193,96 @@ extern "C" int lmoe_sp_lsm_bwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
         }
     });
 }
+
+// ------------------------------------------------------------- packed documents (varlen)
+// model_forward (model.hpp:374-405) runs the mixer once per document of a PackedBatch
+// (model.hpp:86-121): the state starts from zero at every boundary.  Each document is a
+// dense row range of the packed [1, T, H, D] tensors, so the TMA bounds of its views clip
+// exactly at the document end.  cu_seqlens is a HOST array of n_docs + 1 ascending offsets
+// from 0 to T (PackedBatch::boundaries).
+namespace lmoe_host {
+static void check_bounds(const int* cu, int n_docs, int T) {
+    if (!cu || n_docs < 1 || cu[0] != 0 || cu[n_docs] != T)
+        throw Error(LMOE_ERR_ARG, "PackedBatch: boundaries must run from 0 to total length");
+    for (int i = 1; i <= n_docs; ++i)
+        if (cu[i] <= cu[i - 1]) throw Error(LMOE_ERR_ARG, "PackedBatch: boundaries must be strictly ascending");
+}
+static int max_doc(const int* cu, int n_docs) {
+    int m = 0;
+    for (int i = 0; i < n_docs; ++i) m = std::max(m, cu[i + 1] - cu[i]);
+    return m;
+}
+}  // namespace lmoe_host
+
+extern "C" size_t lmoe_lsm_varlen_workspace_size(const lmoe_lsm_desc* desc, int T, const int* cu_seqlens,
+                                                 int n_docs, int H, int D, lmoe_dtype dtype, int backward) {
+    if (!desc || T < 1 || !cu_seqlens || n_docs < 1 || H < 1 || D < 1) return 0;
+    size_t m = 0;
+    for (int i = 0; i < n_docs; ++i) {
+        const int len = cu_seqlens[i + 1] - cu_seqlens[i];
+        if (len < 1) return 0;
+        m = std::max(m, backward ? lmoe_lsm_bwd_workspace_size(desc, 1, len, H, D, dtype)
+                                 : plan_lsm(1, len, H, D).total);
+    }
+    return m;
+}
+
+extern "C" int lmoe_lsm_fwd_varlen(const lmoe_lsm_desc* desc, int T, const int* cu_seqlens, int n_docs, int H,
+                                   int D, lmoe_dtype dtype, const void* q, const void* k, const void* v,
+                                   const void* a_pre, const float* b_pre, const float* a_raw, void* o,
+                                   float* M_out, void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, 1, T, H, D, dtype, q, k, v, o);
+        check_bounds(cu_seqlens, n_docs, T);
+        const size_t esz = dtype == LMOE_BF16 ? 2 : 4;
+        const size_t row = (size_t)H * D * esz;
+        for (int i = 0; i < n_docs; ++i) {
+            const int r0 = cu_seqlens[i], len = cu_seqlens[i + 1] - r0;
+            auto at = [&](const void* p) -> const void* { return p ? static_cast<const uint8_t*>(p) + r0 * row : nullptr; };
+            const int rc = lmoe_lsm_fwd(desc, 1, len, H, D, dtype, at(q), at(k), at(v), at(a_pre),
+                                        b_pre ? b_pre + (size_t)r0 * H : nullptr, a_raw, nullptr, nullptr,
+                                        static_cast<uint8_t*>(o) + r0 * row,
+                                        M_out ? M_out + (size_t)i * H * D * D : nullptr, nullptr, workspace,
+                                        workspace_bytes, stream);
+            if (rc != LMOE_OK) throw Error(rc, lmoe_last_error());
+        }
+    });
+}
+
+extern "C" int lmoe_lsm_bwd_varlen(const lmoe_lsm_desc* desc, int T, const int* cu_seqlens, int n_docs, int H,
+                                   int D, lmoe_dtype dtype, const void* q, const void* k, const void* v,
+                                   const void* a_pre, const float* b_pre, const float* a_raw, const void* dO,
+                                   void* dq, void* dk, void* dv, void* da_pre, float* db_pre, float* da_raw,
+                                   void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
+    return guarded([&]() {
+        validate(desc, 1, T, H, D, dtype, q, k, v, dO);
+        check_bounds(cu_seqlens, n_docs, T);
+        const size_t esz = dtype == LMOE_BF16 ? 2 : 4;
+        const size_t row = (size_t)H * D * esz;
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+        // da_raw sums over documents: each document's contribution lands in a scratch slot
+        // after the largest document's workspace, then accumulates
+        const size_t need = lmoe_lsm_varlen_workspace_size(desc, T, cu_seqlens, n_docs, H, D, dtype, 1);
+        float* dar = nullptr;
+        if (da_raw) {
+            if (!workspace || workspace_bytes < align_up(need, 256) + (size_t)H * 4)
+                throw Error(LMOE_ERR_ARG, "lmoe_lsm_bwd_varlen: workspace too small");
+            dar = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + align_up(need, 256));
+            LMOE_CUDA_CHECK(cudaMemsetAsync(da_raw, 0, (size_t)H * 4, st));
+        }
+        for (int i = 0; i < n_docs; ++i) {
+            const int r0 = cu_seqlens[i], len = cu_seqlens[i + 1] - r0;
+            auto at = [&](const void* p) -> const void* { return p ? static_cast<const uint8_t*>(p) + r0 * row : nullptr; };
+            auto atw = [&](void* p) -> void* { return p ? static_cast<uint8_t*>(p) + r0 * row : nullptr; };
+            const int rc = lmoe_lsm_bwd(desc, 1, len, H, D, dtype, at(q), at(k), at(v), at(a_pre),
+                                        b_pre ? b_pre + (size_t)r0 * H : nullptr, a_raw, nullptr, at(dO), nullptr,
+                                        atw(dq), atw(dk), atw(dv), atw(da_pre),
+                                        db_pre ? db_pre + (size_t)r0 * H : nullptr, dar, nullptr, workspace, need,
+                                        stream);
+            if (rc != LMOE_OK) throw Error(rc, lmoe_last_error());
+            if (da_raw)
+                LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(2, false, da_raw, dar, nullptr, nullptr, nullptr, nullptr,
+                                                              1, H, nullptr, st));
+        }
+    });
+}

@@ -248,3 +248,65 @@ class LsmFunction(torch.autograd.Function):
         gates = LsmGates(b_pre=b_pre) if b_pre is not None else None
         g = lsm_backward_batched(q, k, v, gates, ctx.spec, dO.to(q.dtype), chunk_size=ctx.chunk, check=False)
         return g.dq, g.dk, g.dv, g.db_pre, None, None
+
+
+def _cu_array(cu_seqlens):
+    """Host int32 array of PackedBatch::boundaries (model.hpp:86-121)."""
+    import numpy as np
+    arr = np.ascontiguousarray(np.asarray(list(cu_seqlens), dtype=np.int32))
+    return arr, arr.ctypes.data_as(ctypes.c_void_p), len(arr) - 1
+
+
+def lsm_forward_varlen(q, k, v, gates, spec, cu_seqlens, chunk_size=64, final_states=False, check=True,
+                       stream=None):
+    """Packed documents: q, k, v [1, T, H, D]; document i = rows [cu[i], cu[i+1]); the state is
+    zero at every boundary (model_forward runs the mixer per document, model.hpp:374-405).
+    Returns o (and [n_docs, H, D, D] final states when final_states)."""
+    _, T, H, D = q.shape
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    cu, cu_p, n_docs = _cu_array(cu_seqlens)
+    a_raw = None
+    if spec.instance == LsmInstance.MAMBA2:
+        a_raw = torch.as_tensor(spec.mamba2_a_raw, dtype=torch.float32, device=q.device).reshape(-1).expand(H).contiguous()
+    b_pre = gates.b_pre.to(torch.float32).contiguous() if gates is not None and gates.b_pre is not None else None
+    a_pre = gates.a_pre.to(q.dtype).contiguous() if gates is not None and gates.a_pre is not None else None
+    o = torch.empty_like(q)
+    M = torch.empty(n_docs, H, D, D, dtype=torch.float32, device=q.device) if final_states else None
+    desc = make_desc(spec, chunk_size, check)
+    L = _lib.lib()
+    dt = _DTYPES[q.dtype]
+    ws = _workspace(L.lmoe_lsm_varlen_workspace_size(ctypes.byref(desc), T, cu_p, n_docs, H, D, dt, 0), q.device)
+    st = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+    P = _lib.ptr
+    _lib.check(L.lmoe_lsm_fwd_varlen(ctypes.byref(desc), T, cu_p, n_docs, H, D, dt, P(q), P(k), P(v), P(a_pre),
+                                     P(b_pre), P(a_raw), P(o), P(M), P(ws), ws.numel(), ctypes.c_void_p(st)))
+    return (o, M) if final_states else o
+
+
+def lsm_backward_varlen(q, k, v, gates, spec, dO, cu_seqlens, chunk_size=64, check=True, stream=None):
+    """VJP of lsm_forward_varlen; da_raw sums over documents."""
+    _, T, H, D = q.shape
+    q, k, v, dO = q.contiguous(), k.contiguous(), v.contiguous(), dO.contiguous()
+    cu, cu_p, n_docs = _cu_array(cu_seqlens)
+    a_raw = None
+    if spec.instance == LsmInstance.MAMBA2:
+        a_raw = torch.as_tensor(spec.mamba2_a_raw, dtype=torch.float32, device=q.device).reshape(-1).expand(H).contiguous()
+    b_pre = gates.b_pre.to(torch.float32).contiguous() if gates is not None and gates.b_pre is not None else None
+    a_pre = gates.a_pre.to(q.dtype).contiguous() if gates is not None and gates.a_pre is not None else None
+    g = LsmGrads(dq=torch.empty_like(q), dk=torch.empty_like(q), dv=torch.empty_like(q))
+    if spec.instance == LsmInstance.MAMBA2:
+        g.db_pre = torch.empty(1, T, H, dtype=torch.float32, device=q.device)
+        g.da_raw = torch.empty(H, dtype=torch.float32, device=q.device)
+    if a_pre is not None:
+        g.da_pre = torch.empty_like(a_pre)
+    desc = make_desc(spec, chunk_size, check)
+    L = _lib.lib()
+    dt = _DTYPES[q.dtype]
+    need = L.lmoe_lsm_varlen_workspace_size(ctypes.byref(desc), T, cu_p, n_docs, H, D, dt, 1)
+    ws = _workspace(need + 256 + 4 * H, q.device)
+    st = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+    P = _lib.ptr
+    _lib.check(L.lmoe_lsm_bwd_varlen(ctypes.byref(desc), T, cu_p, n_docs, H, D, dt, P(q), P(k), P(v), P(a_pre),
+                                     P(b_pre), P(a_raw), P(dO), P(g.dq), P(g.dk), P(g.dv), P(g.da_pre), P(g.db_pre),
+                                     P(g.da_raw), P(ws), ws.numel(), ctypes.c_void_p(st)))
+    return g

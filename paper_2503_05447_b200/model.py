@@ -4,6 +4,8 @@
   Model.init(cfg, seed)             build_model (model.hpp:336-362): same shapes and init scales
   Model.from_arrays(arrays)         load parameters (e.g. the reference's own, tests/golden)
   Model.forward(tokens)             model_forward (model.hpp:374-405) for equal-length docs
+  Model.forward_packed(tokens, b)   model_forward over a PackedBatch (model.hpp:86-121):
+                                    positions restart and the mixer runs per document
   Model.forward(tokens, comm, n)    hybrid_sp_forward (parallel.hpp:477-506): this rank's
                                     chunk_range slice of ONE document; L blocks use masked
                                     state SP, N blocks the K/V all-gather
@@ -43,6 +45,11 @@ def _bind():
     L.lmoe_block_fwd.restype = i
     L.lmoe_block_fwd.argtypes = [ctypes.POINTER(_BlockDesc), ctypes.POINTER(_BlockWeights), i, i, i, vp, vp, vp,
                                  i, i, vp, sz, vp]
+    L.lmoe_block_varlen_workspace_size.restype = sz
+    L.lmoe_block_varlen_workspace_size.argtypes = [ctypes.POINTER(_BlockDesc), i, vp, i]
+    L.lmoe_block_fwd_varlen.restype = i
+    L.lmoe_block_fwd_varlen.argtypes = [ctypes.POINTER(_BlockDesc), ctypes.POINTER(_BlockWeights), i, vp, i, vp,
+                                        vp, vp, sz, vp]
     L.lmoe_embed.restype = i
     L.lmoe_embed.argtypes = [vp, i, i, i, i, vp, vp, vp, vp]
     L.lmoe_rmsnorm.restype = i
@@ -199,6 +206,47 @@ class Model:
                                     comm.handle if comm is not None else None, rank, world, ws.data_ptr(),
                                     ws.numel(), st))
         return aux
+
+    def forward_packed(self, tokens, boundaries, stream=None):
+        """model_forward (model.hpp:374-405) over one flat token stream with ascending document
+        boundaries (PackedBatch, model.hpp:86-121): per-document positions, the mixer per
+        document (lmoe_block_fwd_varlen), the MoE over all tokens.
+        Returns (logits fp32 [T, vocab], aux = mean block load-balance loss)."""
+        import numpy as np
+        L = _bind()
+        c = self.cfg
+        dev = self.embedding.device
+        cu = np.ascontiguousarray(np.asarray(list(boundaries), dtype=np.int32))
+        n_docs = len(cu) - 1
+        T = int(cu[-1])
+        tok = tokens.reshape(-1).to(dev, torch.int32).contiguous()
+        if len(cu) < 2 or cu[0] != 0 or tok.numel() != T:
+            raise RuntimeError("PackedBatch: boundaries must run from 0 to total length")
+        if (np.diff(cu) <= 0).any():
+            raise RuntimeError("PackedBatch: boundaries must be strictly ascending")
+        if int(np.diff(cu).max()) > c.max_seq_len:
+            raise RuntimeError("model_forward: document longer than max_seq_len")
+        st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        x = torch.empty(T, c.hidden, dtype=torch.float32, device=dev)
+        for i in range(n_docs):  # positions restart per document (model.hpp:379-384)
+            r0, n = int(cu[i]), int(cu[i + 1] - cu[i])
+            _lib.check(L.lmoe_embed(tok[r0:].data_ptr(), n, n, 0, c.hidden, self.embedding.data_ptr(),
+                                    self.pos_embedding.data_ptr(), x[r0:].data_ptr(), st))
+        aux = torch.zeros(len(self.blocks), dtype=torch.float32, device=dev)
+        cu_p = cu.ctypes.data_as(ctypes.c_void_p)
+        for i, b in enumerate(self.blocks):
+            d = self._desc(b.kind)
+            ws = _workspace(L.lmoe_block_varlen_workspace_size(ctypes.byref(d), T, cu_p, n_docs), dev)
+            w = self._weights(b)
+            _lib.check(L.lmoe_block_fwd_varlen(ctypes.byref(d), ctypes.byref(w), T, cu_p, n_docs, x.data_ptr(),
+                                               aux[i:].data_ptr(), ws.data_ptr(), ws.numel(), st))
+        h = torch.empty(T, c.hidden, dtype=BF16, device=dev)
+        _lib.check(L.lmoe_rmsnorm(x.data_ptr(), T, c.hidden, self.final_norm.data_ptr(), c.norm_eps, h.data_ptr(), st))
+        logits = torch.empty(T, c.vocab_size, dtype=torch.float32, device=dev)
+        ws = _workspace(L.lmoe_gemm_workspace_size(T), dev)
+        _lib.check(L.lmoe_gemm(h.data_ptr(), T, c.hidden, c.hidden, self.lm_head.data_ptr(), c.vocab_size,
+                               logits.data_ptr(), c.vocab_size, 1, ws.data_ptr(), ws.numel(), st))
+        return logits, aux.mean()
 
     def forward(self, tokens, comm=None, n_total=None, stream=None):
         """tokens: int [B, N] (B equal-length documents), or this rank's [1, N_local] slice of

@@ -190,3 +190,59 @@ def test_large_config2_heads_subset():
             want, _, _ = oracle.lsm_chunked(oracle.spec_default(inst), qq, kk, vv, chunk=128)
             err = norm_rel_err(o[0, :, h].float().cpu().numpy(), want)
             assert err < 2e-2, (inst, h, err)
+
+
+
+@pytest.mark.parametrize("inst", ["retnet", "mamba2", "gla"])
+def test_varlen_matches_per_document_calls(inst):
+    """Packed documents (lmoe_lsm_fwd_varlen / _bwd_varlen) equal independent per-document calls
+    (the state is zero at every boundary), forward and backward; one document vs the oracle."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_05447_b200 as pk
+    from paper_2503_05447_b200.lsm import lsm_backward_varlen, lsm_forward_varlen
+    bounds = [0, 300, 337, 1000, 1129]
+    T, H, D = bounds[-1], 2, 128
+    g = torch.Generator(device="cuda").manual_seed(4)
+    q, k, v, dO = (torch.randn(1, T, H, D, device="cuda", generator=g).mul_(0.5).bfloat16() for _ in range(4))
+    spec = pk.LsmSpec.make(inst, D)
+    gates = None
+    if inst == "mamba2":
+        spec.mamba2_a_raw = torch.tensor([0.3, -0.2], device="cuda")
+        gates = pk.LsmGates(b_pre=torch.randn(1, T, H, device="cuda", generator=g))
+    elif inst == "gla":
+        gates = pk.LsmGates(a_pre=torch.randn(1, T, H, D, device="cuda", generator=g).add_(2.0).bfloat16())
+    o, M = lsm_forward_varlen(q, k, v, gates, spec, bounds, final_states=True)
+    gv = lsm_backward_varlen(q, k, v, gates, spec, dO, bounds)
+    dar = torch.zeros(H, device="cuda")
+    for i in range(len(bounds) - 1):
+        r0, r1 = bounds[i], bounds[i + 1]
+        sl = lambda t: None if t is None else t[:, r0:r1].contiguous()
+        gd = None if gates is None else pk.LsmGates(a_pre=sl(gates.a_pre), b_pre=sl(gates.b_pre))
+        fs = pk.MemoryState()
+        od = pk.lsm_forward_batched(sl(q), sl(k), sl(v), gd, spec, 64, final_state=fs)
+        assert torch.equal(o[:, r0:r1], od), i
+        assert torch.equal(M[i], fs.M[0]), i
+        gr = pk.lsm_backward_batched(sl(q), sl(k), sl(v), gd, spec, sl(dO))
+        for n in ("dq", "dk", "dv", "da_pre", "db_pre"):
+            a, b = getattr(gv, n), getattr(gr, n)
+            if b is not None:
+                assert torch.equal(a[:, r0:r1], b), (i, n)
+        if gr.da_raw is not None:
+            dar += gr.da_raw
+    if gv.da_raw is not None:
+        assert torch.allclose(gv.da_raw, dar, rtol=1e-5, atol=1e-6)
+    # document 1 (37 tokens) against the oracle from the zero state
+    r0, r1 = bounds[1], bounds[2]
+    for h in range(H):
+        sd = oracle.spec_default(inst)
+        b = a = None
+        if inst == "mamba2":
+            sd["mamba2_a_raw"] = float(spec.mamba2_a_raw[h])
+            b = gates.b_pre[0, r0:r1, h].cpu().numpy()
+        if inst == "gla":
+            a = gates.a_pre[0, r0:r1, h].float().cpu().numpy()
+        want, _, _ = oracle.lsm_chunked(sd, *(t[0, r0:r1, h].float().cpu().numpy() for t in (q, k, v)), a_pre=a,
+                                        b_pre=b)
+        assert norm_rel_err(o[0, r0:r1, h].float().cpu().numpy(), want) < 2e-2

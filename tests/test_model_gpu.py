@@ -73,3 +73,22 @@ def test_model_config_errors():
     from paper_2503_05447_b200.model import ModelConfig
     with pytest.raises(RuntimeError, match="invalid pattern char 'X'"):
         ModelConfig(pattern="LX").validate()
+
+
+@pytest.mark.parametrize("tag", ["mamba2_hybrid", "gla"])
+def test_packed_documents_match_reference(tag):
+    """model_forward over a PackedBatch of three documents (100 / 37 / 119 tokens): per-document
+    positions and mixer state (the reference's own packed logits, tests/golden/model.npz)."""
+    torch, model, a = _model(tag)
+    tokens = torch.tensor(a["tokens"].astype(np.int64))
+    bounds = a["packed_bounds"].astype(np.int64).tolist()
+    logits, aux = model.forward_packed(tokens, bounds)
+    torch.cuda.synchronize()
+    got = logits.double().cpu().numpy()
+    err = norm_rel_err(got, a["packed_logits"])
+    assert err < TOL_LOGITS, err
+    # documents are independent: the packed logits differ from the one-document run
+    assert norm_rel_err(a["packed_logits"], a["logits"]) > 1e-3
+    assert abs(aux.item() - a["packed_aux"][0]) <= 2e-2 * abs(a["packed_aux"][0])
+    with pytest.raises(RuntimeError, match="strictly ascending"):
+        model.forward_packed(tokens, [0, 100, 100, 256])
