@@ -48,7 +48,10 @@ typedef enum lmoe_dtype { LMOE_F32 = 0, LMOE_BF16 = 1 } lmoe_dtype;
 /* lmoe::LsmInstance numbering (lsm.hpp:30-48) */
 enum lmoe_instance {
     LMOE_BLA = 0, LMOE_LIGHTNING = 1, LMOE_RETNET = 2, LMOE_GLA = 3, LMOE_REBASED = 6,
-    LMOE_MAMBA2 = 13, LMOE_HGRN2 = 14, LMOE_RWKV6 = 15
+    LMOE_MAMBA2 = 13, LMOE_HGRN2 = 14, LMOE_RWKV6 = 15,
+    /* no chunk-parallel form: lmoe_lsm_fwd_recurrent */
+    LMOE_DELTANET = 4, LMOE_GATED_DELTANET = 5, LMOE_GFW = 7, LMOE_GATELOOP = 8, LMOE_TTT = 9,
+    LMOE_TITANS = 10, LMOE_S4 = 11, LMOE_MAMBA = 12, LMOE_RWKV7 = 16
 };
 enum lmoe_feature_map { LMOE_FM_IDENTITY = 0, LMOE_FM_ELU1 = 1, LMOE_FM_SQUARED = 2 };
 enum lmoe_flags { LMOE_FLAG_CHECK = 1, LMOE_FLAG_TIMING = 2 };
@@ -222,6 +225,27 @@ int lmoe_lsm_bwd_varlen(const lmoe_lsm_desc* desc, int T, const int* cu_seqlens,
                         const float* b_pre, const float* a_raw, const void* dO, void* dq, void* dk, void* dv,
                         void* da_pre, float* db_pre, float* da_raw, void* workspace, size_t workspace_bytes,
                         lmoe_stream_t stream);
+
+/* The kinds without a chunk-parallel form (DecayKind TokenOuter / FullElementwise / StateLinear
+ * / Gradient: DeltaNet, GatedDeltaNet, GFW, GateLoop, TTT, Titans, RWKV7, S4, Mamba) run token
+ * by token, as the reference's recurrent_step (lsm.hpp:335-441; lsm_forward_chunked evaluates
+ * them sequentially inside each chunk, lsm.hpp:604-637, and parallel.hpp:309-311 gives them no
+ * SP form).  One CTA per (b, h); the state lives in registers.  Gate and static inputs follow
+ * LsmGates (lsm.hpp:206-247) and LsmSpec (lsm.hpp:134-177); NULL where a kind does not use them. */
+typedef struct lmoe_lsm_recurrent_inputs {
+    const void* a_vec;          /* RWKV7 / Mamba: a_pre [B, N, H, D] in dtype              */
+    const float* a_scal;        /* DeltaNet / GatedDeltaNet / Titans: a_pre [B, N, H] fp32 */
+    const float* b_pre;         /* DeltaNet / GatedDeltaNet / TTT / Titans / RWKV7 [B,N,H] */
+    const void* alpha_pre;      /* GFW / GateLoop: [B, N, H, D] in dtype                   */
+    const void* beta_pre;       /* GFW / GateLoop: [B, N, H, D] in dtype                   */
+    const float* s4_delta_raw;  /* S4: [H, D]                                              */
+    const float* s4_b;          /* S4: [H, D]                                              */
+    const float* s4_A_raw;      /* S4: [H, D, D]                                           */
+    const float* mamba_A_raw;   /* Mamba: [H, D, D]                                        */
+} lmoe_lsm_recurrent_inputs;
+int lmoe_lsm_fwd_recurrent(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
+                           const void* q, const void* k, const void* v, const lmoe_lsm_recurrent_inputs* in,
+                           const float* M0, void* o, float* M_out, lmoe_stream_t stream);
 
 /* Number of kernels one lmoe_lsm_fwd call launches (for launch accounting). */
 int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc);

@@ -115,6 +115,20 @@ def lsm_sequential(spec, q, k, v, a_pre=None, b_pre=None, M0=None, z0=None):
     return o, M, z
 
 
+def lsm_recurrent(spec, q, k, v, a_pre=None, b_pre=None, alpha_pre=None, beta_pre=None, s4_delta_raw=None,
+                  s4_b=None, s4_A_raw=None, mamba_A_raw=None, M0=None):
+    """recurrent_step (lsm.hpp:335-441) for the kinds without a chunk-parallel form."""
+    arrs = list(map(_f64, (q, k, v, a_pre, b_pre, alpha_pre, beta_pre, s4_delta_raw, s4_b, s4_A_raw,
+                           mamba_A_raw, M0)))
+    n, dk = arrs[0].shape
+    dv = arrs[2].shape[1]
+    o = np.zeros((n, dv))
+    M = np.zeros((dk, dv))
+    sp = _spec(spec)
+    _run(lib().lmo_lsm_recurrent, ctypes.byref(sp), n, dk, dv, *[_p(x) for x in arrs], _p(o), _p(M))
+    return o, M
+
+
 def lsm_backward(spec, q, k, v, dO, a_pre=None, b_pre=None, M0=None, dM_final=None):
     q, k, v, a_pre, b_pre, M0, dO, dM_final = map(_f64, (q, k, v, a_pre, b_pre, M0, dO, dM_final))
     n, dk = q.shape

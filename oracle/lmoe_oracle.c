@@ -413,6 +413,106 @@ int lmo_lsm_backward(const lmo_spec* s, int n, int d_k, int d_v, const double* q
     return 0;
 }
 
+/*
+ * recurrent_step (lsm.hpp:335-441) for the kinds without a chunk-parallel form: DeltaNet,
+ * GatedDeltaNet (StateLinear), GFW / GateLoop (TokenOuter), TTT / Titans / RWKV7 (Gradient,
+ * kern::ttt_loss_grad lsm.hpp:328-330), S4 / Mamba (FullElementwise).  Gate layouts
+ * (LsmGates, lsm.hpp:206-247): a_pre (n, d_k) for RWKV7 / Mamba, (n) for DeltaNet /
+ * GatedDeltaNet / Titans; b_pre (n); alpha_pre (n, d_k); beta_pre (n, d_v).  Static params
+ * (LsmSpec::make lsm.hpp:166-177): s4_delta_raw (d_k), s4_b (d_k), s4_A_raw / mamba_A_raw
+ * (d_k, d_v).  No normaliser for these kinds (LsmSpec::validate).  o: (n, d_v).
+ */
+int lmo_lsm_recurrent(const lmo_spec* s, int n, int d_k, int d_v, const double* q, const double* k,
+                      const double* v, const double* a_pre, const double* b_pre, const double* alpha_pre,
+                      const double* beta_pre, const double* s4_delta_raw, const double* s4_b,
+                      const double* s4_A_raw, const double* mamba_A_raw, const double* M0, double* o,
+                      double* M_out, char* err, int errlen) {
+    if (lmo_spec_validate(s, d_k, d_v, err, errlen)) return -1;
+    const int inst = s->instance;
+    if (!(inst == LMO_DELTANET || inst == LMO_GATED_DELTANET || inst == LMO_GFW || inst == LMO_GATELOOP ||
+          inst == LMO_TTT || inst == LMO_TITANS || inst == LMO_RWKV7 || inst == LMO_S4 || inst == LMO_MAMBA)) {
+        set_err(err, errlen, "lmo_lsm_recurrent: separable kind (use lmo_lsm_sequential)");
+        return -1;
+    }
+    const size_t dd = (size_t)d_k * d_v;
+    double* M = (double*)malloc(sizeof(double) * dd);
+    double* P = (double*)malloc(sizeof(double) * dd);
+    double* kk = (double*)malloc(sizeof(double) * d_k);
+    double* c = (double*)malloc(sizeof(double) * d_v);
+    if (M0) memcpy(M, M0, sizeof(double) * dd); else memset(M, 0, sizeof(double) * dd);
+    int rc = 0;
+    for (int t = 0; t < n && rc == 0; ++t) {
+        const double* qt = q + (size_t)t * d_k;
+        const double* kt = k + (size_t)t * d_k;
+        const double* vt = v + (size_t)t * d_v;
+        for (int i = 0; i < d_k; ++i) kk[i] = fmap(s->feature_map, kt[i]);
+        if (inst == LMO_DELTANET || inst == LMO_GATED_DELTANET) {
+            double nrm = 0.0; /* l2_normalize_rows (tensor.hpp:810-825), eps 1e-12 */
+            for (int i = 0; i < d_k; ++i) nrm += kk[i] * kk[i];
+            nrm = sqrt(nrm + 1e-12);
+            for (int i = 0; i < d_k; ++i) kk[i] /= nrm;
+        }
+        /* c = k^ M (vecmat) for the projection / test-time-gradient kinds */
+        for (int j = 0; j < d_v; ++j) {
+            double acc = 0.0;
+            for (int i = 0; i < d_k; ++i) acc += kk[i] * M[(size_t)i * d_v + j];
+            c[j] = acc;
+        }
+        for (int i = 0; i < d_k; ++i)
+            for (int j = 0; j < d_v; ++j) {
+                const size_t e = (size_t)i * d_v + j;
+                double m = M[e];
+                switch (inst) {
+                    case LMO_DELTANET: {
+                        const double a = sigm(a_pre[t]), b = sigm(b_pre[t]);
+                        m = m - a * kk[i] * c[j] + b * kk[i] * vt[j];
+                        break;
+                    }
+                    case LMO_GATED_DELTANET: {
+                        const double a = sigm(a_pre[t]), b = sigm(b_pre[t]);
+                        m = a * (m - kk[i] * c[j]) + b * kk[i] * vt[j];
+                        break;
+                    }
+                    case LMO_GFW:
+                    case LMO_GATELOOP:
+                        m = sigm(alpha_pre[(size_t)t * d_k + i]) * sigm(beta_pre[(size_t)t * d_v + j]) * m +
+                            kk[i] * vt[j];
+                        break;
+                    case LMO_TTT:
+                        m = m - sigm(b_pre[t]) * kk[i] * (c[j] - vt[j]);
+                        break;
+                    case LMO_TITANS:
+                        m = sigm(a_pre[t]) * m - sigm(b_pre[t]) * kk[i] * (c[j] - vt[j]);
+                        break;
+                    case LMO_RWKV7:
+                        m = sigm(a_pre[(size_t)t * d_k + i]) * m - sigm(b_pre[t]) * kk[i] * (c[j] - vt[j]);
+                        break;
+                    case LMO_S4: {
+                        const double dl = softplus(s4_delta_raw[i]);
+                        m = exp(-softplus(s4_A_raw[e]) * dl) * m + dl * s4_b[i] * vt[j];
+                        break;
+                    }
+                    case LMO_MAMBA: {
+                        const double dl = softplus(a_pre[(size_t)t * d_k + i]);
+                        m = exp(-softplus(mamba_A_raw[e]) * dl) * m + dl * kk[i] * vt[j];
+                        break;
+                    }
+                }
+                P[e] = m;
+            }
+        memcpy(M, P, sizeof(double) * dd);
+        rc = check_state(s, M, dd, err, errlen);
+        for (int j = 0; j < d_v && rc == 0; ++j) {
+            double acc = 0.0;
+            for (int i = 0; i < d_k; ++i) acc += fmap(s->feature_map, qt[i]) * M[(size_t)i * d_v + j];
+            o[(size_t)t * d_v + j] = acc;
+        }
+    }
+    if (rc == 0 && M_out) memcpy(M_out, M, sizeof(double) * dd);
+    free(M); free(P); free(kk); free(c);
+    return rc;
+}
+
 /* route (moe.hpp:58-85) with softmax_rows (tensor.hpp:767-789) */
 int lmo_route(const double* logits, int t, int e, int top_k, int* ids, double* gates,
               double* probs, char* err, int errlen) {

@@ -70,6 +70,15 @@ int lmo_lsm_sequential(const lmo_spec* s, int n, int d_k, int d_v,
                        const double* M0, const double* z0,
                        double* o, double* M_out, double* z_out, char* err, int errlen);
 
+/* recurrent_step (lsm.hpp:335-441) token by token for DeltaNet, GatedDeltaNet, GFW, GateLoop,
+ * TTT, Titans, RWKV7, S4, Mamba (no chunk-parallel form).  Gate / static-parameter layouts as
+ * LsmGates (lsm.hpp:206-247) and LsmSpec (lsm.hpp:134-177); NULL where unused. */
+int lmo_lsm_recurrent(const lmo_spec* s, int n, int d_k, int d_v, const double* q, const double* k,
+                      const double* v, const double* a_pre, const double* b_pre, const double* alpha_pre,
+                      const double* beta_pre, const double* s4_delta_raw, const double* s4_b,
+                      const double* s4_A_raw, const double* mamba_A_raw, const double* M0, double* o,
+                      double* M_out, char* err, int errlen);
+
 /*
  * Reverse-mode gradient of L = sum(o .* dO) through the token recurrence
  * (the quantity the reference tape computes via backward(), tensor.hpp:1178,

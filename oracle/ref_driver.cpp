@@ -190,6 +190,49 @@ void golden_lsm_device() {
     }
 }
 
+// ---- non-separable kinds (DecayKind TokenOuter / FullElementwise / StateLinear / Gradient):
+// recurrent_step (lsm.hpp:335-441) token by token, and lsm_forward_chunked (sequential inside
+// each chunk, lsm.hpp:604-637) ----
+void golden_lsm_seq() {
+    struct SV { const char* tag; LsmInstance inst; };
+    const SV kinds[] = {{"deltanet", LsmInstance::DeltaNet}, {"gated_deltanet", LsmInstance::GatedDeltaNet},
+                        {"gfw", LsmInstance::GFW}, {"gateloop", LsmInstance::GateLoop}, {"ttt", LsmInstance::TTT},
+                        {"titans", LsmInstance::Titans}, {"rwkv7", LsmInstance::RWKV7}, {"s4", LsmInstance::S4},
+                        {"mamba", LsmInstance::Mamba}};
+    int vi = 0;
+    for (const SV& sv : kinds) {
+        for (int n : {7, 40}) {
+            const int d = 8;
+            Rng rng(21000 + 31 * vi + n);
+            LsmSpec spec = LsmSpec::make(sv.inst, d, d, &rng);
+            const Tensor q = Tensor::randn({n, d}, rng, 0.5);
+            const Tensor k = Tensor::randn({n, d}, rng, 0.5);
+            const Tensor v = Tensor::randn({n, d}, rng, 0.5);
+            const LsmGates g = LsmGates::random_for(spec, n, rng);
+            const std::string p = std::string("lsm_seq/") + sv.tag + "_n" + std::to_string(n);
+            emit_spec(p, spec);
+            emit(p + "/q", q);
+            emit(p + "/k", k);
+            emit(p + "/v", v);
+            emit(p + "/a_pre", g.a_pre);
+            emit(p + "/b_pre", g.b_pre);
+            emit(p + "/alpha_pre", g.alpha_pre);
+            emit(p + "/beta_pre", g.beta_pre);
+            emit(p + "/s4_delta_raw", spec.s4_delta_raw);
+            emit(p + "/s4_b", spec.s4_b);
+            emit(p + "/s4_A_raw", spec.s4_A_raw);
+            emit(p + "/mamba_A_raw", spec.mamba_A_raw);
+            MemoryState fs;
+            emit(p + "/o_seq", lsm_forward_sequential(q, k, v, g, spec, &fs));
+            emit(p + "/M_seq", fs.M);
+            MemoryState fc;
+            emit(p + "/o_c8", lsm_forward_chunked(q, k, v, g, spec, 8, &fc));
+            emit(p + "/M_c8", fc.M);
+        }
+        ++vi;
+    }
+}
+
 // ---- LSM gradients from the reference tape (tensor.hpp:1178) ----
 void golden_lsm_grad() {
     // appended tags keep the seeds of the earlier ones: the normalised reference defaults
@@ -470,6 +513,7 @@ int cmd_golden(const char* path) {
     g_out = fopen(path, "wb");
     if (!g_out) return 2;
     golden_lsm_small();
+    golden_lsm_seq();
     golden_lsm_device();
     golden_lsm_grad();
     golden_route();

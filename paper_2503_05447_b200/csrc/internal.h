@@ -10,6 +10,8 @@
 
 namespace lmoe_host {
 
+const char* instance_name(int inst);  // lsm_host.cu: the reference's instance names
+
 // LSM mixer over q, k, v (and TokenVector a_pre) [B, N, H, D] views whose token rows are
 // `ld` elements apart (0: H * D); o dense.  world == 1: lsm_forward_chunked; world > 1:
 // sp_lsm_masked_rank with one NCCL all-gather.

@@ -23,6 +23,9 @@ INSTANCES = ["bla", "lightning", "retnet", "gla", "deltanet", "gated_deltanet", 
 
 class LsmInstance:
     BLA, LIGHTNING, RETNET, GLA, REBASED, MAMBA2, HGRN2, RWKV6 = 0, 1, 2, 3, 6, 13, 14, 15
+    # no chunk-parallel form (lsm_forward_recurrent)
+    DELTANET, GATED_DELTANET, GFW, GATELOOP, TTT, TITANS, S4, MAMBA, RWKV7 = 4, 5, 7, 8, 9, 10, 11, 12, 16
+    RECURRENT = (4, 5, 7, 8, 9, 10, 11, 12, 16)
 
 
 class FeatureMap:
@@ -39,6 +42,12 @@ class LsmSpec:
     d_v: int = 0
     scalar_decay: float = 1.0
     mamba2_a_raw: Optional[torch.Tensor] = None
+    # static parameters of S4 / Mamba (LsmSpec::make, lsm.hpp:166-177), per head:
+    # s4_delta_raw, s4_b [H, d_k]; s4_A_raw, mamba_A_raw [H, d_k, d_v] (fp32)
+    s4_delta_raw: Optional[torch.Tensor] = None
+    s4_b: Optional[torch.Tensor] = None
+    s4_A_raw: Optional[torch.Tensor] = None
+    mamba_A_raw: Optional[torch.Tensor] = None
 
     @staticmethod
     def make(instance, d_k, d_v=None):
@@ -62,9 +71,13 @@ class LsmSpec:
 
 @dataclasses.dataclass
 class LsmGates:
-    """lmoe::LsmGates (lsm.hpp:216-261): a_pre [.., N, d_k] (TokenVector), b_pre [.., N]."""
+    """lmoe::LsmGates (lsm.hpp:206-247): a_pre [.., N, d_k] (TokenVector, RWKV7, Mamba) or
+    [.., N] (DeltaNet, GatedDeltaNet, Titans); b_pre [.., N]; alpha_pre [.., N, d_k] and
+    beta_pre [.., N, d_v] (GFW, GateLoop)."""
     a_pre: Optional[torch.Tensor] = None
     b_pre: Optional[torch.Tensor] = None
+    alpha_pre: Optional[torch.Tensor] = None
+    beta_pre: Optional[torch.Tensor] = None
 
 
 @dataclasses.dataclass
@@ -310,3 +323,49 @@ def lsm_backward_varlen(q, k, v, gates, spec, dO, cu_seqlens, chunk_size=64, che
                                      P(b_pre), P(a_raw), P(dO), P(g.dq), P(g.dk), P(g.dv), P(g.da_pre), P(g.db_pre),
                                      P(g.da_raw), P(ws), ws.numel(), ctypes.c_void_p(st)))
     return g
+
+
+class _RecInputs(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("a_vec", "a_scal", "b_pre", "alpha_pre", "beta_pre", "s4_delta_raw",
+                                                "s4_b", "s4_A_raw", "mamba_A_raw")]
+
+
+def lsm_forward_recurrent(q, k, v, gates, spec, initial_state=None, final_state=None, check=True, stream=None):
+    """The kinds without a chunk-parallel form (DeltaNet, GatedDeltaNet, GFW, GateLoop, TTT,
+    Titans, RWKV7, S4, Mamba): recurrent_step (lsm.hpp:335-441) token by token on the device
+    (lmoe_lsm_fwd_recurrent).  q, k, v [B, N, H, D]; gates / static params as LsmGates / LsmSpec."""
+    B, N, H, D = q.shape
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    L = _lib.lib()
+    if not getattr(L, "_rec_bound", False):
+        L.lmoe_lsm_fwd_recurrent.restype = ctypes.c_int
+        L.lmoe_lsm_fwd_recurrent.argtypes = [ctypes.POINTER(_lib.LsmDesc)] + [ctypes.c_int] * 5 + [ctypes.c_void_p] * 8
+        L._rec_bound = True
+    keep = []
+
+    def ptr(t, dtype=None):
+        if t is None:
+            return None
+        t = t.to(dtype or t.dtype).contiguous()
+        keep.append(t)
+        return t.data_ptr()
+
+    g = gates or LsmGates()
+    vec_a = spec.instance in (LsmInstance.RWKV7, LsmInstance.MAMBA)
+    rin = _RecInputs(a_vec=ptr(g.a_pre, q.dtype) if vec_a else None,
+                     a_scal=None if vec_a else ptr(g.a_pre, torch.float32),
+                     b_pre=ptr(g.b_pre, torch.float32), alpha_pre=ptr(g.alpha_pre, q.dtype),
+                     beta_pre=ptr(g.beta_pre, q.dtype), s4_delta_raw=ptr(spec.s4_delta_raw, torch.float32),
+                     s4_b=ptr(spec.s4_b, torch.float32), s4_A_raw=ptr(spec.s4_A_raw, torch.float32),
+                     mamba_A_raw=ptr(spec.mamba_A_raw, torch.float32))
+    M0 = None if initial_state is None else ptr(initial_state.M, torch.float32)
+    o = torch.empty_like(q)
+    M_out = torch.empty(B, H, D, D, dtype=torch.float32, device=q.device) if final_state is not None else None
+    desc = make_desc(spec, 64, check)
+    st = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+    _lib.check(L.lmoe_lsm_fwd_recurrent(ctypes.byref(desc), B, N, H, D, _DTYPES[q.dtype], q.data_ptr(),
+                                        k.data_ptr(), v.data_ptr(), ctypes.byref(rin), M0, o.data_ptr(),
+                                        None if M_out is None else M_out.data_ptr(), ctypes.c_void_p(st)))
+    if final_state is not None:
+        final_state.M, final_state.z, final_state.step = M_out, None, N
+    return o

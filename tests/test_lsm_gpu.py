@@ -246,3 +246,109 @@ def test_varlen_matches_per_document_calls(inst):
         want, _, _ = oracle.lsm_chunked(sd, *(t[0, r0:r1, h].float().cpu().numpy() for t in (q, k, v)), a_pre=a,
                                         b_pre=b)
         assert norm_rel_err(o[0, r0:r1, h].float().cpu().numpy(), want) < 2e-2
+
+
+# ------------------------------------------------ kinds without a chunk-parallel form (8(f) rank 4)
+REC_KINDS = ["deltanet", "gated_deltanet", "gfw", "gateloop", "ttt", "titans", "rwkv7", "s4", "mamba"]
+
+
+def _rec_inputs(d, p, D, B=1, H=1, dtype="bf16"):
+    """Golden lsm_seq record -> padded device inputs (zero q / k / v columns keep the first d x d
+    block of the problem: padded keys add nothing, padded rows of M are never read by q)."""
+    import torch
+    import paper_2503_05447_b200 as pk
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    dd = d[p + "/q"].shape[1]
+    padc = lambda x: np.pad(x, ((0, 0), (0, D - x.shape[1])))
+    dev = lambda x, dt=tdt: torch.tensor(x, dtype=torch.float32, device="cuda").to(dt)
+    q, k, v = (dev(padc(d[p + "/" + n]))[None, :, None] for n in ("q", "k", "v"))
+    g = pk.LsmGates()
+    a = d.get(p + "/a_pre")
+    if a is not None:
+        g.a_pre = dev(padc(a))[None, :, None] if a.ndim == 2 else dev(a, torch.float32)[None, :, None]
+    if p + "/b_pre" in d:
+        g.b_pre = dev(d[p + "/b_pre"], torch.float32)[None, :, None]
+    for n in ("alpha_pre", "beta_pre"):
+        if p + "/" + n in d:
+            setattr(g, n, dev(padc(d[p + "/" + n]))[None, :, None])
+    spec = pk.LsmSpec(instance=int(d[p + "/instance"][0]), feature_map=int(d[p + "/feature_map"][0]))
+    if p + "/s4_delta_raw" in d:
+        spec.s4_delta_raw = dev(np.pad(d[p + "/s4_delta_raw"], (0, D - dd)), torch.float32)[None]
+        spec.s4_b = dev(np.pad(d[p + "/s4_b"], (0, D - dd)), torch.float32)[None]
+        spec.s4_A_raw = dev(np.pad(d[p + "/s4_A_raw"], ((0, D - dd), (0, D - dd))), torch.float32)[None]
+    if p + "/mamba_A_raw" in d:
+        spec.mamba_A_raw = dev(np.pad(d[p + "/mamba_A_raw"], ((0, D - dd), (0, D - dd))), torch.float32)[None]
+    return q, k, v, g, spec
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_recurrent_kinds_match_reference(dtype):
+    """lmoe_lsm_fwd_recurrent for the nine kinds against the f64 oracle (pinned to the
+    reference's recurrent_step, tests/golden/lsm_seq.npz) on the same rounded inputs."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2503_05447_b200.lsm import lsm_forward_recurrent
+    import paper_2503_05447_b200 as pk
+    d = load_golden("lsm_seq")
+    D = 64 if dtype == "f32" else 128
+    tol = 1e-3 if dtype == "f32" else 2e-2
+    ran = 0
+    for p in sorted({k.split("/")[0] for k in d}):
+        q, k, v, g, spec = _rec_inputs(d, p, D, dtype=dtype)
+        fs = pk.MemoryState()
+        o = lsm_forward_recurrent(q, k, v, g, spec, final_state=fs)
+        torch.cuda.synchronize()
+        dd = d[p + "/q"].shape[1]
+        cut = lambda t: None if t is None else t.float().cpu().numpy()
+        sdict = oracle.spec_from_golden(d, p)
+        args = [cut(q[0, :, 0, :dd]), cut(k[0, :, 0, :dd]), cut(v[0, :, 0, :dd])]
+        a = g.a_pre
+        args.append(None if a is None else (cut(a[0, :, 0, :dd]) if a.dim() == 4 else cut(a[0, :, 0])))
+        args.append(None if g.b_pre is None else cut(g.b_pre[0, :, 0]))
+        args.append(None if g.alpha_pre is None else cut(g.alpha_pre[0, :, 0, :dd]))
+        args.append(None if g.beta_pre is None else cut(g.beta_pre[0, :, 0, :dd]))
+        args.append(None if spec.s4_delta_raw is None else cut(spec.s4_delta_raw[0, :dd]))
+        args.append(None if spec.s4_b is None else cut(spec.s4_b[0, :dd]))
+        args.append(None if spec.s4_A_raw is None else cut(spec.s4_A_raw[0, :dd, :dd]))
+        args.append(None if spec.mamba_A_raw is None else cut(spec.mamba_A_raw[0, :dd, :dd]))
+        want_o, want_M = oracle.lsm_recurrent(sdict, *args)
+        assert norm_rel_err(o[0, :, 0, :dd].float().cpu().numpy(), want_o) < tol, (p, dtype)
+        assert norm_rel_err(fs.M[0, 0, :dd, :dd].cpu().numpy(), want_M) < tol, (p, dtype)
+        assert np.abs(o[0, :, 0, dd:].float().cpu().numpy()).max() == 0.0  # padded value columns
+        ran += 1
+    assert ran == 18
+
+
+def test_recurrent_kinds_random_heads_and_errors():
+    """Full head dim, several heads / batch rows, an initial state; error texts."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_05447_b200 as pk
+    from paper_2503_05447_b200.lsm import lsm_forward_recurrent
+    B, N, H, D = 2, 150, 2, 128
+    rng = np.random.default_rng(9)
+    T = lambda x, dt=torch.bfloat16: torch.tensor(x, dtype=torch.float32, device="cuda").to(dt)
+    q, k, v = (T(rng.normal(0, 0.5, (B, N, H, D))) for _ in range(3))
+    M0 = rng.normal(0, 0.1, (B, H, D, D))
+    for inst in ("gated_deltanet", "rwkv7"):
+        spec = pk.LsmSpec.make(inst, D)
+        if inst == "gated_deltanet":
+            g = pk.LsmGates(a_pre=T(rng.normal(2, 1, (B, N, H)), torch.float32),
+                            b_pre=T(rng.normal(0, 1, (B, N, H)), torch.float32))
+        else:
+            g = pk.LsmGates(a_pre=T(rng.normal(2, 1, (B, N, H, D))), b_pre=T(rng.normal(0, 1, (B, N, H)), torch.float32))
+        o = lsm_forward_recurrent(q, k, v, g, spec, initial_state=pk.MemoryState(M=T(M0, torch.float32)))
+        torch.cuda.synchronize()
+        for b in range(B):
+            for h in range(H):
+                sd = oracle.spec_default(inst)
+                a = g.a_pre[b, :, h].float().cpu().numpy()
+                want, _ = oracle.lsm_recurrent(sd, *(t[b, :, h].float().cpu().numpy() for t in (q, k, v)), a,
+                                               g.b_pre[b, :, h].cpu().numpy(), M0=M0[b, h])
+                assert norm_rel_err(o[b, :, h].float().cpu().numpy(), want) < 2e-2, (inst, b, h)
+    with pytest.raises(pk.LmoeError, match="needs a_pre"):
+        lsm_forward_recurrent(q, k, v, pk.LsmGates(), pk.LsmSpec.make("deltanet", D))
+    with pytest.raises(pk.LmoeError, match="chunk-parallel form"):
+        lsm_forward_recurrent(q, k, v, None, pk.LsmSpec.make("retnet", D))

@@ -252,3 +252,21 @@ def test_backward_final_state_gradient_matches_finite_differences():
         fd = (loss(*plus) - loss(*minus)) / 2e-6
         an = float((g[name] * u).sum())
         assert abs(an - fd) < 1e-6 * max(1.0, abs(fd)), (name, an, fd)
+
+
+
+def test_recurrent_kinds_match_reference():
+    """lmo_lsm_recurrent against the reference's recurrent_step / lsm_forward_chunked for the
+    nine kinds without a chunk-parallel form (tests/golden/lsm_seq.npz, d = 8)."""
+    d = load_golden("lsm_seq")
+    ran = 0
+    for p in sorted({k.split("/")[0] for k in d}):
+        spec = oracle.spec_from_golden(d, p)
+        g = lambda n: d.get(p + "/" + n)
+        o, M = oracle.lsm_recurrent(spec, g("q"), g("k"), g("v"), g("a_pre"), g("b_pre"), g("alpha_pre"),
+                                    g("beta_pre"), g("s4_delta_raw"), g("s4_b"), g("s4_A_raw"), g("mamba_A_raw"))
+        assert np.abs(o - g("o_seq")).max() < 1e-10, p
+        assert np.abs(M - g("M_seq")).max() < 1e-10, p
+        assert np.abs(g("o_c8") - g("o_seq")).max() < 1e-10, p  # chunked == sequential (reference)
+        ran += 1
+    assert ran == 18
