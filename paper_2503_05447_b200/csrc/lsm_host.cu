@@ -760,10 +760,10 @@ static void vec_backward(const lmoe_lsm_desc& dd, const BwdPlan& w, int B, int N
     r.state_pass<bf>();
     r.combine(dM_final, nullptr, true, dM0, nullptr, nullptr, 0, 1);
     vp.snap = snapX;
+    vp.snap_fwd = snapM;  // 5: the REV carry also forms the gate gradient's boundary terms
+    vp.bd_out = reinterpret_cast<float*>(ws + w.off_bd);
     LMOE_CUDA_CHECK(lmoe_dev::launch_vec_carry(false, true, sgrid, st, tq, tdo, ta, vp));
-    // 5: boundary terms of the gate gradient
     const long long rows = (long long)B * H * (nchunk + 1) * D;
-    LMOE_CUDA_CHECK(lmoe_dev::launch_vec_boundary_dot(snapM, snapX, reinterpret_cast<float*>(ws + w.off_bd), rows, st));
     // 6: fused chunk backward
     // bf16 outputs leave through TMA bulk stores (dq / dk only when not fp32 intermediates)
     const CUtensorMap tm[11] = {tq, tk, tv, tdo, ta,
@@ -774,7 +774,7 @@ static void vec_backward(const lmoe_lsm_desc& dd, const BwdPlan& w, int B, int N
     if (hg && !out_f32)  // HGRN2's effective key 1 - sigmoid(a) ignores k
         LMOE_CUDA_CHECK(cudaMemsetAsync(dk, 0, (size_t)B * N * H * D * sizeof(bf), st));
     LMOE_CUDA_CHECK(lmoe_dev::launch_vec_bwd_chunk(hg, dim3(nchunk, H, B), st, tm, vp));
-    g_launch_count += 4;
+    g_launch_count += 3;
     c.check_err();
 }
 }  // namespace lmoe_host

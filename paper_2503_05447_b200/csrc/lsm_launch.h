@@ -99,6 +99,8 @@ struct VecBwdParams {
     const float* Min;                     // [BH][nseg][D][D] state entering each segment (carry)
     __nv_bfloat16* snap;                  // carry output [BH][nchunk + 1][D][D]
     const float* bd;                      // [BH][nchunk + 1][D] boundary dots
+    const __nv_bfloat16* snap_fwd;        // REV carry: the forward snapshots (for the boundary dots)
+    float* bd_out;                        // REV carry: boundary dots out
     void* dq;                             // [B, N, H, D] bf16, or fp32 when out_f32
     void* dk;
     __nv_bfloat16* dv;
@@ -109,7 +111,6 @@ struct VecBwdParams {
 };
 cudaError_t launch_vec_carry(bool hgrn2, bool rev, dim3 grid, cudaStream_t st, const CUtensorMap& x1,
                              const CUtensorMap& x2, const CUtensorMap& a, const VecBwdParams& p);
-cudaError_t launch_vec_boundary_dot(const void* M, const void* X, float* bd, long long rows, cudaStream_t st);
 // tm = {q, k, v, dO, a_pre, snapM, snapX, dq, dk, dv, da} (dq / dk maps unused when out_f32)
 cudaError_t launch_vec_bwd_chunk(bool hgrn2, dim3 grid, cudaStream_t st, const CUtensorMap* tm,
                                  const VecBwdParams& p);

@@ -13,9 +13,9 @@
 //   1. lsm_state_pass_vec (forward) + segment combine      -> M at every segment start
 //   2. lsm_vec_carry<FWD>   per segment, chunk by chunk   -> snapM[c] = M before chunk c (bf16)
 //   3. lsm_state_pass_vec<REV> + reverse combine           -> X at every segment end, dM0
-//   4. lsm_vec_carry<REV>                                  -> snapX[c+1] = X after chunk c
-//   5. lsm_vec_boundary_dot                                -> bd[c][k] = <M_c[k,:], X_c[k,:]>
-//   6. lsm_vec_bwd_chunk    one CTA per chunk: dq, dk, dv, da_pre.
+//   4. lsm_vec_carry<REV>                                  -> snapX[c+1] = X after chunk c,
+//                                                             bd[c][k] = <M_c[k,:], X_c[k,:]>
+//   5. lsm_vec_bwd_chunk    one CTA per chunk: dq, dk, dv, da_pre.
 // The gate gradient avoids the sequence-long cancellation of the telescoped identity
 // dla_j = sum_{t>=j} (q.dq - keff.dkeff)_t: inside a chunk [a, b) the same identity holds
 // with the sum stopped at the chunk end plus the exact boundary term
@@ -97,6 +97,10 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
                 const int s = it % NST;
                 if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
                 const int t0 = chunk_idx(it) * kC;
+                // REV: the forward snapshot this chunk's boundary dot reads (owner rows, below)
+                if constexpr (REV)
+                    bulk_prefetch_l2(p.snap_fwd + ((size_t)bh * (p.nchunk + 1) + chunk_idx(it) + 1) * D * D,
+                                     D * D * sizeof(T));
                 uint8_t* st = smem + s * STAGE;
                 mbar_expect_tx(&full[s], STAGE);
 #pragma unroll
@@ -147,14 +151,40 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
             }
             tmem_wait_st();
         }
+        // REV: row c of the forward snapshot idx, loaded before the wait for the MMA so its
+        // latency hides behind it (the TMA warp has prefetched the snapshot into L2)
+        uint4 mrow[REV ? D / 8 : 1];
+        auto load_mrow = [&](int idx) {
+            if constexpr (REV) {
+                const uint4* src = reinterpret_cast<const uint4*>(p.snap_fwd + (((size_t)bh * (p.nchunk + 1) + idx) * D + c) * D);
+#pragma unroll
+                for (int u = 0; u < D / 8; ++u) mrow[u] = src[u];
+            }
+        };
         auto snapshot = [&](int idx, float scale) {
-            // write row c of the TMEM state to snap[idx] (bf16) and rescale it in place
-            __nv_bfloat16* dst = p.snap + (((size_t)bh * (p.nchunk + 1) + idx) * D + c) * D;
+            // write row c of the TMEM state to snap[idx] (bf16) and rescale it in place; REV also
+            // forms the gate gradient's boundary term bd[idx][c] = <M_idx[c, :], X_idx[c, :]>
+            // against the forward snapshot (written by the FWD carry before this pass)
+            const size_t srow = ((size_t)bh * (p.nchunk + 1) + idx) * D + c;
+            __nv_bfloat16* dst = p.snap + srow * D;
+            float bdot = 0.f;
 #pragma unroll
             for (int cb = 0; cb < D / 32; ++cb) {
                 uint32_t r[32];
                 tmem_ld32(tmem + lane_off + cb * 32, r);
                 tmem_wait_ld();
+                if constexpr (REV) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint4 mu = mrow[cb * 4 + u];
+                        const uint32_t mw[4] = {mu.x, mu.y, mu.z, mu.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 f = unpack_bf16(mw[e]);
+                            bdot += f.x * __uint_as_float(r[u * 8 + 2 * e]) + f.y * __uint_as_float(r[u * 8 + 2 * e + 1]);
+                        }
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < 32; j += 8) {
                     uint4 u;
@@ -171,6 +201,7 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
                 }
             }
             tmem_wait_st();
+            if constexpr (REV) p.bd_out[srow] = bdot;
         };
         for (int it = 0; it < nchunks; ++it) {
             const int s = it % NST;
@@ -205,6 +236,7 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
             }
             // state: wait for the previous chunk's MMA, snapshot, decay by the chunk total
             if (owner) {
+                load_mrow(ci + 1);
                 if (it > 0) mbar_wait(acc, (it - 1) & 1);
                 tc_fence_after();
                 snapshot(REV ? ci + 1 : ci, __expf(sGe[c]));
@@ -216,29 +248,15 @@ __global__ void __launch_bounds__(kCarryThreads, 1)
         if (owner) {
             mbar_wait(acc, (nchunks - 1) & 1);
             tc_fence_after();
-            if (REV ? seg == 0 : seg == p.nseg - 1) snapshot(REV ? 0 : p.nchunk, 1.f);
+            if (REV ? seg == 0 : seg == p.nseg - 1) {
+                load_mrow(0);
+                snapshot(REV ? 0 : p.nchunk, 1.f);
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<128>(tmem);
-}
-
-// bd[row] = <M[row, :], X[row, :]> over rows of [BH][nchunk + 1][D] x [D] (one warp per row)
-__global__ void __launch_bounds__(256) lsm_vec_boundary_dot(const __nv_bfloat16* __restrict__ M,
-                                                            const __nv_bfloat16* __restrict__ X,
-                                                            float* __restrict__ bd, long long rows) {
-    const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const uint2 mu = *reinterpret_cast<const uint2*>(M + row * 128 + lane * 4);
-    const uint2 xu = *reinterpret_cast<const uint2*>(X + row * 128 + lane * 4);
-    const float2 m0 = unpack_bf16(mu.x), m1 = unpack_bf16(mu.y);
-    const float2 x0 = unpack_bf16(xu.x), x1 = unpack_bf16(xu.y);
-    float s = m0.x * x0.x + m0.y * x0.y + m1.x * x1.x + m1.y * x1.y;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-    if (lane == 0) bd[row] = s;
 }
 
 // ====================================================================================
@@ -706,12 +724,6 @@ cudaError_t launch_vec_carry(bool hgrn2, bool rev, dim3 grid, cudaStream_t st, c
                              const CUtensorMap& x2, const CUtensorMap& a, const VecBwdParams& p) {
     if (rev) return carry_t<false, true>(grid, st, x1, x2, a, p);
     return hgrn2 ? carry_t<true, false>(grid, st, x1, x2, a, p) : carry_t<false, false>(grid, st, x1, x2, a, p);
-}
-
-cudaError_t launch_vec_boundary_dot(const void* M, const void* X, float* bd, long long rows, cudaStream_t st) {
-    lsm_vec_boundary_dot<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(M),
-                                                                      static_cast<const __nv_bfloat16*>(X), bd, rows);
-    return cudaGetLastError();
 }
 
 template <bool HG>
