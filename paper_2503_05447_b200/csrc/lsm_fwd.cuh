@@ -70,14 +70,17 @@ struct LsmFwdParams {
 };
 
 // per-CTA globaltimer at kernel start (after the prologue) and end, slots after the 64 x 16
-// chunk trace: [cta][2] for up to 2048 CTAs
-__device__ __forceinline__ void trace_cta(const LsmFwdParams& p, int which) {
+// chunk trace: [region][cta][2] for up to 2048 CTAs (region 0 output pass, 1 state pass)
+__device__ __forceinline__ void trace_cta(const LsmFwdParams& p, int which, int region = 0) {
     if (p.trace != nullptr && threadIdx.x == 0) {
         const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         if (cta < 2048) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            p.trace[64 * 16 + cta * 2 + which] = t;
+            p.trace[64 * 16 + region * 4096 + cta * 2 + which] = t;
+            uint32_t sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            if (which == 0 && region < 2) p.trace[64 * 16 + 3 * 4096 + cta * 2 + region] = sm;
         }
     }
 }

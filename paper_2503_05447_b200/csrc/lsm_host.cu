@@ -181,8 +181,8 @@ struct LsmCall {
         p.trace = nullptr;
         if (getenv("LMOE_TRACE")) {
             if (!g_trace) {
-                LMOE_CUDA_CHECK(cudaMalloc(&g_trace, (64 * 16 + 4096) * 8));
-                LMOE_CUDA_CHECK(cudaMemset(g_trace, 0, (64 * 16 + 4096) * 8));
+                LMOE_CUDA_CHECK(cudaMalloc(&g_trace, (64 * 16 + 4 * 4096) * 8));
+                LMOE_CUDA_CHECK(cudaMemset(g_trace, 0, (64 * 16 + 4 * 4096) * 8));
             }
             p.trace = g_trace;
         }
@@ -992,7 +992,7 @@ extern "C" int lmoe_debug_trace_read(unsigned long long* out) {
     return guarded([&]() {
         if (!g_trace) throw Error(LMOE_ERR_ARG, "no trace (set LMOE_TRACE)");
         LMOE_CUDA_CHECK(cudaDeviceSynchronize());
-        LMOE_CUDA_CHECK(cudaMemcpy(out, g_trace, (64 * 16 + 4096) * 8, cudaMemcpyDeviceToHost));
+        LMOE_CUDA_CHECK(cudaMemcpy(out, g_trace, (64 * 16 + 4 * 4096) * 8, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -181,8 +181,10 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *sTmem;
+    trace_cta(p, 0, 1);
     pdl_wait();  // predecessor's outputs (segment states / prefixes) are visible from here
     pdl_trigger();
+    trace_cta(p, 1, 2);
     // forward: last chunk first (weights e^{G_end - G_j} need no pre-pass); REV: first first
     auto chunk_t0 = [&](int it) { return t_begin + (REV ? it : nchunks - 1 - it) * kC; };
 
@@ -344,6 +346,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    trace_cta(p, 1, 1);
     if (warp == 1) tmem_dealloc<128>(tmem);
 }
 
@@ -381,8 +384,8 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
     uint8_t* mop = vT + (TR ? kTileBytes : 0);             // state MMA operand
     float* ringG = reinterpret_cast<float*>(mop + TT::MOP_BYTES);  // [2][128]
     float* ringF = ringG + 256;                                     // [2][128]
-    float* ringS = ringF + 256;                                     // [2][4]
-    float* sZ = ringS + 8;                                          // [128]
+    float* ringS = ringF + 256;                                     // [2][8]
+    float* sZ = ringS + 16;                                         // [128]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sZ + 128);
     uint64_t* full = bars;         // [2]
     uint64_t* empty = bars + 2;    // [2]
@@ -428,6 +431,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
     trace_cta(p, 0);
     pdl_wait();  // predecessor's outputs (segment states / prefixes) are visible from here
     pdl_trigger();
+    trace_cta(p, 0, 2);
     const uint32_t tO = tmem + 256;
     const uint32_t tM = tmem + (kBF16 ? 384 : 320);
 
@@ -546,8 +550,9 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
         }
     } else if (warp == 2) {
         // ---------------- decay factors, one ring slot per chunk ------------------------
-        //   ringG = G (inclusive log decay), ringF = e^{-G} kf (safe) | kf (unsafe),
-        //   ringS = {G_end, safe}
+        //   ringG = G (inclusive log decay), ringF = e^{r_Q - G} kf (safe) | kf (unsafe),
+        //   ringS = {G_end, safe, -, -, r_0..r_3}: r_Q the log decay at the last row of key
+        //   quarter Q (REV: its first row, and ringF = e^{G - r_Q})
         const float spa = (DECAY == kDecayTokenScalar) ? softplus_f(p.a_raw[h]) : 0.f;
         float bvA[4], bvB[4], bvC[4];
         auto nval = [&](int c) { return min(kC, t_end - chunk_t0(c)); };
@@ -559,25 +564,28 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
             if (c >= 2) mbar_wait(&gfree[slot], ((c >> 1) - 1) & 1);
             float G[4], kf[4];
             const float gend = chunk_scan<DECAY>(p, bvA, nval(c), spa, lane, G, kf);
-            // split e^{G_i - G_j} = e^{G_i - r} e^{r - G_j} around the chunk midpoint r = G_63:
-            // both factors stay finite while each half-chunk's decay span is < 80
-            const float r = __shfl_sync(0xFFFFFFFFu, G[3], 15);
-            const float g0 = __shfl_sync(0xFFFFFFFFu, G[0], 0);
-            const bool safe = (g0 - r) < -kSafeLogDecay && (r - gend) < -kSafeLogDecay;
+            // split e^{G_i - G_j} = e^{G_i - r_Q} e^{r_Q - G_j} per 32-key quarter Q (lane / 8),
+            // r_Q = G at the quarter's last key: the key factor is <= 1 and the query factor
+            // only exceeds 1 on the diagonal block, so both stay finite while every quarter's
+            // decay span is < 80 (REV mirrors it with r_Q at the quarter's first key)
+            const float qfirst = __shfl_sync(0xFFFFFFFFu, G[0], lane & ~7);
+            const float qlast = __shfl_sync(0xFFFFFFFFu, G[3], lane | 7);
+            const float r = REV ? qfirst : qlast;
+            const bool safe = __all_sync(0xFFFFFFFFu, (qfirst - qlast) < -kSafeLogDecay);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 ringG[slot * 128 + lane * 4 + u] = G[u];
-                if constexpr (REV)  // column factor e^{G_j - r} of e^{G_j - G_i}; no key kf
+                if constexpr (REV)  // column factor e^{G_j - r_Q} of e^{G_j - G_i}; no key kf
                     ringF[slot * 128 + lane * 4 + u] = (DECAY != kDecayNone && safe) ? __expf(G[u] - r) : 1.f;
                 else
                     ringF[slot * 128 + lane * 4 + u] =
                         (DECAY != kDecayNone && safe) ? __expf(r - G[u]) * kf[u] : kf[u];
             }
             if (lane == 0) {
-                ringS[slot * 4] = gend;
-                ringS[slot * 4 + 1] = safe ? 1.f : 0.f;
-                ringS[slot * 4 + 2] = r;
+                ringS[slot * 8] = gend;
+                ringS[slot * 8 + 1] = safe ? 1.f : 0.f;
             }
+            if ((lane & 7) == 0) ringS[slot * 8 + 4 + (lane >> 3)] = r;
             __syncwarp();
             mbar_arrive(&gfull[slot]);
 #pragma unroll
@@ -658,7 +666,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
         // initial state: operand M_0, TMEM M = e^{G_end(0)} M_0
         {
             mbar_wait(&gfull[0], 0);
-            const float g0 = __expf(ringS[0]);
+            const float g0 = __expf(ringS[0]);  // G_end of chunk 0
             float vals[DH];
             const size_t mslot = p.nomask ? (size_t)bh : (size_t)bh * p.nseg + seg;
             const float* src = p.Min + (mslot * D + (sown ? srow : 0)) * D + hh * DH;
@@ -699,9 +707,9 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
             uint8_t* qt = tiles + s * 3 * kTileBytes;
             uint8_t* kt = qt + kTileBytes;
             mbar_wait(&gfull[slot], (c >> 1) & 1);
-            const float gend = ringS[slot * 4];
-            const bool safe = ringS[slot * 4 + 1] != 0.f;
-            const float gref = ringS[slot * 4 + 2];  // factorisation reference r
+            const float gend = ringS[slot * 8];
+            const bool safe = ringS[slot * 8 + 1] != 0.f;
+            const float* rQ = ringS + slot * 8 + 4;  // per-key-quarter factorisation references
             const float gi = ringG[slot * 128 + row];
             const float* Fs = ringF + slot * 128;
             const float* Gs = ringG + slot * 128;
@@ -726,7 +734,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                 float fk = 1.f;
                 if constexpr (DECAY != kDecayNone && REV) fk = __expf(gi);
                 if constexpr (DECAY != kDecayNone && !REV)
-                    fk = safe ? __expf(gend - gref) * Fs[row] : __expf(gend - gi) * Fs[row];
+                    fk = safe ? __expf(gend - rQ[q]) * Fs[row] : __expf(gend - gi) * Fs[row];
                 uint8_t* qb = qt + (hh * DH / TT::EPB) * kBlockBytes;
                 const int qch0 = (hh * DH % TT::EPB) / TT::EPC;
                 if constexpr (DECAY != kDecayNone || NORM) {
@@ -798,7 +806,12 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
 #pragma unroll
                 for (int i = 0; i < KC / 32; ++i) tmem_ld32(tS + i * 32, r[i]);
                 tmem_wait_ld();
-                const float eq = (DECAY != kDecayNone && safe) ? __expf(REV ? gref - gi : gi - gref) : 1.f;
+                float eq[KC / 32];  // query factor per key quarter of this thread's columns
+#pragma unroll
+                for (int i = 0; i < KC / 32; ++i) {
+                    const float rr = rQ[hh * (KC / 32) + i];
+                    eq[i] = (DECAY != kDecayNone && safe) ? __expf(REV ? rr - gi : gi - rr) : 1.f;
+                }
                 float rs = 0.f;
 #pragma unroll
                 for (int j = 0; j < KC; ++j) {
@@ -806,8 +819,8 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                     float v = __uint_as_float(r[j / 32][j % 32]);
                     float f;
                     if constexpr (DECAY == kDecayNone) f = 1.f;
-                    else if constexpr (REV) f = safe ? eq * Fs[col] : __expf(Gs[col] - gi);
-                    else f = safe ? eq * Fs[col] : __expf(gi - Gs[col]) * Fs[col];
+                    else if constexpr (REV) f = safe ? eq[j / 32] * Fs[col] : __expf(Gs[col] - gi);
+                    else f = safe ? eq[j / 32] * Fs[col] : __expf(gi - Gs[col]) * Fs[col];
                     v = (!p.nomask && (REV ? col >= row : col <= row)) ? v * f : 0.f;
                     if constexpr (TR) v = tf32r(v);
                     rs += v;
@@ -852,7 +865,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
             if (c + 1 < nchunks) {
                 const int ns = (c + 1) & 1;
                 mbar_wait(&gfull[ns], ((c + 1) >> 1) & 1);
-                const float gnext = __expf(ringS[ns * 4]);
+                const float gnext = __expf(ringS[ns * 8]);
                 float vals[DH];
 #pragma unroll
                 for (int cb = 0; cb < DH / 32; ++cb) {

@@ -1,5 +1,7 @@
 """Per-rank step time of the cfg3 SP forward at the slice lengths of T = 1, 2, 4, 8 ranks
-(world 1 on one GPU: everything but the all-gather), to bound strong-scaling efficiency."""
+(world 1 on one GPU: everything but the all-gather), to bound strong-scaling efficiency.
+The Mamba2 per-head decays are the same at every T (the slice length would otherwise shift
+the random stream)."""
 import torch
 
 import paper_2503_05447_b200 as pk
@@ -15,21 +17,29 @@ for inst in ("mamba2", "gla"):
         q, k, v = (torch.randn(1, n, H, D, device="cuda", generator=g).mul_(0.5).bfloat16() for _ in range(3))
         spec = pk.LsmSpec.make(inst, D)
         if inst == "mamba2":
-            spec.mamba2_a_raw = torch.randn(H, device="cuda", generator=g).mul_(0.5)
+            ga = torch.Generator(device="cuda").manual_seed(1)  # same per-head decays at every T
+            spec.mamba2_a_raw = torch.randn(H, device="cuda", generator=ga).mul_(0.5)
             gates = pk.LsmGates(b_pre=torch.randn(1, n, H, device="cuda", generator=g))
         else:
             gates = pk.LsmGates(a_pre=torch.randn(1, n, H, D, device="cuda", generator=g).bfloat16())
+        # graph replay, as bench.py times the step
+        st = torch.cuda.Stream()
         out = torch.empty_like(q)
-        for _ in range(3):
-            sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(20):
-            sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / 20
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False, stream=st.cuda_stream)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=st):
+                sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False, stream=st.cuda_stream)
+            graph.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(50):
+                graph.replay()
+            e1.record(st)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 50
         base = base or ms
-        print("%s T=%d slice=%d: %.3f ms per rank step; ideal %.3f; efficiency bound %.1f%%"
+        print("%s T=%d slice=%d: %.3f ms per rank step (graph); ideal %.3f; efficiency bound %.1f%%"
               % (inst, T, n, ms, base / T, 100 * base / (T * ms)))

@@ -13,9 +13,9 @@ gates = pk.LsmGates(b_pre=torch.randn(1, N, H, device="cuda", generator=g))
 for _ in range(3):
     pk.lsm_forward_batched(q, k, v, gates, spec, 64, check=False)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (64 * 16 + 4096))()
+buf = (ctypes.c_ulonglong * (64 * 16 + 4 * 4096))()
 _lib.check(_lib.lib().lmoe_debug_trace_read(buf))
-t = np.array(buf, dtype=np.int64)[64 * 16:].reshape(-1, 2)
+t = np.array(buf, dtype=np.int64)[64 * 16:64 * 16 + 4096].reshape(-1, 2)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 s, e = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3

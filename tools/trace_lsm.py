@@ -14,7 +14,7 @@ gates = pk.LsmGates(b_pre=torch.randn(1, N, H, device="cuda", generator=g)) if s
 for _ in range(3):
     pk.lsm_forward_batched(q, k, v, gates, spec, 64, check=False)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 1024)()
+buf = (ctypes.c_ulonglong * (64 * 16 + 4 * 4096))()
 _lib.check(_lib.lib().lmoe_debug_trace_read(buf))
 t = np.array(buf, dtype=np.int64).reshape(64, 16)
 t0 = t[0, 10]

@@ -19,7 +19,7 @@ spec = pk.LsmSpec.make("gla", D)
 for _ in range(3):
     pk.lsm_backward_batched(q, k, v, pk.LsmGates(a_pre=a), spec, dO, check=False)
 torch.cuda.synchronize()
-buf = np.zeros(64 * 16, dtype=np.uint64)
+buf = np.zeros(64 * 16 + 4 * 4096, dtype=np.uint64)
 _lib.lib().lmoe_debug_trace_read(ctypes.c_void_p(buf.ctypes.data))
 t = buf.reshape(64, 16)[:3].astype(np.int64)
 t0 = t[0, 0]
