@@ -456,15 +456,33 @@ void lsm_mixer_core(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
     float* M0 = reinterpret_cast<float*>(ws + w.off_M0);
     float* z0 = reinterpret_cast<float*>(ws + w.off_z0);
     const size_t P = (size_t)B * H * payload_floats(desc, D);
+    g_last_gather_elements = (long long)world * (long long)P;
+    // developer knob (tools/sp_scaling_probe.py): run the multi-rank phase structure at world 1,
+    // a device copy standing in for the all-gather
+    const bool force_sp = getenv("LMOE_SP_FORCE") != nullptr;
+    if (world == 1 && !force_sp) {
+        // a gather over one rank is the identity and rank 0 carries nothing in: the local
+        // pass (state pass, segment prefix, output pass); the empty marks keep the phase
+        // timers' layout (all-gather, rank combine)
+        if (dtype == LMOE_BF16) c.state_pass<__nv_bfloat16>();
+        else c.state_pass<float>();
+        c.combine(nullptr, nullptr, true, M_out, z_out, nullptr, 0);
+        c.mark();
+        c.mark();
+        c.mark();
+        if (dtype == LMOE_BF16) c.output_pass<__nv_bfloat16>();
+        else c.output_pass<float>();
+        c.finish_timing();
+        c.check_err();
+        return;
+    }
     if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, payload);
     else sp_phase_a<float>(c, payload);
     c.mark();
-    if (world > 1) {
+    if (world > 1)
         NCCL_CHECK(ncclAllGather(payload, gathered, P, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
-    } else {
+    else
         LMOE_CUDA_CHECK(cudaMemcpyAsync(gathered, payload, P * 4, cudaMemcpyDeviceToDevice, st));
-    }
-    g_last_gather_elements = (long long)world * (long long)P;
     if (dtype == LMOE_BF16) sp_phase_b<__nv_bfloat16>(c, gathered, rank, M0, z0, M_out, z_out);
     else sp_phase_b<float>(c, gathered, rank, M0, z0, M_out, z_out);
     c.finish_timing();

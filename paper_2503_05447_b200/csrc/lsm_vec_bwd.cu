@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
 #pragma unroll
                 for (int blk = 0; blk < 2; ++blk) tma_store_4d(&tmDA, Ot + blk * kBlockBytes, blk * 64, h, t0, b);
                 bulk_commit();
-                bulk_wait0();  // smem must outlive the bulk stores
+                bulk_wait_read0();  // smem must outlive the bulk stores' reads of it
             }
         }
         if (threadIdx.x == 128) vb_mark(p, 2, 11);

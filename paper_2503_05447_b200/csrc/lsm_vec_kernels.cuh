@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
             if (tid == 0) trace_mark(p, c, 8);
         }
     }
-    if (threadIdx.x == 128) bulk_wait0();  // smem must outlive the last O store
+    if (threadIdx.x == 128) bulk_wait_read0();  // smem must outlive the last O store's read of it
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<512>(tmem);

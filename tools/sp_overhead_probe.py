@@ -6,7 +6,9 @@ import torch
 import paper_2503_05447_b200 as pk
 from paper_2503_05447_b200 import _lib, sp
 
-H, D, n = 16, 128, 32768
+import sys
+H, D = 16, 128
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 comm = sp.NcclComm(0, 1)
 g = torch.Generator(device="cuda").manual_seed(0)
 q, k, v = (torch.randn(1, n, H, D, device="cuda", generator=g).mul_(0.5).bfloat16() for _ in range(3))

@@ -1,7 +1,10 @@
 """Per-rank step time of the cfg3 SP forward at the slice lengths of T = 1, 2, 4, 8 ranks
 (world 1 on one GPU: everything but the all-gather), to bound strong-scaling efficiency.
 The Mamba2 per-head decays are the same at every T (the slice length would otherwise shift
-the random stream)."""
+the random stream).  LMOE_SP_FORCE keeps the multi-rank phase structure at world 1 (a device
+copy stands in for the all-gather); the T = 1 baseline is the local path bench.py times."""
+import os
+
 import torch
 
 import paper_2503_05447_b200 as pk
@@ -11,6 +14,7 @@ H, D = 16, 128
 comm = sp.NcclComm(0, 1)
 for inst in ("mamba2", "gla"):
     base = None
+    os.environ.pop("LMOE_SP_FORCE", None)
     for T in (1, 2, 4, 8):
         n = 262144 // T
         g = torch.Generator(device="cuda").manual_seed(0)
@@ -22,6 +26,8 @@ for inst in ("mamba2", "gla"):
             gates = pk.LsmGates(b_pre=torch.randn(1, n, H, device="cuda", generator=g))
         else:
             gates = pk.LsmGates(a_pre=torch.randn(1, n, H, D, device="cuda", generator=g).bfloat16())
+        if T > 1:
+            os.environ["LMOE_SP_FORCE"] = "1"
         # graph replay, as bench.py times the step
         st = torch.cuda.Stream()
         out = torch.empty_like(q)

@@ -16,7 +16,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * (64 * 16 + 4 * 4096))()
 _lib.check(_lib.lib().lmoe_debug_trace_read(buf))
-t = np.array(buf, dtype=np.int64).reshape(64, 16)
+t = np.array(buf, dtype=np.int64)[:64 * 16].reshape(64, 16)
 t0 = t[0, 10]
 names = {10: "load", 9: "S_iss", 6: "QMDM", 7: "PV", 8: "commit", 0: "m:S", 1: "m:xf2", 2: "m:P", 3: "m:mo", 4: "m:mrd", 5: "m:O"}
 order = [10, 9, 0, 1, 2, 6, 7, 8, 3, 4, 5]

@@ -18,7 +18,8 @@ comm = sp.NcclComm(0, 1)
 g = torch.Generator(device="cuda").manual_seed(0)
 q, k, v = (torch.randn(1, n, H, D, device="cuda", generator=g).mul_(0.5).bfloat16() for _ in range(3))
 spec = pk.LsmSpec.make("mamba2", D)
-spec.mamba2_a_raw = torch.randn(H, device="cuda", generator=g).mul_(0.5)
+ga = torch.Generator(device="cuda").manual_seed(1)  # as tools/sp_scaling_probe.py
+spec.mamba2_a_raw = torch.randn(H, device="cuda", generator=ga).mul_(0.5)
 gates = pk.LsmGates(b_pre=torch.randn(1, n, H, device="cuda", generator=g))
 out = torch.empty_like(q)
 st = torch.cuda.Stream()

@@ -21,7 +21,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = np.zeros(64 * 16 + 4 * 4096, dtype=np.uint64)
 _lib.lib().lmoe_debug_trace_read(ctypes.c_void_p(buf.ctypes.data))
-t = buf.reshape(64, 16)[:3].astype(np.int64)
+t = buf[:64 * 16].reshape(64, 16)[:3].astype(np.int64)
 t0 = t[0, 0]
 names = {0: ["start", "scan_done", "q_free"],
          1: ["full", "mx_full", "xf", "p_full", "dq_free"],

@@ -14,7 +14,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * (64 * 16 + 4 * 4096))()
 _lib.check(_lib.lib().lmoe_debug_trace_read(buf))
-t = np.array(buf, dtype=np.int64).reshape(64, 16)
+t = np.array(buf, dtype=np.int64)[:64 * 16].reshape(64, 16)
 t0 = t[0, 10]
 names = ["full", "scan", "xform", "stateop", "s_full", "P", "mo_full", "O", "end"]
 print("chunk  tma " + " ".join("%7s" % n for n in names))
