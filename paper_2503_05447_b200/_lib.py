@@ -33,8 +33,8 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if not _build.up_to_date():
+    path = os.environ.get("LMOE_LIB") or _build.LIB  # LMOE_LIB: developer A/B of a prebuilt library
+    if not os.environ.get("LMOE_LIB") and not _build.up_to_date():
         try:
             _build.build()
         except Exception as e:  # noqa: BLE001
