@@ -284,6 +284,49 @@ def gla_bench(dev, steps=3, warmup=2):
     return out
 
 
+def cfg2_bench(dev, steps=20, warmup=3):
+    """Config-2 side numbers: Lightning (a = 0.95) and RetNet (a = 1 - 1/32)
+    scalar-decay LSM forward, B = 1, N = 32768, H = 16, d = 128, bf16 in / out, through the
+    same call as the headline (world 1: the local pass), CUDA-graph replay; HBM roofline of
+    3 d s_in + d s_out = 1024 B per (token, head) (537 MB per step > L2, no flush needed)."""
+    import torch
+    import paper_2503_05447_b200 as pk
+    from paper_2503_05447_b200 import sp
+    n = 32768
+    comm = sp.NcclComm(0, 1)
+    g = torch.Generator(device=dev).manual_seed(2)
+    q, k, v = (torch.randn(1, n, HEADS, HEAD_DIM, device=dev, generator=g).mul_(0.5).to(torch.bfloat16)
+               for _ in range(3))
+    out_t = torch.empty_like(q)
+    hbm, _, _ = peaks()
+    res = {}
+    st = torch.cuda.Stream(dev)
+    for inst in ("lightning", "retnet"):
+        spec = pk.LsmSpec.make(inst, HEAD_DIM)
+        gates = pk.LsmGates()
+        with torch.cuda.stream(st):
+            for _ in range(warmup):
+                sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out_t, check=False, stream=st.cuda_stream)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=st):
+                sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out_t, check=False, stream=st.cuda_stream)
+            graph.replay()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(steps):
+                graph.replay()
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / steps
+        gbs = 1024 * n * HEADS / (ms / 1e3) / 1e9
+        res[inst] = {"tokens_per_s": n / (ms / 1e3), "ms_per_step": ms, "steps": steps,
+                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                                  "alg_bytes_per_token_head": 1024, "note": "whole step (3 kernels)"}}
+    res["workload"] = "cfg2 scalar-decay LSM forward, N=32768, 16 x 128, bf16, CUDA-graph replay"
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -464,6 +507,7 @@ def main():
             extra["layer"] = layer_bench(dev)
             extra["backward"] = backward_bench(dev)
             extra["gla"] = gla_bench(dev)
+            extra["cfg2"] = cfg2_bench(dev)
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(args.instance, SEQ, os.cpu_count() or 1, 20.0)
         line = {
