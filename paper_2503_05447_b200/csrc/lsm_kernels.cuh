@@ -397,7 +397,8 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
     uint64_t* gfull = bars + 10;   // [2]
     uint64_t* gfree = bars + 12;   // [2]
     uint64_t* xf1 = bars + 14;
-    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 15);
+    uint64_t* o_staged = bars + 15;  // bf16 O of the chunk staged in its Q tile (store warp)
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 16);
 
     const int seg = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int bh = b * p.H + h;
@@ -421,6 +422,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
         mbar_init(m_ready, MT);
         mbar_init(mo_full, 1);
         mbar_init(xf1, MT);
+        mbar_init(o_staged, MT);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(sTmem);
@@ -590,6 +592,21 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
             mbar_arrive(&gfull[slot]);
 #pragma unroll
             for (int u = 0; u < 4; ++u) { bvA[u] = bvB[u]; bvB[u] = bvC[u]; }
+        }
+    } else if (warp == 3) {
+        // ---------------- O store warp (bf16 O): bulk-store each staged chunk, then release
+        // its stage once the store has read the tile, off the math warps' path
+        if (lane == 0 && kBF16 && !p.out_f32) {
+            for (int c = 0; c < nchunks; ++c) {
+                const int s = c % NST;
+                uint8_t* qt = tiles + s * 3 * kTileBytes;
+                mbar_wait(o_staged, c & 1);
+                tma_store_4d(&tmO, qt, 0, h, chunk_t0(c), b);
+                tma_store_4d(&tmO, qt + kBlockBytes, TT::EPB, h, chunk_t0(c), b);
+                bulk_commit();
+                bulk_wait_read0();
+                mbar_arrive(&empty[s]);
+            }
         }
     } else if (warp >= 4) {
         // ---------------- math warps ----------------------------------------------------
@@ -936,14 +953,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                     }
                     tc_fence_before();
                     fence_proxy_async_smem();
-                    named_bar_sync(2, MT);
-                    if (tid == 0) {
-                        tma_store_4d(&tmO, qt, 0, h, t0, b);
-                        tma_store_4d(&tmO, qt + kBlockBytes, TT::EPB, h, t0, b);
-                        bulk_commit();
-                        bulk_wait_read0();
-                        mbar_arrive(&empty[s]);
-                    }
+                    mbar_arrive(o_staged);  // warp 3 stores the tile and releases the stage
                 } else if (kBF16 && p.out_f32) {  // fp32 rows (backward intermediates)
                     float* dstf = reinterpret_cast<float*>(p.o) +
                                   (((size_t)b * p.Nstride + t0 + (vrow ? row : 0)) * p.H + h) * D + hh * DH;
