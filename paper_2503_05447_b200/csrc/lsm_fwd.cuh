@@ -67,39 +67,7 @@ struct LsmFwdParams {
     void* mst;
     int nchunk_tot;
     unsigned long long* trace;  // optional clock64 trace of CTA (0,0,0) [64 chunks][16]
-    // sequence parallelism, rank combine folded into the output pass (sp_fold_carry): the
-    // gathered payloads [world][sp_BH][sp_P] (sp_lw log-decay entries at the end of each), or null
-    const float* sp_gath;
-    int sp_rank, sp_P, sp_lw, sp_BH;
 };
-
-// Sequence parallelism with the rank combine folded into the output pass (no combine kernel
-// between the all-gather and the output pass): the state entering segment `seg` of rank r is
-// its local exclusive prefix (Min, from a zero state) plus the earlier ranks' carried-in state
-// decayed over this rank's segments before `seg`:  Min + e^{Lpre} M_rank_in, where
-// M_rank_in = sum_{i<r} (prod_{i<j<r} D_j) M_i is the decayed prefix of the gathered payloads
-// (parallel.hpp:340-361) and Lpre the sum of the segment log decays before `seg`.
-// Adds the fold to vals[0..N) = elements [off, off + N) of one payload row; li is the
-// log-decay entry of that row (0 for scalar decays).
-template <int N>
-__device__ __forceinline__ void sp_fold_carry(const LsmFwdParams& p, int bh, int seg, int off, int li,
-                                              float (&vals)[N]) {
-    if (p.sp_gath == nullptr || p.sp_rank == 0) return;
-    float acc[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) acc[j] = 0.f;
-    for (int i = 0; i < p.sp_rank; ++i) {
-        const float* pl = p.sp_gath + ((size_t)i * p.sp_BH + bh) * p.sp_P;
-        const float e = __expf(pl[p.sp_P - p.sp_lw + li]);
-#pragma unroll
-        for (int j = 0; j < N; ++j) acc[j] = e * acc[j] + pl[off + j];
-    }
-    float lp = 0.f;
-    for (int s = 0; s < seg; ++s) lp += p.logDseg[((size_t)bh * p.nseg + s) * p.sp_lw + li];
-    const float sc = __expf(lp);
-#pragma unroll
-    for (int j = 0; j < N; ++j) vals[j] += sc * acc[j];
-}
 
 // per-CTA globaltimer at kernel start (after the prologue) and end, slots after the 64 x 16
 // chunk trace: [region][cta][2] for up to 2048 CTAs (region 0 output pass, 1 state pass)

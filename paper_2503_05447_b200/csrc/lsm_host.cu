@@ -308,35 +308,21 @@ static SpWorkspace plan_sp(const lmoe_lsm_desc* d, int B, int N_local, int H, in
 // Phase A of sp_lsm_masked_rank (parallel.hpp:313-327): local state from zero and the
 // payload [M | z? | log D] per (b,h), written to `payload`.
 template <typename T>
-static void sp_phase_a(LsmCall& c, float* payload, bool write_min) {
+static void sp_phase_a(LsmCall& c, float* payload) {
     const int P = (int)payload_floats(c.d, c.D);
     c.state_pass<T>();
-    c.combine(nullptr, nullptr, write_min, payload, c.norm ? payload + c.D * c.D : nullptr,
+    c.combine(nullptr, nullptr, false, payload, c.norm ? payload + c.D * c.D : nullptr,
               payload + P - c.lw, P);
 }
 // Phase B (parallel.hpp:340-373): decayed exclusive prefix over ranks < rank, then the
 // output pass with the carried-in state.
-// Without final-state outputs the rank combine is folded into the output pass
-// (sp_fold_carry): phase A then leaves the local segment prefixes in Min (min_ready), and the
-// output pass reads the gathered payloads directly.  With M_out / z_out one kernel combines
-// ranks and segments and also writes the rank's final state.
-static bool sp_fold(float* M_out, float* z_out) { return !M_out && !z_out; }
 template <typename T>
-static void sp_phase_b(LsmCall& c, const float* gathered, int rank, float* M_out, float* z_out, bool min_ready) {
+static void sp_phase_b(LsmCall& c, const float* gathered, int rank, float* M0, float* z0,
+                       float* M_out, float* z_out) {
     const int P = (int)payload_floats(c.d, c.D);
-    c.mark();  // rank-combine phase (folded into the output pass, or fused with the segment combine)
+    (void)M0; (void)z0;
+    c.mark();  // rank-combine phase (fused with the segment combine below)
     c.mark();
-    if (sp_fold(M_out, z_out)) {
-        if (!min_ready) c.combine(nullptr, nullptr, true, nullptr, nullptr, nullptr, 0);
-        c.p.sp_gath = gathered;
-        c.p.sp_rank = rank;
-        c.p.sp_P = P;
-        c.p.sp_lw = c.lw;
-        c.p.sp_BH = c.B * c.H;
-        c.output_pass<T>();
-        c.p.sp_gath = nullptr;
-        return;
-    }
     LMOE_CUDA_CHECK(lmoe_dev::launch_rank_seg_combine(gathered, P, c.B * c.H, rank, c.p.Sseg, c.p.zseg, c.p.logDseg,
                                                       const_cast<float*>(c.p.Min), const_cast<float*>(c.p.zin),
                                                       M_out, z_out, c.pl.nseg, c.D, c.D, c.norm ? 1 : 0, c.lw,
@@ -467,6 +453,8 @@ void lsm_mixer_core(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
     c.clear_err();
     float* payload = reinterpret_cast<float*>(ws + w.off_payload);
     float* gathered = reinterpret_cast<float*>(ws + w.off_gathered);
+    float* M0 = reinterpret_cast<float*>(ws + w.off_M0);
+    float* z0 = reinterpret_cast<float*>(ws + w.off_z0);
     const size_t P = (size_t)B * H * payload_floats(desc, D);
     g_last_gather_elements = (long long)world * (long long)P;
     // developer knob (tools/sp_scaling_probe.py): run the multi-rank phase structure at world 1,
@@ -488,16 +476,15 @@ void lsm_mixer_core(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
         c.check_err();
         return;
     }
-    const bool fold = sp_fold(M_out, z_out);
-    if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, payload, fold);
-    else sp_phase_a<float>(c, payload, fold);
+    if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, payload);
+    else sp_phase_a<float>(c, payload);
     c.mark();
     if (world > 1)
         NCCL_CHECK(ncclAllGather(payload, gathered, P, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
     else
         LMOE_CUDA_CHECK(cudaMemcpyAsync(gathered, payload, P * 4, cudaMemcpyDeviceToDevice, st));
-    if (dtype == LMOE_BF16) sp_phase_b<__nv_bfloat16>(c, gathered, rank, M_out, z_out, fold);
-    else sp_phase_b<float>(c, gathered, rank, M_out, z_out, fold);
+    if (dtype == LMOE_BF16) sp_phase_b<__nv_bfloat16>(c, gathered, rank, M0, z0, M_out, z_out);
+    else sp_phase_b<float>(c, gathered, rank, M0, z0, M_out, z_out);
     c.finish_timing();
     c.check_err();
 }
@@ -553,6 +540,8 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
         const size_t esz = dtype == LMOE_BF16 ? 2 : 4;
         const size_t P = (size_t)B * H * payload_floats(desc, D);
         float* gathered = reinterpret_cast<float*>(ws + w.off_gathered);
+        float* M0 = reinterpret_cast<float*>(ws + w.off_M0);
+        float* z0 = reinterpret_cast<float*>(ws + w.off_z0);
         auto slice_call = [&](int r) {
             const int base = N / world, rem = N % world;  // chunk_range (parallel.hpp:192-197)
             const int r0 = r * base + std::min(r, rem);
@@ -569,8 +558,8 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
         slice_call(0).clear_err();
         for (int r = 0; r < world; ++r) {
             LsmCall c = slice_call(r);
-            if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, gathered + r * P, false);
-            else sp_phase_a<float>(c, gathered + r * P, false);
+            if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, gathered + r * P);
+            else sp_phase_a<float>(c, gathered + r * P);
         }
         g_last_gather_elements = (long long)world * (long long)P;
         for (int r = 0; r < world; ++r) {
@@ -578,10 +567,10 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
             const bool last = r == world - 1;
             if (dtype == LMOE_BF16) {
                 c.state_pass<__nv_bfloat16>();
-                sp_phase_b<__nv_bfloat16>(c, gathered, r, last ? M_out : nullptr, last ? z_out : nullptr, false);
+                sp_phase_b<__nv_bfloat16>(c, gathered, r, M0, z0, last ? M_out : nullptr, last ? z_out : nullptr);
             } else {
                 c.state_pass<float>();
-                sp_phase_b<float>(c, gathered, r, last ? M_out : nullptr, last ? z_out : nullptr, false);
+                sp_phase_b<float>(c, gathered, r, M0, z0, last ? M_out : nullptr, last ? z_out : nullptr);
             }
             if (last) c.check_err();
         }
@@ -1064,7 +1053,7 @@ static void sp_bwd_payloads(const lmoe_lsm_desc* d, int B, int n, int Nstride, i
                             float* bpay, cudaStream_t st) {
     LsmCall c{d, B, n, Nstride, H, D, dt, q, k, v, b_pre, a_raw, nullptr, ws, plan_lsm(B, n, H, D), st, a_pre};
     c.setup();
-    sp_phase_a<T>(c, fpay, false);
+    sp_phase_a<T>(c, fpay);
     // reverse pass over (phi(q), dO): identity map (phi applied beforehand), no normaliser
     lmoe_lsm_desc dd = *d;
     dd.feature_map = 0;

@@ -692,7 +692,6 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                 const float4 v = sown ? *reinterpret_cast<const float4*>(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
                 vals[j] = v.x; vals[j + 1] = v.y; vals[j + 2] = v.z; vals[j + 3] = v.w;
             }
-            if (sown) sp_fold_carry(p, bh, seg, srow * D + hh * DH, 0, vals);
             write_state_operand(vals);
             state_hook(vals, 0);
 #pragma unroll
@@ -703,11 +702,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                 tmem_st32(tM + lane_off + hh * DH + cb * 32, r);
             }
             if constexpr (NORM) {
-                if (tid < D) {
-                    float zv[1] = {p.zin[((size_t)bh * p.nseg + seg) * D + tid]};
-                    sp_fold_carry(p, bh, seg, D * D + tid, 0, zv);
-                    sZ[tid] = zv[0];
-                }
+                if (tid < D) sZ[tid] = p.zin[((size_t)bh * p.nseg + seg) * D + tid];
                 named_bar_sync(1, MT);
             }
             tmem_wait_st();

@@ -420,21 +420,15 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
             const float* src = p.Min + (((size_t)bh * p.nseg + seg) * D + (sown ? srow : 0)) * D + hh * DH;
 #pragma unroll
             for (int cb = 0; cb < DH / 32; ++cb) {
-                float vals[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) vals[j] = sown ? src[cb * 32 + j] : 0.f;
-                if (sown) sp_fold_carry(p, bh, seg, srow * D + hh * DH + cb * 32, srow, vals);
                 uint32_t r[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(vals[j]);
+                for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(sown ? src[cb * 32 + j] : 0.f);
                 tmem_st32(tM + lane_off + hh * DH + cb * 32, r);
             }
             tmem_wait_st();
             if constexpr (NORM) {
                 if (tid < D) {
-                    float zv[1] = {p.zin[((size_t)bh * p.nseg + seg) * D + tid]};
-                    sp_fold_carry(p, bh, seg, D * D + tid, tid, zv);
-                    sZ[tid] = zv[0];
+                    sZ[tid] = p.zin[((size_t)bh * p.nseg + seg) * D + tid];
                     sZC[tid] = 0.f;
                 }
             }
