@@ -111,10 +111,19 @@ __global__ void sp_rank_seg_combine(const float* __restrict__ gathered, int P, i
     const int ee = isz ? e - nm : e;
     const int row = isz ? ee : ee / dv;
     const int li = lw == 1 ? 0 : row;
+    // decayed prefix over the earlier ranks; the payload loads do not depend on it, so they are
+    // issued 8 ranks at a time ahead of the recurrence
     float acc = 0.f;
-    for (int i = 0; i < rank; ++i) {
-        const float* pl = gathered + ((size_t)i * BH + bh) * P;
-        acc = __expf(pl[P - lw + li]) * acc + pl[e];
+    for (int i0 = 0; i0 < rank; i0 += 8) {
+        float mv[8], dv8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float* pl = gathered + ((size_t)(i0 + u) * BH + bh) * P;
+            mv[u] = i0 + u < rank ? pl[e] : 0.f;
+            dv8[u] = i0 + u < rank ? __expf(pl[P - lw + li]) : 1.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = dv8[u] * acc + mv[u];
     }
     const int stride = isz ? dk : nm;
     const float* src = isz ? zS : S;
