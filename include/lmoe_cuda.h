@@ -292,7 +292,9 @@ int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int
  * entering the slice end, and the local backward (lmoe_lsm_bwd with M0 and dM_final) is then
  * exact for the slice.  Outputs as lmoe_lsm_bwd for the slice; da_raw is this rank's
  * contribution (the sum over ranks is the full gradient); dM0 is meaningful on rank 0.
- * No normaliser in this build. */
+ * Normalised instances (o = num / den) compose two unnormalised SP forwards (num over v, den
+ * over e0, whose state column 0 is z) and two unnormalised SP backwards, as lmoe_lsm_bwd does
+ * locally: 4 collective rounds instead of 1. */
 size_t lmoe_sp_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
                                       lmoe_dtype dtype, int world);
 int lmoe_sp_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D, lmoe_dtype dtype,

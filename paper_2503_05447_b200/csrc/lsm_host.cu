@@ -1039,10 +1039,71 @@ static SpBwdPlan plan_sp_bwd(const lmoe_lsm_desc* d, int B, int N_local, int H, 
     return p;
 }
 
-static void check_sp_bwd_args(const lmoe_lsm_desc* d) {
-    if (d->use_normalizer)
-        throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_sp_lsm_bwd: normalizer SP backward not in this build");
+// Normaliser SP backward (sp_norm_bwd below): o = num / den with num = LSM(q, k, v) and den =
+// column 0 of LSM(q, k, e0), both unnormalised and sequence-parallel (den's state column 0 is
+// the normaliser z, lsm.hpp:584-596), so the VJP is the unnormalised SP backward of num under
+// dO / den plus that of den under -(dO . num) / den^2 -- the composition lmoe_lsm_bwd uses
+// locally, with the SP forward / backward (and their collectives) in place of the local ones.
+struct SpNormPlan {
+    size_t off_e0 = 0, off_num = 0, off_den = 0, off_dO1 = 0, off_dO2 = 0, off_dq2 = 0, off_dk2 = 0, off_dv2 = 0,
+           off_da2 = 0, off_err = 0, off_inner = 0, inner = 0, total = 0;
+};
+static SpNormPlan plan_sp_norm(size_t rows, int D, lmoe_dtype dt, size_t inner) {
+    SpNormPlan p;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    p.inner = inner;
+    p.off_inner = take(inner);
+    const size_t act = rows * D * (dt == LMOE_BF16 ? 2 : 4);
+    p.off_e0 = take(act); p.off_num = take(act); p.off_den = take(act);
+    p.off_dO1 = take(act); p.off_dO2 = take(act);
+    p.off_dq2 = take(act); p.off_dk2 = take(act); p.off_dv2 = take(act); p.off_da2 = take(act);
+    p.off_err = take(64);
+    p.total = off;
+    return p;
 }
+// fwd(desc, v, out, ws, bytes) and bwd(desc, v, dO, dq, dk, dv, da, dM0, ws, bytes) run the
+// unnormalised SP forward / backward of this rank (or of all virtual ranks)
+template <typename Fwd, typename Bwd>
+static void sp_norm_bwd(const lmoe_lsm_desc* desc, size_t rows, int D, lmoe_dtype dt, const void* v, const void* dO,
+                        void* dq, void* dk, void* dv, void* da_pre, float* dM0, uint8_t* ws, const SpNormPlan& w,
+                        cudaStream_t st, Fwd fwd, Bwd bwd) {
+    lmoe_lsm_desc dd = *desc;
+    dd.use_normalizer = 0;
+    const bool bf16 = dt == LMOE_BF16;
+    const bool vec = device_decay_mode(desc->instance) == lmoe_dev::kDecayTokenVector;
+    int* err = reinterpret_cast<int*>(ws + w.off_err);
+    LMOE_CUDA_CHECK(cudaMemsetAsync(err, 0, 64, st));
+    void* e0 = ws + w.off_e0;
+    LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(0, bf16, e0, nullptr, nullptr, nullptr, nullptr, nullptr, rows, D,
+                                                  nullptr, st));
+    fwd(&dd, v, ws + w.off_num);
+    fwd(&dd, e0, ws + w.off_den);
+    LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(1, bf16, nullptr, ws + w.off_num, ws + w.off_den, dO, ws + w.off_dO1,
+                                                  ws + w.off_dO2, rows, D, err, st));
+    g_launch_count += 2;
+    if (desc->flags & LMOE_FLAG_CHECK) {
+        int e = 0;
+        LMOE_CUDA_CHECK(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        LMOE_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (e)
+            throw Error(LMOE_ERR_DEGENERATE, std::string("degenerate normalizer in instance ") + instance_name(desc->instance));
+    }
+    bwd(&dd, v, ws + w.off_dO1, dq, dk, dv, da_pre, dM0);
+    bwd(&dd, e0, ws + w.off_dO2, ws + w.off_dq2, ws + w.off_dk2, ws + w.off_dv2, vec ? ws + w.off_da2 : nullptr,
+        nullptr);
+    LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(2, bf16, dq, ws + w.off_dq2, nullptr, nullptr, nullptr, nullptr, rows,
+                                                  D, nullptr, st));
+    LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(2, bf16, dk, ws + w.off_dk2, nullptr, nullptr, nullptr, nullptr, rows,
+                                                  D, nullptr, st));
+    g_launch_count += 2;
+    if (vec) {
+        LMOE_CUDA_CHECK(lmoe_dev::launch_norm_helpers(2, bf16, da_pre, ws + w.off_da2, nullptr, nullptr, nullptr,
+                                                      nullptr, rows, D, nullptr, st));
+        ++g_launch_count;
+    }
+}
+static void check_sp_bwd_args(const lmoe_lsm_desc* d) { (void)d; }
 
 // One slice: writes the forward payload [M | log D] (from zero) and the reverse-time payload
 // [X | log D] (X = sum_t (phi(q_t) e^{P_t})^T dO_t, P_t = decay from the slice start through t).
@@ -1074,9 +1135,19 @@ static void sp_bwd_payloads(const lmoe_lsm_desc* d, int B, int n, int Nstride, i
 }
 }  // namespace lmoe_host
 
+static SpNormPlan plan_sp_norm_rank(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D, lmoe_dtype dtype,
+                                    int world) {
+    lmoe_lsm_desc dd = *desc;
+    dd.use_normalizer = 0;
+    const size_t inner = std::max(plan_sp_bwd(&dd, B, N_local, H, D, dtype, world).total,
+                                  plan_sp(&dd, B, N_local, H, D, world).total);
+    return plan_sp_norm((size_t)B * N_local * H, D, dtype, inner);
+}
+
 extern "C" size_t lmoe_sp_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
                                                  lmoe_dtype dtype, int world) {
     if (!desc || B < 1 || N_local < 1 || H < 1 || D < 1 || world < 1) return 0;
+    if (desc->use_normalizer) return plan_sp_norm_rank(desc, B, N_local, H, D, dtype, world).total;
     return plan_sp_bwd(desc, B, N_local, H, D, dtype, world).total;
 }
 
@@ -1090,6 +1161,27 @@ extern "C" int lmoe_sp_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N_local, in
         check_sp_bwd_args(desc);
         if (world < 1 || rank < 0 || rank >= world) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd: bad rank");
         if (world > 1 && !nccl_comm) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd: null communicator");
+        if (desc->use_normalizer) {
+            const SpNormPlan w = plan_sp_norm_rank(desc, B, N_local, H, D, dtype, world);
+            if (!workspace || workspace_bytes < w.total)
+                throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd: workspace too small (need " + std::to_string(w.total) + " bytes)");
+            uint8_t* ws = static_cast<uint8_t*>(workspace);
+            auto chk = [](int rc) {
+                if (rc != LMOE_OK) throw Error(rc, lmoe_last_error());
+            };
+            auto fwd = [&](const lmoe_lsm_desc* dd, const void* vv, void* out) {
+                chk(lmoe_sp_lsm_fwd(dd, B, N_local, H, D, dtype, q, k, vv, a_pre, b_pre, a_raw, out, nullptr, nullptr,
+                                    nccl_comm, rank, world, ws + w.off_inner, w.inner, stream));
+            };
+            auto bwd = [&](const lmoe_lsm_desc* dd, const void* vv, const void* g, void* gq, void* gk, void* gv,
+                           void* ga, float* gM0) {
+                chk(lmoe_sp_lsm_bwd(dd, B, N_local, H, D, dtype, q, k, vv, a_pre, b_pre, a_raw, g, gq, gk, gv, ga,
+                                    db_pre, da_raw, gM0, nccl_comm, rank, world, ws + w.off_inner, w.inner, stream));
+            };
+            sp_norm_bwd(desc, (size_t)B * N_local * H, D, dtype, v, dO, dq, dk, dv, da_pre, dM0, ws, w,
+                        reinterpret_cast<cudaStream_t>(stream), fwd, bwd);
+            return;
+        }
         const SpBwdPlan w = plan_sp_bwd(desc, B, N_local, H, D, dtype, world);
         if (!workspace || workspace_bytes < w.total)
             throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd: workspace too small (need " + std::to_string(w.total) + " bytes)");
@@ -1132,9 +1224,19 @@ extern "C" int lmoe_sp_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N_local, in
     });
 }
 
+static SpNormPlan plan_sp_norm_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
+                                        int world) {
+    lmoe_lsm_desc dd = *desc;
+    dd.use_normalizer = 0;
+    const int n = (N + world - 1) / world;
+    const size_t inner = std::max(plan_sp_bwd(&dd, B, n, H, D, dtype, world).total, plan_sp(&dd, B, n, H, D, world).total);
+    return plan_sp_norm((size_t)B * N * H, D, dtype, inner);
+}
+
 extern "C" size_t lmoe_sp_lsm_bwd_loopback_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
                                                           lmoe_dtype dtype, int world) {
     if (!desc || world < 1 || N < world) return 0;
+    if (desc->use_normalizer) return plan_sp_norm_loopback(desc, B, N, H, D, dtype, world).total;
     return plan_sp_bwd(desc, B, (N + world - 1) / world, H, D, dtype, world).total;
 }
 
@@ -1148,6 +1250,27 @@ extern "C" int lmoe_sp_lsm_bwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
         check_sp_bwd_args(desc);
         if (B != 1) throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd_loopback: B == 1 (rank slices are contiguous rows)");
         if (world < 1 || N < world) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");
+        if (desc->use_normalizer) {
+            const SpNormPlan w = plan_sp_norm_loopback(desc, B, N, H, D, dtype, world);
+            if (!workspace || workspace_bytes < w.total)
+                throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd_loopback: workspace too small");
+            uint8_t* ws = static_cast<uint8_t*>(workspace);
+            auto chk = [](int rc) {
+                if (rc != LMOE_OK) throw Error(rc, lmoe_last_error());
+            };
+            auto fwd = [&](const lmoe_lsm_desc* dd, const void* vv, void* out) {
+                chk(lmoe_sp_lsm_fwd_loopback(dd, B, N, H, D, dtype, q, k, vv, a_pre, b_pre, a_raw, out, nullptr,
+                                             nullptr, world, ws + w.off_inner, w.inner, stream));
+            };
+            auto bwd = [&](const lmoe_lsm_desc* dd, const void* vv, const void* g, void* gq, void* gk, void* gv,
+                           void* ga, float* gM0) {
+                chk(lmoe_sp_lsm_bwd_loopback(dd, B, N, H, D, dtype, q, k, vv, a_pre, b_pre, a_raw, g, gq, gk, gv, ga,
+                                             db_pre, da_raw, gM0, world, ws + w.off_inner, w.inner, stream));
+            };
+            sp_norm_bwd(desc, (size_t)B * N * H, D, dtype, v, dO, dq, dk, dv, da_pre, dM0, ws, w,
+                        reinterpret_cast<cudaStream_t>(stream), fwd, bwd);
+            return;
+        }
         const SpBwdPlan w = plan_sp_bwd(desc, B, (N + world - 1) / world, H, D, dtype, world);
         if (!workspace || workspace_bytes < w.total)
             throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd_loopback: workspace too small");
