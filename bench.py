@@ -368,7 +368,8 @@ def main():
                .to(torch.bfloat16) for _ in range(3))
     b_pre = torch.randn(1, n_loc, HEADS, device=dev, generator=g)
     spec = pk.LsmSpec.make(args.instance, HEAD_DIM)
-    spec.mamba2_a_raw = torch.randn(HEADS, device=dev, generator=g).mul_(0.5)
+    # a_raw is a per-head parameter of the whole sequence: the same on every rank
+    spec.mamba2_a_raw = torch.randn(HEADS, device=dev, generator=torch.Generator(device=dev).manual_seed(99)).mul_(0.5)
     gates = pk.LsmGates(b_pre=b_pre) if args.instance == "mamba2" else None
     out = torch.empty_like(q)
     stream = torch.cuda.Stream(dev)  # a side stream (CUDA-graph capture needs a non-default stream)
