@@ -135,6 +135,9 @@ CASES = [  # (name, spec, dtype, B, N, H)
     ("mamba2_short", {"instance": 13}, "bf16", 2, 256, 2),
     ("mamba2_f32", {"instance": 13}, "f32", 2, 333, 2),
     ("mamba2_long", {"instance": 13}, "bf16", 1, 4096, 2),
+    # strong decays: some 32-token key quarters exceed the factorisation bound (exact path)
+    ("mamba2_strong", {"instance": 13}, "bf16", 1, 900, 2),
+    ("mamba2_strong_f32", {"instance": 13}, "f32", 1, 500, 2),
     ("tiny", {"instance": 2, "scalar_decay": 0.9}, "bf16", 1, 1, 1),
 ]
 
@@ -149,8 +152,12 @@ def test_bwd_matches_oracle(case):
     M0 = rng.normal(0, 0.1, (B, H, D, D))
     b_pre = a_raw = None
     if spec["instance"] == 13:
-        b_pre = rng.normal(-1.0 if "long" in name else 0.0, 1.0, (B, N, H))
-        a_raw = rng.normal(0, 0.5, H)
+        if "strong" in name:
+            b_pre = rng.normal(1.5, 1.5, (B, N, H))
+            a_raw = rng.normal(2.5, 0.3, H)
+        else:
+            b_pre = rng.normal(-1.0 if "long" in name else 0.0, 1.0, (B, N, H))
+            a_raw = rng.normal(0, 0.5, H)
     got = _bwd(spec, q, k, v, dO, b_pre, a_raw, M0, dtype=dtype)
     want = _oracle_bwd(spec, q, k, v, dO, b_pre, a_raw, M0)
     tol = TOL[dtype]
@@ -168,7 +175,10 @@ def test_bwd_matches_oracle(case):
                 err = norm_rel_err(got["db_pre"][b, :, h], want["db_pre"][b, :, h])
                 assert err < tol, (name, "db_pre", b, h, err)
         rel = np.abs(got["da_raw"] - want["da_raw"]).max() / max(1e-6, np.abs(want["da_raw"]).max())
-        assert rel < GATE_TOL[dtype], (name, "da_raw", got["da_raw"], want["da_raw"])
+        # da_raw sums the per-token gate terms over the sequence; under strong decays that sum
+        # cancels, and the tf32 rounding of the per-token terms (bounded above) shows up to ~3e-3
+        gtol = max(GATE_TOL[dtype], 5e-3) if "strong" in name else GATE_TOL[dtype]
+        assert rel < gtol, (name, "da_raw", got["da_raw"], want["da_raw"])
 
 
 @pytest.mark.parametrize("inst", [2, 13])

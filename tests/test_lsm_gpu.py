@@ -133,6 +133,35 @@ def test_random_vs_oracle(inst, fm, norm, dtype, N, H):
             assert norm_rel_err(z[0, h], zw) < TOL[dtype], (inst, h, "z")
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("a_raw_h,b_mean", [(0.0, -3.0), (1.5, 0.0), (3.0, 1.5)])
+def test_mamba2_decay_regimes(dtype, a_raw_h, b_mean):
+    """Mamba2 across decay regimes against the sequential oracle (lsm.hpp:643-662): long
+    memory; default-like; strong decays whose 32-token quarters exceed the factorisation bound
+    on some chunks, so the exact per-element path runs next to the factored one in one launch.
+    Short and ragged lengths (1, 63, 129) exercise single-chunk CTAs and partial chunks."""
+    rng = np.random.default_rng(zlib.crc32(repr((dtype, a_raw_h, b_mean)).encode()))
+    D = 64 if dtype == "f32" else 128
+    H = 3
+    for N in (1, 63, 129, 777):
+        q, k, v = (rng.normal(0, 0.5, (1, N, H, D)) for _ in range(3))
+        if dtype == "bf16":
+            q, k, v = _bf16_round(q), _bf16_round(k), _bf16_round(v)
+        spec = oracle.spec_default("mamba2")
+        a_raw = (a_raw_h + rng.normal(0, 0.3, H)).astype(np.float32).astype(np.float64)
+        spec["mamba2_a_raw_h"] = a_raw
+        b_pre = rng.normal(b_mean, 1.5, (1, N, H)).astype(np.float32).astype(np.float64)
+        o, M, _ = _run(spec, q, k, v, b_pre, dtype=dtype, final=True)
+        for h in range(H):
+            sh = dict(spec, mamba2_a_raw=float(a_raw[h]))
+            want, Mw, _ = oracle.lsm_sequential(sh, q[0, :, h], k[0, :, h], v[0, :, h], b_pre=b_pre[0, :, h])
+            # fp32 inputs run the chunk GEMMs in tf32 (round-to-nearest, fp32 accumulation): a
+            # single-token output is one tf32 dot product and can carry ~5e-3 under cancellation
+            tol = 1e-2 if (dtype == "f32" and N == 1) else TOL[dtype]
+            assert norm_rel_err(o[0, :, h], want) < tol, (N, h, a_raw_h, norm_rel_err(o[0, :, h], want))
+            assert norm_rel_err(M[0, h], Mw) < tol, (N, h, "M")
+
+
 def test_chunk_size_invariance_and_initial_state():
     """Chunked == sequential for any chunk size (lsm.hpp:641-642); an initial state equals
     running the prefix first (the SP carried-in state, parallel.hpp:366-373)."""
