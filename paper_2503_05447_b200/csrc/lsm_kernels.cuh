@@ -682,8 +682,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
         if constexpr (kPrep) prep(0);
         // initial state: operand M_0, TMEM M = e^{G_end(0)} M_0
         {
-            mbar_wait(&gfull[0], 0);
-            const float g0 = __expf(ringS[0]);  // G_end of chunk 0
+            // the entering state's load does not depend on the decay warp: issue it first
             float vals[DH];
             const size_t mslot = p.nomask ? (size_t)bh : (size_t)bh * p.nseg + seg;
             const float* src = p.Min + (mslot * D + (sown ? srow : 0)) * D + hh * DH;
@@ -692,6 +691,8 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                 const float4 v = sown ? *reinterpret_cast<const float4*>(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
                 vals[j] = v.x; vals[j + 1] = v.y; vals[j + 2] = v.z; vals[j + 3] = v.w;
             }
+            mbar_wait(&gfull[0], 0);
+            const float g0 = __expf(ringS[0]);  // G_end of chunk 0
             write_state_operand(vals);
             state_hook(vals, 0);
 #pragma unroll
