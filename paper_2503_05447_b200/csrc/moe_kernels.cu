@@ -83,7 +83,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc(1, 0, 1, 128, BN);
+            // SwiGLU: the gate and up B tiles sit back to back in the stage (N atoms 8 KB apart),
+            // so one N = 2 BN MMA covers both and reads the A tile once per K step
+            constexpr uint32_t idesc = umma_idesc(1, 0, 1, 128, NB * BN);
             int it = 0, lt = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
                 const int buf = lt & 1;
@@ -101,9 +103,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         const uint64_t ad = umma_desc_sw128(a0 + kk * 32, 16, 1024);
                         const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
                         mma_ss_f16(acc_t, ad, umma_desc_sw128(b0 + kk * 2048, 8192, 1024), idesc, acc);
-                        if constexpr (NB == 2)
-                            mma_ss_f16(acc_t + BN, ad, umma_desc_sw128(b0 + B_BYTES + kk * 2048, 8192, 1024),
-                                       idesc, acc);
                     }
                     mma_commit(&empty[s]);
                 }
