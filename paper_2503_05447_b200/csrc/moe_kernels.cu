@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 128); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], kGemmEpiThreads); }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<TCOLS>(sTmem);
@@ -110,8 +110,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
     } else {
-        // epilogue: thread (quarter q, lane) owns output row q*32 + lane of the tile
+        // epilogue: thread (quarter q, lane) owns output row q*32 + lane of the tile; the two
+        // warps of a lane quarter take one column half each
         const int q = warp & 3;
+        constexpr int EH = kGemmEpiThreads / 128;  // epilogue warps per lane quarter
+        const int ch = (warp - 2) / 4;             // this warp's column part
         const int r = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         int lt = 0;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const bool valid = r < rows_left;
             const size_t grow = (size_t)row0 + (valid ? r : 0);
 #pragma unroll 1
-            for (int cb = 0; cb < BN; cb += 32) {
+            for (int cb = ch * (BN / EH); cb < (ch + 1) * (BN / EH); cb += 32) {
                 uint32_t a[32];
                 tmem_ld32(acc_t + lane_off + cb, a);
                 if constexpr (EPI == kEpiSwiGLU) {

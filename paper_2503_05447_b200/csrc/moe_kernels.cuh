@@ -5,7 +5,8 @@
 namespace lmoe_dev {
 
 enum GemmEpilogue { kEpiBF16 = 0, kEpiSwiGLU = 1, kEpiF32 = 2 };
-constexpr int kGemmThreads = 192;  // TMA, MMA, 4 epilogue warps
+constexpr int kGemmThreads = 320;  // TMA, MMA, 8 epilogue warps (two per TMEM lane quarter)
+constexpr int kGemmEpiThreads = kGemmThreads - 64;
 
 struct GemmParams {
     const int* num_tiles;   // device: number of valid 128-row tiles
