@@ -203,6 +203,13 @@ __global__ void __launch_bounds__(256) moe_route(const float* __restrict__ logit
                                                  int* __restrict__ ids, float* __restrict__ gates,
                                                  float* __restrict__ probs, int* __restrict__ counts,
                                                  float* __restrict__ prob_colsum) {
+    // per-block expert counts / probability sums: warps reduce into shared memory, and one
+    // global atomic per block and expert follows (per-warp global atomics on the same 64
+    // addresses serialised at L2)
+    __shared__ int s_cnt[64];
+    __shared__ float s_ps[64];
+    if (threadIdx.x < 64) { s_cnt[threadIdx.x] = 0; s_ps[threadIdx.x] = 0.f; }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int wglobal = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int nwarps = gridDim.x * (blockDim.x / 32);
@@ -229,26 +236,27 @@ __global__ void __launch_bounds__(256) moe_route(const float* __restrict__ logit
         }
         ps0 += p0;
         ps1 += p1;
-        // top-k by repeated warp argmax: larger logit first, ties -> lower id (moe.hpp:70-75)
+        // top-k by repeated warp argmax: larger logit first, ties -> lower id (moe.hpp:70-75).
+        // Logits map to order-preserving unsigned keys (0 = taken / absent), so each round is
+        // one redux.sync max plus two ballots; the lowest set id among the maxima wins the tie.
+        auto key = [](float f) -> unsigned {
+            const unsigned u = __float_as_uint(f + 0.f);  // -0 -> +0: equal logits tie on id
+            return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        };
+        const unsigned k0 = has0 ? key(v0) : 0u, k1 = has1 ? key(v1) : 0u;
         bool sel0 = false, sel1 = false;
-        float top = NEG;
+        unsigned topk = 0u;
         for (int r = 0; r < K; ++r) {
-            float bv;
-            int bi;
-            const bool c0 = has0 && !sel0, c1 = has1 && !sel1;
-            if (c0 && (!c1 || v0 >= v1)) { bv = v0; bi = lane; }
-            else if (c1) { bv = v1; bi = lane + 32; }
-            else { bv = NEG; bi = 1 << 30; }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const float ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
-                const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
-                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-            }
-            if (r == 0) top = bv;
+            const unsigned c0 = sel0 ? 0u : k0, c1 = sel1 ? 0u : k1;
+            const unsigned best = __reduce_max_sync(0xFFFFFFFFu, c0 > c1 ? c0 : c1);
+            const unsigned b0 = __ballot_sync(0xFFFFFFFFu, c0 == best && c0 != 0u);
+            const unsigned b1 = __ballot_sync(0xFFFFFFFFu, c1 == best && c1 != 0u);
+            const int bi = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
+            if (r == 0) topk = best;
             if (bi == lane) sel0 = true;
             if (bi == lane + 32) sel1 = true;
         }
+        const float top = __uint_as_float((topk & 0x80000000u) ? (topk & 0x7FFFFFFFu) : ~topk);
         // ascending ids of the selection (moe.hpp:77) + masked softmax (max = top-1 logit)
         const unsigned m0 = __ballot_sync(0xFFFFFFFFu, sel0), m1 = __ballot_sync(0xFFFFFFFFu, sel1);
         const float g0 = sel0 ? __expf(v0 - top) : 0.f, g1 = sel1 ? __expf(v1 - top) : 0.f;
@@ -269,12 +277,17 @@ __global__ void __launch_bounds__(256) moe_route(const float* __restrict__ logit
         }
     }
     if (has0) {
-        if (cnt0) atomicAdd(&counts[lane], cnt0);
-        if (prob_colsum) atomicAdd(&prob_colsum[lane], ps0);
+        if (cnt0) atomicAdd(&s_cnt[lane], cnt0);
+        atomicAdd(&s_ps[lane], ps0);
     }
     if (has1) {
-        if (cnt1) atomicAdd(&counts[lane + 32], cnt1);
-        if (prob_colsum) atomicAdd(&prob_colsum[lane + 32], ps1);
+        if (cnt1) atomicAdd(&s_cnt[lane + 32], cnt1);
+        atomicAdd(&s_ps[lane + 32], ps1);
+    }
+    __syncthreads();
+    if (threadIdx.x < E) {
+        if (s_cnt[threadIdx.x]) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
+        if (prob_colsum) atomicAdd(&prob_colsum[threadIdx.x], s_ps[threadIdx.x]);
     }
 }
 

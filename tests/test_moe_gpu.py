@@ -35,13 +35,17 @@ def test_route_golden_bit_exact():
 
 
 @pytest.mark.parametrize("T,E,k,kind", [(65536, 64, 8, "normal"), (4096, 64, 8, "ties"),
-                                         (3000, 48, 5, "normal"), (1000, 8, 2, "ties")])
+                                         (3000, 48, 5, "normal"), (1000, 8, 2, "ties"),
+                                         (2000, 64, 8, "signed_zeros")])
 def test_route_random_bit_exact(T, E, k, kind):
     torch = _torch()
     from paper_2503_05447_b200 import moe
     rng = np.random.default_rng(T + E + k)
     if kind == "ties":
         logits = (rng.integers(0, 6, (T, E)) * 0.25).astype(np.float32)
+    elif kind == "signed_zeros":  # +0.0 and -0.0 compare equal: the lower id wins the tie
+        logits = (rng.integers(-2, 1, (T, E)) * 0.5).astype(np.float32)
+        logits = np.where(logits == 0, np.where(rng.random((T, E)) < 0.5, -0.0, 0.0), -np.abs(logits)).astype(np.float32)
     else:
         logits = rng.normal(0, 1, (T, E)).astype(np.float32)
     dec = moe.route(torch.tensor(logits, device="cuda"), k)
