@@ -20,6 +20,19 @@
 #include "lsm_launch.h"
 
 namespace lmoe_dev {
+
+// L2 prefetch distance of the gate kernel in CTAs (one wave = the SM count); LMOE_DG_PF = waves
+static int dgate_pf_ahead() {
+    static int v = -1;
+    if (v < 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char* e = getenv("LMOE_DG_PF");
+        v = (e ? atoi(e) : 1) * sms;
+    }
+    return v;
+}
 namespace {
 
 __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x)); }
@@ -120,7 +133,7 @@ __global__ void __launch_bounds__(kDgThreads, 1)
                     const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmDM,
                     const float* __restrict__ b_pre, const float* __restrict__ a_raw,
                     const float* __restrict__ dkf, const T* __restrict__ dk, float* __restrict__ db_pre,
-                    float* __restrict__ da_raw, int N, int H, int nchunk) {
+                    float* __restrict__ da_raw, int N, int H, int nchunk, int p_pf_ahead) {
     using TT = TileTraits<T>;
     using L = DgateSmem<T>;
     constexpr int D = TT::D;
@@ -171,6 +184,23 @@ __global__ void __launch_bounds__(kDgThreads, 1)
             tma_load_4d(smem + L::kO + blk * kBlockBytes, &tmO, bar, blk * TT::EPB, h, t0, b);
             tma_load_2d(smem + L::kM + blk * MBLK, &tmM, bar, blk * TT::EPB, mrow);
             tma_load_2d(smem + L::kDM + blk * MBLK, &tmDM, bar, blk * TT::EPB, mrow);
+        }
+        // warm L2 with the tiles of the CTA one wave ahead (one CTA per SM, linear launch order)
+        if (p_pf_ahead > 0) {
+            const long long lin = c + (long long)gridDim.x * bh + p_pf_ahead;
+            if (lin < (long long)gridDim.x * gridDim.y) {
+                const int c2 = (int)(lin % gridDim.x), bh2 = (int)(lin / gridDim.x);
+                const int b2 = bh2 / H, h2 = bh2 % H, t2 = c2 * kC, mrow2 = (bh2 * nchunk + c2) * D;
+#pragma unroll
+                for (int blk = 0; blk < 2; ++blk) {
+                    tma_prefetch_l2_4d(&tmQ, blk * TT::EPB, h2, t2, b2);
+                    tma_prefetch_l2_4d(&tmK, blk * TT::EPB, h2, t2, b2);
+                    tma_prefetch_l2_4d(&tmV, blk * TT::EPB, h2, t2, b2);
+                    tma_prefetch_l2_4d(&tmO, blk * TT::EPB, h2, t2, b2);
+                    tma_prefetch_l2_2d(&tmM, blk * TT::EPB, mrow2);
+                    tma_prefetch_l2_2d(&tmDM, blk * TT::EPB, mrow2);
+                }
+            }
         }
     }
     // gates while the tiles land: g_t = -softplus(b_t) softplus(a_h), kf_t = softplus(b_t)
@@ -422,7 +452,7 @@ static cudaError_t dgate_t(const CUtensorMap& q, const CUtensorMap& k, const CUt
     if (e != cudaSuccess) return e;
     lsm_mamba_dgate<T><<<dim3(nchunk, B * H), kDgThreads, smem, st>>>(q, k, v, dO, m, dm, b_pre, a_raw, dkf,
                                                                 static_cast<const T*>(dk), db_pre, da_raw, N, H,
-                                                                nchunk);
+                                                                nchunk, dgate_pf_ahead());
     return cudaGetLastError();
 }
 
