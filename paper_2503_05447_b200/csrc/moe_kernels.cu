@@ -451,10 +451,15 @@ __global__ void moe_combine(const __nv_bfloat16* __restrict__ y_perm, const int*
         float acc[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+        // all K row loads in flight before the (ordered) accumulation
+        uint4 vv[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            vv[s] = s < K ? *reinterpret_cast<const uint4*>(y_perm + (size_t)pos[s] * hidden + c) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
             if (s >= K) break;
-            const uint4 v = *reinterpret_cast<const uint4*>(y_perm + (size_t)pos[s] * hidden + c);
+            const uint4 v = vv[s];
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
