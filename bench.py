@@ -162,6 +162,32 @@ def run_reference(args, world, rank):
     print(json.dumps(line))
 
 
+def make_inputs(dev, n_loc, rank, instance="mamba2"):
+    """Synthetic inputs of the config-3 shape, this rank's slice [1, n_loc, H, d] (also used by
+    tests/test_fullshape_gpu.py, so parity is checked on exactly the benchmarked data):
+    q, k, v ~ N(0, 0.5^2) bf16; Mamba2 b_pre ~ N(0, 1) fp32 and a_raw ~ N(0, 0.5^2) per head
+    (the reference's LsmSpec::make / LsmGates defaults, lsm.hpp:177, 222-253)."""
+    import torch
+    import paper_2503_05447_b200 as pk
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q, k, v = (torch.randn(1, n_loc, HEADS, HEAD_DIM, device=dev, generator=g).mul_(0.5)
+               .to(torch.bfloat16) for _ in range(3))
+    b_pre = torch.randn(1, n_loc, HEADS, device=dev, generator=g)
+    spec = pk.LsmSpec.make(instance, HEAD_DIM)
+    # a_raw is a per-head parameter of the whole sequence: the same on every rank
+    spec.mamba2_a_raw = torch.randn(HEADS, device=dev, generator=torch.Generator(device=dev).manual_seed(99)).mul_(0.5)
+    gates = pk.LsmGates(b_pre=b_pre) if instance == "mamba2" else None
+    return q, k, v, b_pre, spec, gates
+
+
+def make_gla_inputs(dev, n=SEQ):
+    """cfg3 GLA side inputs (gla_bench): q, k, v ~ N(0, 0.5^2), dO, a_pre ~ N(0, 1), bf16."""
+    import torch
+    g = torch.Generator(device=dev).manual_seed(21)
+    return tuple(torch.randn(1, n, HEADS, HEAD_DIM, device=dev, generator=g).mul_(s).to(torch.bfloat16)
+                 for s in (0.5, 0.5, 0.5, 1.0, 1.0))
+
+
 def layer_bench(dev, steps=5, warmup=3):
     """SURVEY 8(d) second number: LSM-layer tokens/s on cfg4 (A0.3B-2B Linear-MoE block:
     hidden 1024, 8 heads x 128, GLA, FFN 896, 64 experts top-8; 8 documents x 8192 tokens)
@@ -257,9 +283,7 @@ def gla_bench(dev, steps=3, warmup=2):
     per (token, head))."""
     import torch
     import paper_2503_05447_b200 as pk
-    g = torch.Generator(device=dev).manual_seed(21)
-    q, k, v, dO, a = (torch.randn(1, SEQ, HEADS, HEAD_DIM, device=dev, generator=g).mul_(s).to(torch.bfloat16)
-                      for s in (0.5, 0.5, 0.5, 1.0, 1.0))
+    q, k, v, dO, a = make_gla_inputs(dev)
     gates = pk.LsmGates(a_pre=a)
     spec = pk.LsmSpec.make("gla", HEAD_DIM)
     hbm, _, _ = peaks()
@@ -362,15 +386,7 @@ def main():
     r0, r1 = spm.chunk_range(SEQ, world, rank)
     n_loc = r1 - r0
 
-    # synthetic inputs of the config-3 shape: this rank's slice [1, n_loc, H, d]
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    q, k, v = (torch.randn(1, n_loc, HEADS, HEAD_DIM, device=dev, generator=g).mul_(0.5)
-               .to(torch.bfloat16) for _ in range(3))
-    b_pre = torch.randn(1, n_loc, HEADS, device=dev, generator=g)
-    spec = pk.LsmSpec.make(args.instance, HEAD_DIM)
-    # a_raw is a per-head parameter of the whole sequence: the same on every rank
-    spec.mamba2_a_raw = torch.randn(HEADS, device=dev, generator=torch.Generator(device=dev).manual_seed(99)).mul_(0.5)
-    gates = pk.LsmGates(b_pre=b_pre) if args.instance == "mamba2" else None
+    q, k, v, b_pre, spec, gates = make_inputs(dev, n_loc, rank, args.instance)
     out = torch.empty_like(q)
     stream = torch.cuda.Stream(dev)  # a side stream (CUDA-graph capture needs a non-default stream)
 

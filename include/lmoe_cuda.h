@@ -54,7 +54,10 @@ enum lmoe_instance {
     LMOE_TITANS = 10, LMOE_S4 = 11, LMOE_MAMBA = 12, LMOE_RWKV7 = 16
 };
 enum lmoe_feature_map { LMOE_FM_IDENTITY = 0, LMOE_FM_ELU1 = 1, LMOE_FM_SQUARED = 2 };
-enum lmoe_flags { LMOE_FLAG_CHECK = 1, LMOE_FLAG_TIMING = 2 };
+/* LMOE_FLAG_TEST_DECAY_FAULT: TEST ONLY -- the within-chunk cumulative decay of the scalar-decay
+ * kernels is shifted by one token (the reference's kern::chunk_decay_fault hook, lsm.hpp:310-317,
+ * caught by test_lsm.cpp:221-235); results are then wrong by construction. */
+enum lmoe_flags { LMOE_FLAG_CHECK = 1, LMOE_FLAG_TIMING = 2, LMOE_FLAG_TEST_DECAY_FAULT = 4 };
 
 /* Mirrors the fields of lmoe::LsmSpec (lsm.hpp:126-140) that the separable kinds use.
  * Static per-head parameters (Mamba2 a_raw) are passed as arrays. */
@@ -197,7 +200,9 @@ int lmoe_rmsnorm(const float* x, int rows, int hidden, const float* w, float eps
  *   dM0        : [B,H,D,D] fp32 gradient of the initial state (may be NULL)
  * No recomputation of the forward output is needed: the passes consume q, k, v, dO only
  * (the normaliser composes two unnormalised backwards and two forwards for num / den).
- * TokenVector kinds: bf16 / head_dim 128 only.
+ * TokenVector kinds: bf16 / head_dim 128 only.  Normalised instances: the VJP of the forward
+ * with M_in = M0 and z_in = 0 (there is no z0 input; callers carrying a normaliser state in
+ * must not use this entry point -- the Python mirror raises).
  * ------------------------------------------------------------------------------------- */
 size_t lmoe_lsm_bwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
                                    lmoe_dtype dtype);
@@ -243,9 +248,11 @@ typedef struct lmoe_lsm_recurrent_inputs {
     const float* s4_A_raw;      /* S4: [H, D, D]                                           */
     const float* mamba_A_raw;   /* Mamba: [H, D, D]                                        */
 } lmoe_lsm_recurrent_inputs;
+/* workspace: >= 64 bytes of device memory (the device error flag; no allocation inside). */
 int lmoe_lsm_fwd_recurrent(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
                            const void* q, const void* k, const void* v, const lmoe_lsm_recurrent_inputs* in,
-                           const float* M0, void* o, float* M_out, lmoe_stream_t stream);
+                           const float* M0, void* o, float* M_out, void* workspace, size_t workspace_bytes,
+                           lmoe_stream_t stream);
 
 /* Number of kernels one lmoe_lsm_fwd call launches (for launch accounting). */
 int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc);

@@ -270,17 +270,13 @@ static void attn_launch(int B, int Nq, int Nk, int H, int D, int row_offset, con
     const CUtensorMap tv = make_tmap_4d(v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
     AttnParams p{Nq, Nk, H, row_offset, 1.4426950408889634f / sqrtf((float)D), static_cast<__nv_bfloat16*>(o)};
     constexpr int smem = 5 * kTileBytes + 256;
-    static bool attr = false;
-    if (!attr) {
-        LMOE_CUDA_CHECK(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
+    LMOE_CUDA_CHECK(lmoe_dev::ensure_smem((const void*)attn_fwd_kernel, smem));
     attn_fwd_kernel<<<dim3((Nq + kC - 1) / kC, H, B), kAttnThreads, smem, st>>>(tq, tk, tv, p);
     LMOE_CUDA_CHECK(cudaGetLastError());
     ++g_launch_count;
 }
 
-static long long g_attn_gather_elements = 0;
+static thread_local long long g_attn_gather_elements = 0;
 
 void attn_core(int B, int Nq, int Nk, int H, int D, const void* q, const void* k, const void* v, int ld,
                void* o, int row_offset, cudaStream_t st) {

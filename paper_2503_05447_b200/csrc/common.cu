@@ -1,12 +1,14 @@
 // common.cu -- C-ABI plumbing: thread-local last error, TMA descriptor encoding, device info.
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.h"
 
 namespace lmoe_host {
 
 static thread_local std::string t_last_error;
-long long g_launch_count = 0;
+std::atomic<long long> g_launch_count{0};
 
 void set_last_error(const std::string& msg) { t_last_error = msg; }
 
@@ -83,18 +85,36 @@ CUtensorMap make_tmap_2d(const void* base, CUtensorMapDataType dt, int esize, ui
 }
 
 int num_sms() {
-    static int n = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::atomic<int> cache[64] = {};
+    if (dev < 0 || dev >= 64) dev = 0;
+    int n = cache[dev].load();
     if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         if (n <= 0) n = 148;
+        cache[dev].store(n);
     }
     return n;
 }
 
 }  // namespace lmoe_host
 
+namespace lmoe_dev {
+cudaError_t ensure_smem(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({fn, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({fn, dev});
+    return e;
+}
+}  // namespace lmoe_dev
+
 extern "C" const char* lmoe_last_error(void) { return lmoe_host::t_last_error.c_str(); }
 extern "C" const char* lmoe_version(void) { return "lmoe-b200 0.1 (sm_100a)"; }
-extern "C" long long lmoe_launch_count(void) { return lmoe_host::g_launch_count; }
+extern "C" long long lmoe_launch_count(void) { return lmoe_host::g_launch_count.load(); }

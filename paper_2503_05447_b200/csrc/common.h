@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -63,6 +64,10 @@ int guarded(F&& f) {
 }
 
 // Launch counters (kernels of this library enqueued since process start).
-extern long long g_launch_count;
+extern std::atomic<long long> g_launch_count;
 
 }  // namespace lmoe_host
+
+namespace lmoe_dev {
+cudaError_t ensure_smem(const void* fn, int bytes);  // common.cu; see lsm_launch.h
+}

@@ -440,13 +440,8 @@ static cudaError_t dgate_t(const CUtensorMap& q, const CUtensorMap& k, const CUt
                            const CUtensorMap& dO, const CUtensorMap& m, const CUtensorMap& dm,
                            const float* b_pre, const float* a_raw, const float* dkf, const void* dk,
                            float* db_pre, float* da_raw, int B, int N, int H, cudaStream_t st) {
-    static bool attr = false;
     constexpr int smem = DgateSmem<T>::kTotal;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_mamba_dgate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem((const void*)lsm_mamba_dgate<T>, smem); e != cudaSuccess) return e;
     const int nchunk = (N + kC - 1) / kC;
     cudaError_t e = cudaMemsetAsync(da_raw, 0, sizeof(float) * H, st);
     if (e != cudaSuccess) return e;

@@ -67,6 +67,7 @@ struct LsmFwdParams {
     void* mst;
     int nchunk_tot;
     unsigned long long* trace;  // optional clock64 trace of CTA (0,0,0) [64 chunks][16]
+    int fault;                  // TEST ONLY (LMOE_FLAG_TEST_DECAY_FAULT): decay shifted by one token
 };
 
 // per-CTA globaltimer at kernel start (after the prologue) and end, slots after the 64 x 16

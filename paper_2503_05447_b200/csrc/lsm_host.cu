@@ -28,9 +28,12 @@ struct PhaseTimer {
         return pool[next++];
     }
 };
-static PhaseTimer g_timer;
-static long long g_last_gather_elements = 0;
-static unsigned long long* g_trace = nullptr;
+// Per calling thread (the library keeps no shared mutable state besides the launch counter):
+// the timing events, the SP element accounting (RankGroup::comm_log, parallel.hpp:87-93) and
+// the developer trace buffer belong to the thread that made the call.
+static thread_local PhaseTimer g_timer;
+static thread_local long long g_last_gather_elements = 0;
+static thread_local unsigned long long* g_trace = nullptr;
 
 static const char* kInstanceNames[] = {"bla",    "lightning", "retnet", "gla",   "deltanet",
                                        "gated_deltanet", "rebased", "gfw", "gateloop", "ttt",
@@ -175,6 +178,7 @@ struct LsmCall {
         p.zin = reinterpret_cast<const float*>(ws + pl.off_zin);
         p.o = o;
         p.err = reinterpret_cast<int*>(ws + pl.off_err);
+        p.fault = (d->flags & LMOE_FLAG_TEST_DECAY_FAULT) ? 1 : 0;
         // developer knobs: phase-3 schedule and a clock64 trace of CTA (0,0,0)
         static const int order = getenv("LMOE_OP_ORDER") ? atoi(getenv("LMOE_OP_ORDER")) : 1;
         p.order = order;
@@ -288,19 +292,27 @@ static size_t payload_floats(const lmoe_lsm_desc* d, int D) {
 
 struct SpWorkspace {
     LsmPlan pl;
-    size_t off_payload = 0, off_gathered = 0, off_M0 = 0, off_z0 = 0, total = 0;
+    size_t region = 0;  // bytes of the per-slice LSM region (max over the slice lengths served)
+    size_t off_payload = 0, off_gathered = 0, off_M0 = 0, off_z0 = 0, off_err = 0, total = 0;
 };
 
-static SpWorkspace plan_sp(const lmoe_lsm_desc* d, int B, int N_local, int H, int D, int world) {
+// n_min: the shortest slice this workspace serves (loopback: N / world, while N_local is the
+// longest).  plan_lsm is not monotone in N, so the per-slice region is the max over both
+// lengths; every slice carves its own plan inside [0, region) and shares one error slot.
+static SpWorkspace plan_sp(const lmoe_lsm_desc* d, int B, int N_local, int H, int D, int world,
+                           int n_min = -1) {
     SpWorkspace w;
     w.pl = plan_lsm(B, N_local, H, D);
+    w.region = w.pl.total;
+    if (n_min > 0 && n_min != N_local) w.region = std::max(w.region, plan_lsm(B, n_min, H, D).total);
     const size_t BH = (size_t)B * H, P = payload_floats(d, D);
-    size_t off = align_up(w.pl.total, 256);
+    size_t off = align_up(w.region, 256);
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
     w.off_payload = take(BH * P * 4);
     w.off_gathered = take((size_t)world * BH * P * 4);
     w.off_M0 = take(BH * D * D * 4);
     w.off_z0 = take(BH * D * 4);
+    w.off_err = take(64);
     w.total = off;
     return w;
 }
@@ -519,7 +531,7 @@ extern "C" size_t lmoe_sp_lsm_fwd_loopback_workspace_size(const lmoe_lsm_desc* d
                                                           int H, int D, lmoe_dtype dtype, int world) {
     (void)dtype;
     if (!desc || world < 1 || N < world) return 0;
-    return plan_sp(desc, B, (N + world - 1) / world, H, D, world).total;
+    return plan_sp(desc, B, (N + world - 1) / world, H, D, world, N / world).total;
 }
 
 extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
@@ -532,7 +544,7 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
         validate(desc, B, N, H, D, dtype, q, k, v, o);
         (void)a_pre;
         if (world < 1 || N < world) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");
-        const SpWorkspace w = plan_sp(desc, B, (N + world - 1) / world, H, D, world);
+        const SpWorkspace w = plan_sp(desc, B, (N + world - 1) / world, H, D, world, N / world);
         if (!workspace || workspace_bytes < w.total)
             throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_fwd_loopback: workspace too small");
         uint8_t* ws = static_cast<uint8_t*>(workspace);
@@ -553,6 +565,7 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
                       a_raw, static_cast<uint8_t*>(o) + off, ws, plan_lsm(B, len, H, D), st,
                       a_pre ? static_cast<const uint8_t*>(a_pre) + off : nullptr};
             c.setup();
+            c.p.err = reinterpret_cast<int*>(ws + w.off_err);  // one error slot for all slices
             return c;
         };
         slice_call(0).clear_err();
@@ -651,7 +664,7 @@ extern "C" int lmoe_sp_lsm_nomask_fwd_loopback(const lmoe_lsm_desc* desc, int B,
         validate(desc, B, N, H, D, dtype, q, k, v, o);
         validate_nomask(desc);
         if (world < 1 || N < world) throw Error(LMOE_ERR_ARG, "chunk_range: need at least one row per rank");
-        const SpWorkspace w = plan_sp(desc, B, (N + world - 1) / world, H, D, world);
+        const SpWorkspace w = plan_sp(desc, B, (N + world - 1) / world, H, D, world, N / world);
         if (!workspace || workspace_bytes < w.total)
             throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_nomask_fwd_loopback: workspace too small");
         uint8_t* ws = static_cast<uint8_t*>(workspace);
@@ -670,6 +683,7 @@ extern "C" int lmoe_sp_lsm_nomask_fwd_loopback(const lmoe_lsm_desc* desc, int B,
                       static_cast<const uint8_t*>(v) + off, nullptr, nullptr,
                       static_cast<uint8_t*>(o) + off, ws, plan_lsm(B, len, H, D), st, nullptr};
             c.setup();
+            c.p.err = reinterpret_cast<int*>(ws + w.off_err);
             return c;
         };
         slice_call(0).clear_err();
@@ -1022,9 +1036,10 @@ struct SpBwdPlan {
 };
 static size_t bwd_payload_floats(const lmoe_lsm_desc* d, int D) { return (size_t)D * D + payload_lw(d, D); }
 
-static SpBwdPlan plan_sp_bwd(const lmoe_lsm_desc* d, int B, int N_local, int H, int D, lmoe_dtype dt, int world) {
+static SpBwdPlan plan_sp_bwd(const lmoe_lsm_desc* d, int B, int N_local, int H, int D, lmoe_dtype dt, int world,
+                            int n_min = -1) {
     SpBwdPlan p;
-    p.f = plan_sp(d, B, N_local, H, D, world);
+    p.f = plan_sp(d, B, N_local, H, D, world, n_min);
     size_t off = align_up(p.f.total, 256);
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
     const size_t BH = (size_t)B * H, P = BH * bwd_payload_floats(d, D);
@@ -1034,6 +1049,7 @@ static SpBwdPlan plan_sp_bwd(const lmoe_lsm_desc* d, int B, int N_local, int H, 
     if (d->feature_map != 0) p.off_phq = take((size_t)B * N_local * H * D * (dt == LMOE_BF16 ? 2 : 4));
     p.off_dar = take((size_t)H * 4);
     p.bws = plan_bwd(d, B, N_local, H, D, dt).total;
+    if (n_min > 0 && n_min != N_local) p.bws = std::max(p.bws, plan_bwd(d, B, n_min, H, D, dt).total);
     p.off_bws = take(p.bws);
     p.total = off;
     return p;
@@ -1229,7 +1245,8 @@ static SpNormPlan plan_sp_norm_loopback(const lmoe_lsm_desc* desc, int B, int N,
     lmoe_lsm_desc dd = *desc;
     dd.use_normalizer = 0;
     const int n = (N + world - 1) / world;
-    const size_t inner = std::max(plan_sp_bwd(&dd, B, n, H, D, dtype, world).total, plan_sp(&dd, B, n, H, D, world).total);
+    const size_t inner = std::max(plan_sp_bwd(&dd, B, n, H, D, dtype, world, N / world).total,
+                                  plan_sp(&dd, B, n, H, D, world, N / world).total);
     return plan_sp_norm((size_t)B * N * H, D, dtype, inner);
 }
 
@@ -1237,7 +1254,7 @@ extern "C" size_t lmoe_sp_lsm_bwd_loopback_workspace_size(const lmoe_lsm_desc* d
                                                           lmoe_dtype dtype, int world) {
     if (!desc || world < 1 || N < world) return 0;
     if (desc->use_normalizer) return plan_sp_norm_loopback(desc, B, N, H, D, dtype, world).total;
-    return plan_sp_bwd(desc, B, (N + world - 1) / world, H, D, dtype, world).total;
+    return plan_sp_bwd(desc, B, (N + world - 1) / world, H, D, dtype, world, N / world).total;
 }
 
 extern "C" int lmoe_sp_lsm_bwd_loopback(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
@@ -1271,7 +1288,7 @@ extern "C" int lmoe_sp_lsm_bwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
                         reinterpret_cast<cudaStream_t>(stream), fwd, bwd);
             return;
         }
-        const SpBwdPlan w = plan_sp_bwd(desc, B, (N + world - 1) / world, H, D, dtype, world);
+        const SpBwdPlan w = plan_sp_bwd(desc, B, (N + world - 1) / world, H, D, dtype, world, N / world);
         if (!workspace || workspace_bytes < w.total)
             throw Error(LMOE_ERR_ARG, "lmoe_sp_lsm_bwd_loopback: workspace too small");
         uint8_t* ws = static_cast<uint8_t*>(workspace);

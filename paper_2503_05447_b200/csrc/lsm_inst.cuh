@@ -9,14 +9,9 @@ namespace {
 template <typename T, int DECAY, int FM, bool NORM, bool REV>
 cudaError_t sp_launch(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CUtensorMap& v,
                       const LsmFwdParams& p) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_state_pass<T, DECAY, FM, NORM, REV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             state_pass_smem<T>());
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem((const void*)lsm_state_pass<T, DECAY, FM, NORM, REV>, state_pass_smem<T>());
+        e != cudaSuccess)
+        return e;
     return launch_pdl(lsm_state_pass<T, DECAY, FM, NORM, REV>, grid, dim3(kStatePassThreads), state_pass_smem<T>(),
                       st, k, v, p);
 }
@@ -24,14 +19,9 @@ cudaError_t sp_launch(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CU
 template <typename T, int DECAY, int FM, bool NORM, bool REV>
 cudaError_t op_launch(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& k,
                       const CUtensorMap& v, const CUtensorMap& o, const LsmFwdParams& p) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_output_pass<T, DECAY, FM, NORM, REV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             output_pass_smem<T>());
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem((const void*)lsm_output_pass<T, DECAY, FM, NORM, REV>, output_pass_smem<T>());
+        e != cudaSuccess)
+        return e;
     return launch_pdl(lsm_output_pass<T, DECAY, FM, NORM, REV>, grid, dim3(output_pass_threads<T>()),
                       output_pass_smem<T>(), st, q, k, v, o, p);
 }

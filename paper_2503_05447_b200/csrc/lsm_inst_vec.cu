@@ -8,13 +8,9 @@ namespace {
 template <typename T, int FM, bool NORM, bool HG, bool REV = false>
 cudaError_t spv(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CUtensorMap& v, const CUtensorMap& a,
                 const LsmFwdParams& p) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_state_pass_vec<T, FM, NORM, HG, REV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, state_pass_vec_smem<T>());
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem((const void*)lsm_state_pass_vec<T, FM, NORM, HG, REV>, state_pass_vec_smem<T>());
+        e != cudaSuccess)
+        return e;
     return launch_pdl(lsm_state_pass_vec<T, FM, NORM, HG, REV>, grid, dim3(kStatePassVecThreads),
                       state_pass_vec_smem<T>(), st, k, v, a, p);
 }
@@ -22,13 +18,9 @@ cudaError_t spv(dim3 grid, cudaStream_t st, const CUtensorMap& k, const CUtensor
 template <typename T, int FM, bool NORM, bool HG>
 cudaError_t opv(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                 const CUtensorMap& a, const CUtensorMap& o, const LsmFwdParams& p) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_output_pass_vec<T, FM, NORM, HG>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, output_pass_vec_smem<T>());
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem((const void*)lsm_output_pass_vec<T, FM, NORM, HG>, output_pass_vec_smem<T>());
+        e != cudaSuccess)
+        return e;
     return launch_pdl(lsm_output_pass_vec<T, FM, NORM, HG>, grid, dim3(output_pass_vec_threads<T>()),
                       output_pass_vec_smem<T>(), st, q, k, v, a, o, p);
 }

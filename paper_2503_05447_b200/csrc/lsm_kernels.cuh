@@ -43,9 +43,10 @@ __device__ __forceinline__ float chunk_scan(const LsmFwdParams& p, const float (
             kf[u] = valid ? spb : 0.f;
         }
     }
+    float own[4];
     float run = 0.f;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { run += la[u]; la[u] = run; }
+    for (int u = 0; u < 4; ++u) { own[u] = la[u]; run += la[u]; la[u] = run; }
     float x = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -55,6 +56,10 @@ __device__ __forceinline__ float chunk_scan(const LsmFwdParams& p, const float (
     const float excl = x - run;
 #pragma unroll
     for (int u = 0; u < 4; ++u) la[u] += excl;
+    if (p.fault) {  // TEST ONLY: the reference's off-by-one hook (lsm.hpp:566-572), p_t = prod_{s<t}
+#pragma unroll
+        for (int u = 0; u < 4; ++u) la[u] -= own[u];
+    }
     return __shfl_sync(0xFFFFFFFFu, x, 31);
 }
 

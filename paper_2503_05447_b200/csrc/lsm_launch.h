@@ -9,6 +9,11 @@
 #include "lsm_fwd.cuh"
 
 namespace lmoe_dev {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `fn` on the CURRENT device, once per
+// (kernel, device) pair: function attributes are per device, so a process driving several
+// GPUs (one thread each) sets them on every device it launches on (common.cu).
+cudaError_t ensure_smem(const void* fn, int bytes);
+
 // Launch with programmatic stream serialization (PDL; see ptx.cuh pdl_wait / pdl_trigger).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

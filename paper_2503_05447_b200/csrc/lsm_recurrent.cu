@@ -249,7 +249,7 @@ int rec_kind(int inst) {
 extern "C" int lmoe_lsm_fwd_recurrent(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
                                       const void* q, const void* k, const void* v,
                                       const lmoe_lsm_recurrent_inputs* in, const float* M0, void* o, float* M_out,
-                                      lmoe_stream_t stream) {
+                                      void* workspace, size_t workspace_bytes, lmoe_stream_t stream) {
     return guarded([&]() {
         if (!desc) throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd_recurrent: null descriptor");
         if (N < 1 || B < 1 || H < 1) throw Error(LMOE_ERR_ARG, "lsm_forward_sequential: need N >= 1 rows");
@@ -279,10 +279,9 @@ extern "C" int lmoe_lsm_fwd_recurrent(const lmoe_lsm_desc* desc, int B, int N, i
             throw Error(LMOE_ERR_ARG, std::string("lmoe_lsm_fwd_recurrent: instance ") + instance_name(desc->instance) +
                                           " needs " + need);
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-        int* err = nullptr;
-        static int* s_err = nullptr;
-        if (!s_err) LMOE_CUDA_CHECK(cudaMalloc(&s_err, sizeof(int)));
-        err = s_err;
+        if (!workspace || workspace_bytes < 64)
+            throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd_recurrent: workspace too small (need 64 bytes)");
+        int* err = static_cast<int*>(workspace);
         LMOE_CUDA_CHECK(cudaMemsetAsync(err, 0, sizeof(int), st));
         lmoe_dev::RecParams p{B, N, H, q, k, v, in->a_vec, in->a_scal, in->b_pre, in->alpha_pre, in->beta_pre,
                               in->s4_delta_raw, in->s4_b, in->s4_A_raw, in->mamba_A_raw, M0, o, M_out, err};

@@ -709,13 +709,7 @@ __global__ void __launch_bounds__(kVbThreads, 1)
 template <bool HG, bool REV>
 static cudaError_t carry_t(dim3 grid, cudaStream_t st, const CUtensorMap& x1, const CUtensorMap& x2,
                            const CUtensorMap& a, const VecBwdParams& p) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_vec_carry<HG, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             carry_smem());
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem((const void*)lsm_vec_carry<HG, REV>, carry_smem()); e != cudaSuccess) return e;
     lsm_vec_carry<HG, REV><<<grid, kCarryThreads, carry_smem(), st>>>(x1, x2, a, p);
     return cudaGetLastError();
 }
@@ -728,13 +722,7 @@ cudaError_t launch_vec_carry(bool hgrn2, bool rev, dim3 grid, cudaStream_t st, c
 
 template <bool HG>
 static cudaError_t chunk_t(dim3 grid, cudaStream_t st, const CUtensorMap* tm, const VecBwdParams& p) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(lsm_vec_bwd_chunk<HG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             vb_smem());
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = ensure_smem((const void*)lsm_vec_bwd_chunk<HG>, vb_smem()); e != cudaSuccess) return e;
     lsm_vec_bwd_chunk<HG><<<grid, kVbThreads, vb_smem(), st>>>(tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], tm[6], tm[7],
                                                                 tm[8], tm[9], tm[10], p);
     return cudaGetLastError();

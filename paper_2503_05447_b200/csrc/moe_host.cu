@@ -46,13 +46,7 @@ static MoePlanWs plan_moe(int T, int hidden, int ffn, int E, int K) {
 template <int BN, int EPI>
 static void launch_gemm(const CUtensorMap& a, const CUtensorMap& b0, const CUtensorMap& b1,
                         const lmoe_dev::GemmParams& gp, int max_tiles, int ntiles_n, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        LMOE_CUDA_CHECK(cudaFuncSetAttribute(lmoe_dev::moe_gemm<BN, EPI>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             lmoe_dev::gemm_smem<BN, EPI>()));
-        attr = true;
-    }
+    LMOE_CUDA_CHECK(lmoe_dev::ensure_smem((const void*)lmoe_dev::moe_gemm<BN, EPI>, lmoe_dev::gemm_smem<BN, EPI>()));
     // persistent: one CTA per SM (or fewer when the tile list is short) walks the tile list
     lmoe_dev::GemmParams g = gp;
     g.ntn = ntiles_n;

@@ -102,6 +102,11 @@ def _workspace(nbytes, device):
     return ws
 
 
+# TEST ONLY: set to True to make the scalar-decay kernels shift the within-chunk cumulative
+# decay by one token (the reference's kern::chunk_decay_fault(), lsm.hpp:310-317)
+TEST_DECAY_FAULT = False
+
+
 def make_desc(spec, chunk_size, check=True, timing=False):
     d = _lib.LsmDesc()
     d.instance = int(spec.instance)
@@ -109,7 +114,7 @@ def make_desc(spec, chunk_size, check=True, timing=False):
     d.use_normalizer = int(bool(spec.use_normalizer))
     d.scalar_decay = float(spec.scalar_decay)
     d.chunk_size = int(chunk_size)
-    d.flags = (1 if check else 0) | (2 if timing else 0)
+    d.flags = (1 if check else 0) | (2 if timing else 0) | (4 if TEST_DECAY_FAULT else 0)
     return d
 
 
@@ -222,6 +227,9 @@ def lsm_backward_batched(q, k, v, gates, spec, dO, initial_state=None, dM_final=
     M0 = None
     if initial_state is not None and initial_state.M is not None:
         M0 = initial_state.M.to(torch.float32).contiguous()
+    if spec.use_normalizer and initial_state is not None and initial_state.z is not None:
+        # lmoe_lsm_bwd differentiates the forward with z_in = 0 (its C-ABI carries no z0)
+        raise RuntimeError("lsm_backward_batched: a carried-in normaliser state z is not supported")
     dMf = None if dM_final is None else dM_final.to(torch.float32).contiguous()
     g = LsmGrads(dq=torch.empty_like(q), dk=torch.empty_like(k), dv=torch.empty_like(v))
     g.dM0 = torch.empty(B, H, D, D, dtype=torch.float32, device=dev)
@@ -245,22 +253,32 @@ def lsm_backward_batched(q, k, v, gates, spec, dO, initial_state=None, dM_final=
 
 
 class LsmFunction(torch.autograd.Function):
-    """Autograd binding: forward = lmoe_lsm_fwd, backward = lmoe_lsm_bwd (device only)."""
+    """Autograd binding: forward = lmoe_lsm_fwd, backward = lmoe_lsm_bwd (device only).
+
+    LsmFunction.apply(q, k, v, b_pre, spec, chunk_size[, a_pre, a_raw]): the gate tensors are
+    autograd inputs -- b_pre [B,N,H] (Mamba2), a_pre [B,N,H,D] (GLA / HGRN2 / RWKV6) and a_raw
+    [H] (the Mamba2 decay parameter; defaults to spec.mamba2_a_raw, whose gradient is then
+    dropped, as for any non-input)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, b_pre, spec, chunk_size):
-        gates = LsmGates(b_pre=b_pre) if b_pre is not None else None
-        o = lsm_forward_batched(q, k, v, gates, spec, chunk_size, check=False)
-        ctx.save_for_backward(q, k, v, b_pre)
-        ctx.spec, ctx.chunk = spec, chunk_size
+    def forward(ctx, q, k, v, b_pre, spec, chunk_size, a_pre=None, a_raw=None):
+        import copy
+        sp = spec
+        if a_raw is not None:
+            sp = copy.copy(spec)
+            sp.mamba2_a_raw = a_raw.detach()
+        gates = LsmGates(b_pre=b_pre, a_pre=a_pre) if (b_pre is not None or a_pre is not None) else None
+        o = lsm_forward_batched(q, k, v, gates, sp, chunk_size, check=False)
+        ctx.save_for_backward(q, k, v, b_pre, a_pre)
+        ctx.spec, ctx.chunk = sp, chunk_size
         return o
 
     @staticmethod
     def backward(ctx, dO):
-        q, k, v, b_pre = ctx.saved_tensors
-        gates = LsmGates(b_pre=b_pre) if b_pre is not None else None
+        q, k, v, b_pre, a_pre = ctx.saved_tensors
+        gates = LsmGates(b_pre=b_pre, a_pre=a_pre) if (b_pre is not None or a_pre is not None) else None
         g = lsm_backward_batched(q, k, v, gates, ctx.spec, dO.to(q.dtype), chunk_size=ctx.chunk, check=False)
-        return g.dq, g.dk, g.dv, g.db_pre, None, None
+        return g.dq, g.dk, g.dv, g.db_pre, None, None, g.da_pre, g.da_raw
 
 
 def _cu_array(cu_seqlens):
@@ -339,7 +357,8 @@ def lsm_forward_recurrent(q, k, v, gates, spec, initial_state=None, final_state=
     L = _lib.lib()
     if not getattr(L, "_rec_bound", False):
         L.lmoe_lsm_fwd_recurrent.restype = ctypes.c_int
-        L.lmoe_lsm_fwd_recurrent.argtypes = [ctypes.POINTER(_lib.LsmDesc)] + [ctypes.c_int] * 5 + [ctypes.c_void_p] * 8
+        L.lmoe_lsm_fwd_recurrent.argtypes = ([ctypes.POINTER(_lib.LsmDesc)] + [ctypes.c_int] * 5 + [ctypes.c_void_p] * 9
+                                             + [ctypes.c_size_t, ctypes.c_void_p])
         L._rec_bound = True
     keep = []
 
@@ -362,10 +381,12 @@ def lsm_forward_recurrent(q, k, v, gates, spec, initial_state=None, final_state=
     o = torch.empty_like(q)
     M_out = torch.empty(B, H, D, D, dtype=torch.float32, device=q.device) if final_state is not None else None
     desc = make_desc(spec, 64, check)
+    ws = _workspace(256, q.device)  # the device error flag
     st = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
     _lib.check(L.lmoe_lsm_fwd_recurrent(ctypes.byref(desc), B, N, H, D, _DTYPES[q.dtype], q.data_ptr(),
                                         k.data_ptr(), v.data_ptr(), ctypes.byref(rin), M0, o.data_ptr(),
-                                        None if M_out is None else M_out.data_ptr(), ctypes.c_void_p(st)))
+                                        None if M_out is None else M_out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                        ctypes.c_void_p(st)))
     if final_state is not None:
         final_state.M, final_state.z, final_state.step = M_out, None, N
     return o

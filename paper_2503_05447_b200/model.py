@@ -207,6 +207,12 @@ class Model:
                                     ws.numel(), st))
         return aux
 
+    def _check_tokens(self, tok):
+        """model.hpp:377-378: every id must index the embedding table (lmoe_embed reads
+        embedding[tok] unchecked on the device)."""
+        if tok.numel() and (int(tok.min()) < 0 or int(tok.max()) >= self.cfg.vocab_size):
+            raise RuntimeError("model_forward: token id out of vocabulary range")
+
     def forward_packed(self, tokens, boundaries, stream=None):
         """model_forward (model.hpp:374-405) over one flat token stream with ascending document
         boundaries (PackedBatch, model.hpp:86-121): per-document positions, the mixer per
@@ -226,6 +232,7 @@ class Model:
             raise RuntimeError("PackedBatch: boundaries must be strictly ascending")
         if int(np.diff(cu).max()) > c.max_seq_len:
             raise RuntimeError("model_forward: document longer than max_seq_len")
+        self._check_tokens(tok)
         st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
         x = torch.empty(T, c.hidden, dtype=torch.float32, device=dev)
         for i in range(n_docs):  # positions restart per document (model.hpp:379-384)
@@ -265,9 +272,12 @@ class Model:
                 raise RuntimeError("hybrid_sp_forward: single-document batches only")
             from .sp import chunk_range
             pos0 = chunk_range(n_total, world, rank)[0]
+        if pos0 + N > c.max_seq_len:  # model.hpp:382-383 (positions are document-relative)
+            raise RuntimeError("model_forward: document longer than max_seq_len")
         st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
         T = B * N
         tok = tokens.to(dev, torch.int32).contiguous()
+        self._check_tokens(tok)
         x = torch.empty(T, c.hidden, dtype=torch.float32, device=dev)
         _lib.check(L.lmoe_embed(tok.data_ptr(), T, N, pos0, c.hidden, self.embedding.data_ptr(),
                                 self.pos_embedding.data_ptr(), x.data_ptr(), st))

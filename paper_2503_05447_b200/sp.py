@@ -255,8 +255,7 @@ def sp_forward_nomask_loopback(q, k, v, spec, world, check=True):
     o = torch.empty_like(q)
     desc = make_desc(spec, 64, check)
     dt = _DTYPES[q.dtype]
-    nb = L.lmoe_sp_lsm_nomask_workspace_size(ctypes.byref(desc), B, max(1, (N + world - 1) // world), H, D,
-                                             dt, world)
+    nb = L.lmoe_sp_lsm_fwd_loopback_workspace_size(ctypes.byref(desc), B, N, H, D, dt, world)
     ws = _workspace(nb, q.device)
     st = torch.cuda.current_stream(q.device).cuda_stream
     _lib.check(L.lmoe_sp_lsm_nomask_fwd_loopback(ctypes.byref(desc), B, N, H, D, dt, _lib.ptr(q), _lib.ptr(k),

@@ -39,3 +39,19 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+
+def record_parity(name, err, tol, **extra):
+    """Logs an achieved parity error next to its bound (how much of the budget a test uses):
+    printed, and appended as JSON to $LMOE_PARITY_LOG or gpurun_out/parity_errors.jsonl when
+    that directory exists (the GPU box copies it back; profiles/ keeps the summaries)."""
+    import json
+    rec = {"test": name, "err": float(err), "tol": float(tol), "used": float(err) / float(tol)}
+    rec.update(extra)
+    print("PARITY", json.dumps(rec))
+    path = os.environ.get("LMOE_PARITY_LOG")
+    if not path and os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        path = os.path.join(ROOT, "gpurun_out", "parity_errors.jsonl")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")

@@ -92,3 +92,18 @@ def test_packed_documents_match_reference(tag):
     assert abs(aux.item() - a["packed_aux"][0]) <= 2e-2 * abs(a["packed_aux"][0])
     with pytest.raises(RuntimeError, match="strictly ascending"):
         model.forward_packed(tokens, [0, 100, 100, 256])
+
+
+def test_model_input_errors_mirror_reference():
+    """model.hpp:377-383 -- ids outside the vocabulary and documents longer
+    than the positional table raise the reference's texts before any device read."""
+    torch, model, a = _model("gla")
+    V, L = model.cfg.vocab_size, model.cfg.max_seq_len
+    with pytest.raises(RuntimeError, match="token id out of vocabulary range"):
+        model.forward(torch.tensor([[0, V]]))
+    with pytest.raises(RuntimeError, match="token id out of vocabulary range"):
+        model.forward(torch.tensor([[-1, 0]]))
+    with pytest.raises(RuntimeError, match="document longer than max_seq_len"):
+        model.forward(torch.zeros(1, L + 1, dtype=torch.int64))
+    with pytest.raises(RuntimeError, match="token id out of vocabulary range"):
+        model.forward_packed(torch.tensor([0, V + 3]), [0, 1, 2])

@@ -227,3 +227,50 @@ def test_sp_backward_nccl_world1_and_gla_forward():
     o = sp.sp_forward_masked_loopback(q, k, v, gates, spec, 4)
     o_ref = pk.lsm_forward_batched(q, k, v, gates, spec, 64)
     assert _rel(o, o_ref) < 1e-2
+
+
+@pytest.mark.parametrize("inst", ["mamba2", "retnet"])
+def test_loopback_slices_with_different_plans(inst):
+    """N = 2305 over 2 virtual ranks gives slices of 1153 and 1152 rows whose
+    segment plans differ (1153 -> 5 segments, 1152 -> 9 at H = 16); the workspace covers the
+    larger plan and both slices share one error slot, so forward, unmasked and backward
+    loopbacks equal the single-device results."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_05447_b200 as pk
+    from paper_2503_05447_b200 import sp
+    N, H = 2305, 16
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q, k, v = (torch.randn(1, N, H, 128, device="cuda", generator=g).mul_(0.5).to(torch.bfloat16) for _ in range(3))
+    spec = pk.LsmSpec.make(inst, 128)
+    gates = None
+    if inst == "mamba2":
+        spec.mamba2_a_raw = torch.linspace(-1, 1, H, device="cuda")
+        gates = pk.LsmGates(b_pre=torch.randn(1, N, H, device="cuda", generator=g).sub_(2.0))
+    ref = pk.lsm_forward_batched(q, k, v, gates, spec, 64)
+    o = sp.sp_forward_masked_loopback(q, k, v, gates, spec, 2)
+    torch.cuda.synchronize()
+    assert _rel(o, ref) < 1e-2
+    dO = torch.randn(q.shape, device="cuda", generator=g).to(torch.bfloat16)
+    gr = pk.lsm_backward_batched(q, k, v, gates, spec, dO)
+    gs = sp.sp_backward_masked_loopback(q, k, v, gates, spec, dO, 2)
+    for n in ("dq", "dk", "dv"):
+        assert _rel(getattr(gs, n), getattr(gr, n)) < 1e-2, n
+    if inst == "retnet":
+        plain = pk.LsmSpec(instance=pk.LsmInstance.BLA, feature_map=0, use_normalizer=False)
+        on = sp.sp_forward_nomask_loopback(q, k, v, plain, 2)
+        on1 = sp.sp_forward_nomask_loopback(q, k, v, plain, 1)
+        assert _rel(on, on1) < 1e-2
+
+
+def test_normaliser_backward_rejects_carried_z():
+    """lmoe_lsm_bwd differentiates z_in = 0; a carried-in z is refused."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_05447_b200 as pk
+    x = torch.randn(1, 64, 1, 128, device="cuda").bfloat16()
+    st = pk.MemoryState(M=torch.zeros(1, 1, 128, 128, device="cuda"), z=torch.ones(1, 1, 128, device="cuda"))
+    with pytest.raises(RuntimeError, match="normaliser state z"):
+        pk.lsm_backward_batched(x, x, x, None, pk.LsmSpec.make("bla", 128), x, initial_state=st)
