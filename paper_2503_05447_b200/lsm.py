@@ -271,6 +271,7 @@ class LsmFunction(torch.autograd.Function):
         o = lsm_forward_batched(q, k, v, gates, sp, chunk_size, check=False)
         ctx.save_for_backward(q, k, v, b_pre, a_pre)
         ctx.spec, ctx.chunk = sp, chunk_size
+        ctx.n_in = 6 + (a_pre is not None or a_raw is not None) + (a_raw is not None)
         return o
 
     @staticmethod
@@ -278,7 +279,7 @@ class LsmFunction(torch.autograd.Function):
         q, k, v, b_pre, a_pre = ctx.saved_tensors
         gates = LsmGates(b_pre=b_pre, a_pre=a_pre) if (b_pre is not None or a_pre is not None) else None
         g = lsm_backward_batched(q, k, v, gates, ctx.spec, dO.to(q.dtype), chunk_size=ctx.chunk, check=False)
-        return g.dq, g.dk, g.dv, g.db_pre, None, None, g.da_pre, g.da_raw
+        return (g.dq, g.dk, g.dv, g.db_pre, None, None, g.da_pre, g.da_raw)[:ctx.n_in]
 
 
 def _cu_array(cu_seqlens):

@@ -405,3 +405,30 @@ def test_normalizer_bwd_matches_oracle(case):
     for b in range(B):
         for h in range(H):
             assert norm_rel_err(got["dM0"][b, h], want["dM0"][b, h]) < TOL[dtype], (name, "dM0", b, h)
+
+
+def test_autograd_function_gate_parameters():
+    """a_raw (Mamba2) and a_pre (GLA) are autograd inputs of LsmFunction, so
+    training reaches the decay parameters; the gradients equal lmoe_lsm_bwd's."""
+    torch = _torch()
+    import paper_2503_05447_b200 as pk
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device="cpu").manual_seed(4)
+    B, N, H, D = 1, 300, 2, 128
+    q, k, v = (torch.randn(B, N, H, D, generator=g).mul(0.5).to(dev, torch.bfloat16).requires_grad_() for _ in range(3))
+    b = torch.randn(B, N, H, generator=g).to(dev).requires_grad_()
+    a_raw = torch.tensor([0.2, -0.3], device=dev, requires_grad=True)
+    spec = pk.LsmSpec.make("mamba2", D)
+    o = pk.LsmFunction.apply(q, k, v, b, spec, 64, None, a_raw)
+    dO = torch.randn(o.shape, generator=g).to(dev, torch.bfloat16)
+    o.backward(dO)
+    spec.mamba2_a_raw = a_raw.detach()
+    ref = pk.lsm_backward_batched(q.detach(), k.detach(), v.detach(), pk.LsmGates(b_pre=b.detach()), spec, dO)
+    assert torch.equal(a_raw.grad, ref.da_raw)
+    a = torch.randn(B, N, H, D, generator=g).to(dev, torch.bfloat16).requires_grad_()
+    spec_g = pk.LsmSpec.make("gla", D)
+    q.grad = None
+    o = pk.LsmFunction.apply(q, k, v, None, spec_g, 64, a)
+    o.backward(dO)
+    ref = pk.lsm_backward_batched(q.detach(), k.detach(), v.detach(), pk.LsmGates(a_pre=a.detach()), spec_g, dO)
+    assert torch.equal(a.grad, ref.da_pre) and torch.equal(q.grad, ref.dq)
