@@ -261,8 +261,10 @@ class LsmFunction(torch.autograd.Function):
     dropped, as for any non-input)."""
 
     @staticmethod
-    def forward(ctx, q, k, v, b_pre, spec, chunk_size, a_pre=None, a_raw=None):
+    def forward(ctx, q, k, v, b_pre, spec, chunk_size, *extra):
         import copy
+        a_pre = extra[0] if len(extra) > 0 else None
+        a_raw = extra[1] if len(extra) > 1 else None
         sp = spec
         if a_raw is not None:
             sp = copy.copy(spec)
@@ -271,7 +273,7 @@ class LsmFunction(torch.autograd.Function):
         o = lsm_forward_batched(q, k, v, gates, sp, chunk_size, check=False)
         ctx.save_for_backward(q, k, v, b_pre, a_pre)
         ctx.spec, ctx.chunk = sp, chunk_size
-        ctx.n_in = 6 + (a_pre is not None or a_raw is not None) + (a_raw is not None)
+        ctx.n_in = 6 + len(extra)
         return o
 
     @staticmethod
