@@ -259,10 +259,14 @@ def backward_bench(dev, steps=3, warmup=2):
                          "note": "algorithmic bytes of the op / step time (three chunk passes + gate kernel)"}}
 
 
-def ncu_traffic(path=os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                   "r1_lsm_output_pass.ncu.txt")):
+OUTPASS_NCU = "profiles/r1_lsm_output_pass.ncu.txt"
+FUSED_NCU = "profiles/r2_lsm_fused_fwd.ncu.txt"
+
+
+def ncu_traffic(rel=OUTPASS_NCU):
     """dram read + write bytes per launch of the dominant kernel from the committed ncu --set full
     capture (profiles/), or None when absent."""
+    path = os.path.join(ROOT, rel)
     try:
         vals = {}
         for line in open(path):
@@ -506,16 +510,21 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = SEQ / (te.item() / args.e2e_steps / 1e3)
 
-    # ---- roofline of the dominant kernel (output pass): it moves the full algorithmic
-    # bytes of the op (reads q,k,v,gate, writes o) for this rank's tokens x heads
+    # ---- roofline of the dominant kernel: the single-read kernel (world 1, one launch) or the
+    # output pass (SP): either moves the full algorithmic bytes of the op (reads q,k,v,gate,
+    # writes o) for this rank's tokens x heads
     hbm, tflops, src = peaks()
-    out_pass_ms = phase_ms[5] / max(calls, 1)
+    plan = pk.lsm.forward_plan(spec, 1, n_loc, HEADS, HEAD_DIM)
+    fused = plan["fused"] and world == 1
+    out_pass_ms = (phase_ms[0] if fused else phase_ms[5]) / max(calls, 1)
     units = n_loc * HEADS
     alg_bytes = ALG_BYTES_TH[args.instance] * units
     achieved = alg_bytes / (out_pass_ms / 1e3) / 1e9
     step_alg = ALG_BYTES_TH[args.instance] * units / (ms_step / 1e3) / 1e9
     phase_names = ["state_pass", "local_combine", "all_gather", "rank_combine(fused into next)",
                    "rank_seg_combine", "output_pass"]
+    if fused:
+        phase_names = ["lsm_fused_fwd"]
 
     if rank == 0:
         cb = None
@@ -540,9 +549,11 @@ def main():
                        "l2": "inputs 3 GiB > L2; no flush needed"},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": ncu_traffic(), "peak_source": src,
-                         "traffic_source": "profiles/r1_lsm_output_pass.ncu.txt (ncu --set full, one launch)",
-                         "kernel": "lsm_output_pass",
+                         "frac": achieved / hbm, "traffic": ncu_traffic(FUSED_NCU if fused else OUTPASS_NCU),
+                         "peak_source": src,
+                         "traffic_source": (FUSED_NCU if fused else OUTPASS_NCU) + " (ncu --set full, one launch)",
+                         "kernel": "lsm_fused_fwd" if fused else "lsm_output_pass",
+                         "plan": plan,
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_per_token_head": ALG_BYTES_TH[args.instance]},
             "step_roofline": {"achieved": step_alg, "frac": step_alg / hbm, "unit": "GB/s",

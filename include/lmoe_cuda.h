@@ -254,6 +254,12 @@ int lmoe_lsm_fwd_recurrent(const lmoe_lsm_desc* desc, int B, int N, int H, int D
                            const float* M0, void* o, float* M_out, void* workspace, size_t workspace_bytes,
                            lmoe_stream_t stream);
 
+/* Forward plan of lmoe_lsm_fwd for a shape: info[0] = 1 when the single-read persistent
+ * kernel runs (bf16 / D = 128 scalar-decay kinds without normaliser; one launch), 0 for the
+ * segment-parallel state pass + combine + output pass; info[1] segments per (b,h),
+ * info[2] tokens per segment, info[3] CTAs per (b,h). */
+int lmoe_lsm_fwd_plan(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype, int* info);
+
 /* Number of kernels one lmoe_lsm_fwd call launches (for launch accounting). */
 int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc);
 

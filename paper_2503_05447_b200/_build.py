@@ -21,7 +21,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["common.cu", "lsm_host.cu", "lsm_combine.cu", "lsm_bwd_kernels.cu", "lsm_dgate.cu", "lsm_inst_bf16.cu", "lsm_inst_f32.cu", "lsm_inst_vec.cu", "lsm_vec_bwd.cu", "lsm_recurrent.cu",
+SOURCES = ["common.cu", "lsm_host.cu", "lsm_combine.cu", "lsm_bwd_kernels.cu", "lsm_dgate.cu", "lsm_inst_bf16.cu", "lsm_inst_f32.cu", "lsm_inst_vec.cu", "lsm_vec_bwd.cu", "lsm_recurrent.cu", "lsm_fused.cu",
            "moe_host.cu", "attn.cu", "block.cu"]
 LIBS = ["-lnccl"]
 

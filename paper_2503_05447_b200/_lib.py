@@ -60,6 +60,8 @@ def lib():
     L.lmoe_lsm_fwd_varlen.argtypes = [ctypes.POINTER(LsmDesc), i, vp, i, i, i, i] + [vp] * 9 + [sz, vp]
     L.lmoe_lsm_bwd_varlen.restype = i
     L.lmoe_lsm_bwd_varlen.argtypes = [ctypes.POINTER(LsmDesc), i, vp, i, i, i, i] + [vp] * 14 + [sz, vp]
+    L.lmoe_lsm_fwd_plan.restype = i
+    L.lmoe_lsm_fwd_plan.argtypes = [ctypes.POINTER(LsmDesc), i, i, i, i, i, vp]
     L.lmoe_timing_read.restype = i
     L.lmoe_timing_read.argtypes = [ctypes.POINTER(ctypes.c_float), i]
     _lib = L

@@ -39,6 +39,9 @@ constexpr int kBlockBytes = kC * 128;           // one SW128 column block of a t
 constexpr int kMathThreads = 256;               // 8 epilogue warps (output pass)
 constexpr float kSafeLogDecay = -80.f;          // e^{-G} stays finite in fp32 above this
 
+constexpr int kFusedRing = 2;  // single-read forward: hand-off ring slots per (b,h); a slot is
+                               // rewritten only after its one reader (the next segment) has
+                               // published its own prefix, which the writer has acquired
 enum DecayMode { kDecayNone = 0, kDecayConst = 1, kDecayTokenScalar = 2, kDecayTokenVector = 3 };
 
 struct LsmFwdParams {
@@ -68,6 +71,13 @@ struct LsmFwdParams {
     int nchunk_tot;
     unsigned long long* trace;  // optional clock64 trace of CTA (0,0,0) [64 chunks][16]
     int fault;                  // TEST ONLY (LMOE_FLAG_TEST_DECAY_FAULT): decay shifted by one token
+    // single-read persistent forward (lsm_fused.cuh): P CTAs per (b,h) walk its segments
+    // j, j+P, j+2P, ...; the inclusive prefix state of segment s is handed to segment s+1
+    // through ring[bh][s % R] (fp32 [D][D]) and flags[bh][s % R] = s + 1
+    int fP, fR;
+    float* ring;
+    int* flags;
+    float* Mfin;                // [B*H][D][D] final state (inclusive prefix of the last segment)
 };
 
 // per-CTA globaltimer at kernel start (after the prologue) and end, slots after the 64 x 16

@@ -57,8 +57,40 @@ int device_decay_mode(int inst) {
 
 struct LsmPlan {
     int seg_len = 0, nseg = 0;
-    size_t off_S = 0, off_z = 0, off_logD = 0, off_Min = 0, off_zin = 0, off_err = 0, total = 0;
+    // single-read forward (lsm_fused.cuh): fP CTAs per (b,h), fnseg segments of fseg_len
+    int fP = 0, fseg_len = 0, fnseg = 0;
+    size_t off_S = 0, off_z = 0, off_logD = 0, off_Min = 0, off_zin = 0, off_err = 0, off_ring = 0,
+           off_flags = 0, total = 0;
 };
+
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+// Single-read forward plan: P = floor(#SMs / (B*H)) CTAs per head (all co-resident), segments
+// of c chunks, CTA j of a head taking segments j, j+P, ...  Cost per CTA ~ units x (c x
+// (1 output step + ~0.3 state step) + ~1 per-unit hand-off / fill); c <= 8 keeps every CTA's
+// K/V between its state and output reads in L2 (148 x 8 x 64 KB = 78 MB of 126 MB).
+static void plan_fused(LsmPlan& pl, int B, int N, int H) {
+    const int chunks = (N + lmoe_dev::kC - 1) / lmoe_dev::kC;
+    const int BH = B * H;
+    const int P = num_sms() / BH;
+    if (P < 2 && chunks > 8) return;  // too many heads to split: the segment-parallel passes
+    const int cmax = std::max(1, std::min(16, env_int("LMOE_FUSED_SEGC", 8)));
+    double best = 1e300;
+    for (int c = 1; c <= cmax; ++c) {
+        const int units = (chunks + c - 1) / c;
+        const int per_cta = (units + std::max(P, 1) - 1) / std::max(P, 1);
+        const double cost = per_cta * (1.3 * c + 1.0);
+        if (cost < best - 1e-9) {
+            best = cost;
+            pl.fseg_len = c * lmoe_dev::kC;
+            pl.fnseg = units;
+        }
+    }
+    pl.fP = std::max(1, std::min(P, pl.fnseg));
+}
 
 // Segment length: a multiple of the 128-token tile.  The B*H*nseg CTAs of the
 // segment-parallel passes run one per SM; a pass costs about waves x (chunks per segment +
@@ -93,6 +125,9 @@ static LsmPlan plan_lsm(int B, int N, int H, int D) {
     pl.off_Min = take(heads_nseg * D * D * 4);
     pl.off_zin = take(heads_nseg * D * 4);
     pl.off_err = take(64);
+    plan_fused(pl, B, N, H);
+    pl.off_ring = take(heads * lmoe_dev::kFusedRing * D * D * 4);
+    pl.off_flags = take(heads * lmoe_dev::kFusedRing * 4);
     pl.total = off;
     return pl;
 }
@@ -254,6 +289,31 @@ struct LsmCall {
         ++g_launch_count;
         mark();
     }
+    // the single-read forward applies to bf16 / D = 128 scalar-decay kinds without normaliser
+    // (forward order, no backward side channel); LMOE_FUSED=0 forces the three passes
+    bool fused_ok() const {
+        return env_int("LMOE_FUSED", 1) != 0 && dt == LMOE_BF16 && D == 128 && !norm && !vec && var.rev == 0 &&
+               p.mst == nullptr && !p.out_f32 && !p.nomask && pl.fP >= 1;
+    }
+    void fused(const float* M0, float* M_out) {
+        using bf = __nv_bfloat16;
+        const CUtensorMap tq = tmap<bf>(q), tk = tmap<bf>(k), tv = tmap<bf>(v), to = tmap<bf>(o);
+        lmoe_dev::LsmFwdParams fp = p;
+        fp.seg_len = pl.fseg_len;
+        fp.nseg = pl.fnseg;
+        fp.fP = pl.fP;
+        fp.fR = lmoe_dev::kFusedRing;
+        fp.ring = reinterpret_cast<float*>(ws + pl.off_ring);
+        fp.flags = reinterpret_cast<int*>(ws + pl.off_flags);
+        fp.Min = M0;
+        fp.Mfin = M_out;
+        fp.order = env_int("LMOE_FUSED_HINT", 1);
+        LMOE_CUDA_CHECK(cudaMemsetAsync(fp.flags, 0, (size_t)B * H * lmoe_dev::kFusedRing * 4, st));
+        mark();
+        LMOE_CUDA_CHECK(lmoe_dev::launch_fused_fwd_bf16(var, pl.fP * B * H, st, tq, tk, tv, to, fp));
+        ++g_launch_count;
+        mark();
+    }
     void clear_err() { LMOE_CUDA_CHECK(cudaMemsetAsync(p.err, 0, 64, st)); }
     void check_err() {
         if (!(d->flags & LMOE_FLAG_CHECK)) return;
@@ -275,9 +335,13 @@ template <typename T>
 static void run_local(LsmCall& c, const float* M0, const float* z0, float* M_out, float* z_out) {
     c.setup();
     c.clear_err();
-    c.state_pass<T>();
-    c.combine(M0, z0, true, M_out, z_out, nullptr, 0);
-    c.output_pass<T>();
+    if (c.fused_ok()) {
+        c.fused(M0, M_out);
+    } else {
+        c.state_pass<T>();
+        c.combine(M0, z0, true, M_out, z_out, nullptr, 0);
+        c.output_pass<T>();
+    }
     c.finish_timing();
     c.check_err();
 }
@@ -359,6 +423,24 @@ extern "C" size_t lmoe_lsm_fwd_workspace_size(const lmoe_lsm_desc* desc, int B, 
     (void)desc; (void)dtype;
     if (B < 1 || N < 1 || H < 1 || D < 1) return 0;
     return plan_lsm(B, N, H, D).total;
+}
+
+extern "C" int lmoe_lsm_fwd_plan(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
+                                 int* info) {
+    return guarded([&]() {
+        if (!desc || !info || B < 1 || N < 1 || H < 1 || D < 1) throw Error(LMOE_ERR_ARG, "lmoe_lsm_fwd_plan: bad arguments");
+        const LsmPlan pl = plan_lsm(B, N, H, D);
+        LsmCall c{desc, B, N, N, H, D, dtype, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, pl,
+                  nullptr, nullptr};
+        c.var.decay = device_decay_mode(desc->instance);
+        c.norm = desc->use_normalizer != 0;
+        c.vec = c.var.decay == lmoe_dev::kDecayTokenVector;
+        const bool f = c.var.decay >= 0 && c.fused_ok();
+        info[0] = f ? 1 : 0;
+        info[1] = f ? pl.fnseg : pl.nseg;
+        info[2] = f ? pl.fseg_len : pl.seg_len;
+        info[3] = f ? pl.fP : pl.nseg;
+    });
 }
 
 extern "C" int lmoe_lsm_fwd_num_launches(const lmoe_lsm_desc* desc) {
@@ -476,6 +558,12 @@ void lsm_mixer_core(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
         // a gather over one rank is the identity and rank 0 carries nothing in: the local
         // pass (state pass, segment prefix, output pass); the empty marks keep the phase
         // timers' layout (all-gather, rank combine)
+        if (c.fused_ok()) {  // one single-read launch (timing phase 0)
+            c.fused(nullptr, M_out);
+            c.finish_timing();
+            c.check_err();
+            return;
+        }
         if (dtype == LMOE_BF16) c.state_pass<__nv_bfloat16>();
         else c.state_pass<float>();
         c.combine(nullptr, nullptr, true, M_out, z_out, nullptr, 0);

@@ -45,6 +45,9 @@ cudaError_t launch_state_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, con
 cudaError_t launch_output_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
                                     const CUtensorMap& k, const CUtensorMap& val,
                                     const CUtensorMap& o, const LsmFwdParams& p);
+// single-read persistent forward (lsm_fused.cuh), grid = P * B * H CTAs
+cudaError_t launch_fused_fwd_bf16(LsmVariant v, int grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& k,
+                                  const CUtensorMap& val, const CUtensorMap& o, const LsmFwdParams& p);
 cudaError_t launch_state_pass_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
                                   const CUtensorMap& val, const LsmFwdParams& p);
 cudaError_t launch_output_pass_f32(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,
