@@ -32,6 +32,16 @@
 namespace lmoe_dev {
 
 constexpr int kFusedThreads = 128 + 512;
+
+// developer trace (LMOE_TRACE): globaltimer per (CTA jj of head 0, segment unit, event):
+// 0 A steps start, 1 A accumulated, 2 hand-off acquired, 3 published, 4 C steps done
+__device__ __forceinline__ void fused_mark(const LsmFwdParams& p, int bh, int jj, int un, int ev) {
+    if (p.trace != nullptr && bh == 0 && jj < 16 && un < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[64 * 16 + (jj * 64 + un) * 5 + ev] = t;
+    }
+}
 constexpr int fused_smem() { return 2 * 3 * kTileBytes + 128 * 128 * 2 + 2 * 256 * 4 + 16 * 4 + 24 * 8; }
 
 template <int DECAY, int FM>
@@ -62,9 +72,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     uint64_t* gfree = bars + 12;    // [2]
     uint64_t* xf1 = bars + 14;
     uint64_t* o_staged = bars + 15;
-    uint64_t* xfA = bars + 16;      // A step: K~ transformed
-    uint64_t* accA = bars + 17;     // A steps of a segment accumulated
-    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 18);
+    // A step: K~ transformed.  Two barriers, alternating by A-step parity: the math warps
+    // are not synchronised among themselves during the A steps, so with one barrier a fast
+    // warp's arrival for step i+1 could complete step i's phase while a slow warp was still
+    // transforming (measured: one warp's 32 x 32 block of K left unweighted).  A warp reaches
+    // step i+2 only after the stage of step i was reloaded, i.e. after the MMA consumed step i.
+    uint64_t* xfA = bars + 16;      // [2]
+    uint64_t* accA = bars + 18;     // A steps of a segment accumulated
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 19);
 
     const int BH = p.B * p.H;
     const int bh = blockIdx.x % BH, jj = blockIdx.x / BH;
@@ -85,7 +100,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         mbar_init(mo_full, 1);
         mbar_init(xf1, MT);
         mbar_init(o_staged, MT);
-        mbar_init(xfA, MT);
+        mbar_init(&xfA[0], MT);
+        mbar_init(&xfA[1], MT);
         mbar_init(accA, 1);
         fence_barrier_init();
     }
@@ -156,7 +172,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                 for (int it = 0; it < n; ++it, ++g, ++ag) {
                     const int s = g % NST;
                     mbar_wait(&full[s], (g / NST) & 1);
-                    mbar_wait(xfA, ag & 1);
+                    mbar_wait(&xfA[ag & 1], (ag >> 1) & 1);
                     tc_fence_after();
                     const uint32_t kt = smem_u32(tiles + s * 3 * kTileBytes) + kTileBytes, vt = kt + kTileBytes;
 #pragma unroll
@@ -264,6 +280,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                     }
                     if ((lane & 7) == 0) ringS[slot * 8 + 4 + (lane >> 3)] = qlast;
                 }
+                if (p.fdbg && lane == 0) ringS[slot * 8 + 2] = __int_as_float(g);  // developer aid: step tag
                 __syncwarp();
                 mbar_arrive(&gfull[slot]);
 #pragma unroll
@@ -315,27 +332,34 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                 *reinterpret_cast<uint4*>(dst + sw128_off(row, ch0 + ch)) = v;
             }
         };
-        int g = 0, cg = 0, un = 0;
+        int g = 0, cg = 0, un = 0, ga = 0;
         for (int seg = jj; seg < p.nseg; seg += p.fP, ++un) {
             int tb, te, n;
             span(seg, tb, te, n);
             // ---- A steps: K~ = phi(K) . w (row owners, in place) -----------------------
             float logD = 0.f;
-            for (int it = 0; it < n; ++it, ++g) {
+            if (tid == 0) fused_mark(p, bh, jj, un, 0);
+            for (int it = 0; it < n; ++it, ++g, ++ga) {
                 const int slot = g & 1, s = g % NST;
                 mbar_wait(&gfull[slot], (g >> 1) & 1);
                 const float w = ringG[slot * 128 + row];
                 if (it == n - 1) logD = ringS[slot * 8 + 3];
+                if (p.fdbg) {  // developer aid: count stale ring reads and non-positive weights
+                    const size_t base = (size_t)p.B * p.H * p.nseg * 2 * D * D + (size_t)p.B * p.H * p.nseg;
+                    if (__float_as_int(ringS[slot * 8 + 2]) != g) atomicAdd(reinterpret_cast<int*>(p.fdbg + base), 1);
+                    if (!(w >= 0.f)) atomicAdd(reinterpret_cast<int*>(p.fdbg + base + 1), 1);
+                }
                 mbar_wait(&full[s], (g / NST) & 1);
                 xform_row_part<T, FM, false>(tiles + s * 3 * kTileBytes + kTileBytes, row, hh * DH, DH, w);
                 fence_proxy_async_smem();
-                mbar_arrive(xfA);
+                mbar_arrive(&xfA[ga & 1]);
                 mbar_arrive(&gfree[slot]);
             }
             // ---- chain: M_in = incl(seg - 1); publish incl(seg) = D_seg M_in + S_seg
             auto chain = [&](float gend0) {
                 mbar_wait(accA, un & 1);
                 tc_fence_after();
+                if (tid == 0) fused_mark(p, bh, jj, un, 1);
                 uint32_t r[32];
                 tmem_ld32(tM + lane_off + hh * DH, r);
                 tmem_wait_ld();
@@ -350,11 +374,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                     (void)ld_acquire_gpu(fl);
                     src = p.ring + ((size_t)(bh * R + (seg - 1) % R) * D + row) * D + hh * DH;
                 }
+                if (tid == 0) fused_mark(p, bh, jj, un, 2);
                 float prev[DH];
 #pragma unroll
                 for (int j = 0; j < DH; j += 4) {
                     const float4 v = src ? __ldcg(reinterpret_cast<const float4*>(src + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
                     prev[j] = v.x; prev[j + 1] = v.y; prev[j + 2] = v.z; prev[j + 3] = v.w;
+                }
+                if (p.fdbg) {  // developer aid: [bh][seg][S_seg | M_in] + logD at the end
+                    float* dbg = p.fdbg + ((size_t)bh * p.nseg + seg) * 2 * D * D + (size_t)row * D + hh * DH;
+                    for (int j = 0; j < DH; ++j) { dbg[j] = __uint_as_float(r[j]); dbg[D * D + j] = prev[j]; }
+                    if (tid == 0) p.fdbg[(size_t)p.B * p.H * p.nseg * 2 * D * D + (size_t)bh * p.nseg + seg] = logD;
                 }
                 const float dl = __expf(logD);
                 const bool last = seg + 1 == p.nseg;
@@ -377,6 +407,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                     named_bar_sync(2, MT);
                     if (tid == 0) st_release_gpu(p.flags + bh * R + seg % R, seg + 1);
                 }
+                if (tid == 0) fused_mark(p, bh, jj, un, 3);
                 // the entering state: operand M_in, TMEM M = e^{G_end(chunk 0)} M_in
                 write_state_operand(prev);
                 const float g0 = __expf(gend0);
@@ -408,6 +439,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                 uint8_t* qt = tiles + s * 3 * kTileBytes;
                 uint8_t* kt = qt + kTileBytes;
                 mbar_wait(&gfull[slot], (gc >> 1) & 1);
+                if (p.fdbg && __float_as_int(ringS[slot * 8 + 2]) != gc)
+                    atomicAdd(reinterpret_cast<int*>(p.fdbg + (size_t)p.B * p.H * p.nseg * 2 * D * D + (size_t)p.B * p.H * p.nseg + 2), 1);
                 const float gend = ringS[slot * 8];
                 const bool safe = ringS[slot * 8 + 1] != 0.f;
                 const float* rQ = ringS + slot * 8 + 4;
@@ -511,6 +544,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                     mbar_arrive(o_staged);
                 }
             }
+            if (tid == 0) fused_mark(p, bh, jj, un, 4);
             g += n;
             cg += n;
         }

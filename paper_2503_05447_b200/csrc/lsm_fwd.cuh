@@ -39,7 +39,7 @@ constexpr int kBlockBytes = kC * 128;           // one SW128 column block of a t
 constexpr int kMathThreads = 256;               // 8 epilogue warps (output pass)
 constexpr float kSafeLogDecay = -80.f;          // e^{-G} stays finite in fp32 above this
 
-constexpr int kFusedRing = 2;  // single-read forward: hand-off ring slots per (b,h); a slot is
+constexpr int kFusedRing = 8;  // single-read forward: hand-off ring slots per (b,h) (p.fR <= this used); a slot is
                                // rewritten only after its one reader (the next segment) has
                                // published its own prefix, which the writer has acquired
 enum DecayMode { kDecayNone = 0, kDecayConst = 1, kDecayTokenScalar = 2, kDecayTokenVector = 3 };
@@ -78,6 +78,7 @@ struct LsmFwdParams {
     float* ring;
     int* flags;
     float* Mfin;                // [B*H][D][D] final state (inclusive prefix of the last segment)
+    float* fdbg;                // developer aid (LMOE_FUSED_DEBUG_PTR): per (bh, seg) S_seg, M_in, logD
 };
 
 // per-CTA globaltimer at kernel start (after the prologue) and end, slots after the 64 x 16
