@@ -161,8 +161,13 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     uint64_t* empty = bars + NST;       // [NST]
     uint64_t* wfull = bars + 2 * NST;   // [2]
     uint64_t* wfree = wfull + 2;        // [2]
-    uint64_t* xf = wfree + 2;
-    uint64_t* acc_full = xf + 1;
+    // K~ transformed, one barrier per stage: the four math warps are not synchronised with
+    // each other per chunk, so a fast warp may transform chunk it+1 (its stage is already
+    // loaded) before a slow one finishes chunk it; with a single barrier its arrival would
+    // complete chunk it's phase early (the race measured in lsm_fused.cuh).  A warp reaches
+    // chunk it+NST only after the MMA consumed chunk it (its stage was reloaded).
+    uint64_t* xf = wfree + 2;           // [NST]
+    uint64_t* acc_full = xf + NST;
     uint64_t* kt_free = acc_full + 1;
     uint32_t* sTmem = reinterpret_cast<uint32_t*>(kt_free + 1);
 
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&wfull[i], 32); mbar_init(&wfree[i], 128); }
-        mbar_init(xf, 128);
+        for (int i = 0; i < NST; ++i) mbar_init(&xf[i], 128);
         mbar_init(acc_full, 1);
         mbar_init(kt_free, 1);
         fence_barrier_init();
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
             for (int it = 0; it < nchunks; ++it) {
                 const int s = it % NST;
                 mbar_wait(&full[s], (it / NST) & 1);
-                mbar_wait(xf, it & 1);
+                mbar_wait(&xf[s], (it / NST) & 1);
                 tc_fence_after();
                 const uint32_t kt = smem_u32(tiles + s * 2 * kTileBytes);
                 const uint32_t vt = kt + kTileBytes;
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
                     named_bar_sync(1, 128);  // colsum reads done before the next transform
                 }
             }
-            mbar_arrive(xf);
+            mbar_arrive(&xf[s]);
         }
         // epilogue: S (d_k rows x d_v cols) from TMEM to global
         mbar_wait(acc_full, 0);

@@ -369,7 +369,7 @@ def lsm_forward_recurrent(q, k, v, gates, spec, initial_state=None, final_state=
     L = _lib.lib()
     if not getattr(L, "_rec_bound", False):
         L.lmoe_lsm_fwd_recurrent.restype = ctypes.c_int
-        L.lmoe_lsm_fwd_recurrent.argtypes = ([ctypes.POINTER(_lib.LsmDesc)] + [ctypes.c_int] * 5 + [ctypes.c_void_p] * 9
+        L.lmoe_lsm_fwd_recurrent.argtypes = ([ctypes.POINTER(_lib.LsmDesc)] + [ctypes.c_int] * 5 + [ctypes.c_void_p] * 8
                                              + [ctypes.c_size_t, ctypes.c_void_p])
         L._rec_bound = True
     keep = []
