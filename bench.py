@@ -155,11 +155,19 @@ def run_reference(args, world, rank):
             "warmup": args.warmup, "ms_per_step": SEQ / v * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 (reference f32 mode)",
             "data": "synthetic N(0,0.5^2) q,k,v; N(0,1) gates", "impl": "reference",
-            "config": {"workload": "cfg3 per-token-decay LSM (%s), seq %d, H=%d, d=%d, batch 1"
-                                   % (args.instance, SEQ, HEADS, HEAD_DIM)},
+            "config": headline_config(args.instance, world),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def headline_config(instance, world, rank=0):
+    """The config dict both arms print (ours and --impl reference), so the driver can match them."""
+    base, rem = divmod(SEQ, world)
+    n_loc = base + (1 if rank < rem else 0)
+    return {"workload": "cfg3 per-token-decay LSM (%s) with LSM sequence parallelism" % instance,
+            "seq_len": SEQ, "heads": HEADS, "head_dim": HEAD_DIM, "batch": 1,
+            "tokens_per_rank": n_loc, "parallelism": "sp%d" % world}
 
 
 def make_inputs(dev, n_loc, rank, instance="mamba2"):
@@ -188,7 +196,7 @@ def make_gla_inputs(dev, n=SEQ):
                  for s in (0.5, 0.5, 0.5, 1.0, 1.0))
 
 
-def layer_bench(dev, steps=5, warmup=3):
+def layer_bench(dev, steps=5, warmup=3, cpu=True):
     """SURVEY 8(d) second number: LSM-layer tokens/s on cfg4 (A0.3B-2B Linear-MoE block:
     hidden 1024, 8 heads x 128, GLA, FFN 896, 64 experts top-8; 8 documents x 8192 tokens)
     through lmoe_block_fwd: RMSNorm, fused QKV+gate GEMM, LSM, W_o, RMSNorm, MoE, residuals."""
@@ -222,11 +230,27 @@ def layer_bench(dev, steps=5, warmup=3):
     except Exception:  # noqa: BLE001
         pass
     tf = flops / (ms / 1e3) / 1e12
-    return {"workload": "cfg4 A0.3B-2B Linear-MoE block (GLA LSM + 64-expert top-8 MoE), 8 x 8192 tokens",
-            "tokens_per_s": T / (ms / 1e3), "ms_per_step": ms, "steps": steps,
-            "roofline": {"bound": "tensor", "achieved": tf, "peak": tflops_peak, "unit": "TFLOP/s",
-                         "frac": tf / tflops_peak, "flops_per_step": flops,
-                         "note": "GEMM + LSM flops per block; peak = MEASURED_PEAKS bf16_tflops_sustained"}}
+    res = {"workload": "cfg4 A0.3B-2B Linear-MoE block (GLA LSM + 64-expert top-8 MoE), 8 x 8192 tokens",
+           "tokens_per_s": T / (ms / 1e3), "ms_per_step": ms, "steps": steps,
+           "roofline": {"bound": "tensor", "achieved": tf, "peak": tflops_peak, "unit": "TFLOP/s",
+                        "frac": tf / tflops_peak, "flops_per_step": flops,
+                        "note": "GEMM + LSM flops per block; peak = MEASURED_PEAKS bf16_tflops_sustained"}}
+    # end to end: the fp32 residual stream in from pinned host memory, the block, and back out
+    hx = x0.cpu().pin_memory()
+    hy = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    ems, bi, bo = e2e_ms(dev, (hx,), (x,), lambda: m.run_block(0, x, B, N), hy, x, steps)
+    res["e2e"] = {"value": T / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+                  "path": "pinned host x -> H2D -> lmoe_block_fwd (C-ABI) -> D2H"}
+    if cpu:
+        r = ref_driver(["bench-block", "gla", "L", 256, cfg.hidden, cfg.num_heads, cfg.ffn_dim, cfg.num_experts,
+                        cfg.num_active, os.cpu_count() or 1, 15], 300)
+        if r and r.get("tokens_done", 0) > 0:
+            res["cpu_baseline"] = {
+                "value": r["tokens_per_sec"], "unit": "tokens/s", "cores": r["threads"], "kind": "reference",
+                "sample": "reference Block body of model_forward (rms_norm, LsmMixer GLA, residual, rms_norm, "
+                          "MoeLayer, residual), f32 mode, 256-token documents for 15 s on all host threads "
+                          "(per-token cost is length-independent for the LSM mixer)"}
+    return res
 
 
 def backward_bench(dev, steps=3, warmup=2):
@@ -312,7 +336,226 @@ def gla_bench(dev, steps=3, warmup=2):
     return out
 
 
-def cfg2_bench(dev, steps=20, warmup=3):
+def ref_driver(cmd, timeout):
+    """Runs oracle/_ref/ref_driver (the unmodified reference headers, compiled by
+    oracle/Makefile) and returns its JSON line, or None when the build is absent."""
+    drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    if not os.path.exists(drv):
+        return None
+    out = subprocess.run([drv] + [str(a) for a in cmd], capture_output=True, text=True, timeout=timeout)
+    if out.returncode != 0 or not out.stdout.strip():
+        return None
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def graph_ms(dev, fn, steps, warmup):
+    """Device ms per call of fn (launches on the current stream): captured once as a CUDA
+    graph on a side stream and replayed `steps` times between CUDA events on that stream."""
+    import torch
+    st = torch.cuda.Stream(dev)
+    with torch.cuda.stream(st):
+        for _ in range(warmup):
+            fn()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            fn()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            g.replay()
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / steps
+
+
+def e2e_ms(dev, host_in, dev_in, fn, host_out, dev_out, steps):
+    """End-to-end ms per step through the public API: every step copies its inputs from pinned
+    host memory (H2D), runs fn, and copies the result back (D2H), all inside the timed region.
+    Returns (ms, h2d_bytes, d2h_bytes)."""
+    import torch
+    st = torch.cuda.Stream(dev)
+    with torch.cuda.stream(st):
+        def one():
+            for h, d in zip(host_in, dev_in):
+                d.copy_(h, non_blocking=True)
+            fn()
+            host_out.copy_(dev_out, non_blocking=True)
+        one()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            one()
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+    h2d = sum(x.numel() * x.element_size() for x in host_in)
+    return e0.elapsed_time(e1) / steps, h2d, host_out.numel() * host_out.element_size()
+
+
+def cfg1_bench(dev, steps=50, warmup=5, cpu=True):
+    """Config 1, the reference's own test shape: BLA without decay, B = 1,
+    N = 2048, H = 8, d = 64, fp32 in / out (tf32 tensor cores, fp32 accumulation), chunk 64.
+    Two variants: plain (identity phi, no normaliser; test_lsm.cpp:35, verify.hpp:77-78) and
+    the reference default (elu+1 + normaliser, lsm.hpp:157-160).  16.8 MB per step: the HBM
+    roofline is 2.6 us, so this shape is launch-latency bound; the number says by how much."""
+    import torch
+    import paper_2503_05447_b200 as pk
+    n, h, d = 2048, 8, 64
+    g = torch.Generator(device=dev).manual_seed(1)
+    q, k, v = (torch.randn(1, n, h, d, device=dev, generator=g).mul_(0.5) for _ in range(3))
+    o = torch.empty_like(q)
+    hbm, _, _ = peaks()
+    alg = 4 * d * 4 * n * h  # 3 d s_in + d s_out bytes per (token, head), fp32
+    res = {"workload": "cfg1 BLA (no decay), B=1, N=2048, H=8, d=64, fp32, chunk 64, CUDA-graph replay"}
+    for name, spec in (("plain", pk.LsmSpec(instance=0, feature_map=0)), ("default", pk.LsmSpec.make("bla", d))):
+        fn = lambda: pk.lsm_forward_batched(q, k, v, None, spec, 64, out=o, check=False)
+        ms = graph_ms(dev, fn, steps, warmup)
+        gbs = alg / (ms / 1e3) / 1e9
+        res[name] = {"tokens_per_s": n / (ms / 1e3), "us_per_step": ms * 1e3,
+                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                                  "frac": gbs / hbm, "alg_bytes_per_step": alg}}
+        hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+        ho = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+        ems, bi, bo = e2e_ms(dev, (hq, hk, hv), (q, k, v), fn, ho, o, steps)
+        res[name]["e2e"] = {"value": n / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": bi,
+                            "d2h_bytes_per_step": bo}
+    if cpu:
+        r = ref_driver(["bench-lsm", "bla", 1, n, h, d, 64, os.cpu_count() or 1, 10], 200)
+        if r and r.get("heads_done", 0) > 0:
+            res["cpu_baseline"] = {"value": r["tokens_per_sec"], "unit": "tokens/s", "cores": r["threads"],
+                                   "kind": "reference",
+                                   "sample": "reference lsm_forward_chunked (bla default), f32 mode, chunk 64, "
+                                             "%d of %d heads within 10 s, all host threads"
+                                             % (r["heads_done"], r["heads_total"])}
+    return res
+
+
+def lsm_layer_bench(dev, steps=3, warmup=2):
+    """SURVEY 8(d)'s second number at the headline shape: LSM-layer tokens/s for config 3
+    (Mamba2, one 262144-token document, hidden 2048 = 16 heads x 128): rms_norm, the fused
+    [Wq | Wk | Wv] GEMM, the W_gate_b GEMM (b_pre), the LSM, W_o and the residual add --
+    lmoe_block_fwd with num_experts = 0 (the mixer layer without the MoE)."""
+    import torch
+    from paper_2503_05447_b200.lsm import LsmInstance
+    from paper_2503_05447_b200.model import Model, ModelConfig
+    cfg = ModelConfig(hidden=2048, ffn_dim=128, num_heads=HEADS, num_experts=8, num_active=2, vocab_size=256,
+                      instance=LsmInstance.MAMBA2, pattern="L", max_seq_len=SEQ)
+    m = Model.init(cfg, seed=0, device=str(dev), draw_on_device=True)
+    g = torch.Generator(device=dev).manual_seed(12)
+    x0 = torch.randn(SEQ, cfg.hidden, device=dev, generator=g)
+    x = x0.clone()
+    for _ in range(warmup):
+        m.run_block(0, x, 1, SEQ, moe=False)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        m.run_block(0, x, 1, SEQ, moe=False)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    h, d = cfg.hidden, HEAD_DIM
+    flops = SEQ * (2 * h * 3 * h + 2 * h * 64 + 2 * h * h + HEADS * (4 * d * d + 2 * 64 * d))
+    tflops_peak = 1373.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            tflops_peak = json.load(f)["bf16_tflops_sustained"]
+    except Exception:  # noqa: BLE001
+        pass
+    tf = flops / (ms / 1e3) / 1e12
+    del m
+    torch.cuda.empty_cache()
+    return {"workload": "cfg3 LSM layer (Mamba2, N=262144, hidden 2048 = 16 x 128): rms_norm + QKV/gate GEMMs + "
+                        "LSM + W_o + residual, lmoe_block_fwd without MoE",
+            "tokens_per_s": SEQ / (ms / 1e3), "ms_per_step": ms, "steps": steps,
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": tflops_peak, "unit": "TFLOP/s",
+                         "frac": tf / tflops_peak, "flops_per_step": flops,
+                         "note": "projection GEMM + LSM flops; peak = MEASURED_PEAKS bf16_tflops_sustained"}}
+
+
+def hybrid_bench(dev, steps=2, warmup=1, cpu=True):
+    """Config 5: the hybrid A1B-7B Linear-MoE stack -- hidden 2048, 16 heads x 128,
+    FFN 1024, 64 experts top-8, 16 layers LLLNLLLNLLLNLLLN -- over ONE 131072-token
+    document on one GPU (SP degree 1; the driver's multi-GPU run would split it by chunk_range).
+    GLA LSM layers; N layers are causal softmax attention over the whole document.  Weights drawn
+    on the device with the reference's init scales; x ~ N(0, 1) fp32 residual stream."""
+    import torch
+    from paper_2503_05447_b200.lsm import LsmInstance
+    from paper_2503_05447_b200.model import Model, ModelConfig
+    N = 131072
+    cfg = ModelConfig(hidden=2048, ffn_dim=1024, num_heads=16, num_experts=64, num_active=8, vocab_size=256,
+                      instance=LsmInstance.GLA, pattern="LLLN" * 4, max_seq_len=N)
+    m = Model.init(cfg, seed=0, device=str(dev), draw_on_device=True)
+    g = torch.Generator(device=dev).manual_seed(8)
+    x0 = torch.randn(N, cfg.hidden, device=dev, generator=g)
+    x = x0.clone()
+    nb = len(cfg.pattern)
+
+    def stack():
+        for i in range(nb):
+            m.run_block(i, x, 1, N)
+    for _ in range(warmup):
+        x.copy_(x0)
+        stack()
+    torch.cuda.synchronize(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(nb + 1)]
+    tot, per = 0.0, [0.0] * nb
+    for _ in range(steps):
+        x.copy_(x0)
+        ev[0].record()
+        for i in range(nb):
+            m.run_block(i, x, 1, N)
+            ev[i + 1].record()
+        torch.cuda.synchronize(dev)
+        tot += ev[0].elapsed_time(ev[nb])
+        for i in range(nb):
+            per[i] += ev[i].elapsed_time(ev[i + 1])
+    ms = tot / steps
+    h, H, d, F, E, K = cfg.hidden, cfg.num_heads, 128, cfg.ffn_dim, cfg.num_experts, cfg.num_active
+    moe = 2 * h * E + 6 * K * h * F
+    fl_L = N * (2 * h * 4 * h + 2 * h * h + moe + H * (4 * d * d + 2 * 64 * d))
+    fl_N = N * (2 * h * 3 * h + 2 * h * h + moe) + H * 2 * N * N * d  # causal QK^T + PV
+    flops = 12 * fl_L + 4 * fl_N
+    tflops_peak = 1373.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            tflops_peak = json.load(f)["bf16_tflops_sustained"]
+    except Exception:  # noqa: BLE001
+        pass
+    tf = flops / (ms / 1e3) / 1e12
+    msL = sum(per[i] for i in range(nb) if cfg.pattern[i] == "L") / steps / 12
+    msN = sum(per[i] for i in range(nb) if cfg.pattern[i] == "N") / steps / 4
+    res = {"workload": "cfg5 hybrid A1B-7B stack (16 layers LLLN x 4, GLA + causal attention, 64-expert top-8 MoE), "
+                       "one 131072-token document, 1 GPU",
+           "tokens_per_s": N / (ms / 1e3), "ms_per_step": ms, "steps": steps,
+           "ms_per_L_block": msL, "ms_per_N_block": msN,
+           "roofline": {"bound": "tensor", "achieved": tf, "peak": tflops_peak, "unit": "TFLOP/s",
+                        "frac": tf / tflops_peak, "flops_per_step": flops,
+                        "note": "GEMM + LSM + causal attention flops of the 16 blocks; peak = bf16_tflops_sustained"},
+           "sp8_kv_gather": {"bytes_received_per_rank_per_N_layer": 2 * 7 * (N // 8) * H * d * 2,
+                             "note": "K and V bf16 of the 7 other ranks (SURVEY 8(d) cfg5); not exercised on 1 GPU"}}
+    if cpu:
+        rates = {}
+        for kind in ("L", "N"):
+            r = ref_driver(["bench-block", "gla", kind, 256, h, H, F, E, K, os.cpu_count() or 1, 12], 300)
+            if r and r.get("tokens_done", 0) > 0:
+                rates[kind] = r
+        if len(rates) == 2:
+            v = 1.0 / (12.0 / rates["L"]["tokens_per_sec"] + 4.0 / rates["N"]["tokens_per_sec"])
+            res["cpu_baseline"] = {
+                "value": v, "unit": "tokens/s", "cores": rates["L"]["threads"], "kind": "reference",
+                "sample": "reference Block body of model_forward, f32 mode, L (GLA) and N (dense causal attention) "
+                          "blocks each timed 12 s on 256-token documents on all host threads, composed as "
+                          "12 L + 4 N per token; the reference's dense attention is quadratic, so at the 128K "
+                          "document the CPU is slower than this"}
+    del m
+    torch.cuda.empty_cache()
+    return res
+
+
+def cfg2_bench(dev, steps=20, warmup=3, cpu=True):
     """Config-2 side numbers: Lightning (a = 0.95) and RetNet (a = 1 - 1/32)
     scalar-decay LSM forward, B = 1, N = 32768, H = 16, d = 128, bf16 in / out, through the
     same call as the headline (world 1: the local pass), CUDA-graph replay; HBM roofline of
@@ -351,6 +594,19 @@ def cfg2_bench(dev, steps=20, warmup=3):
         res[inst] = {"tokens_per_s": n / (ms / 1e3), "ms_per_step": ms, "steps": steps,
                      "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
                                   "alg_bytes_per_token_head": 1024, "note": "whole step (3 kernels)"}}
+        hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+        ho = torch.empty(out_t.shape, dtype=out_t.dtype, pin_memory=True)
+        fn = lambda: sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out_t, check=False)
+        ems, bi, bo = e2e_ms(dev, (hq, hk, hv), (q, k, v), fn, ho, out_t, 5)
+        res[inst]["e2e"] = {"value": n / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": bi,
+                            "d2h_bytes_per_step": bo}
+        if cpu:
+            r = ref_driver(["bench-lsm", inst, 1, n, HEADS, HEAD_DIM, 64, os.cpu_count() or 1, 10], 200)
+            if r and r.get("heads_done", 0) > 0:
+                res[inst]["cpu_baseline"] = {
+                    "value": r["tokens_per_sec"], "unit": "tokens/s", "cores": r["threads"], "kind": "reference",
+                    "sample": "reference lsm_forward_chunked, f32 mode, chunk 64, %d of %d heads of %d tokens "
+                              "within 10 s, extrapolated to all heads" % (r["heads_done"], r["heads_total"], n)}
     res["workload"] = "cfg2 scalar-decay LSM forward, N=32768, 16 x 128, bf16, CUDA-graph replay"
     return res
 
@@ -530,10 +786,13 @@ def main():
         cb = None
         extra = {}
         if world == 1 and not args.no_extra:
-            extra["layer"] = layer_bench(dev)
+            extra["layer"] = layer_bench(dev, cpu=not args.no_cpu_baseline)
+            extra["lsm_layer"] = lsm_layer_bench(dev)
             extra["backward"] = backward_bench(dev)
             extra["gla"] = gla_bench(dev)
-            extra["cfg2"] = cfg2_bench(dev)
+            extra["cfg2"] = cfg2_bench(dev, cpu=not args.no_cpu_baseline)
+            extra["cfg1"] = cfg1_bench(dev, cpu=not args.no_cpu_baseline)
+            extra["hybrid"] = hybrid_bench(dev, cpu=not args.no_cpu_baseline)
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(args.instance, SEQ, os.cpu_count() or 1, 20.0)
         line = {
@@ -541,11 +800,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: q,k,v ~ N(0,0.5^2) bf16, Mamba2 b_pre ~ N(0,1) fp32, a_raw ~ N(0,0.5^2)",
-            "config": {"workload": "cfg3 per-token-decay LSM (%s) with LSM sequence parallelism"
-                                   % args.instance,
-                       "seq_len": SEQ, "heads": HEADS, "head_dim": HEAD_DIM, "batch": 1,
-                       "tokens_per_rank": n_loc, "parallelism": "sp%d" % world,
-                       "timed": "CUDA-graph replay of the step" if graph is not None else "direct calls",
+            "config": headline_config(args.instance, world, rank),
+            "timing": {"timed": "CUDA-graph replay of the step" if graph is not None else "direct calls",
                        "l2": "inputs 3 GiB > L2; no flush needed"},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

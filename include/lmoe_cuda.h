@@ -148,6 +148,10 @@ int lmoe_gemm(const void* A, int M, int K, int lda, const void* W, int N, void* 
  * sp_attention_rank (K/V all-gather, row offset from chunk_range of N_total).
  * x: fp32 residual stream [B, N_local, hidden], updated in place; aux: this block's
  * load-balance loss (device scalar).  head_dim = hidden / heads = 128.
+ * num_experts == 0: the mixer layer alone, x += mixer(rms_norm(x, norm_mixer)) (the
+ * "LSM-layer" unit of SURVEY 8(d); the MoE weights are not read).
+ * A non-NULL nccl_comm at world 1 (a 1-rank communicator) runs the SP phase structure with
+ * its all-gathers instead of the local shortcut.
  * ------------------------------------------------------------------------------------- */
 typedef struct lmoe_block_desc {
     int kind;                 /* 'L' or 'N'                                            */
@@ -278,7 +282,10 @@ int lmoe_debug_trace_read(unsigned long long* out /* 64 x 16 */);
  * ONE ncclAllGather moves the all-heads payload [M | z? | log D] (B*H*(D*D [+D] + 1) fp32 per
  * rank; the reference gathers per head, parallel.hpp:447-452), the decayed exclusive
  * prefix over earlier ranks (parallel.hpp:340-361) gives the carried-in state, and the
- * output pass re-evaluates the slice with it.  nccl_comm is an ncclComm_t (world > 1).
+ * output pass re-evaluates the slice with it.  nccl_comm is an ncclComm_t (required for
+ * world > 1).  At world 1, NULL runs the local pass; a 1-rank communicator runs the same
+ * phase structure as world > 1, the ncclAllGather included (how the GPU tests execute the
+ * NCCL path on one device).  The same holds for the unmasked, backward and attention SP calls.
  * ------------------------------------------------------------------------------------- */
 size_t lmoe_sp_payload_floats(const lmoe_lsm_desc* desc, int B, int H, int D);
 size_t lmoe_sp_lsm_fwd_workspace_size(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,

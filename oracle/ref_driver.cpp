@@ -10,6 +10,8 @@
 //   ref_driver golden <out.bin>
 //   ref_driver bench-lsm <instance> <B> <N> <H> <d> <chunk> <threads> <budget_s> [gate_mean]
 //   ref_driver bench-moe <T> <hidden> <ffn> <E> <k> <threads> <budget_s>
+//   ref_driver bench-block <instance> <kind L|N> <doc_len> <hidden> <heads> <ffn> <E> <k>
+//                          <threads> <budget_s>
 //
 // Golden stream format: records of
 //   u32 name_len, name bytes, u32 ndim, u32 shape[ndim], f64 data[prod(shape)]
@@ -622,6 +624,66 @@ int cmd_bench_moe(int argc, char** argv) {
     return 0;
 }
 
+// One Linear-MoE block of the reference model (the loop body of model_forward, model.hpp:387-397:
+// rms_norm -> mixer per document -> residual -> rms_norm -> MoeLayer -> residual), f32 mode, no
+// tape, documents of doc_len tokens processed independently by `threads` workers.  Prints
+// tokens/s over the documents finished within the budget.
+int cmd_bench_block(int argc, char** argv) {
+    if (argc < 12) return 2;
+    auto inst = instance_from_name(argv[2]);
+    if (!inst) return 3;
+    const char kind = argv[3][0];
+    const int len = atoi(argv[4]), hidden = atoi(argv[5]), heads = atoi(argv[6]), ffn = atoi(argv[7]);
+    const int E = atoi(argv[8]), K = atoi(argv[9]);
+    int threads = atoi(argv[10]);
+    const double budget = atof(argv[11]);
+    if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
+    NoGradGuard ng;
+    ModelConfig cfg;
+    cfg.hidden = hidden;
+    cfg.ffn_dim = ffn;
+    cfg.num_heads = heads;
+    cfg.num_layers = 1;
+    cfg.num_experts = E;
+    cfg.num_active = K;
+    cfg.vocab_size = 256;
+    cfg.instance = *inst;
+    cfg.pattern = std::string(1, kind);
+    cfg.max_seq_len = len;
+    cfg.dtype = DType::f32;
+    Rng rng(5);
+    const Model m = build_model(cfg, rng);
+    const Block& b = m.blocks[0];
+    std::vector<int> done(threads, 0);
+    std::atomic<int> failed{0};
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w)
+        pool.emplace_back([&, w]() {
+            Rng r2(70 + w);
+            Tensor x = Tensor::randn({len, hidden}, r2, 1.0, DType::f32);
+            try {
+                while (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < budget) {
+                    const Tensor h = rms_norm(x, b.norm_mixer, cfg.norm_eps);
+                    Tensor y = add(x, b.mixer_forward(h));
+                    const Tensor h2 = rms_norm(y, b.norm_moe, cfg.norm_eps);
+                    auto out = b.moe.forward(h2);
+                    y = add(y, out.first);
+                    done[w] += len;
+                }
+            } catch (const std::exception&) {
+                failed.fetch_add(1);
+            }
+        });
+    for (auto& th : pool) th.join();
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    int total = 0;
+    for (int x : done) total += x;
+    printf("{\"tokens_done\": %d, \"seconds\": %.6f, \"threads\": %d, \"failed\": %d, "
+           "\"tokens_per_sec\": %.3f}\n", total, secs, threads, failed.load(), total / secs);
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -633,6 +695,7 @@ int main(int argc, char** argv) {
         if (!strcmp(argv[1], "golden") && argc >= 3) return cmd_golden(argv[2]);
         if (!strcmp(argv[1], "bench-lsm")) return cmd_bench_lsm(argc, argv);
         if (!strcmp(argv[1], "bench-moe")) return cmd_bench_moe(argc, argv);
+        if (!strcmp(argv[1], "bench-block")) return cmd_bench_block(argc, argv);
     } catch (const std::exception& e) {
         fprintf(stderr, "error: %s\n", e.what());
         return 1;

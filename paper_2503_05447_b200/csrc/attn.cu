@@ -328,7 +328,7 @@ void sp_attn_core(int B, int N_total, int H, int D, const void* q_loc, const voi
                                           static_cast<const uint8_t*>(v_loc) + (size_t)b * len * src_pitch,
                                           src_pitch, row, len, cudaMemcpyDeviceToDevice, st));
     }
-    if (world > 1) {
+    if (nccl_comm) {  // world 1 with a 1-rank communicator runs the gather too
         ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
         ncclResult_t r = ncclGroupStart();
         if (r == ncclSuccess) r = ncclAllGather(dk + rank * send, dk, send, ncclUint8, comm, st);

@@ -129,7 +129,7 @@ static BlockWs plan_block(const lmoe_block_desc* d, int B, int N, int N_total, i
     w.mixer_bytes = d->kind == 'L' ? lsm_mixer_ws(&d->lsm, B, N, d->heads, 128, world)
                                    : sp_attn_ws(B, N_total, d->heads, 128, world);
     w.mixer = take(w.mixer_bytes);
-    w.moe_bytes = lmoe_moe_workspace_size((int)T, d->hidden, d->ffn_dim, d->num_experts, d->top_k);
+    w.moe_bytes = d->num_experts == 0 ? 0 : lmoe_moe_workspace_size((int)T, d->hidden, d->ffn_dim, d->num_experts, d->top_k);
     w.moe = take(w.moe_bytes);
     w.total = off;
     return w;
@@ -204,7 +204,7 @@ static void block_core(const lmoe_block_desc* d, const lmoe_block_weights* wt, i
                 attn_core(1, len, len, H, D, qd, qd + col, qd + 2 * col, w.nc, static_cast<uint8_t*>(o) + r0 * hid * 2,
                           0, st);
             }
-        } else if (world == 1) {
+        } else if (world == 1 && !nccl_comm) {
             attn_core(B, N_local, N_local, H, D, qkv, qkv + col, qkv + 2 * col, w.nc, o, 0, st);
         } else {
             sp_attn_core(B, N_total, H, D, qkv, qkv + col, qkv + 2 * col, w.nc, o, nccl_comm, rank, world,
@@ -212,6 +212,10 @@ static void block_core(const lmoe_block_desc* d, const lmoe_block_weights* wt, i
         }
         // x += o W_o ; h2 = rms_norm(x, norm_moe)
         dense_gemm(o, T, hid, hid, wt->wo, hid, ws + w.mixed, hid, false, ws + w.tiles, st);
+        if (d->num_experts == 0) {  // mixer-only LSM layer (SURVEY 8(d) "LSM-layer tokens/s"): x += o W_o
+            add_rmsnorm(x, ws + w.mixed, false, nullptr, 0.f, nullptr, T, hid, st);
+            return;
+        }
         add_rmsnorm(x, ws + w.mixed, false, wt->norm_moe, d->norm_eps, h, T, hid, st);
         // x += MoE(h2)
         const int rc = lmoe_moe_forward(T, hid, d->ffn_dim, d->num_experts, d->top_k, h, wt->router, wt->w_gate,

@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                     if (!(w >= 0.f)) atomicAdd(reinterpret_cast<int*>(p.fdbg + base + 1), 1);
                 }
                 mbar_wait(&full[s], (g / NST) & 1);
-                xform_row_part<T, FM, false>(tiles + s * 3 * kTileBytes + kTileBytes, row, hh * DH, DH, w);
+                xform_row_part<T, FM, false, DH>(tiles + s * 3 * kTileBytes + kTileBytes, row, hh * DH, w);
                 fence_proxy_async_smem();
                 mbar_arrive(&xfA[ga & 1]);
                 mbar_arrive(&gfree[slot]);
@@ -427,8 +427,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                 const int nvalid = min(kC, te - (tb + c * kC));
                 const float sc = row < nvalid ? 1.f : 0.f;
                 uint8_t* qt = tiles + s * 3 * kTileBytes;
-                xform_row_part<T, FM, false>(qt, row, hh * DH, DH, sc);
-                xform_row_part<T, FM, false>(qt + kTileBytes, row, hh * DH, DH, sc);
+                xform_row_part<T, FM, false, DH>(qt, row, hh * DH, sc);
+                xform_row_part<T, FM, false, DH>(qt + kTileBytes, row, hh * DH, sc);
                 fence_proxy_async_smem();
                 mbar_arrive(xf1);
             };
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                             }
                             *ptr = v;
                         }
-                        xform_row_part<T, 0, false>(kt, row, hh * DH, DH, fk);
+                        xform_row_part<T, 0, false, DH>(kt, row, hh * DH, fk);
                     }
                     fence_proxy_async_smem();
                     mbar_arrive(xf2);

@@ -558,10 +558,11 @@ void lsm_mixer_core(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
     // developer knob (tools/sp_scaling_probe.py): run the multi-rank phase structure at world 1,
     // a device copy standing in for the all-gather
     const bool force_sp = getenv("LMOE_SP_FORCE") != nullptr;
-    if (world == 1 && !force_sp) {
+    if (world == 1 && !force_sp && !nccl_comm) {
         // a gather over one rank is the identity and rank 0 carries nothing in: the local
         // pass (state pass, segment prefix, output pass); the empty marks keep the phase
-        // timers' layout (all-gather, rank combine)
+        // timers' layout (all-gather, rank combine).  With a (1-rank) communicator the SP
+        // structure runs instead, ncclAllGather included.
         if (c.fused_ok()) {  // one single-read launch (timing phase 0)
             c.fused(nullptr, M_out);
             c.finish_timing();
@@ -583,7 +584,7 @@ void lsm_mixer_core(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
     if (dtype == LMOE_BF16) sp_phase_a<__nv_bfloat16>(c, payload);
     else sp_phase_a<float>(c, payload);
     c.mark();
-    if (world > 1)
+    if (nccl_comm)
         NCCL_CHECK(ncclAllGather(payload, gathered, P, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
     else
         LMOE_CUDA_CHECK(cudaMemcpyAsync(gathered, payload, P * 4, cudaMemcpyDeviceToDevice, st));
@@ -733,7 +734,7 @@ extern "C" int lmoe_sp_lsm_nomask_fwd(const lmoe_lsm_desc* desc, int B, int N_lo
         const size_t P = (size_t)B * H * D * D;
         if (dtype == LMOE_BF16) nomask_local_state<__nv_bfloat16>(c, payload);
         else nomask_local_state<float>(c, payload);
-        if (world > 1) {
+        if (nccl_comm) {
             NCCL_CHECK(ncclAllGather(payload, gathered, P, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
         } else {
             LMOE_CUDA_CHECK(cudaMemcpyAsync(gathered, payload, P * 4, cudaMemcpyDeviceToDevice, st));
@@ -1309,7 +1310,7 @@ extern "C" int lmoe_sp_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N_local, in
         else
             sp_bwd_payloads<float>(desc, B, N_local, N_local, H, D, dtype, q, k, v, a_pre, b_pre, a_raw, dO, ws, w,
                                    fpay, bpay, st);
-        if (world > 1) {
+        if (nccl_comm) {
             NCCL_CHECK(ncclGroupStart());
             NCCL_CHECK(ncclAllGather(fpay, fgath, Pf, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));
             NCCL_CHECK(ncclAllGather(bpay, bgath, Pb, ncclFloat, static_cast<ncclComm_t>(nccl_comm), st));

@@ -63,60 +63,56 @@ __device__ __forceinline__ float chunk_scan(const LsmFwdParams& p, const float (
     return __shfl_sync(0xFFFFFFFFu, x, 31);
 }
 
+// One 16-byte chunk (8 bf16 / 4 fp32 values) in registers: x <- round(phi(x) * scale).
+template <typename T, int FM, bool RND>
+__device__ __forceinline__ void xform_chunk(uint4& v, float scale) {
+    if constexpr (sizeof(T) == 2) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float2 f = unpack_bf16(w[i]);
+            w[i] = pack_bf16(fmap_t<FM>(f.x) * scale, fmap_t<FM>(f.y) * scale);
+        }
+    } else {
+        float* f = reinterpret_cast<float*>(&v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float x = fmap_t<FM>(f[i]) * scale;
+            f[i] = RND ? tf32r(x) : x;
+        }
+    }
+}
+
+// Row-owner transform of NCH 16-byte chunks (starting at chunk ch0) of one SW128 row, in
+// place.  All shared loads issue before the first store: with load / transform / store per
+// chunk the compiler cannot prove the swizzled addresses distinct, so every load waited for
+// the previous chunk's store (8 exposed shared-memory round trips per row).
+template <typename T, int FM, bool RND, int NCH>
+__device__ __forceinline__ void xform_chunks(uint8_t* blk, int row, int ch0, float scale) {
+    uint4 v[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) v[ch] = *reinterpret_cast<const uint4*>(blk + sw128_off(row, ch0 + ch));
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) xform_chunk<T, FM, RND>(v[ch], scale);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) *reinterpret_cast<uint4*>(blk + sw128_off(row, ch0 + ch)) = v[ch];
+}
+
 // Row-owner transform of one 128-byte half row (8 x 16B chunks) in place:
 // x <- round(phi(x) * scale); rows beyond the sequence get scale 0.
 template <typename T, int FM, bool RND>
 __device__ __forceinline__ void xform_half_row(uint8_t* blk, int row, float scale) {
-#pragma unroll
-    for (int ch = 0; ch < 8; ++ch) {
-        uint4* ptr = reinterpret_cast<uint4*>(blk + sw128_off(row, ch));
-        uint4 v = *ptr;
-        if constexpr (sizeof(T) == 2) {
-            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float2 f = unpack_bf16(w[i]);
-                w[i] = pack_bf16(fmap_t<FM>(f.x) * scale, fmap_t<FM>(f.y) * scale);
-            }
-        } else {
-            float* f = reinterpret_cast<float*>(&v);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float x = fmap_t<FM>(f[i]) * scale;
-                f[i] = RND ? tf32r(x) : x;
-            }
-        }
-        *ptr = v;
-    }
+    xform_chunks<T, FM, RND, 8>(blk, row, 0, scale);
 }
 
-// Row-owner transform of `ncols` columns starting at col0 of a two-block SW128 tile.
-template <typename T, int FM, bool RND>
-__device__ __forceinline__ void xform_row_part(uint8_t* tile, int row, int col0, int ncols, float scale) {
+// Row-owner transform of NCOLS columns starting at col0 of a two-block SW128 tile (the
+// range stays inside one 128-byte block).
+template <typename T, int FM, bool RND, int NCOLS>
+__device__ __forceinline__ void xform_row_part(uint8_t* tile, int row, int col0, float scale) {
     using TT = TileTraits<T>;
-    uint8_t* blk = tile + (col0 / TT::EPB) * kBlockBytes;
-    const int ch0 = (col0 % TT::EPB) / TT::EPC;
-#pragma unroll
-    for (int ch = 0; ch < ncols / TT::EPC; ++ch) {
-        uint4* ptr = reinterpret_cast<uint4*>(blk + sw128_off(row, ch0 + ch));
-        uint4 v = *ptr;
-        if constexpr (sizeof(T) == 2) {
-            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float2 f = unpack_bf16(w[i]);
-                w[i] = pack_bf16(fmap_t<FM>(f.x) * scale, fmap_t<FM>(f.y) * scale);
-            }
-        } else {
-            float* f = reinterpret_cast<float*>(&v);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float x = fmap_t<FM>(f[i]) * scale;
-                f[i] = RND ? tf32r(x) : x;
-            }
-        }
-        *ptr = v;
-    }
+    static_assert(NCOLS % TT::EPC == 0 && NCOLS <= TT::EPB, "one block, whole chunks");
+    xform_chunks<T, FM, RND, NCOLS / TT::EPC>(tile + (col0 / TT::EPB) * kBlockBytes, row,
+                                             (col0 % TT::EPB) / TT::EPC, scale);
 }
 
 // fp32 only: write one token row's 32 values of column block `hb` (already scaled) into a
@@ -640,8 +636,8 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
             const int nvalid = min(kC, t_end - chunk_t0(c));
             const float sc = row < nvalid ? 1.f : 0.f;
             uint8_t* qt = tiles + s * 3 * kTileBytes;
-            xform_row_part<T, FM, TR>(qt, row, hh * DH, DH, sc);
-            xform_row_part<T, FM, TR>(qt + kTileBytes, row, hh * DH, DH, sc);
+            xform_row_part<T, FM, TR, DH>(qt, row, hh * DH, sc);
+            xform_row_part<T, FM, TR, DH>(qt + kTileBytes, row, hh * DH, sc);
             fence_proxy_async_smem();
             mbar_arrive(xf1);
         };
@@ -765,11 +761,23 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                     fk = safe ? __expf(gend - rQ[q]) * Fs[row] : __expf(gend - gi) * Fs[row];
                 uint8_t* qb = qt + (hh * DH / TT::EPB) * kBlockBytes;
                 const int qch0 = (hh * DH % TT::EPB) / TT::EPC;
+                constexpr int NCH = DH / TT::EPC;
+                // all of this row part's Q (and, bf16, K) chunks are loaded before any store
+                // (see xform_chunks): one shared-memory round trip instead of 2 NCH
+                constexpr bool kBothK = !TR && DECAY != kDecayNone;
+                uint4 vq[NCH], vk[kBothK ? NCH : 1];
                 if constexpr (DECAY != kDecayNone || NORM) {
 #pragma unroll
-                    for (int ch = 0; ch < DH / TT::EPC; ++ch) {
-                        uint4* ptr = reinterpret_cast<uint4*>(qb + sw128_off(row, qch0 + ch));
-                        uint4 v = *ptr;
+                    for (int ch = 0; ch < NCH; ++ch) vq[ch] = *reinterpret_cast<const uint4*>(qb + sw128_off(row, qch0 + ch));
+                }
+                if constexpr (kBothK) {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) vk[ch] = *reinterpret_cast<const uint4*>(kt + (qb - qt) + sw128_off(row, qch0 + ch));
+                }
+                if constexpr (DECAY != kDecayNone || NORM) {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) {
+                        uint4& v = vq[ch];
                         if constexpr (kBF16) {
                             uint32_t* w = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
@@ -787,12 +795,22 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                                 if constexpr (NORM) qz += f[e] * sZ[hh * DH + ch * 4 + e];
                             }
                         }
-                        if constexpr (DECAY != kDecayNone) *ptr = v;
                     }
                 }
-                if constexpr (!TR) {
-                    if constexpr (DECAY != kDecayNone) xform_row_part<T, 0, false>(kt, row, hh * DH, DH, fk);
-                } else {
+                if constexpr (kBothK) {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) xform_chunk<T, 0, false>(vk[ch], fk);
+                }
+                if constexpr (DECAY != kDecayNone) {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) *reinterpret_cast<uint4*>(qb + sw128_off(row, qch0 + ch)) = vq[ch];
+                }
+                if constexpr (kBothK) {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch)
+                        *reinterpret_cast<uint4*>(kt + (qb - qt) + sw128_off(row, qch0 + ch)) = vk[ch];
+                }
+                if constexpr (TR) {
                     float vals[32];
                     load_half_row_f32(kt + hh * kBlockBytes, row, vals);
 #pragma unroll
@@ -831,28 +849,64 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
             auto do_a = [&]() {
                 uint32_t r[KC / 32][32];
                 const uint32_t tS = tmem + bb * 128 + lane_off + hh * KC;
-#pragma unroll
-                for (int i = 0; i < KC / 32; ++i) tmem_ld32(tS + i * 32, r[i]);
-                tmem_wait_ld();
-                float eq[KC / 32];  // query factor per key quarter of this thread's columns
-#pragma unroll
-                for (int i = 0; i < KC / 32; ++i) {
-                    const float rr = rQ[hh * (KC / 32) + i];
-                    eq[i] = (DECAY != kDecayNone && safe) ? __expf(REV ? rr - gi : gi - rr) : 1.f;
-                }
+                // causal mask col <= row (REV: col >= row): a warp's KC key columns against its
+                // 32 rows are all kept, all masked (no TMEM read, P = 0) or the diagonal block
+                const bool zero = !p.nomask && (REV ? hh * KC + KC - 1 < q * 32 : hh * KC > q * 32 + 31);
                 float rs = 0.f;
+                if (!zero) {
 #pragma unroll
-                for (int j = 0; j < KC; ++j) {
-                    const int col = hh * KC + j;
-                    float v = __uint_as_float(r[j / 32][j % 32]);
-                    float f;
-                    if constexpr (DECAY == kDecayNone) f = 1.f;
-                    else if constexpr (REV) f = safe ? eq[j / 32] * Fs[col] : __expf(Gs[col] - gi);
-                    else f = safe ? eq[j / 32] * Fs[col] : __expf(gi - Gs[col]) * Fs[col];
-                    v = (!p.nomask && (REV ? col >= row : col <= row)) ? v * f : 0.f;
-                    if constexpr (TR) v = tf32r(v);
-                    rs += v;
-                    r[j / 32][j % 32] = __float_as_uint(v);
+                    for (int i = 0; i < KC / 32; ++i) tmem_ld32(tS + i * 32, r[i]);
+                    tmem_wait_ld();
+                    // decay factor per column, the branch on `safe` (uniform per chunk) hoisted out
+                    // of the column loop and the ring rows read as float4
+                    if constexpr (DECAY != kDecayNone) {
+                        if (safe) {
+#pragma unroll
+                            for (int i = 0; i < KC / 32; ++i) {
+                                const float rr = rQ[hh * (KC / 32) + i];
+                                const float eq = __expf(REV ? rr - gi : gi - rr);  // query factor of the key quarter
+#pragma unroll
+                                for (int j = 0; j < 32; j += 4) {
+                                    const float4 F = *reinterpret_cast<const float4*>(Fs + hh * KC + i * 32 + j);
+                                    r[i][j] = __float_as_uint(__uint_as_float(r[i][j]) * (eq * F.x));
+                                    r[i][j + 1] = __float_as_uint(__uint_as_float(r[i][j + 1]) * (eq * F.y));
+                                    r[i][j + 2] = __float_as_uint(__uint_as_float(r[i][j + 2]) * (eq * F.z));
+                                    r[i][j + 3] = __float_as_uint(__uint_as_float(r[i][j + 3]) * (eq * F.w));
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < KC / 32; ++i) {
+#pragma unroll
+                                for (int j = 0; j < 32; j += 4) {
+                                    const float4 G = *reinterpret_cast<const float4*>(Gs + hh * KC + i * 32 + j);
+                                    const float g4[4] = {G.x, G.y, G.z, G.w};
+                                    float f4[4];
+                                    if constexpr (REV) {
+#pragma unroll
+                                        for (int u = 0; u < 4; ++u) f4[u] = __expf(g4[u] - gi);
+                                    } else {
+                                        const float4 F = *reinterpret_cast<const float4*>(Fs + hh * KC + i * 32 + j);
+                                        f4[0] = __expf(gi - g4[0]) * F.x; f4[1] = __expf(gi - g4[1]) * F.y;
+                                        f4[2] = __expf(gi - g4[2]) * F.z; f4[3] = __expf(gi - g4[3]) * F.w;
+                                    }
+#pragma unroll
+                                    for (int u = 0; u < 4; ++u) r[i][j + u] = __float_as_uint(__uint_as_float(r[i][j + u]) * f4[u]);
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < KC; ++j) {
+                        const int col = hh * KC + j;
+                        float v = (!p.nomask && (REV ? col < row : col > row)) ? 0.f : __uint_as_float(r[j / 32][j % 32]);
+                        if constexpr (TR) v = tf32r(v);
+                        rs += v;
+                        r[j / 32][j % 32] = __float_as_uint(v);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < KC; ++j) r[j / 32][j % 32] = 0u;
                 }
                 if constexpr (kBF16) {
                     uint32_t pk[KC / 2];
@@ -860,7 +914,9 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                     for (int j = 0; j < KC / 2; ++j)
                         pk[j] = pack_bf16(__uint_as_float(r[(2 * j) / 32][(2 * j) % 32]),
                                           __uint_as_float(r[(2 * j + 1) / 32][(2 * j + 1) % 32]));
-                    named_bar_sync(1, MT);  // all S reads done before P overwrites
+                    // all S reads of this TMEM lane quarter done before P overwrites them: only the
+                    // NQ warps of quarter q share these lanes
+                    named_bar_sync(2 + q, 32 * NQ);
                     if constexpr (KC == 32) {
                         tmem_st16(tmem + bb * 128 + lane_off + hh * 16, pk);
                     } else {

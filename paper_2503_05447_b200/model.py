@@ -128,20 +128,24 @@ class Model:
                   w_up=torch.as_tensor(wu, dtype=torch.float32).to(dev, BF16).contiguous(),
                   w_down=torch.as_tensor(wd, dtype=torch.float32).to(dev, BF16).contiguous())
         if kind == "L" and w_gate_b is not None:
-            g = torch.zeros(cfg.hidden, 64)
-            g[:, :cfg.num_heads] = torch.as_tensor(w_gate_b, dtype=torch.float32)
+            wgb = torch.as_tensor(w_gate_b, dtype=torch.float32)
+            g = torch.zeros(cfg.hidden, 64, device=wgb.device)
+            g[:, :cfg.num_heads] = wgb
             b.w_gate_b = g.to(dev, BF16).contiguous()
             b.a_raw = torch.as_tensor(a_raw, dtype=torch.float32).to(dev).contiguous()
         return b
 
     @staticmethod
-    def init(cfg: ModelConfig, seed=0, device="cuda"):
+    def init(cfg: ModelConfig, seed=0, device="cuda", draw_on_device=False):
         """build_model (model.hpp:336-362) shapes and scales: N(0, 0.02) embeddings, N(0, 1/hidden)
-        mixer and router weights, N(0, 1/hidden) / N(0, 1/ffn) experts (moe.hpp:37-41)."""
+        mixer and router weights, N(0, 1/hidden) / N(0, 1/ffn) experts (moe.hpp:37-41).
+        draw_on_device: draw the weights with a device generator (large configs; a different
+        random stream than the host draw, same distributions)."""
         cfg.validate()
-        g = torch.Generator().manual_seed(seed)
+        gdev = torch.device(device) if draw_on_device else torch.device("cpu")
+        g = torch.Generator(device=gdev).manual_seed(seed)
         h, H, E, F = cfg.hidden, cfg.num_heads, cfg.num_experts, cfg.ffn_dim
-        rn = lambda *shape, s: torch.randn(*shape, generator=g) * s
+        rn = lambda *shape, s: torch.randn(*shape, generator=g, device=gdev) * s
         sh = 1.0 / math.sqrt(h)
         blocks = []
         for kind in cfg.pattern:
@@ -188,8 +192,9 @@ class Model:
         return _BlockWeights(P(b.norm_mixer), P(b.norm_moe), P(b.w_qkv), P(b.w_gate_b), P(b.a_raw), P(b.wo),
                              P(b.router), P(b.w_gate), P(b.w_up), P(b.w_down))
 
-    def run_block(self, i, x, B, N, comm=None, n_total=None, aux=None, stream=None):
-        """Block i on the fp32 residual stream x [B*N, hidden] in place (lmoe_block_fwd)."""
+    def run_block(self, i, x, B, N, comm=None, n_total=None, aux=None, stream=None, moe=True):
+        """Block i on the fp32 residual stream x [B*N, hidden] in place (lmoe_block_fwd).
+        moe=False: the mixer layer alone (x += mixer(rms_norm(x)) W_o; descriptor num_experts = 0)."""
         L = _bind()
         b = self.blocks[i]
         dev = x.device
@@ -200,6 +205,8 @@ class Model:
         if aux is None:
             aux = torch.zeros(1, dtype=torch.float32, device=dev)
         d = self._desc(b.kind)
+        if not moe:
+            d.num_experts = 0
         ws = _workspace(L.lmoe_block_workspace_size(ctypes.byref(d), B, N, n_total, world), dev)
         w = self._weights(b)
         _lib.check(L.lmoe_block_fwd(ctypes.byref(d), ctypes.byref(w), B, N, n_total, x.data_ptr(), aux.data_ptr(),

@@ -70,15 +70,25 @@ def _bind():
 
 class NcclComm:
     """NCCL communicator of the library.  Bootstrap: rank 0 creates the unique id, the
-    process group (gloo or nccl) broadcasts it; every rank calls ncclCommInitRank."""
+    process group (gloo or nccl) broadcasts it; every rank calls ncclCommInitRank.
 
-    def __init__(self, rank, world, device=None):
-        import torch.distributed as dist
+    world == 1: no communicator by default (the entry points then run the local pass, a
+    gather over one rank being the identity).  single_rank_nccl=True creates a real 1-rank
+    NCCL communicator instead, so the SP phase structure runs with its ncclAllGather on one
+    GPU (used by the GPU tests to execute the NCCL path)."""
+
+    def __init__(self, rank, world, device=None, single_rank_nccl=False):
         L = _bind()
         self.rank, self.world = rank, world
         self.handle = ctypes.c_void_p(None)
         if world == 1:
+            if single_rank_nccl:
+                buf = (ctypes.c_uint8 * 128)()
+                _lib.check(L.lmoe_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+                _lib.check(L.lmoe_nccl_comm_init(ctypes.byref(self.handle), 1, 0,
+                                                 ctypes.cast(buf, ctypes.c_void_p)))
             return
+        import torch.distributed as dist
         buf = (ctypes.c_uint8 * 128)()
         if rank == 0:
             _lib.check(L.lmoe_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))

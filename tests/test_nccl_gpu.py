@@ -1,0 +1,128 @@
+"""The NCCL transport executed on one GPU: a real 1-rank communicator (ncclCommInitRank with
+nranks = 1) makes every SP entry point run its multi-rank phase structure with the
+ncclAllGather in the stream, in place of the world-1 shortcut (RankGroup::all_gather,
+parallel.hpp:87-93; masked SP :303-376, unmasked :282-297, attention K/V :380-387, and the
+SP backward).  Each result must equal the path without a communicator, and the step must
+capture into a CUDA graph with the NCCL call inside."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import norm_rel_err, record_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _inputs(inst, N=1100, H=2, D=128, seed=3):
+    torch = _torch()
+    import paper_2503_05447_b200 as pk
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q, k, v = (torch.randn(1, N, H, D, device="cuda", generator=g).mul_(0.5).to(torch.bfloat16)
+               for _ in range(3))
+    spec = pk.LsmSpec.make(inst, D)
+    gates = None
+    if inst == "mamba2":
+        spec.mamba2_a_raw = torch.tensor([0.3, -0.4], device="cuda")[:H]
+        gates = pk.LsmGates(b_pre=torch.randn(1, N, H, device="cuda", generator=g).mul_(0.5).sub_(3.0))
+    return torch, pk, q, k, v, spec, gates
+
+
+@pytest.fixture(scope="module")
+def comm1():
+    _torch()
+    from paper_2503_05447_b200 import sp
+    c = sp.NcclComm(0, 1, single_rank_nccl=True)
+    assert c.handle.value, "1-rank NCCL communicator not created"
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("inst", ["bla", "retnet", "mamba2"])
+def test_masked_sp_through_nccl(comm1, inst):
+    torch, pk, q, k, v, spec, gates = _inputs(inst)
+    from paper_2503_05447_b200 import sp
+    o = sp.sp_lsm_masked_rank(comm1, q, k, v, gates, spec)
+    ref = pk.lsm_forward_batched(q, k, v, gates, spec, 64)
+    torch.cuda.synchronize()
+    err = ((o.float() - ref.float()).abs().max() / ref.float().abs().max()).item()
+    # same chunk kernels, the carried state composed by the rank combine instead of the local
+    # prefix: equal to bf16 output rounding
+    assert err < 1e-2, (inst, err)
+    D = q.shape[-1]
+    per = D * D + (D if spec.use_normalizer else 0) + 1
+    assert sp.last_gather_elements() == q.shape[2] * per  # world * B*H*payload
+    for h in range(q.shape[2]):
+        sd = oracle.spec_default(inst)
+        b = None
+        if inst == "mamba2":
+            sd["mamba2_a_raw"] = float(spec.mamba2_a_raw[h])
+            b = gates.b_pre[0, :, h].cpu().numpy()
+        want, _, _ = oracle.lsm_chunked(sd, *(t[0, :, h].float().cpu().numpy() for t in (q, k, v)), b_pre=b)
+        e = norm_rel_err(o[0, :, h].float().cpu().numpy(), want)
+        record_parity("nccl_masked_sp/%s/h%d" % (inst, h), e, 2e-2)
+        assert e < 2e-2
+
+
+def test_nomask_sp_through_nccl(comm1):
+    torch, pk, q, k, v, spec, _ = _inputs("bla")
+    spec = pk.LsmSpec(instance=0, feature_map=0)  # Alg. 1: undecayed, no normaliser (parallel.hpp:286-289)
+    from paper_2503_05447_b200 import sp
+    o = sp.sp_lsm_nomask_rank(comm1, q, k, v, spec)
+    ref = sp.sp_forward_nomask_loopback(q, k, v, spec, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(o, ref)
+    assert sp.last_gather_elements() == q.shape[2] * 128 * 128
+
+
+@pytest.mark.parametrize("inst", ["retnet", "mamba2"])
+def test_sp_backward_through_nccl(comm1, inst):
+    torch, pk, q, k, v, spec, gates = _inputs(inst, N=700)
+    from paper_2503_05447_b200 import sp
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dO = torch.randn(q.shape, device="cuda", generator=g).to(torch.bfloat16)
+    got = sp.sp_lsm_backward_rank(comm1, q, k, v, gates, spec, dO)
+    want = pk.lsm_backward_batched(q, k, v, gates, spec, dO)
+    torch.cuda.synchronize()
+    names = ["dq", "dk", "dv"] + (["db_pre", "da_raw"] if inst == "mamba2" else [])
+    for n in names:
+        a, b = getattr(got, n).float(), getattr(want, n).float()
+        err = ((a - b).abs().max() / b.abs().max().clamp_min(1e-30)).item()
+        assert err < 1e-2, (inst, n, err)
+
+
+def test_attention_sp_through_nccl(comm1):
+    torch = _torch()
+    from paper_2503_05447_b200 import attn, sp
+    g = torch.Generator(device="cuda").manual_seed(9)
+    N, H, D = 1000, 2, 128
+    q, k, v = (torch.randn(1, N, H, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    o = attn.sp_attention_rank(comm1, q, k, v, N)
+    ref = attn.softmax_attention_parallel(q, k, v, True)
+    torch.cuda.synchronize()
+    assert torch.equal(o, ref)
+    assert attn.last_gather_elements() == 2 * N * H * D  # K and V, test_parallel.cpp:195-210
+
+
+def test_nccl_step_in_cuda_graph(comm1):
+    """The bench's timed region replays a CUDA graph of the step: with a communicator the graph
+    holds the ncclAllGather, and the replay reproduces the direct call bit for bit."""
+    torch, pk, q, k, v, spec, gates = _inputs("mamba2", N=4096)
+    from paper_2503_05447_b200 import sp
+    st = torch.cuda.Stream()
+    out = torch.empty_like(q)
+    with torch.cuda.stream(st):
+        direct = sp.sp_lsm_masked_rank(comm1, q, k, v, gates, spec, stream=st.cuda_stream).clone()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=st):
+            sp.sp_lsm_masked_rank(comm1, q, k, v, gates, spec, out=out, stream=st.cuda_stream)
+        out.zero_()
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, direct)
