@@ -344,7 +344,7 @@ int lmoe_nccl_comm_destroy(void* comm);
 size_t lmoe_moe_workspace_size(int T, int hidden, int ffn, int E, int top_k);
 /* route (moe.hpp:58-85) + load_balance_loss (moe.hpp:90-103) on fp32 logits [T, E]:
  * ids [T, k] (ascending per token, ties -> lower id), gates [T, k] renormalised over the
- * selection, probs [T, E] (nullable), counts [E], aux (nullable).  E <= 64, k <= 8. */
+ * selection, probs [T, E] (nullable), counts [E], aux (nullable).  E <= 256, k <= 32. */
 int lmoe_moe_route(const float* logits, int T, int E, int top_k, int* ids, float* gates,
                    float* probs, int* counts, float* aux, void* workspace, size_t workspace_bytes,
                    lmoe_stream_t stream);

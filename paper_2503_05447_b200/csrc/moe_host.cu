@@ -80,14 +80,19 @@ static void route_core(const float* logits, int T, int E, int K, int* ids, float
                        int* counts, float* colsum, cudaStream_t st) {
     LMOE_CUDA_CHECK(cudaMemsetAsync(counts, 0, E * 4, st));
     LMOE_CUDA_CHECK(cudaMemsetAsync(colsum, 0, E * 4, st));
-    lmoe_dev::moe_route<<<std::min((T + 7) / 8, num_sms() * 8), 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
+    const dim3 grid(std::min((T + 7) / 8, num_sms() * 8));
+    if (E <= 32) lmoe_dev::moe_route<1><<<grid, 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
+    else if (E <= 64) lmoe_dev::moe_route<2><<<grid, 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
+    else if (E <= 128) lmoe_dev::moe_route<4><<<grid, 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
+    else lmoe_dev::moe_route<8><<<grid, 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
     LMOE_CUDA_CHECK(cudaGetLastError());
     ++g_launch_count;
 }
 
 static void check_route_args(int T, int E, int K) {
     if (K < 1 || K > E) throw Error(LMOE_ERR_ARG, "route: bad top_k");
-    if (E > 64 || K > 8) throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_moe: device routing supports E <= 64, top_k <= 8");
+    if (E > lmoe_dev::kMoeMaxE || K > lmoe_dev::kMoeMaxK)
+        throw Error(LMOE_ERR_UNSUPPORTED, "lmoe_moe: device routing supports E <= 256, top_k <= 32");
     if (T < 1) throw Error(LMOE_ERR_ARG, "lmoe_moe: need T >= 1");
 }
 
@@ -207,7 +212,8 @@ extern "C" int lmoe_moe_forward(int T, int hidden, int ffn, int E, int top_k, co
         // 4. stable dispatch positions (tokens ascending within each expert)
         lmoe_dev::moe_block_counts<<<w.nblk, 256, 0, st>>>(ids, T, E, top_k, P(w.blk_cnt));
         lmoe_dev::moe_block_scan<<<E, 256, 0, st>>>(P(w.blk_cnt), P(w.offsets), w.nblk, E, P(w.blk_base));
-        lmoe_dev::moe_assign<<<w.nblk, 256, 0, st>>>(ids, T, E, top_k, P(w.blk_base), P(w.slot_pos), P(w.perm_token));
+        if (top_k <= 8) lmoe_dev::moe_assign<8><<<w.nblk, 256, 0, st>>>(ids, T, E, top_k, P(w.blk_base), P(w.slot_pos), P(w.perm_token));
+        else lmoe_dev::moe_assign<32><<<w.nblk, 256, 0, st>>>(ids, T, E, top_k, P(w.blk_base), P(w.slot_pos), P(w.perm_token));
         // 5. permute rows
         lmoe_dev::moe_gather<<<(int)((rows + 7) / 8), 256, 0, st>>>(
             static_cast<const uint4*>(x), P(w.perm_token), (int)rows, hidden / 8,
@@ -232,8 +238,12 @@ extern "C" int lmoe_moe_forward(int T, int hidden, int ffn, int E, int top_k, co
             launch_gemm<256, lmoe_dev::kEpiBF16>(ta, td, td, gp, w.max_tiles, hidden / 256, st);
         }
         // 8. combine in ascending expert order
-        lmoe_dev::moe_combine<<<(T + 7) / 8, 256, 0, st>>>(
-            reinterpret_cast<const __nv_bfloat16*>(ws + w.y_perm), P(w.slot_pos), gates, T, top_k, hidden, y, y_f32);
+        if (top_k <= 8)
+            lmoe_dev::moe_combine<8><<<(T + 7) / 8, 256, 0, st>>>(
+                reinterpret_cast<const __nv_bfloat16*>(ws + w.y_perm), P(w.slot_pos), gates, T, top_k, hidden, y, y_f32);
+        else
+            lmoe_dev::moe_combine<32><<<(T + 7) / 8, 256, 0, st>>>(
+                reinterpret_cast<const __nv_bfloat16*>(ws + w.y_perm), P(w.slot_pos), gates, T, top_k, hidden, y, y_f32);
         LMOE_CUDA_CHECK(cudaGetLastError());
         ++g_launch_count;
     });

@@ -196,102 +196,128 @@ template __global__ void moe_gemm<64, kEpiF32>(const __grid_constant__ CUtensorM
                                                const __grid_constant__ CUtensorMap, GemmParams);
 
 // ====================================================================================
-// Routing: each warp walks tokens (lane owns experts lane and lane + 32, E <= 64); counts
-// and probability column sums stay in registers until one atomic per expert per warp.
+// Routing: each warp walks tokens; lane owns experts lane + 32 i (i < NE, E <= 32 NE);
+// counts and probability column sums stay in registers until one shared-memory atomic per
+// expert per warp, then one global atomic per block and expert.
 // ====================================================================================
+template <int NE>
 __global__ void __launch_bounds__(256) moe_route(const float* __restrict__ logits, int T, int E, int K,
                                                  int* __restrict__ ids, float* __restrict__ gates,
                                                  float* __restrict__ probs, int* __restrict__ counts,
                                                  float* __restrict__ prob_colsum) {
     // per-block expert counts / probability sums: warps reduce into shared memory, and one
-    // global atomic per block and expert follows (per-warp global atomics on the same 64
+    // global atomic per block and expert follows (per-warp global atomics on the same
     // addresses serialised at L2)
-    __shared__ int s_cnt[64];
-    __shared__ float s_ps[64];
-    if (threadIdx.x < 64) { s_cnt[threadIdx.x] = 0; s_ps[threadIdx.x] = 0.f; }
+    __shared__ int s_cnt[32 * NE];
+    __shared__ float s_ps[32 * NE];
+    for (int i = threadIdx.x; i < 32 * NE; i += blockDim.x) { s_cnt[i] = 0; s_ps[i] = 0.f; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int wglobal = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int nwarps = gridDim.x * (blockDim.x / 32);
-    const bool has0 = lane < E, has1 = lane + 32 < E;
     const float NEG = -INFINITY;
-    int cnt0 = 0, cnt1 = 0;
-    float ps0 = 0.f, ps1 = 0.f;
+    bool has[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) has[i] = lane + 32 * i < E;
+    int cnt[NE];
+    float ps[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) { cnt[i] = 0; ps[i] = 0.f; }
+    // logits map to order-preserving unsigned keys (0 = taken / absent)
+    auto key = [](float f) -> unsigned {
+        const unsigned u = __float_as_uint(f + 0.f);  // -0 -> +0: equal logits tie on id
+        return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    };
     for (int t = wglobal; t < T; t += nwarps) {
         const float* l = logits + (size_t)t * E;
-        const float v0 = has0 ? l[lane] : NEG;
-        const float v1 = has1 ? l[lane + 32] : NEG;
+        float v[NE];
+#pragma unroll
+        for (int i = 0; i < NE; ++i) v[i] = has[i] ? l[lane + 32 * i] : NEG;
         // full softmax (tensor.hpp:767-789): max-subtracted over all logits
-        float mx = fmaxf(v0, v1);
+        float mx = v[0];
+#pragma unroll
+        for (int i = 1; i < NE; ++i) mx = fmaxf(mx, v[i]);
 #pragma unroll
         for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-        const float e0 = has0 ? __expf(v0 - mx) : 0.f, e1 = has1 ? __expf(v1 - mx) : 0.f;
-        float zs = e0 + e1;
+        float e[NE];
+        float zs = 0.f;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            e[i] = has[i] ? __expf(v[i] - mx) : 0.f;
+            zs += e[i];
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) zs += __shfl_xor_sync(0xFFFFFFFFu, zs, o);
-        const float p0 = e0 / zs, p1 = e1 / zs;
-        if (probs) {
-            if (has0) probs[(size_t)t * E + lane] = p0;
-            if (has1) probs[(size_t)t * E + lane + 32] = p1;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const float pr = e[i] / zs;
+            if (probs && has[i]) probs[(size_t)t * E + lane + 32 * i] = pr;
+            ps[i] += pr;
         }
-        ps0 += p0;
-        ps1 += p1;
         // top-k by repeated warp argmax: larger logit first, ties -> lower id (moe.hpp:70-75).
-        // Logits map to order-preserving unsigned keys (0 = taken / absent), so each round is
-        // one redux.sync max plus two ballots; the lowest set id among the maxima wins the tie.
-        auto key = [](float f) -> unsigned {
-            const unsigned u = __float_as_uint(f + 0.f);  // -0 -> +0: equal logits tie on id
-            return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-        };
-        const unsigned k0 = has0 ? key(v0) : 0u, k1 = has1 ? key(v1) : 0u;
-        bool sel0 = false, sel1 = false;
+        // Per round: the lane's best untaken candidate (first maximum in ascending id order),
+        // one redux.sync max over the keys, one redux.sync min over the ids holding it.
+        unsigned k[NE];
+        bool sel[NE];
+#pragma unroll
+        for (int i = 0; i < NE; ++i) { k[i] = has[i] ? key(v[i]) : 0u; sel[i] = false; }
         unsigned topk = 0u;
         for (int r = 0; r < K; ++r) {
-            const unsigned c0 = sel0 ? 0u : k0, c1 = sel1 ? 0u : k1;
-            const unsigned best = __reduce_max_sync(0xFFFFFFFFu, c0 > c1 ? c0 : c1);
-            const unsigned b0 = __ballot_sync(0xFFFFFFFFu, c0 == best && c0 != 0u);
-            const unsigned b1 = __ballot_sync(0xFFFFFFFFu, c1 == best && c1 != 0u);
-            const int bi = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
+            unsigned cb = 0u, cid = 0xFFFFFFFFu;
+#pragma unroll
+            for (int i = 0; i < NE; ++i) {
+                const unsigned c = sel[i] ? 0u : k[i];
+                if (c > cb) { cb = c; cid = (unsigned)(lane + 32 * i); }
+            }
+            const unsigned best = __reduce_max_sync(0xFFFFFFFFu, cb);
+            const unsigned bid = __reduce_min_sync(0xFFFFFFFFu, (cb == best && cb != 0u) ? cid : 0xFFFFFFFFu);
             if (r == 0) topk = best;
-            if (bi == lane) sel0 = true;
-            if (bi == lane + 32) sel1 = true;
+#pragma unroll
+            for (int i = 0; i < NE; ++i)
+                if ((unsigned)(lane + 32 * i) == bid) sel[i] = true;
         }
         const float top = __uint_as_float((topk & 0x80000000u) ? (topk & 0x7FFFFFFFu) : ~topk);
         // ascending ids of the selection (moe.hpp:77) + masked softmax (max = top-1 logit)
-        const unsigned m0 = __ballot_sync(0xFFFFFFFFu, sel0), m1 = __ballot_sync(0xFFFFFFFFu, sel1);
-        const float g0 = sel0 ? __expf(v0 - top) : 0.f, g1 = sel1 ? __expf(v1 - top) : 0.f;
-        float gz = g0 + g1;
+        float g[NE];
+        float gz = 0.f;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            g[i] = sel[i] ? __expf(v[i] - top) : 0.f;
+            gz += g[i];
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) gz += __shfl_xor_sync(0xFFFFFFFFu, gz, o);
-        if (sel0) {
-            const int slot = __popc(m0 & ((1u << lane) - 1u));
-            ids[(size_t)t * K + slot] = lane;
-            gates[(size_t)t * K + slot] = g0 / gz;
-            ++cnt0;
-        }
-        if (sel1) {
-            const int slot = __popc(m0) + __popc(m1 & ((1u << lane) - 1u));
-            ids[(size_t)t * K + slot] = lane + 32;
-            gates[(size_t)t * K + slot] = g1 / gz;
-            ++cnt1;
+        int base = 0;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, sel[i]);
+            if (sel[i]) {
+                const int slot = base + __popc(m & ((1u << lane) - 1u));
+                ids[(size_t)t * K + slot] = lane + 32 * i;
+                gates[(size_t)t * K + slot] = g[i] / gz;
+                ++cnt[i];
+            }
+            base += __popc(m);
         }
     }
-    if (has0) {
-        if (cnt0) atomicAdd(&s_cnt[lane], cnt0);
-        atomicAdd(&s_ps[lane], ps0);
-    }
-    if (has1) {
-        if (cnt1) atomicAdd(&s_cnt[lane + 32], cnt1);
-        atomicAdd(&s_ps[lane + 32], ps1);
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+        if (!has[i]) continue;
+        if (cnt[i]) atomicAdd(&s_cnt[lane + 32 * i], cnt[i]);
+        atomicAdd(&s_ps[lane + 32 * i], ps[i]);
     }
     __syncthreads();
-    if (threadIdx.x < E) {
-        if (s_cnt[threadIdx.x]) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
-        if (prob_colsum) atomicAdd(&prob_colsum[threadIdx.x], s_ps[threadIdx.x]);
+    for (int i = threadIdx.x; i < E; i += blockDim.x) {
+        if (s_cnt[i]) atomicAdd(&counts[i], s_cnt[i]);
+        if (prob_colsum) atomicAdd(&prob_colsum[i], s_ps[i]);
     }
 }
+template __global__ void moe_route<1>(const float*, int, int, int, int*, float*, float*, int*, float*);
+template __global__ void moe_route<2>(const float*, int, int, int, int*, float*, float*, int*, float*);
+template __global__ void moe_route<4>(const float*, int, int, int, int*, float*, float*, int*, float*);
+template __global__ void moe_route<8>(const float*, int, int, int, int*, float*, float*, int*, float*);
 
-// offsets / tile list / aux, one block of 256 threads (E <= 64).
+// offsets / tile list / aux, one block of 256 threads (E <= kMoeMaxE).
 // offsets[e] = sum_{e'<e} counts[e']; per group the 128-row GEMM tiles;
 // aux = E * sum_e (counts_e / (T k)) (colsum_e / T)   (moe.hpp:90-103)
 __global__ void __launch_bounds__(256) moe_plan(const int* __restrict__ counts, const float* __restrict__ prob_colsum,
@@ -299,8 +325,8 @@ __global__ void __launch_bounds__(256) moe_plan(const int* __restrict__ counts, 
                                                 int* __restrict__ group_end, int* __restrict__ tile_group,
                                                 int* __restrict__ tile_row0, int* __restrict__ num_tiles,
                                                 float* __restrict__ aux) {
-    __shared__ int s_off[65], s_toff[65];
-    __shared__ double s_aux[64];
+    __shared__ int s_off[kMoeMaxE + 1], s_toff[kMoeMaxE + 1];
+    __shared__ double s_aux[kMoeMaxE];
     const int tid = threadIdx.x;
     if (tid == 0) {
         int off = 0, nt = 0;
@@ -343,8 +369,8 @@ __global__ void __launch_bounds__(256) moe_plan(const int* __restrict__ counts, 
 // the block among earlier tokens routed to e (token-ascending, moe.hpp:137-139).
 __global__ void moe_block_counts(const int* __restrict__ ids, int T, int E, int K,
                                  int* __restrict__ blk_cnt) {
-    __shared__ int c[64];
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) c[i] = 0;
+    __shared__ int c[kMoeMaxE];
+    for (int i = threadIdx.x; i < kMoeMaxE; i += blockDim.x) c[i] = 0;
     __syncthreads();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < T)
@@ -383,27 +409,29 @@ __global__ void __launch_bounds__(256) moe_block_scan(const int* __restrict__ bl
     }
 }
 
+template <int KM>
 __global__ void __launch_bounds__(256) moe_assign(const int* __restrict__ ids, int T, int E, int K,
                                                   const int* __restrict__ blk_base,
                                                   int* __restrict__ slot_pos,
                                                   int* __restrict__ perm_token) {
-    __shared__ int warp_tot[8][64];
-    __shared__ int base[64];
+    __shared__ int warp_tot[8][kMoeMaxE];
+    __shared__ int base[kMoeMaxE];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int t = blockIdx.x * 256 + tid;
-    int my[8];
+    int my[KM];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) my[s] = (s < K && t < T) ? ids[(size_t)t * K + s] : -1;
-    for (int i = tid; i < 64; i += 256) base[i] = i < E ? blk_base[(size_t)blockIdx.x * E + i] : 0;
-    // per expert: rank of this token among earlier tokens of the block routed to e
-    int rank[8];
+    for (int s = 0; s < KM; ++s) my[s] = (s < K && t < T) ? ids[(size_t)t * K + s] : -1;
+    for (int i = tid; i < E; i += 256) base[i] = blk_base[(size_t)blockIdx.x * E + i];
+    // per expert: rank of this token among earlier tokens of the warp routed to e (a token
+    // holds each expert at most once; its ids ascend, so slot search can stop early)
+    int rank[KM];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) rank[s] = 0;
+    for (int s = 0; s < KM; ++s) rank[s] = 0;
     for (int e = 0; e < E; ++e) {
         bool hit = false;
         int hs = 0;
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
+        for (int s = 0; s < KM; ++s)
             if (my[s] == e) { hit = true; hs = s; }
         const unsigned m = __ballot_sync(0xFFFFFFFFu, hit);
         if (lane == 0) warp_tot[w][e] = __popc(m);
@@ -411,7 +439,7 @@ __global__ void __launch_bounds__(256) moe_assign(const int* __restrict__ ids, i
     }
     __syncthreads();
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < KM; ++s) {
         if (my[s] < 0) continue;
         const int e = my[s];
         int before = 0;
@@ -421,6 +449,8 @@ __global__ void __launch_bounds__(256) moe_assign(const int* __restrict__ ids, i
         perm_token[pos] = t;
     }
 }
+template __global__ void moe_assign<8>(const int*, int, int, int, const int*, int*, int*);
+template __global__ void moe_assign<32>(const int*, int, int, int, const int*, int*, int*);
 
 // x_perm[pos] = x[perm_token[pos]]   (one warp per row, 16-byte vectors)
 __global__ void moe_gather(const uint4* __restrict__ x, const int* __restrict__ perm_token,
@@ -433,17 +463,19 @@ __global__ void moe_gather(const uint4* __restrict__ x, const int* __restrict__ 
 }
 
 // y[t] = sum_s gate[t,s] * y_perm[slot_pos[t,s]], slots in ascending expert order
-// (moe.hpp:145-146 accumulates expert by expert).  One warp per token, 8 bf16 per lane-step.
+// (moe.hpp:145-146 accumulates expert by expert).  One warp per token, 8 bf16 per lane-step;
+// the row loads of up to 8 slots are in flight before their ordered accumulation.
+template <int KM>
 __global__ void moe_combine(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__ slot_pos,
                             const float* __restrict__ gates, int T, int K, int hidden,
                             void* __restrict__ y, int y_f32) {
     const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     if (t >= T) return;
     const int lane = threadIdx.x & 31;
-    int pos[8];
-    float g[8];
+    int pos[KM];
+    float g[KM];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < KM; ++s) {
         pos[s] = s < K ? slot_pos[(size_t)t * K + s] : 0;
         g[s] = s < K ? gates[(size_t)t * K + s] : 0.f;
     }
@@ -451,21 +483,25 @@ __global__ void moe_combine(const __nv_bfloat16* __restrict__ y_perm, const int*
         float acc[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-        // all K row loads in flight before the (ordered) accumulation
-        uint4 vv[8];
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
-            vv[s] = s < K ? *reinterpret_cast<const uint4*>(y_perm + (size_t)pos[s] * hidden + c) : make_uint4(0, 0, 0, 0);
+        for (int s0 = 0; s0 < KM; s0 += 8) {
+            if (s0 >= K) break;
+            uint4 vv[8];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-            if (s >= K) break;
-            const uint4 v = vv[s];
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            for (int s = 0; s < 8; ++s)
+                vv[s] = s0 + s < K ? *reinterpret_cast<const uint4*>(y_perm + (size_t)pos[s0 + s] * hidden + c)
+                                   : make_uint4(0, 0, 0, 0);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float2 f = unpack_bf16(w[i]);
-                acc[2 * i] += g[s] * f.x;
-                acc[2 * i + 1] += g[s] * f.y;
+            for (int s = 0; s < 8; ++s) {
+                if (s0 + s >= K) break;
+                const uint4 v = vv[s];
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f = unpack_bf16(w[i]);
+                    acc[2 * i] += g[s0 + s] * f.x;
+                    acc[2 * i + 1] += g[s0 + s] * f.y;
+                }
             }
         }
         if (y_f32) {
@@ -482,5 +518,7 @@ __global__ void moe_combine(const __nv_bfloat16* __restrict__ y_perm, const int*
         }
     }
 }
+template __global__ void moe_combine<8>(const __nv_bfloat16*, const int*, const float*, int, int, int, void*, int);
+template __global__ void moe_combine<32>(const __nv_bfloat16*, const int*, const float*, int, int, int, void*, int);
 
 }  // namespace lmoe_dev

@@ -5,6 +5,9 @@
 namespace lmoe_dev {
 
 enum GemmEpilogue { kEpiBF16 = 0, kEpiSwiGLU = 1, kEpiF32 = 2 };
+// routing / dispatch limits of the device kernels (the reference routes any E, top_k)
+constexpr int kMoeMaxE = 256;
+constexpr int kMoeMaxK = 32;
 constexpr int kGemmThreads = 320;  // TMA, MMA, 8 epilogue warps (two per TMEM lane quarter)
 constexpr int kGemmEpiThreads = kGemmThreads - 64;
 
@@ -37,6 +40,7 @@ __device__ __forceinline__ float silu_f(float x) { return x / (1.f + __expf(-x))
 template <int BN, int EPI>
 __global__ void moe_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                          const __grid_constant__ CUtensorMap tmB1, GemmParams p);
+template <int NE>
 __global__ void moe_route(const float* __restrict__ logits, int T, int E, int K, int* __restrict__ ids,
                           float* __restrict__ gates, float* __restrict__ probs, int* __restrict__ counts,
                           float* __restrict__ prob_colsum);
@@ -47,10 +51,12 @@ __global__ void moe_plan(const int* __restrict__ counts, const float* __restrict
 __global__ void moe_block_counts(const int* __restrict__ ids, int T, int E, int K, int* __restrict__ blk_cnt);
 __global__ void moe_block_scan(const int* __restrict__ blk_cnt, const int* __restrict__ offsets, int nblk,
                                int E, int* __restrict__ blk_base);
+template <int KM>
 __global__ void moe_assign(const int* __restrict__ ids, int T, int E, int K, const int* __restrict__ blk_base,
                            int* __restrict__ slot_pos, int* __restrict__ perm_token);
 __global__ void moe_gather(const uint4* __restrict__ x, const int* __restrict__ perm_token, int rows,
                            int row_vec, uint4* __restrict__ x_perm);
+template <int KM>
 __global__ void moe_combine(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__ slot_pos,
                             const float* __restrict__ gates, int T, int K, int hidden, void* __restrict__ y,
                             int y_f32);

@@ -36,7 +36,11 @@ def test_route_golden_bit_exact():
 
 @pytest.mark.parametrize("T,E,k,kind", [(65536, 64, 8, "normal"), (4096, 64, 8, "ties"),
                                          (3000, 48, 5, "normal"), (1000, 8, 2, "ties"),
-                                         (2000, 64, 8, "signed_zeros")])
+                                         (2000, 64, 8, "signed_zeros"),
+                                         # beyond 64 experts / top-8 (up to the device limits 256 / 32)
+                                         (3000, 128, 16, "normal"), (2000, 256, 32, "ties"),
+                                         (1500, 100, 3, "signed_zeros"), (1000, 200, 12, "normal"),
+                                         (700, 33, 32, "normal")])
 def test_route_random_bit_exact(T, E, k, kind):
     torch = _torch()
     from paper_2503_05447_b200 import moe
@@ -80,7 +84,8 @@ def _expected_rows(x, wg, wu, wd, ids, gates, rows):
 
 
 @pytest.mark.parametrize("T,hidden,ffn,E,k", [(300, 256, 128, 8, 2), (1000, 256, 256, 64, 8),
-                                              (4096, 1024, 896, 64, 8)])
+                                              (4096, 1024, 896, 64, 8), (600, 256, 128, 128, 16),
+                                              (500, 256, 128, 256, 20)])
 def test_moe_forward_vs_oracle(T, hidden, ffn, E, k):
     torch = _torch()
     from paper_2503_05447_b200 import moe
@@ -124,3 +129,14 @@ def test_moe_golden_small_via_oracle_path():
         y, aux, _ = oracle.moe_forward(d[p + "/x"], d[p + "/router"], d[p + "/w_gate"],
                                        d[p + "/w_up"], d[p + "/w_down"], int(d[p + "/top_k"][0]))
         assert np.abs(y - d[p + "/y"]).max() < 1e-13
+
+
+def test_route_limits_error_text():
+    torch = _torch()
+    from paper_2503_05447_b200 import moe
+    import paper_2503_05447_b200 as pk
+    logits = torch.zeros(4, 300, device="cuda")
+    with pytest.raises(pk.LmoeError, match="device routing supports E <= 256, top_k <= 32"):
+        moe.route(logits, 2)
+    with pytest.raises(pk.LmoeError, match="route: bad top_k"):
+        moe.route(logits[:, :8], 9)

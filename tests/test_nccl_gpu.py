@@ -118,10 +118,11 @@ def test_nccl_step_in_cuda_graph(comm1):
     st = torch.cuda.Stream()
     out = torch.empty_like(q)
     with torch.cuda.stream(st):
-        direct = sp.sp_lsm_masked_rank(comm1, q, k, v, gates, spec, stream=st.cuda_stream).clone()
+        # check=False: the device-error readback synchronises the stream, which capture forbids
+        direct = sp.sp_lsm_masked_rank(comm1, q, k, v, gates, spec, check=False, stream=st.cuda_stream).clone()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=st):
-            sp.sp_lsm_masked_rank(comm1, q, k, v, gates, spec, out=out, stream=st.cuda_stream)
+            sp.sp_lsm_masked_rank(comm1, q, k, v, gates, spec, out=out, check=False, stream=st.cuda_stream)
         out.zero_()
         graph.replay()
     torch.cuda.synchronize()
