@@ -258,6 +258,32 @@ int lmoe_lsm_fwd_recurrent(const lmoe_lsm_desc* desc, int B, int N, int H, int D
                            const float* M0, void* o, float* M_out, void* workspace, size_t workspace_bytes,
                            lmoe_stream_t stream);
 
+/* Backward of lmoe_lsm_fwd_recurrent: the tape VJP of recurrent_step (lsm.hpp:335-441) over
+ * the sequence (tensor.hpp:1178-1215) for the same kinds, with loss gradient dO [B, N, H, D]
+ * (dtype) and the optional final-state gradient dM_final [B, H, D, D] fp32.  One CTA per
+ * (b, h): a forward pass saving the state every 32 tokens, then the blocks in reverse (states
+ * recomputed from the checkpoint).  Outputs: dq, dk, dv [B, N, H, D] dtype, the gate /
+ * static-parameter gradients of `grads` (NULL where the kind has no such input; static ones
+ * summed over the batch), dM0 [B, H, D, D] fp32 (may be NULL). */
+typedef struct lmoe_lsm_recurrent_grads {
+    void* da_vec;            /* RWKV7 / Mamba: [B, N, H, D] dtype                        */
+    float* da_scal;          /* DeltaNet / GatedDeltaNet / Titans: [B, N, H]             */
+    float* db_pre;           /* DeltaNet / GatedDeltaNet / TTT / Titans / RWKV7 [B,N,H]  */
+    void* dalpha_pre;        /* GFW / GateLoop: [B, N, H, D] dtype                       */
+    void* dbeta_pre;         /* GFW / GateLoop: [B, N, H, D] dtype                       */
+    float* ds4_delta_raw;    /* S4: [H, D]                                               */
+    float* ds4_b;            /* S4: [H, D]                                               */
+    float* ds4_A_raw;        /* S4: [H, D, D]                                            */
+    float* dmamba_A_raw;     /* Mamba: [H, D, D]                                         */
+} lmoe_lsm_recurrent_grads;
+size_t lmoe_lsm_bwd_recurrent_workspace_size(const lmoe_lsm_desc* desc, int B, int N, int H, int D,
+                                             lmoe_dtype dtype);
+int lmoe_lsm_bwd_recurrent(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype,
+                           const void* q, const void* k, const void* v, const lmoe_lsm_recurrent_inputs* in,
+                           const float* M0, const void* dO, const float* dM_final, void* dq, void* dk,
+                           void* dv, const lmoe_lsm_recurrent_grads* grads, float* dM0, void* workspace,
+                           size_t workspace_bytes, lmoe_stream_t stream);
+
 /* Forward plan of lmoe_lsm_fwd for a shape: info[0] = 1 when the single-read persistent
  * kernel runs (bf16 / D = 128 scalar-decay kinds without normaliser; one launch), 0 for the
  * segment-parallel state pass + combine + output pass; info[1] segments per (b,h),

@@ -276,6 +276,56 @@ void golden_lsm_grad() {
     }
 }
 
+// ---- gradients of the recurrent kinds from the reference tape (tensor.hpp:1178) over
+// recurrent_step (lsm.hpp:335-441): every input and static parameter requires grad ----
+void golden_lsm_rec_grad() {
+    struct SV { const char* tag; LsmInstance inst; };
+    const SV kinds[] = {{"deltanet", LsmInstance::DeltaNet}, {"gated_deltanet", LsmInstance::GatedDeltaNet},
+                        {"gfw", LsmInstance::GFW}, {"gateloop", LsmInstance::GateLoop}, {"ttt", LsmInstance::TTT},
+                        {"titans", LsmInstance::Titans}, {"rwkv7", LsmInstance::RWKV7}, {"s4", LsmInstance::S4},
+                        {"mamba", LsmInstance::Mamba}};
+    int vi = 0;
+    for (const SV& sv : kinds) {
+        const int n = 37, d = 4;
+        Rng rng(31000 + 17 * vi);
+        LsmSpec spec = LsmSpec::make(sv.inst, d, d, &rng);
+        for (Tensor* t : {&spec.s4_delta_raw, &spec.s4_b, &spec.s4_A_raw, &spec.mamba_A_raw})
+            if (t->defined()) t->set_requires_grad(true);
+        Tensor q = Tensor::randn({n, d}, rng, 0.5, DType::f64, true);
+        Tensor k = Tensor::randn({n, d}, rng, 0.5, DType::f64, true);
+        Tensor v = Tensor::randn({n, d}, rng, 0.5, DType::f64, true);
+        LsmGates g = LsmGates::random_for(spec, n, rng);
+        for (Tensor* t : {&g.a_pre, &g.b_pre, &g.alpha_pre, &g.beta_pre})
+            if (t->defined()) t->set_requires_grad(true);
+        const Tensor w = Tensor::randn({n, d}, rng, 1.0);
+        const Tensor o = lsm_forward_chunked(q, k, v, g, spec, 8);
+        backward(sum(mul(o, w)));
+        const std::string p = std::string("lsm_rec_grad/") + sv.tag;
+        emit_spec(p, spec);
+        emit(p + "/q", q);
+        emit(p + "/k", k);
+        emit(p + "/v", v);
+        emit(p + "/dO", w);
+        emit(p + "/o", o);
+        auto grad_of = [&](const Tensor& t) {
+            return t.has_grad() ? t.grad() : std::vector<double>(t.size(), 0.0);
+        };
+        emit(p + "/dq", {n, d}, grad_of(q));
+        emit(p + "/dk", {n, d}, grad_of(k));
+        emit(p + "/dv", {n, d}, grad_of(v));
+        const char* names[] = {"a_pre", "b_pre", "alpha_pre", "beta_pre", "s4_delta_raw", "s4_b", "s4_A_raw",
+                               "mamba_A_raw"};
+        const Tensor* ts[] = {&g.a_pre, &g.b_pre, &g.alpha_pre, &g.beta_pre, &spec.s4_delta_raw, &spec.s4_b,
+                              &spec.s4_A_raw, &spec.mamba_A_raw};
+        for (int i = 0; i < 8; ++i) {
+            if (!ts[i]->defined()) continue;
+            emit(p + "/" + names[i], *ts[i]);
+            emit(p + "/d" + names[i], ts[i]->shape(), grad_of(*ts[i]));
+        }
+        ++vi;
+    }
+}
+
 // ---- routing (moe.hpp:58-103), KATs of test_moe.cpp:9-62 plus random ----
 void golden_route() {
     NoGradGuard ng;
@@ -518,6 +568,7 @@ int cmd_golden(const char* path) {
     golden_lsm_seq();
     golden_lsm_device();
     golden_lsm_grad();
+    golden_lsm_rec_grad();
     golden_route();
     golden_moe();
     golden_sp();

@@ -116,6 +116,8 @@ struct VecBwdParams {
     int out_f32;                          // dq / dk as fp32 d phi(q) / d keff (feature-map chain rule)
     int* err;                             // [2]: half-chunk decay span out of the fp32 range
     unsigned long long* trace;            // optional clock64 phase trace of one CTA [16 x 16]
+    int pf_ahead;                         // lsm_vec_bwd_chunk: L2-prefetch the tiles of the CTA
+                                          // this many launch slots ahead (one wave; 0 = off)
 };
 cudaError_t launch_vec_carry(bool hgrn2, bool rev, dim3 grid, cudaStream_t st, const CUtensorMap& x1,
                              const CUtensorMap& x2, const CUtensorMap& a, const VecBwdParams& p);

@@ -374,6 +374,27 @@ __global__ void __launch_bounds__(kVbThreads, 1)
             mbar_expect_tx(mx_full, 2 * kTileBytes);
 #pragma unroll
             for (int blk = 0; blk < 2; ++blk) tma_load_2d(Xt + blk * kBlockBytes, &tmX, mx_full, blk * 64, xrow);
+            // warm L2 with the tiles of the CTA one wave ahead (one CTA per SM, linear launch
+            // order): its loads then come from L2 while this SM computes (as lsm_mamba_dgate)
+            if (p.pf_ahead > 0) {
+                const long long lin = ci + (long long)gridDim.x * (h + (long long)gridDim.y * b) + p.pf_ahead;
+                if (lin < (long long)gridDim.x * gridDim.y * gridDim.z) {
+                    const int c2 = (int)(lin % gridDim.x), bh2 = (int)(lin / gridDim.x);
+                    const int h2 = bh2 % p.H, b2 = bh2 / p.H, t2 = c2 * kC;
+                    const int mrow2 = (bh2 * (p.nchunk + 1) + c2) * D, xrow2 = mrow2 + D;
+#pragma unroll
+                    for (int blk = 0; blk < 2; ++blk) {
+                        const int c0 = blk * 64;
+                        tma_prefetch_l2_4d(&tmA, c0, h2, t2, b2);
+                        tma_prefetch_l2_4d(&tmQ, c0, h2, t2, b2);
+                        tma_prefetch_l2_4d(&tmK, c0, h2, t2, b2);
+                        tma_prefetch_l2_4d(&tmV, c0, h2, t2, b2);
+                        tma_prefetch_l2_4d(&tmDO, c0, h2, t2, b2);
+                        tma_prefetch_l2_2d(&tmM, c0, mrow2);
+                        tma_prefetch_l2_2d(&tmX, c0, xrow2);
+                    }
+                }
+            }
             mbar_wait(scan_done, 0);  // the scan scratch in the M region is dead
             vb_mark(p, 0, 1);
 #pragma unroll

@@ -204,6 +204,13 @@ class LsmGrads:
     db_pre: Optional[torch.Tensor] = None
     da_raw: Optional[torch.Tensor] = None
     dM0: Optional[torch.Tensor] = None
+    # recurrent kinds (lsm_backward_recurrent): GFW / GateLoop gates, S4 / Mamba static parameters
+    dalpha_pre: Optional[torch.Tensor] = None
+    dbeta_pre: Optional[torch.Tensor] = None
+    ds4_delta_raw: Optional[torch.Tensor] = None
+    ds4_b: Optional[torch.Tensor] = None
+    ds4_A_raw: Optional[torch.Tensor] = None
+    dmamba_A_raw: Optional[torch.Tensor] = None
 
 
 def _mamba_a_raw(spec, H, device):
@@ -402,3 +409,73 @@ def lsm_forward_recurrent(q, k, v, gates, spec, initial_state=None, final_state=
     if final_state is not None:
         final_state.M, final_state.z, final_state.step = M_out, None, N
     return o
+
+
+class _RecGrads(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("da_vec", "da_scal", "db_pre", "dalpha_pre", "dbeta_pre",
+                                                "ds4_delta_raw", "ds4_b", "ds4_A_raw", "dmamba_A_raw")]
+
+
+def lsm_backward_recurrent(q, k, v, gates, spec, dO, initial_state=None, dM_final=None, check=True, stream=None):
+    """Gradients of lsm_forward_recurrent (the reference tape over recurrent_step, lsm.hpp:335-441)
+    for DeltaNet, GatedDeltaNet, GFW, GateLoop, TTT, Titans, RWKV7, S4, Mamba
+    (lmoe_lsm_bwd_recurrent).  Returns LsmGrads: dq, dk, dv, the gate gradients that apply
+    (da_pre, db_pre, dalpha_pre, dbeta_pre), the static ones (ds4_*, dmamba_A_raw; summed over
+    the batch) and dM0."""
+    B, N, H, D = q.shape
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    L = _lib.lib()
+    if not getattr(L, "_recb_bound", False):
+        L.lmoe_lsm_bwd_recurrent_workspace_size.restype = ctypes.c_size_t
+        L.lmoe_lsm_bwd_recurrent_workspace_size.argtypes = [ctypes.POINTER(_lib.LsmDesc)] + [ctypes.c_int] * 5
+        L.lmoe_lsm_bwd_recurrent.restype = ctypes.c_int
+        L.lmoe_lsm_bwd_recurrent.argtypes = ([ctypes.POINTER(_lib.LsmDesc)] + [ctypes.c_int] * 5
+                                             + [ctypes.c_void_p] * 13 + [ctypes.c_size_t, ctypes.c_void_p])
+        L._recb_bound = True
+    keep = []
+
+    def ptr(t, dtype=None):
+        if t is None:
+            return None
+        t = t.to(dtype or t.dtype).contiguous()
+        keep.append(t)
+        return t.data_ptr()
+
+    dev = q.device
+    g = gates or LsmGates()
+    inst = spec.instance
+    vec_a = inst in (LsmInstance.RWKV7, LsmInstance.MAMBA)
+    rin = _RecInputs(a_vec=ptr(g.a_pre, q.dtype) if vec_a else None,
+                     a_scal=None if vec_a else ptr(g.a_pre, torch.float32),
+                     b_pre=ptr(g.b_pre, torch.float32), alpha_pre=ptr(g.alpha_pre, q.dtype),
+                     beta_pre=ptr(g.beta_pre, q.dtype), s4_delta_raw=ptr(spec.s4_delta_raw, torch.float32),
+                     s4_b=ptr(spec.s4_b, torch.float32), s4_A_raw=ptr(spec.s4_A_raw, torch.float32),
+                     mamba_A_raw=ptr(spec.mamba_A_raw, torch.float32))
+    gr = LsmGrads(dq=torch.empty_like(q), dk=torch.empty_like(k), dv=torch.empty_like(v))
+    gr.dM0 = torch.empty(B, H, D, D, dtype=torch.float32, device=dev)
+    if g.a_pre is not None:
+        gr.da_pre = torch.empty(g.a_pre.shape, dtype=q.dtype if vec_a else torch.float32, device=dev)
+    if g.b_pre is not None:
+        gr.db_pre = torch.empty(g.b_pre.shape, dtype=torch.float32, device=dev)
+    if g.alpha_pre is not None:
+        gr.dalpha_pre = torch.empty(g.alpha_pre.shape, dtype=q.dtype, device=dev)
+        gr.dbeta_pre = torch.empty(g.beta_pre.shape, dtype=q.dtype, device=dev)
+    for name in ("s4_delta_raw", "s4_b", "s4_A_raw", "mamba_A_raw"):
+        t = getattr(spec, name)
+        if t is not None:
+            setattr(gr, "d" + name, torch.empty(t.shape, dtype=torch.float32, device=dev))
+    P = lambda t: None if t is None else t.data_ptr()
+    rg = _RecGrads(da_vec=P(gr.da_pre) if vec_a else None, da_scal=None if vec_a else P(gr.da_pre),
+                   db_pre=P(gr.db_pre), dalpha_pre=P(gr.dalpha_pre), dbeta_pre=P(gr.dbeta_pre),
+                   ds4_delta_raw=P(gr.ds4_delta_raw), ds4_b=P(gr.ds4_b), ds4_A_raw=P(gr.ds4_A_raw),
+                   dmamba_A_raw=P(gr.dmamba_A_raw))
+    M0 = None if initial_state is None else ptr(initial_state.M, torch.float32)
+    dMf = None if dM_final is None else ptr(dM_final, torch.float32)
+    desc = make_desc(spec, 64, check)
+    ws = _workspace(L.lmoe_lsm_bwd_recurrent_workspace_size(ctypes.byref(desc), B, N, H, D, _DTYPES[q.dtype]), dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    _lib.check(L.lmoe_lsm_bwd_recurrent(ctypes.byref(desc), B, N, H, D, _DTYPES[q.dtype], q.data_ptr(), k.data_ptr(),
+                                        v.data_ptr(), ctypes.byref(rin), M0, ptr(dO, q.dtype), dMf,
+                                        gr.dq.data_ptr(), gr.dk.data_ptr(), gr.dv.data_ptr(), ctypes.byref(rg),
+                                        gr.dM0.data_ptr(), ws.data_ptr(), ws.numel(), ctypes.c_void_p(st)))
+    return gr

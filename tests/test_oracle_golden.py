@@ -270,3 +270,36 @@ def test_recurrent_kinds_match_reference():
         assert np.abs(g("o_c8") - g("o_seq")).max() < 1e-10, p  # chunked == sequential (reference)
         ran += 1
     assert ran == 18
+
+
+REC_INPUTS = ("a_pre", "b_pre", "alpha_pre", "beta_pre", "s4_delta_raw", "s4_b", "s4_A_raw", "mamba_A_raw")
+
+
+def rec_loss(d, p, x, w, Mw=None):
+    """sum(o * w) [+ sum(M_N * Mw)] of the f64 oracle recurrence (lmo_lsm_recurrent) at inputs x."""
+    sd = oracle.spec_from_golden(d, p)
+    o, M = oracle.lsm_recurrent(sd, x["q"], x["k"], x["v"], *(x.get(n) for n in REC_INPUTS), M0=x.get("M0"))
+    return float((o * w).sum() + (0.0 if Mw is None else (M * Mw).sum()))
+
+
+def test_recurrent_kinds_tape_gradients_pin_the_oracle():
+    """The reference tape's gradients of the nine recurrent kinds (tests/golden/lsm_rec_grad.npz,
+    tensor.hpp:1178 over recurrent_step lsm.hpp:335-441) equal central differences of the f64
+    oracle recurrence along random directions -- the check the GPU backward tests then use at
+    sizes the tape cannot reach (tensor.hpp:1222-1240 is the reference's own FD oracle)."""
+    d = load_golden("lsm_rec_grad")
+    rng = np.random.default_rng(5)
+    for p in golden_cases(d):
+        x = {n: d[p + "/" + n] for n in ("q", "k", "v") + REC_INPUTS if p + "/" + n in d}
+        w = d[p + "/dO"]
+        for name in x:
+            g = d[p + "/d" + name]
+            for _ in range(2):
+                u = rng.normal(0, 1, x[name].shape)
+                eps = 1e-5
+                xp, xm = dict(x), dict(x)
+                xp[name] = x[name] + eps * u
+                xm[name] = x[name] - eps * u
+                fd = (rec_loss(d, p, xp, w) - rec_loss(d, p, xm, w)) / (2 * eps)
+                an = float((g * u).sum())
+                assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)), (p, name, fd, an)
