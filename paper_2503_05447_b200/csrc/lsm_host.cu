@@ -898,7 +898,7 @@ static void vec_backward(const lmoe_lsm_desc& dd, const BwdPlan& w, int B, int N
                                 c.tmap<bf>(da)};
     if (hg && !out_f32)  // HGRN2's effective key 1 - sigmoid(a) ignores k
         LMOE_CUDA_CHECK(cudaMemsetAsync(dk, 0, (size_t)B * N * H * D * sizeof(bf), st));
-    vp.pf_ahead = env_int("LMOE_VB_PF", 1) * num_sms();  // developer A/B knob: 0 = no L2 prefetch
+    vp.pf_ahead = env_int("LMOE_VB_PF", 0) * num_sms();  // developer A/B knob (measured: no gain, off)
     LMOE_CUDA_CHECK(lmoe_dev::launch_vec_bwd_chunk(hg, dim3(nchunk, H, B), st, tm, vp));
     g_launch_count += 3;
     c.check_err();

@@ -507,13 +507,21 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
 #pragma unroll
                 for (int j = 0; j < L::EPC; ++j) zc[j] = 0.f;
                 bool bad = false;
-                // one row of q~ / k~ with the current factors
-                auto xform_row = [&](int ii, const float (&Ef)[L::EPC], const float (&Eif)[L::EPC]) {
+                // one row of q~ / k~ with the current factors.  The next row's chunks are loaded
+                // before this row's stores (rows walk in order): with load / transform / store per
+                // row, every load waited for the previous row's stores (possible aliasing)
+                auto ld_row = [&](int ii, uint4& uq, uint4& uk) {
+                    const int i = rg * L::R + ii;
+                    uq = ld_chunk_raw(qt, i, cg);
+                    uk = ld_chunk_raw(kt, i, cg);
+                };
+                auto xform_row = [&](int ii, const uint4& uq, const uint4& uk, const float (&Ef)[L::EPC],
+                                     const float (&Eif)[L::EPC]) {
                     const int i = rg * L::R + ii;
                     const float vm = i < nvalid ? 1.f : 0.f;
                     float xq[L::EPC], xk[L::EPC];
-                    ld_chunk<T>(qt, i, cg, xq);
-                    ld_chunk<T>(kt, i, cg, xk);
+                    unpack_chunk<T>(uq, xq);
+                    unpack_chunk<T>(uk, xk);
 #pragma unroll
                     for (int j = 0; j < L::EPC; ++j) {
                         const float keff = HG ? xk[j] : fmap_t<FM>(xk[j]);
@@ -535,22 +543,33 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
                 };
                 // range of the midpoint split (|G - r| < 80, as the log-space check): the extreme
                 // factors are the first row (lower half) and the last row (upper half)
+                uint4 cq, ck;
                 if (lower) {  // warp-uniform: half-warps share a row group pair
+                    ld_row(L::R - 1, cq, ck);
 #pragma unroll
                     for (int kk = 0; kk < L::R; ++kk) {
                         const int ii = L::R - 1 - kk;  // exclusive suffix: walk upwards
-                        xform_row(ii, E, Ei);
+                        uint4 nq = cq, nk = ck;
+                        if (kk + 1 < L::R) ld_row(ii - 1, nq, nk);
+                        xform_row(ii, cq, ck, E, Ei);
+                        cq = nq;
+                        ck = nk;
 #pragma unroll
                         for (int j = 0; j < L::EPC; ++j) { E[j] *= isg[ii][j]; Ei[j] *= sg[ii][j]; }
                     }
 #pragma unroll
                     for (int j = 0; j < L::EPC; ++j) bad |= !(E[j] * sg[0][j] < 5.54e34f);
                 } else {
+                    ld_row(0, cq, ck);
 #pragma unroll
                     for (int ii = 0; ii < L::R; ++ii) {  // inclusive prefix: walk downwards
+                        uint4 nq = cq, nk = ck;
+                        if (ii + 1 < L::R) ld_row(ii + 1, nq, nk);
 #pragma unroll
                         for (int j = 0; j < L::EPC; ++j) { E[j] *= sg[ii][j]; Ei[j] *= isg[ii][j]; }
-                        xform_row(ii, E, Ei);
+                        xform_row(ii, cq, ck, E, Ei);
+                        cq = nq;
+                        ck = nk;
                     }
 #pragma unroll
                     for (int j = 0; j < L::EPC; ++j) bad |= !(E[j] > 1.81e-35f);

@@ -46,6 +46,26 @@ struct VecLayout {
     static constexpr int R = kC / RG;               // rows per thread (8 at NT = 256)
 };
 
+// the raw 16-byte chunk (row, cg) of a two-block SW128 tile, and its EPC values
+__device__ __forceinline__ uint4 ld_chunk_raw(const uint8_t* tile, int row, int cg) {
+    return *reinterpret_cast<const uint4*>(tile + (cg >> 3) * kBlockBytes + sw128_off(row, cg & 7));
+}
+template <typename T>
+__device__ __forceinline__ void unpack_chunk(const uint4& u, float (&x)[TileTraits<T>::EPC]) {
+    if constexpr (sizeof(T) == 2) {
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = unpack_bf16(w[i]);
+            x[2 * i] = f.x;
+            x[2 * i + 1] = f.y;
+        }
+    } else {
+        x[0] = __uint_as_float(u.x); x[1] = __uint_as_float(u.y);
+        x[2] = __uint_as_float(u.z); x[3] = __uint_as_float(u.w);
+    }
+}
+
 // EPC consecutive values of (row, chunk cg) of a two-block SW128 tile
 template <typename T>
 __device__ __forceinline__ void ld_chunk(const uint8_t* tile, int row, int cg, float (&x)[TileTraits<T>::EPC]) {
