@@ -283,7 +283,7 @@ def backward_bench(dev, steps=3, warmup=2):
                          "note": "algorithmic bytes of the op / step time (three chunk passes + gate kernel)"}}
 
 
-OUTPASS_NCU = "profiles/r1_lsm_output_pass.ncu.txt"
+OUTPASS_NCU = "profiles/r2_lsm_output_pass.ncu.txt"
 FUSED_NCU = "profiles/r2_lsm_fused_fwd.ncu.txt"
 
 
