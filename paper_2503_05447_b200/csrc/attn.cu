@@ -27,6 +27,7 @@
 namespace lmoe_dev {
 
 constexpr int kAttnThreads = 256;
+constexpr int kAttnKV = 3;  // K/V pipeline stages
 constexpr float kRescaleLog2 = 8.f;
 
 __device__ __forceinline__ float ex2(float x) {
@@ -48,15 +49,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     constexpr int D = 128, EPB = 64;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* qt = smem;                       // 32 KB
-    uint8_t* kv = smem + kTileBytes;          // 2 stages x [K | V] = 128 KB
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 5 * kTileBytes);
+    // kAttnKV stages x [K | V] (64 KB each): the load of tile j + kAttnKV starts when PV_j
+    // completes, so with three stages it has one more tile time to come from L2 than with two
+    uint8_t* kv = smem + kTileBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (1 + 2 * kAttnKV) * kTileBytes);
     uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;   // [2]
-    uint64_t* kv_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;    // [2]
-    uint64_t* p_full = bars + 7;    // [2]
-    uint64_t* o_done = bars + 9;
-    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* kv_full = bars + 1;             // [kAttnKV]
+    uint64_t* kv_empty = bars + 1 + kAttnKV;  // [kAttnKV]
+    uint64_t* s_full = bars + 1 + 2 * kAttnKV;  // [2]
+    uint64_t* p_full = s_full + 2;              // [2]
+    uint64_t* o_done = p_full + 2;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(o_done + 1);
 
     const int ntq = (p.Nq + kC - 1) / kC;
     const int qtile = ntq - 1 - blockIdx.x;  // heavy (late) tiles first
@@ -68,9 +71,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kAttnKV; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 128);
         }
@@ -91,8 +96,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             tma_load_4d(qt, &tmQ, q_full, 0, h, q0, b);
             tma_load_4d(qt + kBlockBytes, &tmQ, q_full, EPB, h, q0, b);
             for (int j = 0; j < nkv; ++j) {
-                const int s = j & 1;
-                if (j >= 2) mbar_wait(&kv_empty[s], ((j >> 1) - 1) & 1);
+                const int s = j % kAttnKV;
+                if (j >= kAttnKV) mbar_wait(&kv_empty[s], ((j / kAttnKV) - 1) & 1);
                 uint8_t* kt = kv + s * 2 * kTileBytes;
                 uint8_t* vt = kt + kTileBytes;
                 mbar_expect_tx(&kv_full[s], 2 * kTileBytes);
@@ -108,29 +113,29 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             constexpr uint32_t idPV = umma_idesc(1, 0, 1, 128, D);
             const uint32_t qa = smem_u32(qt);
             auto issue_S = [&](int j) {
-                const int s = j & 1;
-                mbar_wait(&kv_full[s], (j >> 1) & 1);
+                const int s = j % kAttnKV, sb = j & 1;  // K/V stage, S buffer
+                mbar_wait(&kv_full[s], (j / kAttnKV) & 1);
                 tc_fence_after();
                 const uint32_t kt = smem_u32(kv + s * 2 * kTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint32_t off = (kk >> 2) * kBlockBytes + (kk & 3) * 32;
-                    mma_ss_f16(tmem + s * 128, umma_desc_sw128(qa + off, 16, 1024),
+                    mma_ss_f16(tmem + sb * 128, umma_desc_sw128(qa + off, 16, 1024),
                                umma_desc_sw128(kt + off, 16, 1024), idS, kk > 0);
                 }
-                mma_commit(&s_full[s]);
+                mma_commit(&s_full[sb]);
             };
             mbar_wait(q_full, 0);
             issue_S(0);
             for (int j = 0; j < nkv; ++j) {
-                const int s = j & 1;
+                const int s = j % kAttnKV, sb = j & 1;
                 if (j + 1 < nkv) issue_S(j + 1);
-                mbar_wait(&p_full[s], (j >> 1) & 1);
+                mbar_wait(&p_full[sb], (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t vt = smem_u32(kv + s * 2 * kTileBytes + kTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_ts_f16(tO, tmem + s * 128 + kk * 8,
+                    mma_ts_f16(tO, tmem + sb * 128 + kk * 8,
                                umma_desc_sw128(vt + kk * 16 * 128, kBlockBytes, 1024), idPV, (j > 0 || kk > 0));
                 mma_commit(&kv_empty[s]);
                 mma_commit(o_done);
@@ -146,15 +151,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             const int s = j & 1;
             mbar_wait(&s_full[s], (j >> 1) & 1);
             tc_fence_after();
+            // the row's 128 scores: all four TMEM loads in flight before one wait
+            uint32_t u[128];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb)
+                tmem_ld32(tmem + s * 128 + lo + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(u + cb * 32));
+            tmem_wait_ld();
             float x[128];
 #pragma unroll
-            for (int cb = 0; cb < 4; ++cb) {
-                uint32_t u[32];
-                tmem_ld32(tmem + s * 128 + lo + cb * 32, u);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) x[cb * 32 + i] = __uint_as_float(u[i]) * p.scale_log2;
-            }
+            for (int i = 0; i < 128; ++i) x[i] = __uint_as_float(u[i]) * p.scale_log2;
             const int k0 = j * kC;
             const bool full = k0 + kC - 1 <= p.row_offset + q0 && k0 + kC <= p.Nk;  // no masking
             if (!full) {
@@ -162,9 +167,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 for (int i = 0; i < 128; ++i)
                     if (k0 + i > grow || k0 + i >= p.Nk) x[i] = -INFINITY;
             }
-            float mx = -INFINITY;
+            // row max over 8 independent accumulators (a single chain is 128 dependent FMNMX)
+            float mx8[8];
 #pragma unroll
-            for (int i = 0; i < 128; ++i) mx = fmaxf(mx, x[i]);
+            for (int a = 0; a < 8; ++a) mx8[a] = x[a];
+#pragma unroll
+            for (int i = 8; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], x[i]);
+#pragma unroll
+            for (int a = 4; a > 0; a >>= 1)
+#pragma unroll
+                for (int c = 0; c < a; ++c) mx8[c] = fmaxf(mx8[c], mx8[c + a]);
+            const float mx = mx8[0];
             const float m_new = fmaxf(m, mx);
             const bool grow_max = m_new > m + kRescaleLog2;  // includes the first tile (m = -inf)
             if (__any_sync(0xFFFFFFFFu, grow_max && j > 0)) {
@@ -185,19 +198,26 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             }
             if (grow_max) m = m_new;
             // P (bf16, packed in pairs) over the first 64 columns of S_j, 32 keys at a time
-            float ls = 0.f;
+            float ls8[8];  // row sum over 8 independent accumulators
+#pragma unroll
+            for (int a = 0; a < 8; ++a) ls8[a] = 0.f;
 #pragma unroll
             for (int cb = 0; cb < 4; ++cb) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const float a = ex2(x[cb * 32 + 2 * i] - m), c2 = ex2(x[cb * 32 + 2 * i + 1] - m);
-                    ls += a + c2;
+                    ls8[(2 * i) & 7] += a;
+                    ls8[(2 * i + 1) & 7] += c2;
                     pk[i] = pack_bf16(a, c2);
                 }
                 tmem_st16(tmem + s * 128 + lo + cb * 16, pk);
             }
-            l += ls;
+#pragma unroll
+            for (int a = 4; a > 0; a >>= 1)
+#pragma unroll
+                for (int c = 0; c < a; ++c) ls8[c] += ls8[c + a];
+            l += ls8[0];
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&p_full[s]);
@@ -269,7 +289,7 @@ static void attn_launch(int B, int Nq, int Nk, int H, int D, int row_offset, con
     const CUtensorMap tk = make_tmap_4d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
     const CUtensorMap tv = make_tmap_4d(v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
     AttnParams p{Nq, Nk, H, row_offset, 1.4426950408889634f / sqrtf((float)D), static_cast<__nv_bfloat16*>(o)};
-    constexpr int smem = 5 * kTileBytes + 256;
+    constexpr int smem = (1 + 2 * kAttnKV) * kTileBytes + 256;
     LMOE_CUDA_CHECK(lmoe_dev::ensure_smem((const void*)attn_fwd_kernel, smem));
     attn_fwd_kernel<<<dim3((Nq + kC - 1) / kC, H, B), kAttnThreads, smem, st>>>(tq, tk, tv, p);
     LMOE_CUDA_CHECK(cudaGetLastError());

@@ -1,8 +1,11 @@
 """Per-rank step time of the cfg3 SP forward at the slice lengths of T = 1, 2, 4, 8 ranks
-(world 1 on one GPU: everything but the all-gather), to bound strong-scaling efficiency.
-The Mamba2 per-head decays are the same at every T (the slice length would otherwise shift
-the random stream).  LMOE_SP_FORCE keeps the multi-rank phase structure at world 1 (a device
-copy stands in for the all-gather); the T = 1 baseline is the local path bench.py times."""
+(one GPU), to bound strong-scaling efficiency.  The Mamba2 per-head decays are the same at
+every T (the slice length would otherwise shift the random stream).  For T > 1 the step runs
+through a real 1-rank NCCL communicator: the multi-rank phase structure with its
+ncclAllGather (of this rank's payload only); the T = 1 baseline is the local path bench.py
+times.  The projection adds the gather of the other T - 1 ranks' payloads (B*H*(D*D + 1) fp32
+each) at the measured NVLink peer-copy bandwidth (770 GB/s, B200_PROFILING.md) plus a 10 us
+collective latency."""
 import os
 
 import torch
@@ -11,10 +14,11 @@ import paper_2503_05447_b200 as pk
 from paper_2503_05447_b200 import sp
 
 H, D = 16, 128
-comm = sp.NcclComm(0, 1)
+comm = sp.NcclComm(0, 1, single_rank_nccl=True)
+local = sp.NcclComm(0, 1)
+PAYLOAD = H * (D * D + 1) * 4
 for inst in ("mamba2", "gla"):
     base = None
-    os.environ.pop("LMOE_SP_FORCE", None)
     for T in (1, 2, 4, 8):
         n = 262144 // T
         g = torch.Generator(device="cuda").manual_seed(0)
@@ -26,17 +30,16 @@ for inst in ("mamba2", "gla"):
             gates = pk.LsmGates(b_pre=torch.randn(1, n, H, device="cuda", generator=g))
         else:
             gates = pk.LsmGates(a_pre=torch.randn(1, n, H, D, device="cuda", generator=g).bfloat16())
-        if T > 1:
-            os.environ["LMOE_SP_FORCE"] = "1"
+        cm = comm if T > 1 else local
         # graph replay, as bench.py times the step
         st = torch.cuda.Stream()
         out = torch.empty_like(q)
         with torch.cuda.stream(st):
             for _ in range(3):
-                sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False, stream=st.cuda_stream)
+                sp.sp_lsm_masked_rank(cm, q, k, v, gates, spec, 64, out=out, check=False, stream=st.cuda_stream)
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=st):
-                sp.sp_lsm_masked_rank(comm, q, k, v, gates, spec, 64, out=out, check=False, stream=st.cuda_stream)
+                sp.sp_lsm_masked_rank(cm, q, k, v, gates, spec, 64, out=out, check=False, stream=st.cuda_stream)
             graph.replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -47,5 +50,7 @@ for inst in ("mamba2", "gla"):
             torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 50
         base = base or ms
-        print("%s T=%d slice=%d: %.3f ms per rank step (graph); ideal %.3f; efficiency bound %.1f%%"
-              % (inst, T, n, ms, base / T, 100 * base / (T * ms)))
+        gather_ms = 0.0 if T == 1 else ((T - 1) * PAYLOAD / 770e9 + 10e-6) * 1e3
+        print("%s T=%d slice=%d: %.3f ms per rank step (graph, NCCL 1-rank); + modelled gather %.3f ms; "
+              "ideal %.3f; efficiency bound %.1f%%, with the gather %.1f%%"
+              % (inst, T, n, ms, gather_ms, base / T, 100 * base / (T * ms), 100 * base / (T * (ms + gather_ms))))
