@@ -808,7 +808,7 @@ namespace lmoe_host {
 struct BwdPlan {
     LsmPlan pl;
     size_t off_dphq = 0, off_dkef = 0, off_phq = 0, off_phk = 0, off_M0T = 0, off_dMfT = 0,
-           off_MfinT = 0, off_dkf = 0, off_mst = 0, off_dmst = 0, off_bd = 0, total = 0;
+           off_MfinT = 0, off_dkfin = 0, off_dkf = 0, off_mst = 0, off_dmst = 0, off_bd = 0, total = 0;
 };
 static BwdPlan plan_bwd(const lmoe_lsm_desc* d, int B, int N, int H, int D, lmoe_dtype dt) {
     BwdPlan w;
@@ -826,6 +826,7 @@ static BwdPlan plan_bwd(const lmoe_lsm_desc* d, int B, int N, int H, int D, lmoe
     w.off_M0T = take(BH * D * D * 4);
     w.off_dMfT = take(BH * D * D * 4);
     w.off_MfinT = take(BH * D * D * 4);
+    w.off_dkfin = take(BH * D * D * 4);
     w.off_dkf = take(BH * N * 4);
     const size_t nchunk = (N + lmoe_dev::kC - 1) / lmoe_dev::kC;
     if (d && device_decay_mode(d->instance) == lmoe_dev::kDecayTokenScalar) {
@@ -1062,8 +1063,12 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
             dMfT = F(w.off_dMfT);
         }
         // side: 1 / 2 = write the per-chunk state operands (dq pass: M_c^T, dk pass: dM_c^T)
+        // shared_T (the dv pass): its keys / values are the dk pass's values / keys with the same
+        // reverse-time decay weights, so its segment states, carried-in states and final state
+        // are the transposes of the dk pass's (no state pass, no combine; the initial states
+        // dM_final and dM_final^T are transposes too)
         auto pass = [&](const void* qq, const void* kk, const void* vv, void* oo, bool rev, bool out_f32,
-                        bool kfq, const float* init, float* fin, int side) {
+                        bool kfq, const float* init, float* fin, int side, bool shared_T = false) {
             LsmCall c{&dd, B, N, N, H, D, dtype, qq, kk, vv, b_pre, a_raw, oo, ws, w.pl, st, nullptr};
             c.setup();
             c.var.rev = rev ? 1 : 0;
@@ -1073,8 +1078,18 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
             if (mamba && side == 1) c.p.mst = ws + w.off_mst;
             if (mamba && side == 2) c.p.mst = ws + w.off_dmst;
             c.clear_err();
-            if (bf16) c.state_pass<__nv_bfloat16>(); else c.state_pass<float>();
-            c.combine(init, nullptr, true, fin, nullptr, nullptr, 0, rev ? 1 : 0);
+            if (shared_T) {
+                float* minT = c.p.Sseg;  // the segment-state region is free in this pass
+                c.mark();  // phase-timer layout of a pass: the "state pass" is the transposes
+                LMOE_CUDA_CHECK(lmoe_dev::launch_transpose_states(c.p.Min, minT, BH * w.pl.nseg, D, st));
+                if (fin) LMOE_CUDA_CHECK(lmoe_dev::launch_transpose_states(F(w.off_dkfin), fin, BH, D, st));
+                g_launch_count += fin ? 2 : 1;
+                c.p.Min = minT;
+                c.mark();
+            } else {
+                if (bf16) c.state_pass<__nv_bfloat16>(); else c.state_pass<float>();
+                c.combine(init, nullptr, true, fin, nullptr, nullptr, 0, rev ? 1 : 0);
+            }
             if (bf16) c.output_pass<__nv_bfloat16>(); else c.output_pass<float>();
             c.finish_timing();
             c.check_err();
@@ -1083,8 +1098,8 @@ extern "C" int lmoe_lsm_bwd(const lmoe_lsm_desc* desc, int B, int N, int H, int 
         // passes (the kf row scale of the REV epilogue), in the input dtype; otherwise fp32
         // intermediates go through the chain-rule kernel
         pass(dO, v, phk, direct ? dq : dphq, false, !direct, false, M0T, F(w.off_MfinT), 1);
-        pass(v, dO, phq, direct ? dk : dkef, true, !direct, direct && mamba, dMfT, nullptr, 2);
-        pass(phk, phq, dO, dv, true, false, mamba, dM_final, dM0, 0);
+        pass(v, dO, phq, direct ? dk : dkef, true, !direct, direct && mamba, dMfT, dM0 ? F(w.off_dkfin) : nullptr, 2);
+        pass(phk, phq, dO, dv, true, false, mamba, dM_final, dM0, 0, true);
         if (!direct) {
             LMOE_CUDA_CHECK(lmoe_dev::launch_bwd_finish(bf16, desc->feature_map, mamba, q, k, dphq, dkef, b_pre, dq,
                                                         dk, F(w.off_dkf), B, N, H, st));
