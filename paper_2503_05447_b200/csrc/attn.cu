@@ -162,9 +162,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             for (int cb = 0; cb < 4; ++cb)
                 tmem_ld32(tmem + s * 128 + lo + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(u + cb * 32));
             tmem_wait_ld();
+            // raw scores: the log2(e)/sqrt(d) scale is folded into the exponent's FFMA below (the
+            // softmax warps are issue-bound; this drops one FMUL per score)
             float x[128];
 #pragma unroll
-            for (int i = 0; i < 128; ++i) x[i] = __uint_as_float(u[i]) * p.scale_log2;
+            for (int i = 0; i < 128; ++i) x[i] = __uint_as_float(u[i]);
             const int k0 = j * kC;
             const bool full = k0 + kC - 1 <= p.row_offset + q0 && k0 + kC <= p.Nk;  // no masking
             if (!full) {
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             for (int a = 4; a > 0; a >>= 1)
 #pragma unroll
                 for (int c = 0; c < a; ++c) mx8[c] = fmaxf(mx8[c], mx8[c + a]);
-            const float mx = mx8[0];
+            const float mx = mx8[0] * p.scale_log2;  // scale > 0: the max commutes with it
             const float m_new = fmaxf(m, mx);
             const bool grow_max = m_new > m + kRescaleLog2;  // includes the first tile (m = -inf)
             if (__any_sync(0xFFFFFFFFu, grow_max && j > 0)) {
@@ -213,7 +215,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 for (int i = 0; i < 16; ++i) {
                     // (a quarter of these on an FMA-pipe polynomial 2^x was measured: 1045 -> 915
                     // TFLOP/s; the softmax warps are issue-bound, one per scheduler, not MUFU-bound)
-                    const float a = ex2(x[cb * 32 + 2 * i] - m), c2 = ex2(x[cb * 32 + 2 * i + 1] - m);
+                    const float a = ex2(fmaf(x[cb * 32 + 2 * i], p.scale_log2, -m));
+                    const float c2 = ex2(fmaf(x[cb * 32 + 2 * i + 1], p.scale_log2, -m));
                     ls8[(2 * i) & 7] += a;
                     ls8[(2 * i + 1) & 7] += c2;
                     pk[i] = pack_bf16(a, c2);
@@ -249,6 +252,260 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     w.z = pack_bf16(__uint_as_float(u[c * 8 + 4]) * inv, __uint_as_float(u[c * 8 + 5]) * inv);
                     w.w = pack_bf16(__uint_as_float(u[c * 8 + 6]) * inv, __uint_as_float(u[c * 8 + 7]) * inv);
                     *reinterpret_cast<uint4*>(dst + cb * 32 + c * 8) = w;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------------------------------------------------
+// Two query tiles per CTA (A = rows q0..q0+127, B = the next 128), softmax ping-pong: two
+// softmax warpgroups, one per tile, so each scheduler runs two softmax warps, and the tensor
+// core computes one tile's PV and next scores while the other tile's softmax runs.
+//   warps 0 TMA, 1 MMA, 2-5 softmax tile A, 6-9 softmax tile B (TMEM lane quarter = warp % 4)
+//   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512); P packed into its S buffer
+//   MMA order for key tile j: S_A(j), PV_B(j-1), S_B(j), PV_A(j)
+// K/V tile j is released after PV_B(j) (the later tile reaches at least as far as A).
+// ------------------------------------------------------------------------------------
+constexpr int kPPThreads = 320;  // 204 registers per thread (384 threads would cap at 168 and spill)
+constexpr int kPPKV = 2;
+
+__global__ void __launch_bounds__(kPPThreads, 1)
+    attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+    constexpr int D = 128, EPB = 64;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* qt = smem;                   // [A | B], 32 KB each
+    uint8_t* kv = smem + 2 * kTileBytes;  // kPPKV stages x [K | V]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (2 + 2 * kPPKV) * kTileBytes);
+    uint64_t* q_full = bars;
+    uint64_t* k_full = bars + 1;             // [kPPKV]
+    uint64_t* v_full = k_full + kPPKV;       // [kPPKV]
+    uint64_t* kv_empty = v_full + kPPKV;     // [kPPKV]
+    uint64_t* s_full = kv_empty + kPPKV;     // [2] per tile
+    uint64_t* p_full = s_full + 2;           // [2]
+    uint64_t* o_done = p_full + 2;           // [2]
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(o_done + 2);
+
+    const int ntq = (p.Nq + kC - 1) / kC;
+    const int npair = (ntq + 1) / 2;
+    const int pair = npair - 1 - blockIdx.x;  // heavy (late) pairs first
+    const int h = blockIdx.y, b = blockIdx.z;
+    const bool hasB = 2 * pair + 1 < ntq;
+    const int nkt = (p.Nk + kC - 1) / kC;
+    auto nkv_of = [&](int t) {
+        const int q0 = (2 * pair + t) * kC;
+        const int last_row = p.row_offset + min(q0 + kC, p.Nq) - 1;
+        return min((last_row + kC) / kC, nkt);
+    };
+    const int nkvA = nkv_of(0), nkvB = hasB ? nkv_of(1) : 0;
+    const int nkv = max(nkvA, nkvB);
+    const int warp = warp_id(), lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < kPPKV; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&s_full[t], 1);
+            mbar_init(&p_full[t], 128);
+            mbar_init(&o_done[t], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
+            mbar_expect_tx(q_full, (hasB ? 2 : 1) * kTileBytes);
+            for (int t = 0; t < (hasB ? 2 : 1); ++t)
+                for (int blk = 0; blk < 2; ++blk)
+                    tma_load_4d(qt + t * kTileBytes + blk * kBlockBytes, &tmQ, q_full, blk * EPB, h,
+                                (2 * pair + t) * kC, b);
+            for (int j = 0; j < nkv; ++j) {
+                const int s = j % kPPKV;
+                if (j >= kPPKV) mbar_wait(&kv_empty[s], ((j / kPPKV) - 1) & 1);
+                uint8_t* kt = kv + s * 2 * kTileBytes;
+                uint8_t* vt = kt + kTileBytes;
+                mbar_expect_tx(&k_full[s], kTileBytes);
+                for (int blk = 0; blk < 2; ++blk)
+                    tma_load_4d(kt + blk * kBlockBytes, &tmK, &k_full[s], blk * EPB, h, j * kC, b);
+                mbar_expect_tx(&v_full[s], kTileBytes);
+                for (int blk = 0; blk < 2; ++blk)
+                    tma_load_4d(vt + blk * kBlockBytes, &tmV, &v_full[s], blk * EPB, h, j * kC, b);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idS = umma_idesc(1, 0, 0, 128, 128);
+            constexpr uint32_t idPV = umma_idesc(1, 0, 1, 128, D);
+            auto issue_S = [&](int t, int j) {
+                const uint32_t qa = smem_u32(qt + t * kTileBytes);
+                const uint32_t kt = smem_u32(kv + (j % kPPKV) * 2 * kTileBytes);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * kBlockBytes + (kk & 3) * 32;
+                    mma_ss_f16(tmem + t * 128, umma_desc_sw128(qa + off, 16, 1024),
+                               umma_desc_sw128(kt + off, 16, 1024), idS, kk > 0);
+                }
+                mma_commit(&s_full[t]);
+            };
+            auto issue_PV = [&](int t, int j) {
+                mbar_wait(&p_full[t], j & 1);
+                mbar_wait(&v_full[j % kPPKV], (j / kPPKV) & 1);
+                tc_fence_after();
+                const uint32_t vt = smem_u32(kv + (j % kPPKV) * 2 * kTileBytes + kTileBytes);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_ts_f16(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                               umma_desc_sw128(vt + kk * 16 * 128, kBlockBytes, 1024), idPV, (j > 0 || kk > 0));
+                mma_commit(&o_done[t]);
+            };
+            mbar_wait(q_full, 0);
+            for (int j = 0; j < nkv; ++j) {
+                mbar_wait(&k_full[j % kPPKV], (j / kPPKV) & 1);
+                tc_fence_after();
+                if (j < nkvA) issue_S(0, j);
+                if (j >= 1 && j - 1 < nkvB) {
+                    issue_PV(1, j - 1);
+                    mma_commit(&kv_empty[(j - 1) % kPPKV]);
+                }
+                if (j < nkvB) issue_S(1, j);
+                if (j < nkvA) {
+                    issue_PV(0, j);
+                    if (j >= nkvB) mma_commit(&kv_empty[j % kPPKV]);  // B does not use this tile
+                }
+            }
+            if (nkvB >= 1) {
+                issue_PV(1, nkvB - 1);
+                mma_commit(&kv_empty[(nkvB - 1) % kPPKV]);
+            }
+        }
+    } else if (warp >= 2) {
+        const int t = (warp - 2) >> 2;  // tile of this softmax warpgroup
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const int q0 = (2 * pair + t) * kC;
+        const int nkv_t = t ? nkvB : nkvA;
+        const int grow = p.row_offset + q0 + r;
+        const uint32_t lo = (uint32_t)(q * 32) << 16;
+        const uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
+        if (t == 0 || hasB) {
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < nkv_t; ++j) {
+                mbar_wait(&s_full[t], j & 1);
+                tc_fence_after();
+                // two passes over the row's 128 scores in TMEM, 64 at a time (the whole row in
+                // registers would exceed the 168 registers of 3 warps per scheduler): row max,
+                // then exponentials and the packed P.  Raw scores; the scale is folded into the
+                // exponent's FFMA.
+                const int k0 = j * kC;
+                const bool full = k0 + kC - 1 <= p.row_offset + q0 && k0 + kC <= p.Nk;
+                auto load_half = [&](int hf, uint32_t (&u)[64]) {
+                    tmem_ld32(tS + lo + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
+                    tmem_ld32(tS + lo + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+                    tmem_wait_ld();
+                    if (!full) {
+#pragma unroll
+                        for (int i = 0; i < 64; ++i) {
+                            const int key = k0 + hf * 64 + i;
+                            if (key > grow || key >= p.Nk) u[i] = __float_as_uint(-INFINITY);
+                        }
+                    }
+                };
+                float mx8[8];
+#pragma unroll
+                for (int a = 0; a < 8; ++a) mx8[a] = -INFINITY;
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t u[64];
+                    load_half(hf, u);
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(u[i]));
+                }
+#pragma unroll
+                for (int a = 4; a > 0; a >>= 1)
+#pragma unroll
+                    for (int c = 0; c < a; ++c) mx8[c] = fmaxf(mx8[c], mx8[c + a]);
+                const float m_new = fmaxf(m, mx8[0] * p.scale_log2);
+                const bool grow_max = m_new > m + kRescaleLog2;
+                if (__any_sync(0xFFFFFFFFu, grow_max && j > 0)) {
+                    const float alpha = grow_max ? ex2(m - m_new) : 1.f;
+                    mbar_wait(&o_done[t], (j - 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int cb = 0; cb < 4; ++cb) {
+                        uint32_t w[32];
+                        tmem_ld32(tO + lo + cb * 32, w);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
+                        tmem_st32(tO + lo + cb * 32, w);
+                    }
+                    l *= alpha;
+                }
+                if (grow_max) m = m_new;
+                float ls8[8];
+#pragma unroll
+                for (int a = 0; a < 8; ++a) ls8[a] = 0.f;
+                uint32_t pk[2][32];
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t u[64];
+                    load_half(hf, u);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float a = ex2(fmaf(__uint_as_float(u[2 * i]), p.scale_log2, -m));
+                        const float c2 = ex2(fmaf(__uint_as_float(u[2 * i + 1]), p.scale_log2, -m));
+                        ls8[(2 * i) & 7] += a;
+                        ls8[(2 * i + 1) & 7] += c2;
+                        pk[hf][i] = pack_bf16(a, c2);
+                    }
+                }
+                // P overwrites the scores only after both passes read them
+                tmem_st32(tS + lo, pk[0]);
+                tmem_st32(tS + lo + 32, pk[1]);
+#pragma unroll
+                for (int a = 4; a > 0; a >>= 1)
+#pragma unroll
+                    for (int c = 0; c < a; ++c) ls8[c] += ls8[c + a];
+                l += ls8[0];
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&p_full[t]);
+            }
+            // epilogue: O / l -> global bf16
+            mbar_wait(&o_done[t], (nkv_t - 1) & 1);
+            tc_fence_after();
+            const float inv = 1.f / l;
+            const bool vrow = q0 + r < p.Nq;
+            __nv_bfloat16* dst = p.o + (((size_t)b * p.Nq + q0 + (vrow ? r : 0)) * p.H + h) * D;
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) {
+                uint32_t w[32];
+                tmem_ld32(tO + lo + cb * 32, w);
+                tmem_wait_ld();
+                if (vrow) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint4 o4;
+                        o4.x = pack_bf16(__uint_as_float(w[c * 8 + 0]) * inv, __uint_as_float(w[c * 8 + 1]) * inv);
+                        o4.y = pack_bf16(__uint_as_float(w[c * 8 + 2]) * inv, __uint_as_float(w[c * 8 + 3]) * inv);
+                        o4.z = pack_bf16(__uint_as_float(w[c * 8 + 4]) * inv, __uint_as_float(w[c * 8 + 5]) * inv);
+                        o4.w = pack_bf16(__uint_as_float(w[c * 8 + 6]) * inv, __uint_as_float(w[c * 8 + 7]) * inv);
+                        *reinterpret_cast<uint4*>(dst + cb * 32 + c * 8) = o4;
+                    }
                 }
             }
         }
@@ -296,9 +553,19 @@ static void attn_launch(int B, int Nq, int Nk, int H, int D, int row_offset, con
     const CUtensorMap tk = make_tmap_4d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
     const CUtensorMap tv = make_tmap_4d(v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
     AttnParams p{Nq, Nk, H, row_offset, 1.4426950408889634f / sqrtf((float)D), static_cast<__nv_bfloat16*>(o)};
-    constexpr int smem = (1 + 2 * kAttnKV) * kTileBytes + 256;
-    LMOE_CUDA_CHECK(lmoe_dev::ensure_smem((const void*)attn_fwd_kernel, smem));
-    attn_fwd_kernel<<<dim3((Nq + kC - 1) / kC, H, B), kAttnThreads, smem, st>>>(tq, tk, tv, p);
+    // two query tiles per CTA with the softmax ping-pong; LMOE_ATTN_PP=0 (developer A/B) runs
+    // the one-tile kernel
+    static const bool pp = getenv("LMOE_ATTN_PP") == nullptr || atoi(getenv("LMOE_ATTN_PP")) != 0;
+    if (pp) {
+        constexpr int smem = (2 + 2 * kPPKV) * kTileBytes + 256;
+        LMOE_CUDA_CHECK(lmoe_dev::ensure_smem((const void*)attn_fwd_pp_kernel, smem));
+        const int ntq = (Nq + kC - 1) / kC;
+        attn_fwd_pp_kernel<<<dim3((ntq + 1) / 2, H, B), kPPThreads, smem, st>>>(tq, tk, tv, p);
+    } else {
+        constexpr int smem = (1 + 2 * kAttnKV) * kTileBytes + 256;
+        LMOE_CUDA_CHECK(lmoe_dev::ensure_smem((const void*)attn_fwd_kernel, smem));
+        attn_fwd_kernel<<<dim3((Nq + kC - 1) / kC, H, B), kAttnThreads, smem, st>>>(tq, tk, tv, p);
+    }
     LMOE_CUDA_CHECK(cudaGetLastError());
     ++g_launch_count;
 }

@@ -850,8 +850,9 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
                 uint32_t r[KC / 32][32];
                 const uint32_t tS = tmem + bb * 128 + lane_off + hh * KC;
                 // causal mask col <= row (REV: col >= row): a warp's KC key columns against its
-                // 32 rows are all kept, all masked (no TMEM read, P = 0) or the diagonal block
-                const bool zero = !p.nomask && (REV ? hh * KC + KC - 1 < q * 32 : hh * KC > q * 32 + 31);
+                // 32 rows are all kept, all masked (no TMEM read, P = 0) or the diagonal block.
+                // nomask (Alg. 1): no intra-chunk term at all (the gathered state holds every key)
+                const bool zero = p.nomask || (REV ? hh * KC + KC - 1 < q * 32 : hh * KC > q * 32 + 31);
                 float rs = 0.f;
                 if (!zero) {
 #pragma unroll
@@ -899,7 +900,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
 #pragma unroll
                     for (int j = 0; j < KC; ++j) {
                         const int col = hh * KC + j;
-                        float v = (!p.nomask && (REV ? col < row : col > row)) ? 0.f : __uint_as_float(r[j / 32][j % 32]);
+                        float v = (REV ? col >= row : col <= row) ? __uint_as_float(r[j / 32][j % 32]) : 0.f;
                         if constexpr (TR) v = tf32r(v);
                         rs += v;
                         r[j / 32][j % 32] = __float_as_uint(v);
