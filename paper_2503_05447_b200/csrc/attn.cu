@@ -553,9 +553,10 @@ static void attn_launch(int B, int Nq, int Nk, int H, int D, int row_offset, con
     const CUtensorMap tk = make_tmap_4d(k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
     const CUtensorMap tv = make_tmap_4d(v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, H, Nk, B, 64, kC, 0, ldkv);
     AttnParams p{Nq, Nk, H, row_offset, 1.4426950408889634f / sqrtf((float)D), static_cast<__nv_bfloat16*>(o)};
-    // two query tiles per CTA with the softmax ping-pong; LMOE_ATTN_PP=0 (developer A/B) runs
-    // the one-tile kernel
-    static const bool pp = getenv("LMOE_ATTN_PP") == nullptr || atoi(getenv("LMOE_ATTN_PP")) != 0;
+    // one query tile per CTA with three K/V stages; LMOE_ATTN_PP=1 (developer A/B) runs the
+    // two-tile softmax ping-pong, measured 0-10% slower at the cfg5 rank shapes (its two Q tiles
+    // leave room for only two K/V stages, and the three stages are what made the difference)
+    static const bool pp = getenv("LMOE_ATTN_PP") != nullptr && atoi(getenv("LMOE_ATTN_PP")) != 0;
     if (pp) {
         constexpr int smem = (2 + 2 * kPPKV) * kTileBytes + 256;
         LMOE_CUDA_CHECK(lmoe_dev::ensure_smem((const void*)attn_fwd_pp_kernel, smem));
