@@ -34,7 +34,8 @@ namespace lmoe_dev {
 constexpr int kFusedThreads = 128 + 512;
 
 // developer trace (LMOE_TRACE): globaltimer per (CTA jj of head 0, segment unit, event):
-// 0 A steps start, 1 A accumulated, 2 hand-off acquired, 3 published, 4 C steps done
+// 0 A steps start, 1 look-back start (A accumulated, C chunk 0's P done), 2 window's flags
+// observed, 3 entering state folded, 4 C steps done
 __device__ __forceinline__ void fused_mark(const LsmFwdParams& p, int bh, int jj, int un, int ev) {
     if (p.trace != nullptr && bh == 0 && jj < 16 && un < 64) {
         unsigned long long t;
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const int hh = mw >> 2;             // column group
         const int row = q * 32 + lane;      // token row (S, O, Q, K tiles) / d_k row (state)
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const int R = p.fR;  // kFusedRing
+        const int R = p.fR;  // aggregate ring slots per (b,h)
         auto write_state_operand = [&](const float* vals) {  // DH values of state row `row`
             uint8_t* dst = mop + (hh * DH / EPB) * (D * 128);
             const int ch0 = (hh * DH % EPB) / EPC;
@@ -355,7 +356,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                 mbar_arrive(&xfA[ga & 1]);
                 mbar_arrive(&gfree[slot]);
             }
-            // ---- chain: M_in = incl(seg - 1); publish incl(seg) = D_seg M_in + S_seg
+            // ---- look-back: publish this segment's aggregate (S_seg, log D_seg); the entering
+            // state is this CTA's own inclusive prefix of segment seg - P (or M0 in the first
+            // round) carried through the other CTAs' aggregates of segments (seg - P, seg):
+            //   M_in(seg) = D_{seg-1} (... (D_{seg-P+1} incl(seg-P) + S_{seg-P+1}) ...) + S_{seg-1}
+            // No serial hand-off chain: a segment waits only for the state steps of the P - 1
+            // segments before it, which run concurrently.  The order of the additions is fixed,
+            // so the result does not depend on timing.
             auto chain = [&](float gend0) {
                 mbar_wait(accA, un & 1);
                 tc_fence_after();
@@ -363,57 +370,93 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                 uint32_t r[32];
                 tmem_ld32(tM + lane_off + hh * DH, r);
                 tmem_wait_ld();
-                const float* src = nullptr;
-                if (seg == 0) {
-                    if (p.Min) src = p.Min + ((size_t)bh * D + row) * D + hh * DH;
-                } else {
-                    const int* fl = p.flags + bh * R + (seg - 1) % R;
-                    if (lane == 0)
-                        while (ld_acquire_gpu(fl) != seg) __nanosleep(32);
-                    __syncwarp();
-                    (void)ld_acquire_gpu(fl);
-                    src = p.ring + ((size_t)(bh * R + (seg - 1) % R) * D + row) * D + hh * DH;
-                }
-                if (tid == 0) fused_mark(p, bh, jj, un, 2);
-                float prev[DH];
+                const int P = p.fP;
+                {
+                    const int slot = bh * R + seg % R;
+                    float* dst = p.ring + ((size_t)slot * D + row) * D + hh * DH;
 #pragma unroll
-                for (int j = 0; j < DH; j += 4) {
-                    const float4 v = src ? __ldcg(reinterpret_cast<const float4*>(src + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    prev[j] = v.x; prev[j + 1] = v.y; prev[j + 2] = v.z; prev[j + 3] = v.w;
+                    for (int j = 0; j < DH; j += 4)
+                        __stcg(reinterpret_cast<float4*>(dst + j),
+                               make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                           __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+                    if (tid == 0) __stcg(p.ringD + slot, logD);
+                    // the barrier orders every thread's stores before thread 0's fence; the fence
+                    // is cumulative, so the release publishes them all
+                    named_bar_sync(2, MT);
+                    if (tid == 0) {
+                        __threadfence();
+                        st_release_gpu(p.flags + slot, seg + 1);
+                    }
                 }
+                float X[DH];
+                int s0 = 0;
+                const float* own = p.incl + ((size_t)(bh * P + jj) * D + row) * D + hh * DH;
+                if (seg >= P) {
+                    s0 = seg - P + 1;
+#pragma unroll
+                    for (int j = 0; j < DH; j += 4) {
+                        const float4 v = __ldcg(reinterpret_cast<const float4*>(own + j));
+                        X[j] = v.x; X[j + 1] = v.y; X[j + 2] = v.z; X[j + 3] = v.w;
+                    }
+                } else {
+                    const float* m0 = p.Min ? p.Min + ((size_t)bh * D + row) * D + hh * DH : nullptr;
+#pragma unroll
+                    for (int j = 0; j < DH; j += 4) {
+                        const float4 v = m0 ? __ldcg(reinterpret_cast<const float4*>(m0 + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        X[j] = v.x; X[j + 1] = v.y; X[j + 2] = v.z; X[j + 3] = v.w;
+                    }
+                }
+                // one thread observes every flag of the window (relaxed polls, then a fence: the
+                // acquire), the barrier carries that to all math threads, and then the aggregates
+                // are read with no flag wait between them
+                if (tid == 0) {
+                    for (int s2 = s0; s2 < seg; ++s2)
+                        while (ld_relaxed_gpu(p.flags + bh * R + s2 % R) != s2 + 1) __nanosleep(20);
+                    __threadfence();
+                }
+                named_bar_sync(2, MT);
+                if (tid == 0) fused_mark(p, bh, jj, un, 2);  // window observed
+                for (int s2 = s0; s2 < seg; ++s2) {
+                    const int slot = bh * R + s2 % R;
+                    const float dl = __expf(__ldcg(p.ringD + slot));
+                    const float* src = p.ring + ((size_t)slot * D + row) * D + hh * DH;
+#pragma unroll
+                    for (int j = 0; j < DH; j += 4) {
+                        const float4 v = __ldcg(reinterpret_cast<const float4*>(src + j));
+                        X[j] = fmaf(dl, X[j], v.x);
+                        X[j + 1] = fmaf(dl, X[j + 1], v.y);
+                        X[j + 2] = fmaf(dl, X[j + 2], v.z);
+                        X[j + 3] = fmaf(dl, X[j + 3], v.w);
+                    }
+                }
+                if (tid == 0) fused_mark(p, bh, jj, un, 3);  // M_in folded
                 if (p.fdbg) {  // developer aid: [bh][seg][S_seg | M_in] + logD at the end
                     float* dbg = p.fdbg + ((size_t)bh * p.nseg + seg) * 2 * D * D + (size_t)row * D + hh * DH;
-                    for (int j = 0; j < DH; ++j) { dbg[j] = __uint_as_float(r[j]); dbg[D * D + j] = prev[j]; }
+                    for (int j = 0; j < DH; ++j) { dbg[j] = __uint_as_float(r[j]); dbg[D * D + j] = X[j]; }
                     if (tid == 0) p.fdbg[(size_t)p.B * p.H * p.nseg * 2 * D * D + (size_t)bh * p.nseg + seg] = logD;
                 }
+                // own inclusive prefix (read back by this thread next round), or the final state
                 const float dl = __expf(logD);
                 const bool last = seg + 1 == p.nseg;
-                float* dst = last ? (p.Mfin ? p.Mfin + ((size_t)bh * D + row) * D + hh * DH : nullptr)
-                                  : p.ring + ((size_t)(bh * R + seg % R) * D + row) * D + hh * DH;
+                float* idst = last ? (p.Mfin ? p.Mfin + ((size_t)bh * D + row) * D + hh * DH : nullptr) : const_cast<float*>(own);
                 bool bad = false;
 #pragma unroll
                 for (int j = 0; j < DH; j += 4) {
                     float4 v;
-                    v.x = fmaf(dl, prev[j], __uint_as_float(r[j]));
-                    v.y = fmaf(dl, prev[j + 1], __uint_as_float(r[j + 1]));
-                    v.z = fmaf(dl, prev[j + 2], __uint_as_float(r[j + 2]));
-                    v.w = fmaf(dl, prev[j + 3], __uint_as_float(r[j + 3]));
+                    v.x = fmaf(dl, X[j], __uint_as_float(r[j]));
+                    v.y = fmaf(dl, X[j + 1], __uint_as_float(r[j + 1]));
+                    v.z = fmaf(dl, X[j + 2], __uint_as_float(r[j + 2]));
+                    v.w = fmaf(dl, X[j + 3], __uint_as_float(r[j + 3]));
                     bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
-                    if (dst) __stcg(reinterpret_cast<float4*>(dst + j), v);
+                    if (idst) __stcg(reinterpret_cast<float4*>(idst + j), v);
                 }
                 if (bad) atomicOr(&p.err[1], 1);
-                if (!last) {
-                    __threadfence();
-                    named_bar_sync(2, MT);
-                    if (tid == 0) st_release_gpu(p.flags + bh * R + seg % R, seg + 1);
-                }
-                if (tid == 0) fused_mark(p, bh, jj, un, 3);
                 // the entering state: operand M_in, TMEM M = e^{G_end(chunk 0)} M_in
-                write_state_operand(prev);
+                write_state_operand(X);
                 const float g0 = __expf(gend0);
                 uint32_t w32[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) w32[j] = __float_as_uint(prev[j] * g0);
+                for (int j = 0; j < 32; ++j) w32[j] = __float_as_uint(X[j] * g0);
                 tmem_st32(tM + lane_off + hh * DH, w32);
                 tmem_wait_st();
                 fence_proxy_async_smem();
@@ -450,50 +493,76 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                 mbar_wait(&s_full[bb], (cc >> 1) & 1);
                 tc_fence_after();
                 if constexpr (!kPrep) mbar_wait(&full[s], (gc / NST) & 1);
-                // (b) Q~ = phiQ e^{G_i}, K~ = phiK kf e^{G_end - G_i}
+                // (b) Q~ = phiQ e^{G_i}, K~ = phiK kf e^{G_end - G_i}: this row part's Q and K
+                // chunks all loaded before any store (see xform_chunks, lsm_kernels.cuh)
                 {
                     if constexpr (DECAY != kDecayNone) {
                         const float fq = __expf(gi);
                         const float fk = safe ? __expf(gend - rQ[q]) * Fs[row] : __expf(gend - gi) * Fs[row];
                         uint8_t* qb = qt + (hh * DH / EPB) * kBlockBytes;
+                        uint8_t* kb = kt + (hh * DH / EPB) * kBlockBytes;
                         const int qch0 = (hh * DH % EPB) / EPC;
+                        constexpr int NCH = DH / EPC;
+                        uint4 vq[NCH], vk[NCH];
 #pragma unroll
-                        for (int ch = 0; ch < DH / EPC; ++ch) {
-                            uint4* ptr = reinterpret_cast<uint4*>(qb + sw128_off(row, qch0 + ch));
-                            uint4 v = *ptr;
-                            uint32_t* wv = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float2 f = unpack_bf16(wv[e]);
-                                wv[e] = pack_bf16(f.x * fq, f.y * fq);
-                            }
-                            *ptr = v;
+                        for (int ch = 0; ch < NCH; ++ch) {
+                            vq[ch] = *reinterpret_cast<const uint4*>(qb + sw128_off(row, qch0 + ch));
+                            vk[ch] = *reinterpret_cast<const uint4*>(kb + sw128_off(row, qch0 + ch));
                         }
-                        xform_row_part<T, 0, false, DH>(kt, row, hh * DH, fk);
+#pragma unroll
+                        for (int ch = 0; ch < NCH; ++ch) {
+                            xform_chunk<T, 0, false>(vq[ch], fq);
+                            xform_chunk<T, 0, false>(vk[ch], fk);
+                        }
+#pragma unroll
+                        for (int ch = 0; ch < NCH; ++ch) {
+                            *reinterpret_cast<uint4*>(qb + sw128_off(row, qch0 + ch)) = vq[ch];
+                            *reinterpret_cast<uint4*>(kb + sw128_off(row, qch0 + ch)) = vk[ch];
+                        }
                     }
                     fence_proxy_async_smem();
                     mbar_arrive(xf2);
                 }
-                // (a) S -> P (packed bf16 into the S buffer)
+                // (a) S -> P (packed bf16 into the S buffer): warps above the diagonal skip the
+                // TMEM read; the `safe` branch is hoisted out of the column loop
                 {
                     uint32_t r[32];
                     const uint32_t tS = tmem + bb * 128 + lane_off + hh * KC;
-                    tmem_ld32(tS, r);
-                    tmem_wait_ld();
-                    const float eq = (DECAY != kDecayNone && safe) ? __expf(gi - rQ[hh]) : 1.f;
+                    if (hh <= q) {
+                        tmem_ld32(tS, r);
+                        tmem_wait_ld();
+                        if (DECAY == kDecayNone || safe) {
+                            const float eq = (DECAY != kDecayNone) ? __expf(gi - rQ[hh]) : 1.f;
 #pragma unroll
-                    for (int j = 0; j < KC; ++j) {
-                        const int col = hh * KC + j;
-                        float v = __uint_as_float(r[j]);
-                        float f;
-                        if constexpr (DECAY == kDecayNone) f = Fs[col];
-                        else f = safe ? eq * Fs[col] : __expf(gi - Gs[col]) * Fs[col];
-                        r[j] = __float_as_uint(col <= row ? v * f : 0.f);
+                            for (int j = 0; j < KC; j += 4) {
+                                const float4 F = *reinterpret_cast<const float4*>(Fs + hh * KC + j);
+                                r[j] = __float_as_uint(__uint_as_float(r[j]) * (eq * F.x));
+                                r[j + 1] = __float_as_uint(__uint_as_float(r[j + 1]) * (eq * F.y));
+                                r[j + 2] = __float_as_uint(__uint_as_float(r[j + 2]) * (eq * F.z));
+                                r[j + 3] = __float_as_uint(__uint_as_float(r[j + 3]) * (eq * F.w));
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < KC; j += 4) {
+                                const float4 G = *reinterpret_cast<const float4*>(Gs + hh * KC + j);
+                                const float4 F = *reinterpret_cast<const float4*>(Fs + hh * KC + j);
+                                r[j] = __float_as_uint(__uint_as_float(r[j]) * (__expf(gi - G.x) * F.x));
+                                r[j + 1] = __float_as_uint(__uint_as_float(r[j + 1]) * (__expf(gi - G.y) * F.y));
+                                r[j + 2] = __float_as_uint(__uint_as_float(r[j + 2]) * (__expf(gi - G.z) * F.z));
+                                r[j + 3] = __float_as_uint(__uint_as_float(r[j + 3]) * (__expf(gi - G.w) * F.w));
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < KC; ++j)
+                            if (hh * KC + j > row) r[j] = 0u;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < KC; ++j) r[j] = 0u;
                     }
                     uint32_t pk[KC / 2];
 #pragma unroll
                     for (int j = 0; j < KC / 2; ++j) pk[j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-                    named_bar_sync(1, MT);  // all S reads done before P overwrites
+                    named_bar_sync(3 + q, 32 * NQ);  // this lane quarter's S reads done before P overwrites
                     tmem_st16(tmem + bb * 128 + lane_off + hh * 16, pk);
                     tmem_wait_st();
                     tc_fence_before();

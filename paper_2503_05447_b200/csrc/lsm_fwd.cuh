@@ -39,9 +39,9 @@ constexpr int kBlockBytes = kC * 128;           // one SW128 column block of a t
 constexpr int kMathThreads = 256;               // 8 epilogue warps (output pass)
 constexpr float kSafeLogDecay = -80.f;          // e^{-G} stays finite in fp32 above this
 
-constexpr int kFusedRing = 8;  // single-read forward: hand-off ring slots per (b,h) (p.fR <= this used); a slot is
-                               // rewritten only after its one reader (the next segment) has
-                               // published its own prefix, which the writer has acquired
+// single-read forward: the aggregate of segment s lives in ring slot s % fR with fR = 2 fP.  Its
+// readers are the segments (s, s + fP); the writer of s + 2 fP first needs the aggregate of a
+// segment that each of those readers publishes only after its look-back has read slot s.
 enum DecayMode { kDecayNone = 0, kDecayConst = 1, kDecayTokenScalar = 2, kDecayTokenVector = 3 };
 
 struct LsmFwdParams {
@@ -74,9 +74,11 @@ struct LsmFwdParams {
     // single-read persistent forward (lsm_fused.cuh): P CTAs per (b,h) walk its segments
     // j, j+P, j+2P, ...; the inclusive prefix state of segment s is handed to segment s+1
     // through ring[bh][s % R] (fp32 [D][D]) and flags[bh][s % R] = s + 1
-    int fP, fR;
-    float* ring;
-    int* flags;
+    int fP, fR;                 // CTAs per (b,h); aggregate ring slots per (b,h) (2 fP)
+    float* ring;                // [B*H][fR][D][D] segment aggregates S_seg
+    int* flags;                 // [B*H][fR] = segment + 1 once its aggregate is published
+    float* ringD;               // [B*H][fR] segment log decays
+    float* incl;                // [B*H][fP][D][D] each CTA's inclusive prefix of its last segment
     float* Mfin;                // [B*H][D][D] final state (inclusive prefix of the last segment)
     float* fdbg;                // developer aid (LMOE_FUSED_DEBUG_PTR): per (bh, seg) S_seg, M_in, logD
 };

@@ -60,7 +60,7 @@ struct LsmPlan {
     // single-read forward (lsm_fused.cuh): fP CTAs per (b,h), fnseg segments of fseg_len
     int fP = 0, fseg_len = 0, fnseg = 0;
     size_t off_S = 0, off_z = 0, off_logD = 0, off_Min = 0, off_zin = 0, off_err = 0, off_ring = 0,
-           off_flags = 0, total = 0;
+           off_flags = 0, off_ringD = 0, off_incl = 0, total = 0;
 };
 
 static int env_int(const char* name, int dflt) {
@@ -126,8 +126,11 @@ static LsmPlan plan_lsm(int B, int N, int H, int D) {
     pl.off_zin = take(heads_nseg * D * 4);
     pl.off_err = take(64);
     plan_fused(pl, B, N, H);
-    pl.off_ring = take(heads * lmoe_dev::kFusedRing * D * D * 4);
-    pl.off_flags = take(heads * lmoe_dev::kFusedRing * 4);
+    const size_t fR = 2 * (size_t)std::max(pl.fP, 1);
+    pl.off_ring = take(heads * fR * D * D * 4);
+    pl.off_flags = take(heads * fR * 4);
+    pl.off_ringD = take(heads * fR * 4);
+    pl.off_incl = take(heads * (size_t)std::max(pl.fP, 1) * D * D * 4);
     pl.total = off;
     return pl;
 }
@@ -305,14 +308,16 @@ struct LsmCall {
         fp.seg_len = pl.fseg_len;
         fp.nseg = pl.fnseg;
         fp.fP = pl.fP;
-        fp.fR = std::max(2, std::min(lmoe_dev::kFusedRing, env_int("LMOE_FUSED_RING", 2)));
+        fp.fR = 2 * pl.fP;
         fp.ring = reinterpret_cast<float*>(ws + pl.off_ring);
         fp.flags = reinterpret_cast<int*>(ws + pl.off_flags);
+        fp.ringD = reinterpret_cast<float*>(ws + pl.off_ringD);
+        fp.incl = reinterpret_cast<float*>(ws + pl.off_incl);
         fp.Min = M0;
         fp.Mfin = M_out;
         fp.order = env_int("LMOE_FUSED_HINT", 1);
         fp.fdbg = getenv("LMOE_FUSED_DEBUG_PTR") ? reinterpret_cast<float*>(strtoull(getenv("LMOE_FUSED_DEBUG_PTR"), nullptr, 10)) : nullptr;
-        LMOE_CUDA_CHECK(cudaMemsetAsync(fp.flags, 0, (size_t)B * H * lmoe_dev::kFusedRing * 4, st));
+        LMOE_CUDA_CHECK(cudaMemsetAsync(fp.flags, 0, (size_t)B * H * fp.fR * 4, st));
         mark();
         LMOE_CUDA_CHECK(lmoe_dev::launch_fused_fwd_bf16(var, pl.fP * B * H, st, tq, tk, tv, to, fp));
         ++g_launch_count;

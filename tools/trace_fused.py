@@ -1,7 +1,7 @@
 """Segment timeline of the single-read forward (lsm_fused_fwd) for head 0 at the cfg3 shape
 (LMOE_TRACE=1): per CTA and segment unit, globaltimer (us from the first event) of
-A start, A accumulated, hand-off acquired, published, C done.  Prints per-unit phase
-durations and the hand-off gaps along the chain."""
+A start, look-back start, window flags observed, entering state folded, C done.  Columns:
+A (state steps), wait (publish + flag poll), chain (folding the window's aggregates), C."""
 import ctypes
 import os
 import sys
