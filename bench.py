@@ -772,7 +772,8 @@ def main():
     hbm, tflops, src = peaks()
     plan = pk.lsm.forward_plan(spec, 1, n_loc, HEADS, HEAD_DIM)
     fused = plan["fused"] and world == 1
-    out_pass_ms = (phase_ms[0] if fused else phase_ms[5]) / max(calls, 1)
+    local = plan["local"]  # local-state forward: output pass first (phase 0)
+    out_pass_ms = (phase_ms[0] if (fused or local) else phase_ms[5]) / max(calls, 1)
     units = n_loc * HEADS
     alg_bytes = ALG_BYTES_TH[args.instance] * units
     achieved = alg_bytes / (out_pass_ms / 1e3) / 1e9
@@ -781,6 +782,10 @@ def main():
                    "rank_seg_combine", "output_pass"]
     if fused:
         phase_names = ["lsm_fused_fwd"]
+    if local:
+        phase_names = (["output_pass(local state)", "-", "seg_combine", "local_fix", "-", "-"] if world == 1 else
+                       ["output_pass(local state)", "-", "local_combine", "all_gather", "rank_seg_combine",
+                        "local_fix"])
 
     if rank == 0:
         cb = None

@@ -285,9 +285,10 @@ int lmoe_lsm_bwd_recurrent(const lmoe_lsm_desc* desc, int B, int N, int H, int D
                            size_t workspace_bytes, lmoe_stream_t stream);
 
 /* Forward plan of lmoe_lsm_fwd for a shape: info[0] = 1 when the single-read persistent
- * kernel runs (bf16 / D = 128 scalar-decay kinds without normaliser; one launch), 0 for the
- * segment-parallel state pass + combine + output pass; info[1] segments per (b,h),
- * info[2] tokens per segment, info[3] CTAs per (b,h). */
+ * kernel runs (opt-in), 2 for the local-state forward (decaying scalar kinds, bf16 / D = 128,
+ * no normaliser: output pass from zero states, segment combine, correction of each segment's
+ * first chunks; no state pass), 0 for the segment-parallel state pass + combine + output
+ * pass; info[1] segments per (b,h), info[2] tokens per segment, info[3] CTAs per (b,h). */
 int lmoe_lsm_fwd_plan(const lmoe_lsm_desc* desc, int B, int N, int H, int D, lmoe_dtype dtype, int* info);
 
 /* Number of kernels one lmoe_lsm_fwd call launches (for launch accounting). */

@@ -70,6 +70,11 @@ struct LsmFwdParams {
     void* mst;
     int nchunk_tot;
     unsigned long long* trace;  // optional clock64 trace of CTA (0,0,0) [64 chunks][16]
+    // local-state forward (decaying scalar kinds, see lsm_local_fix): every segment but the
+    // first starts from a zero state; the output pass writes each segment's final state to
+    // Sseg and its total log decay to logDseg; Mloc0 = the initial state of segment 0 or null
+    int local;
+    const float* Mloc0;
     int fault;                  // TEST ONLY (LMOE_FLAG_TEST_DECAY_FAULT): decay shifted by one token
     // single-read persistent forward (lsm_fused.cuh): P CTAs per (b,h) walk its segments
     // j, j+P, j+2P, ...; the inclusive prefix state of segment s is handed to segment s+1

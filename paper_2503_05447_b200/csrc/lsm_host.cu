@@ -181,6 +181,7 @@ struct LsmCall {
     lmoe_dev::LsmVariant var{};
     bool norm = false;
     bool vec = false;
+    bool sp_local = false;  // SP phase A ran the local-state output pass (phase B corrects)
     int lw = 1;  // log-decay entries per state: 1, or D for TokenVector kinds
     int ld = 0;  // elements per token row of q, k, v, a_pre (0: H * D); o is always dense
 
@@ -323,6 +324,42 @@ struct LsmCall {
         ++g_launch_count;
         mark();
     }
+    // Local-state forward (decaying scalar kinds): the output pass runs every segment but the
+    // first from a zero state and writes each segment's final state; the combine turns those
+    // into the entering states; lsm_local_fix adds (q e^{Gseg}) M_in to the first chunks of each
+    // segment, until the decay from the segment start leaves the fp32 range.  No state pass: the
+    // step reads q, k, v once plus the corrected chunks' q and o.  For a constant decay the
+    // corrected span is known: taken when it costs less than the state pass it replaces.
+    bool local_ok() const {
+        if (env_int("LMOE_LOCAL", 1) == 0 || fused_ok()) return false;
+        if (!(dt == LMOE_BF16 && D == 128 && !norm && !vec && var.rev == 0 && var.fm == 0 && p.mst == nullptr &&
+              !p.out_f32 && !p.nomask))
+            return false;
+        if (var.decay == lmoe_dev::kDecayTokenScalar) return true;
+        if (var.decay != lmoe_dev::kDecayConst || !(p.log_a < 0.f)) return false;
+        const double span_tokens = 88.0 / -(double)p.log_a;  // tokens until e^{G} < e^{-88}
+        const double fix_bytes = 768.0 * std::min<double>(span_tokens + lmoe_dev::kC, pl.seg_len) * (pl.nseg - 1);
+        return fix_bytes < 0.8 * 512.0 * N;
+    }
+    void local_pass(const float* M0, float* M_out) {
+        using bf = __nv_bfloat16;
+        // every segment from a zero state (segment states are then the combine's inputs); with
+        // an initial state segment 0 is corrected too (its entering state M0)
+        p.local = 1;
+        p.Mloc0 = nullptr;
+        output_pass<bf>();  // timing phase 0
+        p.local = 0;
+        combine(M0, nullptr, true, M_out, nullptr, nullptr, 0);  // phase 2
+        mark();
+        const int nfix = M0 ? pl.nseg : pl.nseg - 1;  // the last nfix segments
+        if (nfix > 0) {
+            const CUtensorMap tq = tmap<bf>(q), to = tmap<bf>(o);
+            LMOE_CUDA_CHECK(lmoe_dev::launch_local_fix_bf16(var.decay, dim3(nfix, H, B), st, tq, to, p));
+            ++g_launch_count;
+        }
+        mark();  // phase 3: the correction
+        mark();
+    }
     void clear_err() { LMOE_CUDA_CHECK(cudaMemsetAsync(p.err, 0, 64, st)); }
     void check_err() {
         if (!(d->flags & LMOE_FLAG_CHECK)) return;
@@ -346,6 +383,8 @@ static void run_local(LsmCall& c, const float* M0, const float* z0, float* M_out
     c.clear_err();
     if (c.fused_ok()) {
         c.fused(M0, M_out);
+    } else if (c.local_ok() && z0 == nullptr && z_out == nullptr) {
+        c.local_pass(M0, M_out);
     } else {
         c.state_pass<T>();
         c.combine(M0, z0, true, M_out, z_out, nullptr, 0);
@@ -395,6 +434,18 @@ static SpWorkspace plan_sp(const lmoe_lsm_desc* d, int B, int N_local, int H, in
 template <typename T>
 static void sp_phase_a(LsmCall& c, float* payload) {
     const int P = (int)payload_floats(c.d, c.D);
+    if constexpr (sizeof(T) == 2) {
+        if (c.o != nullptr && c.local_ok()) {  // local-state forward: the output pass first, from zero
+                                               // states (payload-only callers, o == NULL, skip it)
+            c.sp_local = true;
+            c.p.local = 1;
+            c.p.Mloc0 = nullptr;
+            c.output_pass<T>();
+            c.p.local = 0;
+            c.combine(nullptr, nullptr, false, payload, nullptr, payload + P - c.lw, P);
+            return;
+        }
+    }
     c.state_pass<T>();
     c.combine(nullptr, nullptr, false, payload, c.norm ? payload + c.D * c.D : nullptr,
               payload + P - c.lw, P);
@@ -413,6 +464,17 @@ static void sp_phase_b(LsmCall& c, const float* gathered, int rank, float* M0, f
                                                       M_out, z_out, c.pl.nseg, c.D, c.D, c.norm ? 1 : 0, c.lw,
                                                       c.st));
     ++g_launch_count;
+    if (c.sp_local) {  // the entering states are known now: correct each segment's first chunks
+        c.mark();
+        const int nfix = rank > 0 ? c.pl.nseg : c.pl.nseg - 1;  // rank 0 carries nothing into segment 0
+        if (nfix > 0) {
+            const CUtensorMap tq = c.tmap<__nv_bfloat16>(c.q), to = c.tmap<__nv_bfloat16>(c.o);
+            LMOE_CUDA_CHECK(lmoe_dev::launch_local_fix_bf16(c.var.decay, dim3(nfix, c.H, c.B), c.st, tq, to, c.p));
+            ++g_launch_count;
+        }
+        c.mark();
+        return;
+    }
     c.output_pass<T>();
 }
 
@@ -442,10 +504,13 @@ extern "C" int lmoe_lsm_fwd_plan(const lmoe_lsm_desc* desc, int B, int N, int H,
         LsmCall c{desc, B, N, N, H, D, dtype, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, pl,
                   nullptr, nullptr};
         c.var.decay = device_decay_mode(desc->instance);
+        c.var.fm = desc->feature_map;
         c.norm = desc->use_normalizer != 0;
         c.vec = c.var.decay == lmoe_dev::kDecayTokenVector;
+        c.p.log_a = c.var.decay == lmoe_dev::kDecayConst ? logf(desc->scalar_decay) : 0.f;
         const bool f = c.var.decay >= 0 && c.fused_ok();
-        info[0] = f ? 1 : 0;
+        const bool loc = !f && c.var.decay >= 0 && c.local_ok();
+        info[0] = f ? 1 : (loc ? 2 : 0);
         info[1] = f ? pl.fnseg : pl.nseg;
         info[2] = f ? pl.fseg_len : pl.seg_len;
         info[3] = f ? pl.fP : pl.nseg;
@@ -574,6 +639,12 @@ void lsm_mixer_core(const lmoe_lsm_desc* desc, int B, int N_local, int H, int D,
             c.check_err();
             return;
         }
+        if (c.local_ok() && z_out == nullptr) {  // local-state forward (phases: output, -, combine, fix)
+            c.local_pass(nullptr, M_out);
+            c.finish_timing();
+            c.check_err();
+            return;
+        }
         if (dtype == LMOE_BF16) c.state_pass<__nv_bfloat16>();
         else c.state_pass<float>();
         c.combine(nullptr, nullptr, true, M_out, z_out, nullptr, 0);
@@ -677,7 +748,10 @@ extern "C" int lmoe_sp_lsm_fwd_loopback(const lmoe_lsm_desc* desc, int B, int N,
             LsmCall c = slice_call(r);
             const bool last = r == world - 1;
             if (dtype == LMOE_BF16) {
+                // the slices share the segment-state region: recompute this slice's states; in the
+                // local-state mode phase A already wrote its output from zero states
                 c.state_pass<__nv_bfloat16>();
+                c.sp_local = c.local_ok();
                 sp_phase_b<__nv_bfloat16>(c, gathered, r, M0, z0, last ? M_out : nullptr, last ? z_out : nullptr);
             } else {
                 c.state_pass<float>();

@@ -566,12 +566,14 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
         auto nval = [&](int c) { return min(kC, t_end - chunk_t0(c)); };
         load_gates<DECAY>(p, b, h, chunk_t0(0), nval(0), lane, bvA);
         if (nchunks > 1) load_gates<DECAY>(p, b, h, chunk_t0(1), nval(1), lane, bvB);
+        float gtot = 0.f;  // the segment's total log decay (local-state mode)
         for (int c = 0; c < nchunks; ++c) {
             const int slot = c & 1;
             if (c + 2 < nchunks) load_gates<DECAY>(p, b, h, chunk_t0(c + 2), nval(c + 2), lane, bvC);
             if (c >= 2) mbar_wait(&gfree[slot], ((c >> 1) - 1) & 1);
             float G[4], kf[4];
             const float gend = chunk_scan<DECAY>(p, bvA, nval(c), spa, lane, G, kf);
+            gtot += gend;
             // split e^{G_i - G_j} = e^{G_i - r_Q} e^{r_Q - G_j} per 32-key quarter Q (lane / 8),
             // r_Q = G at the quarter's last key: the key factor is <= 1 and the query factor
             // only exceeds 1 on the diagonal block, so both stay finite while every quarter's
@@ -599,6 +601,7 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) { bvA[u] = bvB[u]; bvB[u] = bvC[u]; }
         }
+        if (p.local && lane == 0) p.logDseg[(size_t)bh * p.nseg + seg] = gtot;
     } else if (warp == 3) {
         // ---------------- O store warp (bf16 O): bulk-store each staged chunk, then release
         // its stage once the store has read the tile, off the math warps' path
@@ -692,9 +695,14 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
             float vals[DH];
             const size_t mslot = p.nomask ? (size_t)bh : (size_t)bh * p.nseg + seg;
             const float* src = p.Min + (mslot * D + (sown ? srow : 0)) * D + hh * DH;
+            bool have = sown;
+            if (p.local) {  // local-state mode: only segment 0 enters with a state (Mloc0)
+                have = sown && seg == 0 && p.Mloc0 != nullptr;
+                src = have ? p.Mloc0 + ((size_t)bh * D + srow) * D + hh * DH : nullptr;
+            }
 #pragma unroll
             for (int j = 0; j < DH; j += 4) {
-                const float4 v = sown ? *reinterpret_cast<const float4*>(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 v = have ? *reinterpret_cast<const float4*>(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
                 vals[j] = v.x; vals[j + 1] = v.y; vals[j + 2] = v.z; vals[j + 3] = v.w;
             }
             mbar_wait(&gfull[0], 0);
@@ -1067,11 +1075,180 @@ __global__ void __launch_bounds__(output_pass_threads<T>(), 1)
             }
             if (NST == 1 && kPrep && c + 1 < nchunks) prep(c + 1);
         }
+        // local-state mode: the segment's final state (TMEM M after the last chunk's dM, which
+        // the last iteration's mo_full wait covered) -> Sseg, the combine's input
+        if (p.local && sown) {
+            float* dst = p.Sseg + (((size_t)bh * p.nseg + seg) * D + srow) * D + hh * DH;
+#pragma unroll
+            for (int cb = 0; cb < DH / 32; ++cb) {
+                uint32_t r[32];
+                tmem_ld32(tM + lane_off + hh * DH + cb * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(dst + cb * 32 + j) =
+                        make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                    __uint_as_float(r[j + 3]));
+            }
+        }
     }
     tc_fence_before();
     __syncthreads();
     trace_cta(p, 1);
     if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ====================================================================================
+// Local-state correction (decaying scalar kinds, bf16, identity feature map).  The output
+// pass ran every segment from a zero state; with M_in(s) from the segment combine the exact
+// output is
+//     o_t = o_t^local + (q_t e^{Gseg_t}) M_in(s),   Gseg_t = log decay from the segment start
+//                                                   through token t (inclusive)
+// and e^{Gseg_t} only decreases along the segment, so the correction stops at the first chunk
+// that starts below e^{-88} (the fp32 normal range: below it the term is smaller than any
+// representable output difference).  For Mamba2 / Lightning / RetNet that is a few chunks
+// per segment, so the step reads q, k, v once (no state pass).  One CTA per (segment, head):
+// thread 0 issues TMA and the MMAs; the 8 warps transform Q~ and add the product to O.
+// ====================================================================================
+constexpr int kFixThreads = 256;
+constexpr int fix_smem() { return 3 * kTileBytes + 128 * 4 + 64; }
+
+template <int DECAY>
+__global__ void __launch_bounds__(kFixThreads, 1)
+    lsm_local_fix(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, LsmFwdParams p) {
+    using T = __nv_bfloat16;
+    using TT = TileTraits<T>;
+    constexpr int D = 128;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* qt = smem;                   // Q~ tile
+    uint8_t* ot = smem + kTileBytes;      // O tile (read, updated, stored)
+    uint8_t* mop = smem + 2 * kTileBytes; // bf16 M_in operand (the output pass's layout)
+    float* sG = reinterpret_cast<float*>(smem + 3 * kTileBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sG + 128);
+    uint64_t* full = bars;
+    uint64_t* mma_done = bars + 1;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 2);
+    __shared__ float sGcum, sGend;
+
+    const int seg = p.nseg - (int)gridDim.x + blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // the last gridDim.x segments
+    const int bh = b * p.H + h;
+    const int t_begin = seg * p.seg_len;
+    const int t_end = min(p.N, t_begin + p.seg_len);
+    const int nchunks = (t_end - t_begin + kC - 1) / kC;
+    const int warp = warp_id(), lane = lane_id(), tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(full, 1);
+        mbar_init(mma_done, 1);
+        fence_barrier_init();
+        sGcum = 0.f;
+    }
+    if (warp == 0) tmem_alloc<128>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+    pdl_wait();
+    pdl_trigger();
+    // M_in(seg) -> bf16 operand: thread (row, column half)
+    {
+        const int row = tid & 127, half = tid >> 7;
+        const float* src = p.Min + (((size_t)bh * p.nseg + seg) * D + row) * D + half * 64;
+        uint8_t* dst = mop + half * (D * 128);
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+            const float4 a = *reinterpret_cast<const float4*>(src + ch * 8);
+            const float4 c = *reinterpret_cast<const float4*>(src + ch * 8 + 4);
+            uint4 v;
+            v.x = pack_bf16(a.x, a.y); v.y = pack_bf16(a.z, a.w);
+            v.z = pack_bf16(c.x, c.y); v.w = pack_bf16(c.z, c.w);
+            *reinterpret_cast<uint4*>(dst + sw128_off(row, ch)) = v;
+        }
+    }
+    const float spa = (DECAY == kDecayTokenScalar) ? softplus_f(p.a_raw[h]) : 0.f;
+    const int q = warp & 3, half = warp >> 2;  // TMEM lane quarter, column half
+    const int row = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    for (int c = 0; c < nchunks; ++c) {
+        __syncthreads();  // sGcum of the previous chunk, previous O store read
+        if (sGcum < -88.f) break;  // every later factor is below the fp32 normal range
+        const int t0 = t_begin + c * kC;
+        const int nvalid = min(kC, t_end - t0);
+        if (tid == 0) {
+            bulk_wait_read0();  // the previous chunk's O store has read the tile
+            mbar_expect_tx(full, 4 * kBlockBytes);
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) {
+                tma_load_4d(qt + blk * kBlockBytes, &tmQ, full, blk * TT::EPB, h, t0, b);
+                tma_load_4d(ot + blk * kBlockBytes, &tmO, full, blk * TT::EPB, h, t0, b);
+            }
+        }
+        if (warp == 0) {  // the chunk's inclusive log decay G_t (chunk-local), as the decay warp
+            float bv[4], G[4], kf[4];
+            load_gates<DECAY>(p, b, h, t0, nvalid, lane, bv);
+            const float gend = chunk_scan<DECAY>(p, bv, nvalid, spa, lane, G, kf);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sG[lane * 4 + u] = G[u];
+            if (lane == 0) sGend = gend;
+        }
+        __syncthreads();
+        mbar_wait(full, c & 1);
+        // Q~ = q e^{Gcum + G_t} in place: thread (row = tid % 128, column half)
+        {
+            const int r2 = tid & 127, hf = tid >> 7;
+            const float f = r2 < nvalid ? __expf(sGcum + sG[r2]) : 0.f;
+            xform_chunks<T, 0, false, 8>(qt + hf * kBlockBytes, r2, 0, f);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            constexpr uint32_t idQM = umma_idesc(1, 0, 1, 128, D);
+            const uint32_t qa = smem_u32(qt), mb = smem_u32(mop);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t off = (kk >> 2) * kBlockBytes + (kk & 3) * 32;
+                mma_ss_f16(tmem, umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(mb + kk * 16 * 128, D * 128, 1024),
+                           idQM, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(mma_done);
+        }
+        mbar_wait(mma_done, c & 1);
+        tc_fence_after();
+        // O += Q~ M_in for this thread's row and 64 columns, in the O tile, then one bulk store
+        {
+            uint32_t r[64];
+            tmem_ld32(tmem + lane_off + half * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+            tmem_ld32(tmem + lane_off + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+            tmem_wait_ld();
+            uint8_t* ob = ot + half * kBlockBytes;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                uint4* ptr = reinterpret_cast<uint4*>(ob + sw128_off(row, ch));
+                uint4 v = *ptr;
+                uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = unpack_bf16(w[e]);
+                    w[e] = pack_bf16(f.x + __uint_as_float(r[ch * 8 + 2 * e]), f.y + __uint_as_float(r[ch * 8 + 2 * e + 1]));
+                }
+                *ptr = v;
+            }
+        }
+        tc_fence_before();
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_4d(&tmO, ot, 0, h, t0, b);
+            tma_store_4d(&tmO, ot + kBlockBytes, TT::EPB, h, t0, b);
+            bulk_commit();
+            sGcum += sGend;
+        }
+    }
+    if (tid == 0) bulk_wait0();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<128>(tmem);
 }
 
 }  // namespace lmoe_dev

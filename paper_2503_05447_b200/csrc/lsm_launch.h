@@ -40,6 +40,9 @@ struct LsmVariant {
     int rev = 0;  // reverse-time backward pass (fm = 0, norm = 0)
 };
 
+// local-state correction of the output pass (lsm_local_fix): grid (nseg - 1, H, B)
+cudaError_t launch_local_fix_bf16(int decay, dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& o,
+                                  const LsmFwdParams& p);
 cudaError_t launch_state_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
                                    const CUtensorMap& val, const LsmFwdParams& p);
 cudaError_t launch_output_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,

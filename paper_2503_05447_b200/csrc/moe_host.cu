@@ -7,6 +7,9 @@
 
 namespace lmoe_host {
 
+// blocks of the routing kernel (a warp per token, 8 per block, at most 8 blocks per SM)
+static int route_blocks(int T) { return std::min((T + 7) / 8, num_sms() * 8); }
+
 struct MoePlanWs {
     size_t logits, ids, gates, colsum, counts, offsets, group_end, tile_group, tile_row0, num_tiles,
         aux, blk_cnt, blk_base, slot_pos, perm_token, x_perm, h, y_perm, dense_tiles, total;
@@ -23,7 +26,7 @@ static MoePlanWs plan_moe(int T, int hidden, int ffn, int E, int K) {
     w.logits = take((size_t)T * E * 4);
     w.ids = take(rows * 4);
     w.gates = take(rows * 4);
-    w.colsum = take((size_t)E * 4);
+    w.colsum = take((size_t)route_blocks(T) * E * 4);  // per route block partial column sums
     w.counts = take((size_t)E * 4);
     w.offsets = take((size_t)(E + 1) * 4);
     w.group_end = take((size_t)E * 4);
@@ -79,8 +82,7 @@ __global__ void router_small(const __nv_bfloat16* __restrict__ x, const __nv_bfl
 static void route_core(const float* logits, int T, int E, int K, int* ids, float* gates, float* probs,
                        int* counts, float* colsum, cudaStream_t st) {
     LMOE_CUDA_CHECK(cudaMemsetAsync(counts, 0, E * 4, st));
-    LMOE_CUDA_CHECK(cudaMemsetAsync(colsum, 0, E * 4, st));
-    const dim3 grid(std::min((T + 7) / 8, num_sms() * 8));
+    const dim3 grid(route_blocks(T));
     if (E <= 32) lmoe_dev::moe_route<1><<<grid, 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
     else if (E <= 64) lmoe_dev::moe_route<2><<<grid, 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
     else if (E <= 128) lmoe_dev::moe_route<4><<<grid, 256, 0, st>>>(logits, T, E, K, ids, gates, probs, counts, colsum);
@@ -145,7 +147,7 @@ extern "C" int lmoe_moe_route(const float* logits, int T, int E, int top_k, int*
         cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
         float* colsum = reinterpret_cast<float*>(ws + w.colsum);
         route_core(logits, T, E, top_k, ids, gates, probs, counts, colsum, st);
-        lmoe_dev::moe_plan<<<1, 256, 0, st>>>(counts, colsum, T, E, top_k,
+        lmoe_dev::moe_plan<<<1, 256, 0, st>>>(counts, colsum, route_blocks(T), T, E, top_k,
                                              reinterpret_cast<int*>(ws + w.offsets),
                                              reinterpret_cast<int*>(ws + w.group_end),
                                              reinterpret_cast<int*>(ws + w.tile_group),
@@ -206,7 +208,7 @@ extern "C" int lmoe_moe_forward(int T, int hidden, int ffn, int E, int top_k, co
         // 2. route + counts + probability column sums
         route_core(logits, T, E, top_k, ids, gates, nullptr, P(w.counts), colsum, st);
         // 3. offsets, GEMM tile list, aux loss
-        lmoe_dev::moe_plan<<<1, 256, 0, st>>>(P(w.counts), colsum, T, E, top_k, P(w.offsets), P(w.group_end),
+        lmoe_dev::moe_plan<<<1, 256, 0, st>>>(P(w.counts), colsum, route_blocks(T), T, E, top_k, P(w.offsets), P(w.group_end),
                                              P(w.tile_group), P(w.tile_row0), P(w.num_tiles),
                                              aux ? aux : reinterpret_cast<float*>(ws + w.aux));
         // 4. stable dispatch positions (tokens ascending within each expert)

@@ -205,12 +205,12 @@ __global__ void __launch_bounds__(256) moe_route(const float* __restrict__ logit
                                                  int* __restrict__ ids, float* __restrict__ gates,
                                                  float* __restrict__ probs, int* __restrict__ counts,
                                                  float* __restrict__ prob_colsum) {
-    // per-block expert counts / probability sums: warps reduce into shared memory, and one
-    // global atomic per block and expert follows (per-warp global atomics on the same
-    // addresses serialised at L2)
+    // per-block expert counts (integer atomics) and probability column sums: each warp keeps
+    // its own row of partial sums, summed in warp order, and the block writes its partial to
+    // prob_colsum[block][e] (no float atomics: the aux loss is bitwise repeatable)
     __shared__ int s_cnt[32 * NE];
-    __shared__ float s_ps[32 * NE];
-    for (int i = threadIdx.x; i < 32 * NE; i += blockDim.x) { s_cnt[i] = 0; s_ps[i] = 0.f; }
+    __shared__ float s_ps[8][32 * NE];
+    for (int i = threadIdx.x; i < 32 * NE; i += blockDim.x) s_cnt[i] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int wglobal = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -300,16 +300,20 @@ __global__ void __launch_bounds__(256) moe_route(const float* __restrict__ logit
             base += __popc(m);
         }
     }
+    const int warp = threadIdx.x >> 5;
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
-        if (!has[i]) continue;
-        if (cnt[i]) atomicAdd(&s_cnt[lane + 32 * i], cnt[i]);
-        atomicAdd(&s_ps[lane + 32 * i], ps[i]);
+        s_ps[warp][lane + 32 * i] = ps[i];
+        if (has[i] && cnt[i]) atomicAdd(&s_cnt[lane + 32 * i], cnt[i]);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < E; i += blockDim.x) {
         if (s_cnt[i]) atomicAdd(&counts[i], s_cnt[i]);
-        if (prob_colsum) atomicAdd(&prob_colsum[i], s_ps[i]);
+        if (prob_colsum) {
+            float t = 0.f;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_ps[w][i];
+            prob_colsum[(size_t)blockIdx.x * E + i] = t;
+        }
     }
 }
 template __global__ void moe_route<1>(const float*, int, int, int, int*, float*, float*, int*, float*);
@@ -321,7 +325,7 @@ template __global__ void moe_route<8>(const float*, int, int, int, int*, float*,
 // offsets[e] = sum_{e'<e} counts[e']; per group the 128-row GEMM tiles;
 // aux = E * sum_e (counts_e / (T k)) (colsum_e / T)   (moe.hpp:90-103)
 __global__ void __launch_bounds__(256) moe_plan(const int* __restrict__ counts, const float* __restrict__ prob_colsum,
-                                                int T, int E, int K, int* __restrict__ offsets,
+                                                int nrb, int T, int E, int K, int* __restrict__ offsets,
                                                 int* __restrict__ group_end, int* __restrict__ tile_group,
                                                 int* __restrict__ tile_row0, int* __restrict__ num_tiles,
                                                 float* __restrict__ aux) {
@@ -341,7 +345,10 @@ __global__ void __launch_bounds__(256) moe_plan(const int* __restrict__ counts, 
     }
     if (tid < E) {
         const int c = counts[tid];
-        s_aux[tid] = prob_colsum ? ((double)c / ((double)T * K)) * ((double)prob_colsum[tid] / T) : 0.0;
+        double colsum = 0.0;  // the route blocks' partials, in block order
+        if (prob_colsum)
+            for (int bk = 0; bk < nrb; ++bk) colsum += prob_colsum[(size_t)bk * E + tid];
+        s_aux[tid] = prob_colsum ? ((double)c / ((double)T * K)) * (colsum / T) : 0.0;
     }
     __syncthreads();
     if (tid <= E) offsets[tid] = s_off[tid];

@@ -44,7 +44,7 @@ template <int NE>
 __global__ void moe_route(const float* __restrict__ logits, int T, int E, int K, int* __restrict__ ids,
                           float* __restrict__ gates, float* __restrict__ probs, int* __restrict__ counts,
                           float* __restrict__ prob_colsum);
-__global__ void moe_plan(const int* __restrict__ counts, const float* __restrict__ prob_colsum, int T,
+__global__ void moe_plan(const int* __restrict__ counts, const float* __restrict__ prob_colsum, int nrb, int T,
                          int E, int K, int* __restrict__ offsets, int* __restrict__ group_end,
                          int* __restrict__ tile_group, int* __restrict__ tile_row0,
                          int* __restrict__ num_tiles, float* __restrict__ aux);

@@ -168,12 +168,14 @@ def lsm_forward_batched(q, k, v, gates, spec, chunk_size=64, initial_state=None,
 
 
 def forward_plan(spec, B, N, H, D, dtype=torch.bfloat16):
-    """lmoe_lsm_fwd_plan: {"fused": single-read persistent kernel?, "segments", "seg_len",
-    "ctas_per_head"} for a [B, N, H, D] forward of this spec."""
+    """lmoe_lsm_fwd_plan: {"fused": single-read persistent kernel?, "local": local-state output
+    pass + combine + correction (no state pass)?, "segments", "seg_len", "ctas_per_head"} for a
+    [B, N, H, D] forward of this spec."""
     info = (ctypes.c_int * 4)()
     desc = make_desc(spec, 64)
     _lib.check(_lib.lib().lmoe_lsm_fwd_plan(ctypes.byref(desc), B, N, H, D, _DTYPES[dtype], info))
-    return {"fused": bool(info[0]), "segments": info[1], "seg_len": info[2], "ctas_per_head": info[3]}
+    return {"fused": info[0] == 1, "local": info[0] == 2, "segments": info[1], "seg_len": info[2],
+            "ctas_per_head": info[3]}
 
 
 def lsm_forward_chunked(q, k, v, gates, spec, chunk_size, final_state=None):
