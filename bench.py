@@ -5,8 +5,10 @@ config 3: per-token-decay LSM, seq 256K, H=16, d=128, bf16; SP over 1/2/4/8 GPUs
   torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU, NCCL)
 
 A step = one LSM forward over the whole 256K-token sequence, all 16 heads, split across
-ranks by chunk_range (parallel.hpp:192-197): local state pass, ONE ncclAllGather of the
-per-rank state payload, decayed prefix, output pass (lmoe_sp_lsm_fwd).  Inputs (3 x 1 GiB)
+ranks by chunk_range (parallel.hpp:192-197) through lmoe_sp_lsm_fwd.  For Mamba2 that is the
+local-state forward: the output pass from zero segment states, the segment combine (and at
+N > 1 ONE ncclAllGather of the per-rank state payload plus the decayed rank prefix), then the
+correction of each segment's first chunks.  Inputs (3 x 1 GiB)
 are resident in HBM and larger than L2, so no flush is needed between steps.  Timing:
 CUDA events on the launching stream, barrier + synchronize on both sides, max over ranks.
 Prints ONE JSON line on rank 0.

@@ -332,9 +332,10 @@ struct LsmCall {
     // corrected span is known: taken when it costs less than the state pass it replaces.
     bool local_ok() const {
         if (env_int("LMOE_LOCAL", 1) == 0 || fused_ok()) return false;
-        if (!(dt == LMOE_BF16 && D == 128 && !norm && !vec && var.rev == 0 && var.fm == 0 && p.mst == nullptr &&
+        if (!(dt == LMOE_BF16 && D == 128 && !norm && var.rev == 0 && var.fm == 0 && p.mst == nullptr &&
               !p.out_f32 && !p.nomask))
             return false;
+        if (vec) return env_int("LMOE_LOCAL_VEC", 1) != 0;  // lsm_local_fix_vec
         if (var.decay == lmoe_dev::kDecayTokenScalar) return true;
         if (var.decay != lmoe_dev::kDecayConst || !(p.log_a < 0.f)) return false;
         const double span_tokens = 88.0 / -(double)p.log_a;  // tokens until e^{G} < e^{-88}
@@ -351,14 +352,21 @@ struct LsmCall {
         p.local = 0;
         combine(M0, nullptr, true, M_out, nullptr, nullptr, 0);  // phase 2
         mark();
-        const int nfix = M0 ? pl.nseg : pl.nseg - 1;  // the last nfix segments
-        if (nfix > 0) {
-            const CUtensorMap tq = tmap<bf>(q), to = tmap<bf>(o);
-            LMOE_CUDA_CHECK(lmoe_dev::launch_local_fix_bf16(var.decay, dim3(nfix, H, B), st, tq, to, p));
-            ++g_launch_count;
-        }
-        mark();  // phase 3: the correction
+        local_fix(M0 ? pl.nseg : pl.nseg - 1);  // phase 3: the correction
         mark();
+    }
+    // correct the last nfix segments' first chunks with the entering states in p.Min
+    void local_fix(int nfix) {
+        using bf = __nv_bfloat16;
+        if (nfix <= 0) return;
+        const CUtensorMap tq = tmap<bf>(q), to = tmap<bf>(o);
+        if (vec) {
+            const CUtensorMap ta = tmap<bf>(a_pre);
+            LMOE_CUDA_CHECK(lmoe_dev::launch_local_fix_vec_bf16(dim3(nfix, H, B), st, tq, ta, to, p));
+        } else {
+            LMOE_CUDA_CHECK(lmoe_dev::launch_local_fix_bf16(var.decay, dim3(nfix, H, B), st, tq, to, p));
+        }
+        ++g_launch_count;
     }
     void clear_err() { LMOE_CUDA_CHECK(cudaMemsetAsync(p.err, 0, 64, st)); }
     void check_err() {
@@ -466,12 +474,7 @@ static void sp_phase_b(LsmCall& c, const float* gathered, int rank, float* M0, f
     ++g_launch_count;
     if (c.sp_local) {  // the entering states are known now: correct each segment's first chunks
         c.mark();
-        const int nfix = rank > 0 ? c.pl.nseg : c.pl.nseg - 1;  // rank 0 carries nothing into segment 0
-        if (nfix > 0) {
-            const CUtensorMap tq = c.tmap<__nv_bfloat16>(c.q), to = c.tmap<__nv_bfloat16>(c.o);
-            LMOE_CUDA_CHECK(lmoe_dev::launch_local_fix_bf16(c.var.decay, dim3(nfix, c.H, c.B), c.st, tq, to, c.p));
-            ++g_launch_count;
-        }
+        c.local_fix(rank > 0 ? c.pl.nseg : c.pl.nseg - 1);  // rank 0 carries nothing into segment 0
         c.mark();
         return;
     }

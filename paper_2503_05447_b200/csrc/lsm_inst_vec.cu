@@ -62,4 +62,10 @@ cudaError_t launch_output_pass_vec_f32(LsmVariant v, dim3 grid, cudaStream_t st,
     VEC_VARIANTS(opv, float, grid, st, q, k, val, a, o, p)
 }
 
+cudaError_t launch_local_fix_vec_bf16(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& a,
+                                      const CUtensorMap& o, const LsmFwdParams& p) {
+    if (cudaError_t e = ensure_smem((const void*)lsm_local_fix_vec<128>, fix_vec_smem()); e != cudaSuccess) return e;
+    return launch_pdl(lsm_local_fix_vec<128>, grid, dim3(kFixVecThreads), fix_vec_smem(), st, q, a, o, p);
+}
+
 }  // namespace lmoe_dev

@@ -43,6 +43,9 @@ struct LsmVariant {
 // local-state correction of the output pass (lsm_local_fix): grid (nseg - 1, H, B)
 cudaError_t launch_local_fix_bf16(int decay, dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& o,
                                   const LsmFwdParams& p);
+// the same for TokenVector decays (lsm_local_fix_vec, lsm_vec_kernels.cuh)
+cudaError_t launch_local_fix_vec_bf16(dim3 grid, cudaStream_t st, const CUtensorMap& q, const CUtensorMap& a,
+                                      const CUtensorMap& o, const LsmFwdParams& p);
 cudaError_t launch_state_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& k,
                                    const CUtensorMap& val, const LsmFwdParams& p);
 cudaError_t launch_output_pass_bf16(LsmVariant v, dim3 grid, cudaStream_t st, const CUtensorMap& q,

@@ -415,14 +415,16 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
         const int srow = TR ? q * 16 + lane : row;  // state row (d_k index)
         const bool sown = TR ? lane < 16 : true;
 
-        // initial state: M_T <- M_in (fp32), z <- z_in
+        // initial state: M_T <- M_in (fp32), z <- z_in; zero in local mode (lsm_local_fix_vec)
+        const bool local = kBF16 && p.local;
+        float gtot = 0.f;  // local mode, tid < D: the segment's log decay of column tid
         {
             const float* src = p.Min + (((size_t)bh * p.nseg + seg) * D + (sown ? srow : 0)) * D + hh * DH;
 #pragma unroll
             for (int cb = 0; cb < DH / 32; ++cb) {
                 uint32_t r[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(sown ? src[cb * 32 + j] : 0.f);
+                for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(sown && !local ? src[cb * 32 + j] : 0.f);
                 tmem_st32(tM + lane_off + hh * DH + cb * 32, r);
             }
             tmem_wait_st();
@@ -493,6 +495,8 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
                         pfx *= pg;
                     }
                     sEG[tid] = pfx;
+                    // both half products are >= e^{-80} unless the chunk raises the range error
+                    if (local) gtot += __logf(sfx) + __logf(pfx);
                 }
                 named_bar_sync(1, NM);
                 if (tid == 0) trace_mark(p, c, 1);
@@ -768,11 +772,192 @@ __global__ void __launch_bounds__(output_pass_vec_threads<T>(), 1)
             }
             if (tid == 0) trace_mark(p, c, 8);
         }
+        if constexpr (kBF16) {
+            if (local) {  // the segment's state from zero and its per-column log decay (combine inputs)
+                float* dst = p.Sseg + (((size_t)bh * p.nseg + seg) * D + srow) * D + hh * DH;
+                uint32_t r[32];
+                tmem_ld32(tM + lane_off + hh * DH, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                                      __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                if (tid < D) p.logDseg[((size_t)bh * p.nseg + seg) * D + tid] = gtot;
+            }
+        }
     }
     if (threadIdx.x == 128) bulk_wait_read0();  // smem must outlive the last O store's read of it
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ====================================================================================
+// Local-state correction, TokenVector decays (bf16, identity feature map; the vector
+// counterpart of lsm_local_fix, lsm_kernels.cuh).  The output pass ran every segment from a
+// zero state; with M_in(s) from the segment combine
+//     o_t = o_t^local + (q_t . E_t) M_in(s),   E_t[k] = prod_{u in seg, u <= t} sigmoid(a_u[k])
+// E_t only decreases along the segment, so the correction stops after the first chunk that
+// leaves every column below e^{-88}.  With a ~ N(0, 1) gates a column decays by ~e^{-0.8} per
+// token: one or two chunks per segment.  Thread (column d = tid % 128, row half tid / 128)
+// scans E down its column in linear space (sigmoid products; an underflow to zero is the
+// exact value's fp32 image) -- pass 1 the half's product, pass 2 the prefix and q~ = q E.
+// ====================================================================================
+constexpr int kFixVecThreads = 256;
+constexpr int fix_vec_smem() { return 4 * kTileBytes + 3 * 128 * 4 + 64; }
+
+template <int D>  // 128 (a template: this header is included by several translation units)
+__global__ void __launch_bounds__(kFixVecThreads, 1)
+    lsm_local_fix_vec(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmO, LsmFwdParams p) {
+    using T = __nv_bfloat16;
+    using TT = TileTraits<T>;
+    static_assert(D == TT::D, "bf16 tiles are 128 columns");
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if (smem_u32(smem) & 1023) __trap();
+    uint8_t* qt = smem;                    // Q~ tile
+    uint8_t* at = smem + kTileBytes;       // gate tile
+    uint8_t* ot = smem + 2 * kTileBytes;   // O tile (read, updated, stored)
+    uint8_t* mop = smem + 3 * kTileBytes;  // bf16 M_in operand
+    float* sP = reinterpret_cast<float*>(smem + 4 * kTileBytes);  // [D] E at the chunk start
+    float* sH = sP + D;                                           // [2][D] half products
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * D);
+    uint64_t* full = bars;
+    uint64_t* mma_done = bars + 1;
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(bars + 2);
+
+    const int seg = p.nseg - (int)gridDim.x + blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int bh = b * p.H + h;
+    const int t_begin = seg * p.seg_len;
+    const int t_end = min(p.N, t_begin + p.seg_len);
+    const int nchunks = (t_end - t_begin + kC - 1) / kC;
+    const int warp = warp_id(), lane = lane_id(), tid = threadIdx.x;
+    const int d = tid & 127, hf = tid >> 7;
+    if (tid == 0) {
+        mbar_init(full, 1);
+        mbar_init(mma_done, 1);
+        fence_barrier_init();
+    }
+    if (tid < D) sP[tid] = 1.f;
+    if (warp == 0) tmem_alloc<128>(sTmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *sTmem;
+    pdl_wait();
+    pdl_trigger();
+    {  // M_in(seg) -> bf16 operand: thread (row, column half)
+        const int row = tid & 127, half = tid >> 7;
+        const float* src = p.Min + (((size_t)bh * p.nseg + seg) * D + row) * D + half * 64;
+        uint8_t* dst = mop + half * (D * 128);
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+            const float4 a = *reinterpret_cast<const float4*>(src + ch * 8);
+            const float4 c = *reinterpret_cast<const float4*>(src + ch * 8 + 4);
+            uint4 v;
+            v.x = pack_bf16(a.x, a.y); v.y = pack_bf16(a.z, a.w);
+            v.z = pack_bf16(c.x, c.y); v.w = pack_bf16(c.z, c.w);
+            *reinterpret_cast<uint4*>(dst + sw128_off(row, ch)) = v;
+        }
+    }
+    const int q4 = warp & 3, half = warp >> 2;  // TMEM lane quarter, column half
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    bool alive = true;
+    for (int c = 0; c < nchunks; ++c) {
+        // the previous chunk's E update and O store read; stop once every column is below e^{-88}
+        if (!__syncthreads_or(alive)) break;
+        const int t0 = t_begin + c * kC;
+        const int nvalid = min(kC, t_end - t0);
+        if (tid == 0) {
+            bulk_wait_read0();
+            mbar_expect_tx(full, 6 * kBlockBytes);
+#pragma unroll
+            for (int blk = 0; blk < 2; ++blk) {
+                tma_load_4d(qt + blk * kBlockBytes, &tmQ, full, blk * TT::EPB, h, t0, b);
+                tma_load_4d(at + blk * kBlockBytes, &tmA, full, blk * TT::EPB, h, t0, b);
+                tma_load_4d(ot + blk * kBlockBytes, &tmO, full, blk * TT::EPB, h, t0, b);
+            }
+        }
+        mbar_wait(full, c & 1);
+        const int r0 = hf * 64, r1 = min(r0 + 64, nvalid);
+        auto sig = [&](int r) {
+            const float ex = ex2_ftz(-ld_elem<T>(at, r, d) * 1.4426950408889634f);
+            return rcp_ftz(1.f + ex);
+        };
+        {  // pass 1: this half's product
+            float pr = 1.f;
+            for (int r = r0; r < r1; ++r) pr *= sig(r);
+            sH[hf * D + d] = pr;
+        }
+        __syncthreads();
+        {  // pass 2: inclusive prefix, q~ = q E (rows past the sequence end: 0)
+            float e = sP[d] * (hf ? sH[d] : 1.f);
+            for (int r = r0; r < r0 + 64; ++r) {
+                float x = 0.f;
+                if (r < r1) {
+                    e *= sig(r);
+                    x = ld_elem<T>(qt, r, d) * e;
+                }
+                st_elem<T>(qt, r, d, x);
+            }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            constexpr uint32_t idQM = umma_idesc(1, 0, 1, 128, D);
+            const uint32_t qa = smem_u32(qt), mb = smem_u32(mop);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const uint32_t off = (kk >> 2) * kBlockBytes + (kk & 3) * 32;
+                mma_ss_f16(tmem, umma_desc_sw128(qa + off, 16, 1024), umma_desc_sw128(mb + kk * 16 * 128, D * 128, 1024),
+                           idQM, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(mma_done);
+        }
+        if (tid < D) {
+            const float e = sP[d] * sH[d] * sH[D + d];
+            sP[d] = e;
+            alive = e > 6.05e-39f;  // e^{-88}
+        } else {
+            alive = false;
+        }
+        mbar_wait(mma_done, c & 1);
+        tc_fence_after();
+        {  // O += Q~ M_in for this thread's row and 64 columns, in the O tile, then one bulk store
+            uint32_t r[64];
+            tmem_ld32(tmem + lane_off + half * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+            tmem_ld32(tmem + lane_off + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+            tmem_wait_ld();
+            uint8_t* ob = ot + half * kBlockBytes;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                uint4* ptr = reinterpret_cast<uint4*>(ob + sw128_off(row, ch));
+                uint4 v = *ptr;
+                uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = unpack_bf16(w[e]);
+                    w[e] = pack_bf16(f.x + __uint_as_float(r[ch * 8 + 2 * e]), f.y + __uint_as_float(r[ch * 8 + 2 * e + 1]));
+                }
+                *ptr = v;
+            }
+        }
+        tc_fence_before();
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_4d(&tmO, ot, 0, h, t0, b);
+            tma_store_4d(&tmO, ot + kBlockBytes, TT::EPB, h, t0, b);
+            bulk_commit();
+        }
+    }
+    if (tid == 0) bulk_wait0();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<128>(tmem);
 }
 
 template <typename T>

@@ -4,7 +4,9 @@ produces the entering states, and the first chunks of each segment get (q e^{Gse
 until the decay from the segment start leaves the fp32 range -- no state pass.  It must equal
 the segment-parallel three-pass path (LMOE_LOCAL=0) and the float64 oracle (lsm_forward_chunked,
 lsm.hpp:668-708), final state and carried-in initial state included, for strong, default and
-long-memory decays (the last makes the correction span whole segments)."""
+long-memory decays (the last makes the correction span whole segments).  The TokenVector kinds
+(GLA, HGRN2, RWKV6) take the same structure with per-column decay (lsm_local_fix_vec,
+lsm_vec_kernels.cuh), checked the same way with gates from strong to slow decay."""
 import numpy as np
 import pytest
 
@@ -31,6 +33,9 @@ def _case(torch, inst, N, H, gate_mean, a_raw, seed):
     if inst == "mamba2":
         spec.mamba2_a_raw = torch.full((H,), float(a_raw), device="cuda")
         gates = pk.LsmGates(b_pre=torch.randn(1, N, H, device="cuda", generator=g).mul_(0.5).add_(gate_mean))
+    elif inst in ("gla", "hgrn2", "rwkv6"):
+        a = torch.randn(1, N, H, D, device="cuda", generator=g).mul_(a_raw).add_(gate_mean)
+        gates = pk.LsmGates(a_pre=a.to(torch.bfloat16))
     M0 = torch.randn(1, H, D, D, device="cuda", generator=g).mul_(0.05)
     return pk, q, k, v, spec, gates, M0
 
@@ -41,6 +46,12 @@ def _case(torch, inst, N, H, gate_mean, a_raw, seed):
     ("mamba2", 5000, 2, 2.0, 2.0),       # strong decay
     ("mamba2", 60000, 16, 0.0, 0.3),     # 9 long segments per head (the cfg3 layout)
     ("lightning", 120000, 16, 0.0, 0.0),  # constant decay, segments longer than the corrected span
+    # TokenVector: (gate mean, gate std) -- a ~ N(0, 1) as the bench, slow columns, long memory
+    ("gla", 60000, 16, 0.0, 1.0),
+    ("gla", 20000, 2, 2.0, 0.5),          # sigma ~ 0.88: ~6 corrected chunks
+    ("gla", 9000, 2, 5.0, 0.3),           # sigma ~ 0.993: corrections span whole segments
+    ("hgrn2", 20000, 2, 1.0, 1.0),
+    ("rwkv6", 20000, 2, 0.0, 1.0),
 ])
 def test_local_equals_three_pass_and_oracle(monkeypatch, inst, N, H, gate_mean, a_raw):
     torch = _torch()
@@ -61,12 +72,14 @@ def test_local_equals_three_pass_and_oracle(monkeypatch, inst, N, H, gate_mean, 
     assert e < 1e-2 and em < 1e-2, (e, em)
     for h in sorted({0, H - 1}):
         sd = oracle.spec_default(inst)
-        b = None
+        b = a = None
         if inst == "mamba2":
             sd["mamba2_a_raw"] = float(a_raw)
             b = gates.b_pre[0, :, h].cpu().numpy()
-        want, wM, _ = oracle.lsm_chunked(sd, *(t[0, :, h].float().cpu().numpy() for t in (q, k, v)), b_pre=b,
-                                         M0=M0[0, h].double().cpu().numpy())
+        if gates is not None and gates.a_pre is not None:
+            a = gates.a_pre[0, :, h].float().cpu().numpy()
+        want, wM, _ = oracle.lsm_chunked(sd, *(t[0, :, h].float().cpu().numpy() for t in (q, k, v)), a_pre=a,
+                                         b_pre=b, M0=M0[0, h].double().cpu().numpy())
         err = norm_rel_err(o1[0, :, h].cpu().numpy(), want)
         errM = norm_rel_err(m1[0, h].cpu().numpy(), wM)
         record_parity("local_vs_oracle/%s/%d/h%d" % (inst, N, h), err, 2e-2)
@@ -74,7 +87,7 @@ def test_local_equals_three_pass_and_oracle(monkeypatch, inst, N, H, gate_mean, 
 
 
 def test_local_plan_selection():
-    """Decaying scalar kinds take the local path; undecayed, vector-decay, normalised and short
+    """Decaying scalar and vector kinds take the local path; undecayed, normalised and short
     constant-decay shapes (where the corrected span would cost more than the state pass) do not."""
     _torch()
     import paper_2503_05447_b200 as pk
@@ -83,5 +96,6 @@ def test_local_plan_selection():
     assert pk.lsm.forward_plan(mk("retnet", D), 1, 262144, 16, D)["local"]
     assert not pk.lsm.forward_plan(mk("retnet", D), 1, 32768, 16, D)["local"]
     assert not pk.lsm.forward_plan(pk.LsmSpec(instance=0, feature_map=0), 1, 262144, 16, D)["local"]
-    assert not pk.lsm.forward_plan(mk("gla", D), 1, 262144, 16, D)["local"]
+    assert pk.lsm.forward_plan(mk("gla", D), 1, 262144, 16, D)["local"]
+    assert pk.lsm.forward_plan(mk("hgrn2", D), 1, 262144, 16, D)["local"]
     assert not pk.lsm.forward_plan(mk("bla", D), 1, 262144, 16, D)["local"]
