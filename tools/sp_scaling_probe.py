@@ -49,6 +49,14 @@ for inst in ("mamba2", "gla"):
             e1.record(st)
             torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 50
+        # evented phases of the same call outside the graph (phase layout: lsm_host.cu marks)
+        from paper_2503_05447_b200 import _lib
+        _lib.timing_read(8)
+        for _ in range(10):
+            sp.sp_lsm_masked_rank(cm, q, k, v, gates, spec, 64, out=out, check=False, timing=True)
+        torch.cuda.synchronize()
+        calls, ph = _lib.timing_read(8)
+        print("  phases (ms, evented, not graphed):", " ".join("%.4f" % (x / max(calls, 1)) for x in ph))
         base = base or ms
         gather_ms = 0.0 if T == 1 else ((T - 1) * PAYLOAD / 770e9 + 10e-6) * 1e3
         print("%s T=%d slice=%d: %.3f ms per rank step (graph, NCCL 1-rank); + modelled gather %.3f ms; "
