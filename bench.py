@@ -287,6 +287,7 @@ def backward_bench(dev, steps=3, warmup=2):
 
 OUTPASS_NCU = "profiles/r2_lsm_output_pass.ncu.txt"
 FUSED_NCU = "profiles/r2_lsm_fused_fwd.ncu.txt"
+LOCAL_NCU = "profiles/r2_local_output_pass.ncu.txt"  # the output pass in local-state mode (default)
 
 
 def ncu_traffic(rel=OUTPASS_NCU):
@@ -802,6 +803,7 @@ def main():
             extra["hybrid"] = hybrid_bench(dev, cpu=not args.no_cpu_baseline)
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference(args.instance, SEQ, os.cpu_count() or 1, 20.0)
+        prof_file = FUSED_NCU if fused else (LOCAL_NCU if plan.get("local") else OUTPASS_NCU)
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -812,9 +814,9 @@ def main():
                        "l2": "inputs 3 GiB > L2; no flush needed"},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": ncu_traffic(FUSED_NCU if fused else OUTPASS_NCU),
+                         "frac": achieved / hbm, "traffic": ncu_traffic(prof_file),
                          "peak_source": src,
-                         "traffic_source": (FUSED_NCU if fused else OUTPASS_NCU) + " (ncu --set full, one launch)",
+                         "traffic_source": prof_file + " (ncu --set full, one launch)",
                          "kernel": "lsm_fused_fwd" if fused else "lsm_output_pass",
                          "plan": plan,
                          "alg_bytes_per_launch": alg_bytes,
