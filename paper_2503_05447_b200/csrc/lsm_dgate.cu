@@ -6,7 +6,7 @@
 // (with the initial / final states as extra keys / queries).  The telescoped form
 // sum_{t >= j} (phi(q_t).dphi(q_t) - keff_t.dkeff_t) cancels nearly equal totals, which
 // bf16 operand rounding cannot survive.  Here every term is a product of fp32 tensor-core
-// accumulators, evaluated per 128-token chunk c (one CTA, fully parallel):
+// accumulators, evaluated per 128-token chunk c (persistent CTAs, chunks independent):
 //     dg_j = C(j) + sum_{t in [j, end]} X_t + sum_{s in [start, j)} Y_s + e^{g_c} <M_c, dM_c>
 //   C(j)  within-chunk straddle: C(j) = sum_{i < j} (colsum_i - rowsum_i) of strictly
 //         lower A (S = phiQ phiK^T and dP = dO V^T on tcgen05, A in fp32 registers)
@@ -21,18 +21,6 @@
 
 namespace lmoe_dev {
 
-// L2 prefetch distance of the gate kernel in CTAs (one wave = the SM count); LMOE_DG_PF = waves
-static int dgate_pf_ahead() {
-    static int v = -1;
-    if (v < 0) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const char* e = getenv("LMOE_DG_PF");
-        v = (e ? atoi(e) : 1) * sms;
-    }
-    return v;
-}
 namespace {
 
 __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x)); }
@@ -93,7 +81,7 @@ struct DgateSmem {
     static constexpr int kQ = 0, kK = kTileBytes, kV = 2 * kTileBytes, kO = 3 * kTileBytes;
     static constexpr int kM = 4 * kTileBytes, kDM = kM + kMT;
     static constexpr int kMisc = kDM + kMT;  // sG, sKf, 5 x [2][128] partials, scratch, barriers
-    static constexpr int kTotal = kMisc + (2 + 5 * 4) * 128 * 4 + 32 * 4 + 64;
+    static constexpr int kTotal = kMisc + (2 + 5 * 4) * 128 * 4 + 64 * 4 + 64;
 };
 
 }  // namespace
@@ -102,6 +90,9 @@ struct DgateSmem {
 // w / 4 of every row-wise phase; the 128-entry scans run on warps 0-3 (named barrier 1).
 constexpr int kDgNH = 4;
 constexpr int kDgThreads = 128 * kDgNH;
+// MMA-issuing thread.  Issuing the next chunk's MMAs from warp 4 during this chunk's final
+// scans was measured slower (2.34 vs 2.24 ms at config 3) than issuing at the chunk start.
+constexpr int kDgMma = 0;
 
 // 128-thread inclusive prefix sum over warps 0-3 (named barrier 1); `ws` holds 4 floats
 __device__ __forceinline__ float scan128_w03(float x, float* ws) {
@@ -117,6 +108,25 @@ __device__ __forceinline__ float scan128_w03(float x, float* ws) {
     for (int i = 0; i < warp; ++i) x += ws[i];
     return x;
 }
+// three inclusive prefix sums at once over warps 0-3 (named barrier 1); `ws` holds 12 floats;
+// tb receives the total of b
+__device__ __forceinline__ void scan3_w03(float& a, float& b, float& c, float& tb, float* ws) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float ya = __shfl_up_sync(0xFFFFFFFFu, a, o);
+        const float yb = __shfl_up_sync(0xFFFFFFFFu, b, o);
+        const float yc = __shfl_up_sync(0xFFFFFFFFu, c, o);
+        if (lane >= o) { a += ya; b += yb; c += yc; }
+    }
+    if (lane == 31) { ws[warp] = a; ws[4 + warp] = b; ws[8 + warp] = c; }
+    named_bar_sync(1, 128);
+    float pa = 0.f, pb = 0.f, pc = 0.f;
+    for (int i = 0; i < warp; ++i) { pa += ws[i]; pb += ws[4 + i]; pc += ws[8 + i]; }
+    tb = ws[4] + ws[5] + ws[6] + ws[7];
+    named_bar_sync(1, 128);  // ws reusable
+    a += pa; b += pb; c += pc;
+}
 __device__ __forceinline__ float sum128_w03(float x, float* ws) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
@@ -126,6 +136,27 @@ __device__ __forceinline__ float sum128_w03(float x, float* ws) {
     return ws[0] + ws[1] + ws[2] + ws[3];
 }
 
+// Column sums of a warp's 32 x 32 block (row = lane, column = register): a butterfly
+// transpose-reduce, 31 shuffles; returns the sum of column `lane`.
+__device__ __forceinline__ float warp_colsum32(float (&a)[32]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const bool up = (lane & w) != 0;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+            const float send = up ? a[i] : a[i + w];
+            const float keep = up ? a[i + w] : a[i];
+            a[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, w);
+        }
+    }
+    return a[0];
+}
+
+// Persistent: CTA i takes chunks lin = i, i + grid, ... (lin = c + nchunk * bh).  One set of
+// tiles per CTA; every tile is consumed (MMAs committed, row reads of K / O / V and the M, dM
+// dot done) before the A-matrix phase, so the next chunk's loads are issued at that point and
+// land while this chunk's straddle sums, scans and gate outputs run.
 template <typename T>
 __global__ void __launch_bounds__(kDgThreads, 1)
     lsm_mamba_dgate(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -133,7 +164,7 @@ __global__ void __launch_bounds__(kDgThreads, 1)
                     const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmDM,
                     const float* __restrict__ b_pre, const float* __restrict__ a_raw,
                     const float* __restrict__ dkf, const T* __restrict__ dk, float* __restrict__ db_pre,
-                    float* __restrict__ da_raw, int N, int H, int nchunk, int p_pf_ahead) {
+                    float* __restrict__ da_raw, int N, int H, int nchunk, int total, int p_pf_ahead) {
     using TT = TileTraits<T>;
     using L = DgateSmem<T>;
     constexpr int D = TT::D;
@@ -142,25 +173,22 @@ __global__ void __launch_bounds__(kDgThreads, 1)
     float* sG = reinterpret_cast<float*>(smem + L::kMisc);
     float* sKf = sG + 128;
     constexpr int NH = kDgNH;
-    float* sX = sKf + 128;   // [NH][128] row-part partials: X, Y, row sums, column sums, dkf
-    float* sY = sX + NH * 128;
+    float* sX = sKf + 128;   // [NH][128] partials: X, Y, row sums (per column part), column sums
+    float* sY = sX + NH * 128;  // (per row quadrant), dkf
     float* sR = sY + NH * 128;
     float* sC = sR + NH * 128;
     float* sF = sC + NH * 128;
-    float* ws = sF + NH * 128;  // 32 floats scratch
-    uint64_t* bar = reinterpret_cast<uint64_t*>(ws + 32);
+    float* ws = sF + NH * 128;  // 64 floats scratch: [0, 4) scans, [8, 24) <M, dM> parts, [32, 44) scan3
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ws + 64);
     uint64_t* mma_done = bar + 1;
     uint32_t* sTmem = reinterpret_cast<uint32_t*>(bar + 2);
 
-    const int c = blockIdx.x, bh = blockIdx.y;
-    const int b = bh / H, h = bh % H;
-    const int t0 = c * kC;
-    const int nvalid = min(kC, N - t0);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t = (warp & 3) * 32 + lane;  // TMEM lane == query row t
     const int hc = warp >> 2;              // column part of the row-wise phases
     constexpr int PW = D / NH;             // state columns per thread (bf16 32, tf32 16)
-    constexpr int SW = 128 / NH;           // S / dP columns (and A rows) per thread
+    constexpr int SW = 128 / NH;           // S / dP columns per thread
+    static_assert(SW == 32, "one 32-column block of S / dP per thread");
 
     if (tid == 0) {
         mbar_init(bar, 1);
@@ -173,9 +201,11 @@ __global__ void __launch_bounds__(kDgThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *sTmem;
 
-    if (tid == 0) {
-        mbar_expect_tx(bar, 4 * kTileBytes + 2 * L::kMT);
+    // all six tiles of chunk `lin` on `bar` (thread 0), and an L2 prefetch p_pf_ahead chunks on
+    auto issue = [&](int lin) {
+        const int c = lin % nchunk, bh = lin / nchunk, b = bh / H, h = bh % H, t0 = c * kC;
         const int mrow = (bh * nchunk + c) * D;
+        mbar_expect_tx(bar, 4 * kTileBytes + 2 * L::kMT);
 #pragma unroll
         for (int blk = 0; blk < 2; ++blk) {
             tma_load_4d(smem + L::kQ + blk * kBlockBytes, &tmQ, bar, blk * TT::EPB, h, t0, b);
@@ -185,64 +215,29 @@ __global__ void __launch_bounds__(kDgThreads, 1)
             tma_load_2d(smem + L::kM + blk * MBLK, &tmM, bar, blk * TT::EPB, mrow);
             tma_load_2d(smem + L::kDM + blk * MBLK, &tmDM, bar, blk * TT::EPB, mrow);
         }
-        // warm L2 with the tiles of the CTA one wave ahead (one CTA per SM, linear launch order)
-        if (p_pf_ahead > 0) {
-            const long long lin = c + (long long)gridDim.x * bh + p_pf_ahead;
-            if (lin < (long long)gridDim.x * gridDim.y) {
-                const int c2 = (int)(lin % gridDim.x), bh2 = (int)(lin / gridDim.x);
-                const int b2 = bh2 / H, h2 = bh2 % H, t2 = c2 * kC, mrow2 = (bh2 * nchunk + c2) * D;
+        const long long l2 = (long long)lin + p_pf_ahead;
+        if (p_pf_ahead > 0 && l2 < total) {
+            const int c2 = (int)(l2 % nchunk), bh2 = (int)(l2 / nchunk);
+            const int b2 = bh2 / H, h2 = bh2 % H, t2 = c2 * kC, mrow2 = (bh2 * nchunk + c2) * D;
 #pragma unroll
-                for (int blk = 0; blk < 2; ++blk) {
-                    tma_prefetch_l2_4d(&tmQ, blk * TT::EPB, h2, t2, b2);
-                    tma_prefetch_l2_4d(&tmK, blk * TT::EPB, h2, t2, b2);
-                    tma_prefetch_l2_4d(&tmV, blk * TT::EPB, h2, t2, b2);
-                    tma_prefetch_l2_4d(&tmO, blk * TT::EPB, h2, t2, b2);
-                    tma_prefetch_l2_2d(&tmM, blk * TT::EPB, mrow2);
-                    tma_prefetch_l2_2d(&tmDM, blk * TT::EPB, mrow2);
-                }
+            for (int blk = 0; blk < 2; ++blk) {
+                tma_prefetch_l2_4d(&tmQ, blk * TT::EPB, h2, t2, b2);
+                tma_prefetch_l2_4d(&tmK, blk * TT::EPB, h2, t2, b2);
+                tma_prefetch_l2_4d(&tmV, blk * TT::EPB, h2, t2, b2);
+                tma_prefetch_l2_4d(&tmO, blk * TT::EPB, h2, t2, b2);
+                tma_prefetch_l2_2d(&tmM, blk * TT::EPB, mrow2);
+                tma_prefetch_l2_2d(&tmDM, blk * TT::EPB, mrow2);
             }
         }
-    }
-    // gates while the tiles land: g_t = -softplus(b_t) softplus(a_h), kf_t = softplus(b_t)
-    const float spa = softplus_f(a_raw[h]);
-    float bv = 0.f, kf = 0.f;
-    if (t < nvalid) {
-        bv = b_pre[((size_t)b * N + t0 + t) * H + h];
-        kf = softplus_f(bv);
-    }
-    // dkf_t = phi(k_t) . dkeff_t: given, or from dk = kf dkeff (identity feature map); the
-    // global dk row is read before the tiles are needed (latency overlaps the TMA loads)
-    float dkrow[PW];
-    const bool dk_direct = dkf == nullptr;
-    if (dk_direct && t < nvalid) {
-        const T* dkr = dk + (((size_t)b * N + t0 + t) * H + h) * D + hc * PW;
-        if constexpr (sizeof(T) == 2) {
-#pragma unroll
-            for (int j = 0; j < PW; j += 8) {
-                const uint4 u = *reinterpret_cast<const uint4*>(dkr + j);
-                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 f = unpack_bf16(w[e]);
-                    dkrow[j + 2 * e] = f.x;
-                    dkrow[j + 2 * e + 1] = f.y;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < PW; ++j) dkrow[j] = dkr[j];
-        }
-    }
-    if (warp < 4) {
-        const float G = scan128_w03(t < nvalid ? -kf * spa : 0.f, ws);
-        sG[t] = G;
-        sKf[t] = kf;
-    }
-    if (tid == 0) {
-        mbar_wait(bar, 0);
+    };
+    if (tid == 0 && (int)blockIdx.x < total) issue(blockIdx.x);
+
+    // S = phiQ phiK^T (cols 0..127), dP = dO V^T (128..255), Z = phiQ M_c (256..),
+    // W = phiK dM_c (384..): all operands K-major.  Issued by thread kDgMma once the chunk's
+    // tiles have landed (phase `phase` of `bar`); the previous chunk's TMEM reads are done.
+    auto issue_mma = [&](uint32_t phase) {
+        mbar_wait(bar, phase);
         tc_fence_after();
-        // S = phiQ phiK^T (cols 0..127), dP = dO V^T (128..255), Z = phiQ M_c (256..),
-        // W = phiK dM_c (384..): all operands K-major
         constexpr uint32_t idSq = umma_idesc(TT::FMT, 0, 0, 128, 128);
         constexpr uint32_t idSt = umma_idesc(TT::FMT, 0, 0, 128, D);
         const uint32_t q = smem_u32(smem + L::kQ), k = smem_u32(smem + L::kK);
@@ -266,169 +261,209 @@ __global__ void __launch_bounds__(kDgThreads, 1)
             }
         }
         mma_commit(mma_done);
-    }
-    __syncthreads();  // sG / sKf visible
-    const float gend = sG[127];
-    // B_c partial: <M_c, dM_c> over this thread's 16-byte slices of the (identically laid out) tiles
-    float bpart = 0.f;
-    {
-        const uint8_t* pm = smem + L::kM + tid * 16;
-        const uint8_t* pd = smem + L::kDM + tid * 16;
-        mbar_wait(bar, 0);
-#pragma unroll 4
-        for (int i = 0; i < L::kMT; i += kDgThreads * 16) {
-            const uint4 a = *reinterpret_cast<const uint4*>(pm + i);
-            const uint4 d = *reinterpret_cast<const uint4*>(pd + i);
-            const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, dw[4] = {d.x, d.y, d.z, d.w};
+    };
+    auto load_b = [&](int lin) -> float {
+        if (lin >= total) return 0.f;
+        const int c = lin % nchunk, bh = lin / nchunk, t0 = c * kC;
+        return t < min(kC, N - t0) ? b_pre[((size_t)(bh / H) * N + t0 + t) * H + bh % H] : 0.f;
+    };
+    float bv_next = load_b(blockIdx.x);
+    uint32_t ph = 0;
+    for (int lin = blockIdx.x; lin < total; lin += gridDim.x, ph ^= 1u) {
+        const int c = lin % nchunk, bh = lin / nchunk;
+        const int b = bh / H, h = bh % H;
+        const int t0 = c * kC;
+        const int nvalid = min(kC, N - t0);
+        // gates: g_t = -softplus(b_t) softplus(a_h), kf_t = softplus(b_t); b_t was loaded one
+        // chunk ahead, the next chunk's is requested now
+        const float spa = softplus_f(a_raw[h]);
+        const float bv = t < nvalid ? bv_next : 0.f;
+        const float kf = t < nvalid ? softplus_f(bv) : 0.f;
+        bv_next = load_b(lin + gridDim.x);
+        // dkf_t = phi(k_t) . dkeff_t: given, or from dk = kf dkeff (identity feature map); the
+        // global dk row is read before the tiles are needed (latency overlaps the TMA loads)
+        // raw words: unpacked where they are used, so the load latency stays hidden
+        constexpr int NRAW = sizeof(T) == 2 ? PW / 8 : PW / 4;
+        uint4 dkraw[NRAW];
+        const bool dk_direct = dkf == nullptr;
+        if (dk_direct && t < nvalid) {
+            const uint4* dkr = reinterpret_cast<const uint4*>(dk + (((size_t)b * N + t0 + t) * H + h) * D + hc * PW);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if constexpr (sizeof(T) == 2) {
-                    const float2 fa = unpack_bf16(aw[e]), fd = unpack_bf16(dw[e]);
-                    bpart += fa.x * fd.x + fa.y * fd.y;
-                } else {
-                    bpart += __uint_as_float(aw[e]) * __uint_as_float(dw[e]);
+            for (int j = 0; j < NRAW; ++j) dkraw[j] = __ldg(dkr + j);
+        }
+        if (tid == kDgMma) issue_mma(ph);  // first: the MMAs do not need the gates
+        if (warp < 4) {
+            const float G = scan128_w03(t < nvalid ? -kf * spa : 0.f, ws);
+            sG[t] = G;
+            sKf[t] = kf;
+        }
+        __syncthreads();  // sG / sKf visible
+        const float gend = sG[127];
+        // B_c partial: <M_c, dM_c> over this thread's 16-byte slices of the (identically laid out) tiles
+        float bpart = 0.f;
+        {
+            const uint8_t* pm = smem + L::kM + tid * 16;
+            const uint8_t* pd = smem + L::kDM + tid * 16;
+            mbar_wait(bar, ph);
+#pragma unroll 4
+            for (int i = 0; i < L::kMT; i += kDgThreads * 16) {
+                const uint4 a = *reinterpret_cast<const uint4*>(pm + i);
+                const uint4 d = *reinterpret_cast<const uint4*>(pd + i);
+                const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, dw[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if constexpr (sizeof(T) == 2) {
+                        const float2 fa = unpack_bf16(aw[e]), fd = unpack_bf16(dw[e]);
+                        bpart += fa.x * fd.x + fa.y * fd.y;
+                    } else {
+                        bpart += __uint_as_float(aw[e]) * __uint_as_float(dw[e]);
+                    }
                 }
             }
         }
-    }
-    // dkf_t partial from this half of the K row
-    float dkf_part = 0.f;
-    if (dk_direct && t < nvalid) {
-        float vk[32];
-        tile_row32<T>(smem + L::kK, kBlockBytes, t, (hc * PW) & ~31, vk);
+        // dkf_t partial from this part of the K row
+        float dkf_part = 0.f;
+        if (dk_direct && t < nvalid) {
+            float dkrow[PW];
 #pragma unroll
-        for (int j = 0; j < PW; ++j) dkf_part += vk[j] * dkrow[j];
-        if (PW == 16 && (hc & 1)) {  // odd parts: the upper 16 of the 32 loaded columns
-            dkf_part = 0.f;
+            for (int j = 0; j < NRAW; ++j) {
+                const uint32_t w[4] = {dkraw[j].x, dkraw[j].y, dkraw[j].z, dkraw[j].w};
+                if constexpr (sizeof(T) == 2) {
 #pragma unroll
-            for (int j = 0; j < PW; ++j) dkf_part += vk[(16 + j) & 31] * dkrow[j];
-        }
-    }
-    mbar_wait(mma_done, 0);
-    tc_fence_after();
-    const uint32_t lo = (uint32_t)((warp & 3) * 32) << 16;
-    // X_t, Y_t partials from this half of the Z, W rows against dO / V rows (smem)
-    float xs = 0.f, ys = 0.f;
-    {
-        static_assert(PW == 32 || PW == 16, "state columns per thread");
-        const int col = hc * PW;
-        uint32_t rz[32], rw[32];
-        if constexpr (PW == 32) {
-            tmem_ld32(tmem + 256 + lo + col, rz);
-            tmem_ld32(tmem + 384 + lo + col, rw);
-        } else {
-            uint32_t z16[16], w16[16];
-            tmem_ld16(tmem + 256 + lo + col, z16);
-            tmem_ld16(tmem + 384 + lo + col, w16);
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f = unpack_bf16(w[e]);
+                        dkrow[j * 8 + 2 * e] = f.x;
+                        dkrow[j * 8 + 2 * e + 1] = f.y;
+                    }
+                } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) { rz[j] = z16[j]; rw[j] = w16[j]; }
-        }
-        tmem_wait_ld();
-        float vo[32], vv[32];
-        tile_row32<T>(smem + L::kO, kBlockBytes, t, col & ~31, vo);
-        tile_row32<T>(smem + L::kV, kBlockBytes, t, col & ~31, vv);
-        // static register indices (PW == 16: odd parts read the upper half of the 32 loaded)
-        if (PW == 32 || (hc & 1) == 0) {
-#pragma unroll
-            for (int j = 0; j < PW; ++j) {
-                xs += __uint_as_float(rz[j]) * vo[j];
-                ys += __uint_as_float(rw[j]) * vv[j];
+                    for (int e = 0; e < 4; ++e) dkrow[j * 4 + e] = __uint_as_float(w[e]);
+                }
             }
-        } else {
+            float vk[32];
+            tile_row32<T>(smem + L::kK, kBlockBytes, t, (hc * PW) & ~31, vk);
 #pragma unroll
-            for (int j = 0; j < PW; ++j) {
-                xs += __uint_as_float(rz[j]) * vo[(16 + j) & 31];
-                ys += __uint_as_float(rw[j]) * vv[(16 + j) & 31];
+            for (int j = 0; j < PW; ++j) dkf_part += vk[j] * dkrow[j];
+            if (PW == 16 && (hc & 1)) {  // odd parts: the upper 16 of the 32 loaded columns
+                dkf_part = 0.f;
+#pragma unroll
+                for (int j = 0; j < PW; ++j) dkf_part += vk[(16 + j) & 31] * dkrow[j];
             }
         }
-    }
-    sX[hc * 128 + t] = xs;
-    sY[hc * 128 + t] = ys;
-    sF[hc * 128 + t] = dkf_part;
-    const float Gt = sG[t];
-    __syncthreads();  // all MMAs consumed Q/K (mma_done) and all threads past their tile reads
-    // strictly lower A_ts = S_ts kf_s dP_ts e^{G_t - G_s} (s < t), this thread's 64 columns:
-    // row sums here, rows to shared memory (XOR-swizzled by t) for the column sums
-    float* As = reinterpret_cast<float*>(smem + L::kQ);  // 128 x 128 fp32 over the Q, K tiles
-    float rsum = 0.f;
+        mbar_wait(mma_done, ph);
+        tc_fence_after();
+        const uint32_t lo = (uint32_t)((warp & 3) * 32) << 16;
+        // X_t, Y_t partials from this part of the Z, W rows against dO / V rows (smem)
+        float xs = 0.f, ys = 0.f;
+        {
+            static_assert(PW == 32 || PW == 16, "state columns per thread");
+            const int col = hc * PW;
+            uint32_t rz[32], rw[32];
+            if constexpr (PW == 32) {
+                tmem_ld32(tmem + 256 + lo + col, rz);
+                tmem_ld32(tmem + 384 + lo + col, rw);
+            } else {
+                uint32_t z16[16], w16[16];
+                tmem_ld16(tmem + 256 + lo + col, z16);
+                tmem_ld16(tmem + 384 + lo + col, w16);
 #pragma unroll
-    for (int cb = 0; cb < SW / 32; ++cb) {
-        const int s0 = hc * SW + cb * 32;
-        uint32_t rs[32], rp[32];
-        tmem_ld32(tmem + lo + s0, rs);
-        tmem_ld32(tmem + 128 + lo + s0, rp);
-        tmem_wait_ld();
+                for (int j = 0; j < 16; ++j) { rz[j] = z16[j]; rw[j] = w16[j]; }
+            }
+            tmem_wait_ld();
+            float vo[32], vv[32];
+            tile_row32<T>(smem + L::kO, kBlockBytes, t, col & ~31, vo);
+            tile_row32<T>(smem + L::kV, kBlockBytes, t, col & ~31, vv);
+            // static register indices (PW == 16: odd parts read the upper half of the 32 loaded)
+            if (PW == 32 || (hc & 1) == 0) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const int s = s0 + j;
-            float a = 0.f;
-            if (s < t) a = __uint_as_float(rs[j]) * __uint_as_float(rp[j]) * sKf[s] * __expf(Gt - sG[s]);
-            rsum += a;
-            As[t * 128 + (s ^ (t & 31))] = a;
-        }
-    }
-    sR[hc * 128 + t] = rsum;
-    __syncthreads();
-    // column t over rows r > t, this thread's half of the rows; four independent accumulators
-    // so the shared-memory loads pipeline (rows r <= t are zero in the strictly lower A)
-    {
-        float c4[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int j = 0; j < PW; ++j) {
+                    xs += __uint_as_float(rz[j]) * vo[j];
+                    ys += __uint_as_float(rw[j]) * vv[j];
+                }
+            } else {
 #pragma unroll
-        for (int rr = 0; rr < SW; rr += 4) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int r = hc * SW + rr + u;
-                c4[u] += As[r * 128 + (t ^ (r & 31))];
+                for (int j = 0; j < PW; ++j) {
+                    xs += __uint_as_float(rz[j]) * vo[(16 + j) & 31];
+                    ys += __uint_as_float(rw[j]) * vv[(16 + j) & 31];
+                }
             }
         }
-        sC[hc * 128 + t] = (c4[0] + c4[1]) + (c4[2] + c4[3]);
-    }
-    __syncthreads();
-    if (warp < 4) {
-        float xsum = 0.f, ysum = 0.f, rs = 0.f, cs = 0.f;
+        sX[hc * 128 + t] = xs;
+        sY[hc * 128 + t] = ys;
+        sF[hc * 128 + t] = dkf_part;
+        const float Gt = sG[t];
+        __syncthreads();  // MMAs committed, every tile read done: the tiles are free
+        if (tid == 0 && lin + (int)gridDim.x < total) issue(lin + gridDim.x);
+        // strictly lower A_ts = S_ts kf_s dP_ts e^{G_t - G_s} (s < t) over this thread's 32
+        // columns: row sums in the thread, column sums by the warp transpose-reduce
+        float rsum = 0.f, csum;
+        {
+            const int s0 = hc * SW;
+            uint32_t rs[32], rp[32];
+            tmem_ld32(tmem + lo + s0, rs);
+            tmem_ld32(tmem + 128 + lo + s0, rp);
+            tmem_wait_ld();
+            float a[32];
 #pragma unroll
-        for (int i = 0; i < NH; ++i) {
-            xsum += sX[i * 128 + t]; ysum += sY[i * 128 + t];
-            rs += sR[i * 128 + t]; cs += sC[i * 128 + t];
+            for (int j = 0; j < 32; ++j) {
+                const int s = s0 + j;
+                a[j] = 0.f;
+                if (s < t) a[j] = __uint_as_float(rs[j]) * __uint_as_float(rp[j]) * sKf[s] * __expf(Gt - sG[s]);
+                rsum += a[j];
+            }
+            csum = warp_colsum32(a);
         }
-        const float X = t < nvalid ? __expf(Gt) * xsum : 0.f;
-        const float Y = t < nvalid ? __expf(gend - Gt) * sKf[t] * ysum : 0.f;
-        // dg_t = C(t) + sum_{u >= t} X_u + sum_{s < t} Y_s + e^{g_c} <M_c, dM_c>
-        const float dlt = cs - rs;
-        const float Cin = scan128_w03(dlt, ws) - dlt;    // exclusive prefix
-        const float Xin = scan128_w03(X, ws);
-        const float Xtot = sum128_w03(X, ws);
-        const float Xsuf = Xtot - Xin + X;
-        const float Yin = scan128_w03(Y, ws);
-        const float Ypre = Yin - Y;
-        sX[t] = Cin + Xsuf + Ypre;  // dg without the boundary term
-    }
-    // boundary term over all 256 threads
+        sR[hc * 128 + t] = rsum;
+        sC[(warp & 3) * 128 + hc * SW + lane] = csum;  // column hc*32+lane over row quadrant warp&3
+        __syncthreads();
+        if (warp < 4) {
+            float xsum = 0.f, ysum = 0.f, rs = 0.f, cs = 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bpart += __shfl_xor_sync(0xFFFFFFFFu, bpart, o);
-    if (lane == 0) ws[8 + warp] = bpart;
-    __syncthreads();
-    if (warp < 4) {
-        float Bc = 0.f;
-#pragma unroll
-        for (int i = 0; i < 4 * NH; ++i) Bc += ws[8 + i];
-        Bc *= __expf(gend);
-        const float dg = sX[t] + Bc;
-        float dkf_t = 0.f;
-        if (t < nvalid) {
-            float f = 0.f;
-#pragma unroll
-            for (int i = 0; i < NH; ++i) f += sF[i * 128 + t];
-            dkf_t = dk_direct ? f / kf : dkf[(size_t)bh * N + t0 + t];
+            for (int i = 0; i < NH; ++i) {
+                xsum += sX[i * 128 + t]; ysum += sY[i * 128 + t];
+                rs += sR[i * 128 + t]; cs += sC[i * 128 + t];
+            }
+            const float X = t < nvalid ? __expf(Gt) * xsum : 0.f;
+            const float Y = t < nvalid ? __expf(gend - Gt) * sKf[t] * ysum : 0.f;
+            // dg_t = C(t) + sum_{u >= t} X_u + sum_{s < t} Y_s + e^{g_c} <M_c, dM_c>
+            const float dlt = cs - rs;
+            float Cin = dlt, Xin = X, Yin = Y, Xtot;
+            scan3_w03(Cin, Xin, Yin, Xtot, ws + 32);  // inclusive prefixes, one barrier pair
+            Cin -= dlt;                               // exclusive
+            const float Xsuf = Xtot - Xin + X;
+            const float Ypre = Yin - Y;
+            sX[t] = Cin + Xsuf + Ypre;  // dg without the boundary term
         }
-        float dr = 0.f;
-        if (t < nvalid) {
-            const size_t row = ((size_t)b * N + t0 + t) * H + h;
-            db_pre[row] = sigm(bv) * (dkf_t - spa * dg);
-            dr = dg * -kf;
+        // boundary term over all threads
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) bpart += __shfl_xor_sync(0xFFFFFFFFu, bpart, o);
+        if (lane == 0) ws[8 + warp] = bpart;
+        __syncthreads();
+        if (warp < 4) {
+            float Bc = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4 * NH; ++i) Bc += ws[8 + i];
+            Bc *= __expf(gend);
+            const float dg = sX[t] + Bc;
+            float dkf_t = 0.f;
+            if (t < nvalid) {
+                float f = 0.f;
+#pragma unroll
+                for (int i = 0; i < NH; ++i) f += sF[i * 128 + t];
+                dkf_t = dk_direct ? f / kf : dkf[(size_t)bh * N + t0 + t];
+            }
+            float dr = 0.f;
+            if (t < nvalid) {
+                const size_t row = ((size_t)b * N + t0 + t) * H + h;
+                db_pre[row] = sigm(bv) * (dkf_t - spa * dg);
+                dr = dg * -kf;
+            }
+            dr = sum128_w03(dr, ws);
+            if (tid == 0) atomicAdd(da_raw + h, dr * sigm(a_raw[h]));
         }
-        dr = sum128_w03(dr, ws);
-        if (tid == 0) atomicAdd(da_raw + h, dr * sigm(a_raw[h]));
+        tc_fence_before();
+        __syncthreads();  // TMEM, sG / sKf and the partials are reused by the next chunk
+        tc_fence_after();
     }
     tc_fence_before();
     __syncthreads();
@@ -443,11 +478,21 @@ static cudaError_t dgate_t(const CUtensorMap& q, const CUtensorMap& k, const CUt
     constexpr int smem = DgateSmem<T>::kTotal;
     if (cudaError_t e = ensure_smem((const void*)lsm_mamba_dgate<T>, smem); e != cudaSuccess) return e;
     const int nchunk = (N + kC - 1) / kC;
-    cudaError_t e = cudaMemsetAsync(da_raw, 0, sizeof(float) * H, st);
-    if (e != cudaSuccess) return e;
-    lsm_mamba_dgate<T><<<dim3(nchunk, B * H), kDgThreads, smem, st>>>(q, k, v, dO, m, dm, b_pre, a_raw, dkf,
-                                                                static_cast<const T*>(dk), db_pre, da_raw, N, H,
-                                                                nchunk, dgate_pf_ahead());
+    const int total = nchunk * B * H;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // L2 prefetch distance in chunks beyond the directly loaded next one (LMOE_DG_PF waves)
+    const char* e = getenv("LMOE_DG_PF");
+    const int pf = (e ? atoi(e) : 0) * sms;  // off: the next chunk's direct loads overlap already
+    int grid = std::min(total, sms);
+    if (const char* g = getenv("LMOE_DG_GRID"))  // test knob: fewer CTAs, many chunks each
+        grid = std::max(1, std::min(grid, atoi(g)));
+    cudaError_t r = cudaMemsetAsync(da_raw, 0, sizeof(float) * H, st);
+    if (r != cudaSuccess) return r;
+    lsm_mamba_dgate<T><<<grid, kDgThreads, smem, st>>>(q, k, v, dO, m, dm, b_pre, a_raw, dkf,
+                                                       static_cast<const T*>(dk), db_pre, da_raw, N, H,
+                                                       nchunk, total, pf > 0 ? pf + grid : 0);
     return cudaGetLastError();
 }
 

@@ -181,6 +181,16 @@ def test_bwd_matches_oracle(case):
         assert rel < gtol, (name, "da_raw", got["da_raw"], want["da_raw"])
 
 
+@pytest.mark.parametrize("case", [c for c in CASES if c[0] in ("mamba2_long", "mamba2_strong", "mamba2_f32")],
+                         ids=lambda c: c[0])
+def test_dgate_persistent_many_chunks_per_cta(case, monkeypatch):
+    """The gate kernel is persistent (one CTA per SM, chunks lin = i, i + grid, ...); with 5
+    CTAs every CTA runs many chunks, so the next-chunk load overlap and the per-chunk barrier
+    phases are exercised at test sizes."""
+    monkeypatch.setenv("LMOE_DG_GRID", "5")
+    test_bwd_matches_oracle(case)
+
+
 @pytest.mark.parametrize("inst", [2, 13])
 def test_final_state_gradient_matches_finite_differences(inst):
     """dM_final path: d/dtheta [<dO, O> + <dMf, M_N>] vs central differences of the f64 oracle."""
