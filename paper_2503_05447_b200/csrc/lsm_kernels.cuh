@@ -257,7 +257,10 @@ __global__ void __launch_bounds__(kStatePassThreads, 1)
         for (int it = 0; it < nchunks; ++it) {
             const int slot = it & 1;
             if (it + 2 < nchunks) load_gates<DECAY>(p, b, h, chunk_t0(it + 2), nval(it + 2), lane, bvC);
-            if (it >= 2) mbar_wait(&wfree[slot], ((it >> 1) - 1) & 1);
+            // the math warps release a ring slot only when they read it (kXform); without the
+            // transform nothing reads the ring, and waiting here deadlocked every decay-free bf16
+            // segment of three or more chunks
+            if (kXform && it >= 2) mbar_wait(&wfree[slot], ((it >> 1) - 1) & 1);
             float la[4], kf[4];
             const float gend = chunk_scan<DECAY>(p, bvA, nval(it), spa, lane, la, kf);
 #pragma unroll

@@ -381,3 +381,22 @@ def test_recurrent_kinds_random_heads_and_errors():
         lsm_forward_recurrent(q, k, v, pk.LsmGates(), pk.LsmSpec.make("deltanet", D))
     with pytest.raises(pk.LmoeError, match="chunk-parallel form"):
         lsm_forward_recurrent(q, k, v, None, pk.LsmSpec.make("retnet", D))
+
+
+@pytest.mark.parametrize("N", [2305, 2433])
+def test_decay_free_bf16_long_segments(N):
+    """A decay-free bf16 state pass with identity map and no normaliser has no per-token
+    transform; its decay warp must not wait for ring-slot releases nobody makes.  At H = 16
+    these lengths plan 3-chunk segments (the deadlock hit every segment of >= 3 chunks)."""
+    import torch
+    import paper_2503_05447_b200 as pk
+    H = 16
+    g = torch.Generator(device="cuda").manual_seed(N)
+    q, k, v = (torch.randn(1, N, H, 128, device="cuda", generator=g).mul_(0.5).to(torch.bfloat16) for _ in range(3))
+    plain = pk.LsmSpec(instance=pk.LsmInstance.BLA, feature_map=0, use_normalizer=False)
+    o = pk.lsm_forward_batched(q, k, v, None, plain, 64)
+    torch.cuda.synchronize()
+    sd = dict(oracle.spec_default(0), feature_map=0, use_normalizer=0)
+    for h in (0, H - 1):
+        want, _, _ = oracle.lsm_chunked(sd, *(t[0, :, h].float().cpu().numpy() for t in (q, k, v)), chunk=64)
+        assert norm_rel_err(o[0, :, h].float().cpu().numpy(), want) < 2e-2
