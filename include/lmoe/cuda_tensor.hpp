@@ -16,7 +16,9 @@
 // Bridge rules (all exact except the stated device precision):
 //   * head dims are zero-padded to the kernel width (fp32 path D = 64 when d <= 64 and the
 //     decay is not per-column; otherwise bf16 D = 128).  Zero columns of q, k, v leave every
-//     output and state entry unchanged, so the padding is exact.
+//     output and state entry unchanged, so the padding is exact -- provided phi(0) = 0.  The
+//     elu+1 map has phi(0) = 1, so with padding the bridge applies it on the host (in f64,
+//     lsm.hpp feature map) and runs the device with the identity map.
 //   * f64 / f32 Tensors are rounded to the device type (fp32 -> tf32 tensor cores, or bf16);
 //     results are returned in the input Tensor's dtype.  North-star bounds: norm-relative
 //     1e-3 (fp32 path) / 2e-2 (bf16 path) against the reference in f64.
@@ -28,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -129,6 +132,7 @@ struct LsmDev {
     LsmPlan pl;
     int n;
     DevBuf q, k, v, o, a_pre, b_pre, a_raw, M, z;
+    bool host_fmap = false;  // elu+1 applied here (padded columns must map to 0)
     LsmDev(const lmoe::Tensor& qm, const lmoe::Tensor& km, const lmoe::Tensor& vm, const lmoe::LsmGates& g, const lmoe::LsmSpec& spec)
         : pl(plan_for(spec)), n(qm.shape()[0]),
           q((size_t)n * pl.D * (pl.bf16 ? 2 : 4)), k((size_t)n * pl.D * (pl.bf16 ? 2 : 4)),
@@ -145,8 +149,19 @@ struct LsmDev {
             const auto img = pack(t, n, cols, pl.D, pl.bf16);
             h2d(b.p, img.data(), img.size());
         };
-        up(q, qm, dk);
-        up(k, km, dk);
+        host_fmap = spec.feature_map == lmoe::FeatureMap::EluPlusOne && dk < pl.D;
+        if (host_fmap) {
+            auto phi = [&](const lmoe::Tensor& t) {
+                std::vector<double> y(t.data());
+                for (double& e : y) e = e > 0.0 ? e + 1.0 : std::exp(e);  // elu(x) + 1
+                return lmoe::Tensor::from_data({n, dk}, std::move(y));
+            };
+            up(q, phi(qm), dk);
+            up(k, phi(km), dk);
+        } else {
+            up(q, qm, dk);
+            up(k, km, dk);
+        }
         up(v, vm, dv);
         if (a_pre.p) {
             if (!g.a_pre.defined()) throw Error(LMOE_ERR_ARG, "lsm_forward_chunked: gates.a_pre required for this instance");
@@ -210,7 +225,8 @@ inline lmoe::Tensor lsm_forward_chunked(const lmoe::Tensor& q_mat, const lmoe::T
     spec.validate();  // the reference's own checks and texts ("LsmSpec: normalizer unsupported ...")
     if (chunk_size < 1) throw std::runtime_error("lsm_forward_chunked: chunk_size must be >= 1");
     bridge::LsmDev x(q_mat, k_mat, v_mat, gates, spec);
-    const lmoe_lsm_desc d = bridge::desc_for(spec, chunk_size);
+    lmoe_lsm_desc d = bridge::desc_for(spec, chunk_size);
+    if (x.host_fmap) d.feature_map = 0;
     Workspace ws;
     void* w = ws.get(lmoe_lsm_fwd_workspace_size(&d, 1, x.n, 1, x.pl.D, x.pl.dt));
     check(lmoe_lsm_fwd(&d, 1, x.n, 1, x.pl.D, x.pl.dt, x.q.p, x.k.p, x.v.p, x.a_pre.p, x.b_pre.as<float>(),
@@ -230,7 +246,8 @@ inline lmoe::Tensor sp_lsm_masked_rank(void* nccl_comm, int rank, int world, con
     if (!has_closed_chunk_form(spec.instance))
         throw std::runtime_error("sp_forward_masked: state-dependent instances have no chunk-parallel form");
     bridge::LsmDev x(q_loc, k_loc, v_loc, g_loc, spec);
-    const lmoe_lsm_desc d = bridge::desc_for(spec, 64);
+    lmoe_lsm_desc d = bridge::desc_for(spec, 64);
+    if (x.host_fmap) d.feature_map = 0;
     Workspace ws;
     void* w = ws.get(lmoe_sp_lsm_fwd_workspace_size(&d, 1, x.n, 1, x.pl.D, x.pl.dt, world));
     check(lmoe_sp_lsm_fwd(&d, 1, x.n, 1, x.pl.D, x.pl.dt, x.q.p, x.k.p, x.v.p, x.a_pre.p, x.b_pre.as<float>(),
