@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(256) moe_plan(const int* __restrict__ counts, 
         s_aux[tid] = prob_colsum ? ((double)c / ((double)T * K)) * (colsum / T) : 0.0;
     }
     __syncthreads();
-    if (tid <= E) offsets[tid] = s_off[tid];
+    for (int i = tid; i <= E; i += blockDim.x) offsets[i] = s_off[i];  // E + 1 entries (257 at E = 256)
     if (tid < E) group_end[tid] = s_off[tid + 1];
     const int nt = s_toff[E];
     for (int i = tid; i < nt; i += blockDim.x) {

@@ -140,3 +140,21 @@ def test_route_limits_error_text():
         moe.route(logits, 2)
     with pytest.raises(pk.LmoeError, match="route: bad top_k"):
         moe.route(logits[:, :8], 9)
+
+
+def test_dispatch_offsets_total_written_at_256_experts():
+    """moe_plan writes all E + 1 offsets: at E = 256 the total offsets[256] lies beyond the
+    256-thread block's one-entry-per-thread store (it was left stale); the workspace is
+    pre-filled with garbage so a missed store shows."""
+    torch = _torch()
+    from paper_2503_05447_b200 import moe
+    T, E, k = 300, 256, 4
+    g = torch.Generator(device="cuda").manual_seed(3)
+    layer = moe.MoeLayer.init(moe.MoeConfig(E, k, 256, 128), generator=g)
+    x = torch.randn(T, 256, device="cuda", generator=g).to(torch.bfloat16)
+    nbytes = moe._bind().lmoe_moe_workspace_size(T, 256, 128, E, k)
+    moe._workspace(nbytes, x.device).fill_(0x7F)
+    layer.forward(x)
+    _, _, off = layer.dispatch(T)
+    off = off.cpu().numpy()
+    assert off[0] == 0 and off[E] == T * k and np.all(np.diff(off) >= 0)
