@@ -216,10 +216,9 @@ extern "C" int lmoe_moe_forward(int T, int hidden, int ffn, int E, int top_k, co
         lmoe_dev::moe_block_scan<<<E, 256, 0, st>>>(P(w.blk_cnt), P(w.offsets), w.nblk, E, P(w.blk_base));
         if (top_k <= 8) lmoe_dev::moe_assign<8><<<w.nblk, 256, 0, st>>>(ids, T, E, top_k, P(w.blk_base), P(w.slot_pos), P(w.perm_token));
         else lmoe_dev::moe_assign<32><<<w.nblk, 256, 0, st>>>(ids, T, E, top_k, P(w.blk_base), P(w.slot_pos), P(w.perm_token));
-        // 5. permute rows
-        lmoe_dev::moe_gather<<<(int)((rows + 7) / 8), 256, 0, st>>>(
-            static_cast<const uint4*>(x), P(w.perm_token), (int)rows, hidden / 8,
-            reinterpret_cast<uint4*>(ws + w.x_perm));
+        // 5. permute rows: each token row read once, written to its top_k dispatch rows
+        lmoe_dev::moe_scatter<<<(T + 7) / 8, 256, 0, st>>>(static_cast<const uint4*>(x), P(w.slot_pos), T, top_k,
+                                                          hidden / 8, reinterpret_cast<uint4*>(ws + w.x_perm));
         LMOE_CUDA_CHECK(cudaGetLastError());
         g_launch_count += 5;
         // 6. H = silu(Xp Wg) * (Xp Wu)   (grouped, per-expert B operands)

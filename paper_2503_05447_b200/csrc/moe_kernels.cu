@@ -459,14 +459,32 @@ __global__ void __launch_bounds__(256) moe_assign(const int* __restrict__ ids, i
 template __global__ void moe_assign<8>(const int*, int, int, int, const int*, int*, int*);
 template __global__ void moe_assign<32>(const int*, int, int, int, const int*, int*, int*);
 
-// x_perm[pos] = x[perm_token[pos]]   (one warp per row, 16-byte vectors)
-__global__ void moe_gather(const uint4* __restrict__ x, const int* __restrict__ perm_token,
-                           int rows, int row_vec, uint4* __restrict__ x_perm) {
-    const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (r >= rows) return;
-    const uint4* src = x + (size_t)perm_token[r] * row_vec;
-    uint4* dst = x_perm + (size_t)r * row_vec;
-    for (int i = threadIdx.x & 31; i < row_vec; i += 32) dst[i] = src[i];
+// x_perm[slot_pos[t, s]] = x[t] for s < K: one warp per token reads its row once and writes
+// it to its K dispatch rows.  (A gather in dispatch-row order read every token row K times in
+// expert order and missed L2: 1.90 GB of DRAM per call at config 4 against 1.21 GB.)
+__global__ void moe_scatter(const uint4* __restrict__ x, const int* __restrict__ slot_pos, int T, int K,
+                            int row_vec, uint4* __restrict__ x_perm) {
+    const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (t >= T) return;
+    const int lane = threadIdx.x & 31;
+    const int my_pos = lane < K ? slot_pos[(size_t)t * K + lane] : 0;  // K <= 32
+    const uint4* src = x + (size_t)t * row_vec;
+    for (int base = 0; base < row_vec; base += 128) {
+        uint4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int i = base + j * 32 + lane;
+            if (i < row_vec) v[j] = __ldg(src + i);
+        }
+        for (int s = 0; s < K; ++s) {
+            uint4* dst = x_perm + (size_t)__shfl_sync(0xFFFFFFFFu, my_pos, s) * row_vec;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int i = base + j * 32 + lane;
+                if (i < row_vec) dst[i] = v[j];
+            }
+        }
+    }
 }
 
 // y[t] = sum_s gate[t,s] * y_perm[slot_pos[t,s]], slots in ascending expert order

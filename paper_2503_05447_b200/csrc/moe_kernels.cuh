@@ -54,8 +54,8 @@ __global__ void moe_block_scan(const int* __restrict__ blk_cnt, const int* __res
 template <int KM>
 __global__ void moe_assign(const int* __restrict__ ids, int T, int E, int K, const int* __restrict__ blk_base,
                            int* __restrict__ slot_pos, int* __restrict__ perm_token);
-__global__ void moe_gather(const uint4* __restrict__ x, const int* __restrict__ perm_token, int rows,
-                           int row_vec, uint4* __restrict__ x_perm);
+__global__ void moe_scatter(const uint4* __restrict__ x, const int* __restrict__ slot_pos, int T, int K,
+                            int row_vec, uint4* __restrict__ x_perm);
 template <int KM>
 __global__ void moe_combine(const __nv_bfloat16* __restrict__ y_perm, const int* __restrict__ slot_pos,
                             const float* __restrict__ gates, int T, int K, int hidden, void* __restrict__ y,
